@@ -1,0 +1,302 @@
+"""Benchmark of the TGV primal-dual hot path (BASELINE.json metric:
+"TGV voxel-iterations/sec at 1/2/4/8 B200; achieved HBM GB/s vs peak").
+
+A step is one full solve of the workload: reset the state from the resident
+histograms, `iters` iterations of (dual + primal/over-relaxation), and one
+energy/gap evaluation (all SURVEY.md §8(a) rows).  value = voxels x iters x
+steps / time, over all ranks.  Inputs are synthetic (synth/, seeded).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--iters I]
+  python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+
+Multi-GPU (torchrun, one rank per GPU): the grid is split in z-slabs across
+ranks (strong scaling of the same workload); NCCL halo exchange inside the
+library; the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "TGV voxel-iterations/sec"
+UNIT = "vox-it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--iters", type=int, default=None, help="iterations per step (default: the workload's)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
+    return ap.parse_args()
+
+
+def slab(nz, rank, world):
+    base, rem = divmod(nz, world)
+    z0 = rank * base + min(rank, rem)
+    return z0, z0 + base + (1 if rank < rem else 0)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][1]),
+                "power_w_max": max((num(r[2]) or 0) for r in rows), "samples": len(rows), "reasons": reasons}
+
+
+def cpu_oracle_rate(workload: str, target_s: float, steps: int = 0, warmup: int = 0):
+    """Time the fp64 oracle (as it stands) on this host on a bounded sample of
+    the workload: the full grid for k iterations, all host threads."""
+    import oracle
+    import synth
+    wl = synth.workload(workload)
+    h = synth.make_histograms(workload)
+    threads = oracle.max_threads()
+    o = oracle.Oracle(wl.shape, lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma,
+                      centers=np.asarray(wl.centers)).load(h)
+    t0 = time.perf_counter()
+    o.iterate(1, threads=threads)
+    t1 = time.perf_counter() - t0
+    if steps:  # reference arm: `warmup` untimed + `steps` timed single-iteration steps
+        for _ in range(warmup):
+            o.iterate(1, threads=threads)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o.iterate(1, threads=threads)
+        el = time.perf_counter() - t0
+        return wl.nvox * steps / el, threads, f"{workload} full grid {wl.shape}, {steps} timed iterations of 1", el
+    k = int(max(1, min(1000, round(target_s / max(t1, 1e-6)))))
+    t0 = time.perf_counter()
+    o.iterate(k, threads=threads)
+    el = time.perf_counter() - t0
+    return wl.nvox * k / el, threads, f"{workload} full grid {wl.shape}, {k} iterations (after 1 warm-up)", el
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    wl = synth.workload(a.workload)
+    v, threads, sample, el = cpu_oracle_rate(a.workload, 0, steps=a.steps, warmup=a.warmup)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * el / a.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "iters_per_step": 1},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2107_14790_b200 import Solver
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = synth.workload(a.workload)
+    iters = a.iters or wl.iters
+    nx, ny, nz = wl.shape
+    z0, z1 = slab(nz, rank, world)
+    counts = synth.make_histograms(a.workload, z0, z1)
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
+    if world > 1:
+        s = Solver.distributed(wl.shape, list(wl.centers), z0, z1, local, **kw)
+    else:
+        s = Solver(wl.shape, list(wl.centers), device=local, **kw)
+    s.load(counts)
+    info = s.info()
+    nvox_local = (z1 - z0) * ny * nx
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        s.reset()
+        s.iterate(iters)
+        s.energy()
+
+    for _ in range(a.warmup):
+        step()
+    # ---- timed region: device-resident inputs --------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    s.set_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    barrier()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    tm = s.timing()
+    s.set_timing(False)
+    clk = clocks.stop()
+    ms_t = torch.tensor([ms, wall * 1e3 / a.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t[0])
+    value = wl.nvox * iters / (ms_max * 1e-3)
+
+    # roofline of the dominant kernel (primal: largest bytes and time per launch)
+    peak, peak_src = measured_peaks()
+    k_primal = tm["primal_ms"] / max(1, tm["primal_launches"])
+    k_dual = tm["dual_ms"] / max(1, tm["dual_launches"])
+    dom, kms, bpv = ("primal", k_primal, info["bytes_primal"]) if k_primal >= k_dual else \
+        ("dual", k_dual, info["bytes_dual"])
+    achieved = bpv * nvox_local / (kms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(a.workload, {}).get(dom)
+        except Exception:
+            traffic = None
+    step_kernel_ms = tm["primal_ms"] + tm["dual_ms"] + tm["energy_ms"]
+    launches_per_step = (tm["dual_launches"] + tm["primal_launches"]) / a.steps + 3  # + init + 2 energy kernels
+
+    # ---- e2e: host buffers, H2D + D2H inside the timed region ------------------
+    e2e = None
+    if not a.no_e2e:
+        hc = torch.from_numpy(counts).pin_memory()
+        hu = torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory()
+        from paper_2107_14790_b200 import tgv
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            tgv.tgv_load_histograms(s.ctx, hc)
+            s.iterate(iters)
+            s.energy()
+            tgv.tgv_read_u(s.ctx, hu)
+        torch.cuda.synchronize()
+        el = torch.tensor([(time.perf_counter() - t0) / a.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": wl.nvox * iters / float(el[0]), "unit": UNIT, "h2d_bytes_per_step": int(hc.numel() * 4),
+               "d2h_bytes_per_step": int(hu.numel() * 4 + 6 * 8)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, threads, sample, _ = cpu_oracle_rate(a.workload, a.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "iters_per_step": iters,
+                       "step": "reset + iters x (dual, primal+over-relax) + energy/gap",
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "l2": f"no flush: resident state+histograms {info['device_bytes'] / 1e9:.2f} GB per GPU "
+                             f">> 126 MB L2"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_voxel": bpv, "kernel_ms": kms,
+                         "schedule_gbs": (info["bytes_dual"] + info["bytes_primal"]) * wl.nvox * iters
+                         / (ms_max * 1e-3) / 1e9 / world,
+                         "kernel_share_of_step": step_kernel_ms / a.steps / ms},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches_per_step * a.steps)),
+            "kernel_ms": {"dual": k_dual, "primal": k_primal,
+                          "energy": tm["energy_ms"] / max(1, tm["energy_launches"])},
+            "wall_ms_per_step": float(ms_t[1]),
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

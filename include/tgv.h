@@ -1,0 +1,192 @@
+/*
+ * tgv.h -- C ABI of the B200 (sm_100a) TGV primal-dual solver.
+ *
+ * The library minimises, over an nx x ny x nz voxel grid (x fastest), the
+ * discrete TGV functional of PAPER.md Eq. 2 (§3.2)
+ *
+ *     E(u, v) = sum_x  alpha1 |grad u - v|_2 + alpha0 |E(v)|_F
+ *                      + lambda sum_b h_b |u - c_b|
+ *
+ * with E(v) = (grad v + grad v^T)/2 (Eq. 3), the indicator
+ * u in [-1, 1] and the data term written through per-voxel
+ * vote histograms h_b over bin centres c_b (Alg. 1
+ * PAPER.md:252-278), by the primal-dual method the paper cites
+ * ("we use the primal-dual method [pock2011tgv]").  The
+ * discretisation and every reading of a point the paper leaves open are listed
+ * in DESIGN.md §2 (R1-R17); the defining passages are cited per call below.
+ *
+ * Conventions for every call:
+ *   - returns int status: TGV_OK (0) or a negative TGV_E* code; no C++
+ *     exception ever crosses the ABI;
+ *   - host buffers are owned by the caller, read or written only during the
+ *     call and never retained; pinned (page-locked) buffers make the copies
+ *     faster but are not required;
+ *   - the context owns ALL device memory, streams, events and the NCCL
+ *     communicator; one context per (process, GPU); calls on one context must
+ *     not run concurrently;
+ *   - a CUDA or NCCL failure poisons the context: that call returns
+ *     TGV_ECUDA / TGV_ENCCL and every later call except tgv_destroy,
+ *     tgv_last_error and tgv_status_string returns TGV_ESTATE;
+ *   - calls marked COLLECTIVE must be made by every rank of the communicator
+ *     in the same order.
+ */
+#ifndef TGV_H
+#define TGV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define TGV_OK 0
+#define TGV_EINVAL (-1) /* bad argument: NULL pointer, size mismatch, invalid parameter */
+#define TGV_ENOMEM (-2) /* device or pinned-host allocation failed */
+#define TGV_ECUDA (-3)  /* CUDA runtime failure (context poisoned) */
+#define TGV_ENCCL (-4)  /* NCCL failure (context poisoned) */
+#define TGV_ESTATE (-5) /* call not valid in this state (e.g. iterate before load; poisoned) */
+#define TGV_ERANGE (-6) /* a histogram count exceeds 65535 (device counts are u16) */
+
+/* ---- field ids for tgv_read_field / tgv_write_field -------------------- */
+#define TGV_FIELD_U 0      /* primal indicator u                                   */
+#define TGV_FIELD_V 1      /* primal vector field v: 1 + k, k = x, y, z            */
+#define TGV_FIELD_UBAR 4   /* over-relaxed u: ubar = 2 u_new - u_old               */
+#define TGV_FIELD_VBAR 5   /* over-relaxed v: 5 + k                                */
+#define TGV_FIELD_P 8      /* dual of grad u - v: 8 + k                            */
+#define TGV_FIELD_Q 11     /* dual of E(v): 11 + m, m = xx, yy, zz, xy, xz, yz     */
+#define TGV_NUM_FIELDS 17
+
+typedef struct tgv_ctx tgv_ctx; /* opaque */
+
+/* Grid layout.  The global dense grid is nx x ny x nz voxels, voxel (x,y,z)
+ * stored x fastest.  This rank owns the z-slab [z_begin, z_end)
+ * (multi-GPU: contiguous slabs, rank r below rank r+1, every slab non-empty;
+ * SURVEY.md §8(e)).  brick = {0,0,0} selects the plain linear layout; any
+ * other value is reserved for block-sparse brick sets (SURVEY.md §8(f)
+ * NEXT-3) and currently returns TGV_EINVAL. */
+typedef struct {
+    int64_t nx, ny, nz;
+    int64_t z_begin, z_end;
+    int32_t brick[3];
+} tgv_layout;
+
+/* Solver parameters (R1, R3, R5, R7).
+ *   nbins        number of histogram bins, 1..16 (the paper uses 8, Alg. 1)
+ *   bin_centers  nbins floats, strictly increasing, within [-1, 1]; copied at create.
+ *                The paper's bins are c_b = -0.875 + 0.25 b (R3).
+ *   lambda       data-term weight (>= 0); Eq. 2 literally is lambda = 1 (R1)
+ *   alpha0       weight of |E(v)| (>= 0);  alpha1 weight of |grad u - v| (>= 0)
+ *   tau, sigma   primal / dual step sizes (> 0), required tau*sigma*16 <= 1
+ *                (16 bounds ||K||^2 of the discrete operator, R7). */
+typedef struct {
+    int32_t nbins;
+    const float* bin_centers;
+    float lambda, alpha0, alpha1, tau, sigma;
+} tgv_params;
+
+/* Kernel timing (device time from CUDA events on the launching stream). */
+typedef struct {
+    double dual_ms, primal_ms, energy_ms, halo_ms; /* summed device ms since last reset */
+    int64_t dual_launches, primal_launches, energy_launches, halo_exchanges;
+} tgv_timing;
+
+/* Static facts about a context. */
+typedef struct {
+    int64_t row_pitch;        /* floats per stored row (>= nx, multiple of 32)          */
+    int64_t device_bytes;     /* device memory owned by the context                     */
+    int32_t count_bytes;      /* bytes per stored histogram count (2 = u16)             */
+    int32_t count_slots;      /* histogram slots stored per voxel (8 or 16)             */
+    int64_t bytes_dual;       /* algorithmic HBM bytes per voxel of one dual launch     */
+    int64_t bytes_primal;     /* algorithmic HBM bytes per voxel of one primal launch   */
+    int32_t nranks, rank;
+} tgv_info_t;
+
+/* Rank 0 creates the NCCL unique id; the caller broadcasts the 128 bytes
+ * (e.g. with torch.distributed) to every rank before tgv_create. */
+int tgv_get_unique_id(uint8_t uid[128]);
+
+/* COLLECTIVE (nranks > 1).  Validates layout and parameters, selects
+ * cuda_device, allocates the state (u, v, ubar, vbar, p, q in fp32 SoA planes
+ * with one halo plane below and above the slab, 68 B per voxel) and the
+ * histogram store, creates streams/events and, if nranks > 1, the NCCL
+ * communicator from uid (uid must be NULL iff nranks == 1).
+ * Errors: TGV_EINVAL for any invalid argument (see tgv_params / tgv_layout;
+ * also non-contiguous slabs across ranks), TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL.
+ * On error *out is NULL. */
+int tgv_create(const tgv_layout* layout, const tgv_params* params, int rank, int nranks, const uint8_t* uid,
+               int cuda_device, tgv_ctx** out);
+
+/* Load this rank's histograms and reset the state.
+ *   counts    host, uint32 [z_end - z_begin][ny][nx][nbins] (row-major, bins fastest)
+ *   n_counts  number of uint32 elements; must equal (z_end-z_begin)*ny*nx*nbins
+ * The counts are copied to the device in chunks and packed to u16.  Then
+ * (R9): u = sum_b h_b c_b / W (0 where W = 0), v = p = q = 0,
+ * ubar = u, vbar = 0, iteration counter 0.
+ * Errors: TGV_EINVAL (NULL, size mismatch), TGV_ERANGE (a count > 65535; the
+ * previous histograms are then lost and the context needs another load),
+ * TGV_ECUDA.  Not collective. */
+int tgv_load_histograms(tgv_ctx* ctx, const uint32_t* counts, int64_t n_counts);
+
+/* Reset the state from the loaded histograms as tgv_load_histograms does,
+ * without a host copy.  TGV_ESTATE before the first successful load. */
+int tgv_reset(tgv_ctx* ctx);
+
+/* COLLECTIVE.  Run n >= 0 full iterations of the scheme:
+ *   p <- P_alpha1(p + sigma (grad ubar - vbar)),  q <- P_alpha0(q + sigma E(vbar))
+ *   u+ = clamp(prox_{tau lambda h}(u + tau div p), -1, 1),  v+ = v + tau (p + div2 q)
+ *   ubar = 2 u+ - u,  vbar = 2 v+ - v
+ * where P_a is the Euclidean (Frobenius for q) projection onto the ball of
+ * radius a and the prox is the exact weighted median of the histogram-L1
+ * term.  Multi-GPU: one-plane halos exchanged by NCCL send/recv each
+ * half-step.  Blocks until the device work is done.
+ * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load / poisoned), TGV_ECUDA, TGV_ENCCL. */
+int tgv_iterate(tgv_ctx* ctx, int32_t n);
+
+/* Copy this rank's u to the host: u_out float [z_end-z_begin][ny][nx];
+ * n_voxels must equal (z_end-z_begin)*ny*nx.  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_read_u(tgv_ctx* ctx, float* u_out, int64_t n_voxels);
+
+/* Copy one state field (TGV_FIELD_*) of this rank to the host, same layout
+ * and size rule as tgv_read_u.  Errors as tgv_read_u; TGV_EINVAL for a bad id. */
+int tgv_read_field(tgv_ctx* ctx, int field, float* out, int64_t n_voxels);
+
+/* Overwrite one state field from the host (test hook; the halo planes are
+ * refreshed by the next iterate / energy).  Errors as tgv_read_field. */
+int tgv_write_field(tgv_ctx* ctx, int field, const float* in, int64_t n_voxels);
+
+/* COLLECTIVE.  Energy and restricted primal-dual gap of the current state
+ * (R14), per-voxel terms in fp64 from the fp32
+ * state, deterministic fixed-order reduction, fp64 NCCL all-reduce:
+ *   out[0] E = alpha1-term + alpha0-term + data-term
+ *   out[1] sum alpha1 |grad u - v|_2          out[2] sum alpha0 |E(v)|_F
+ *   out[3] sum lambda sum_b h_b |u - c_b|
+ *   out[4] gap_V = E - D_V,  D_V = sum min_{u in [-1,1]}(lambda sum_b h_b |u - c_b| - u div p)
+ *                                  - V |p + div2 q|_1,  V = 2
+ *   out[5] max_x,k |v_k|  (gap_V >= 0 is guaranteed while this is <= V)
+ * Errors: TGV_EINVAL (NULL), TGV_ESTATE, TGV_ECUDA, TGV_ENCCL. */
+int tgv_energy(tgv_ctx* ctx, double out[6]);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing inside tgv_iterate
+ * and tgv_energy; tgv_get_timing returns the sums since the last enable. */
+int tgv_set_timing(tgv_ctx* ctx, int enable);
+int tgv_get_timing(const tgv_ctx* ctx, tgv_timing* out);
+
+/* Static facts (pitch, device bytes, algorithmic bytes per voxel per launch). */
+int tgv_info(const tgv_ctx* ctx, tgv_info_t* out);
+
+/* Release everything; NULL-safe.  Not collective (NCCL comm is aborted if a
+ * peer failed, destroyed otherwise). */
+void tgv_destroy(tgv_ctx* ctx);
+
+/* Static string for a status code. */
+const char* tgv_status_string(int status);
+
+/* Human-readable detail of the last failure on ctx ("" if none; ctx may be NULL
+ * for failures of tgv_create, which are kept per thread). */
+const char* tgv_last_error(const tgv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGV_H */

@@ -1,0 +1,268 @@
+"""Thin ctypes binding of the C ABI in include/tgv.h (argument marshalling only).
+
+Every step of the solver runs in libtgv.so's sm_100a kernels; this module
+never computes.  The functions carry the ABI's names; ``Solver`` is a small
+convenience wrapper (context lifetime, torch.distributed bootstrap of the NCCL
+unique id, numpy/torch host buffers).  There is no fallback: if libtgv.so is
+missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libtgv.so")
+
+TGV_OK, TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL, TGV_ESTATE, TGV_ERANGE = 0, -1, -2, -3, -4, -5, -6
+FIELD_U, FIELD_V, FIELD_UBAR, FIELD_VBAR, FIELD_P, FIELD_Q, NUM_FIELDS = 0, 1, 4, 5, 8, 11, 17
+FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 10],
+          "q": [11, 12, 13, 14, 15, 16]}
+
+EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
+           "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_timing", "tgv_get_timing", "tgv_info",
+           "tgv_destroy", "tgv_status_string", "tgv_last_error"]
+
+
+class tgv_layout(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+                ("z_begin", ctypes.c_int64), ("z_end", ctypes.c_int64), ("brick", ctypes.c_int32 * 3)]
+
+
+class tgv_params(ctypes.Structure):
+    _fields_ = [("nbins", ctypes.c_int32), ("bin_centers", ctypes.POINTER(ctypes.c_float)),
+                ("lambda_", ctypes.c_float), ("alpha0", ctypes.c_float), ("alpha1", ctypes.c_float),
+                ("tau", ctypes.c_float), ("sigma", ctypes.c_float)]
+
+
+class tgv_timing(ctypes.Structure):
+    _fields_ = [("dual_ms", ctypes.c_double), ("primal_ms", ctypes.c_double), ("energy_ms", ctypes.c_double),
+                ("halo_ms", ctypes.c_double), ("dual_launches", ctypes.c_int64),
+                ("primal_launches", ctypes.c_int64), ("energy_launches", ctypes.c_int64),
+                ("halo_exchanges", ctypes.c_int64)]
+
+
+class tgv_info_t(ctypes.Structure):
+    _fields_ = [("row_pitch", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32),
+                ("count_slots", ctypes.c_int32), ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64),
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtgv.so not built ({LIB_PATH}); run __graft_entry__.build() -- there is no fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    lib.tgv_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.tgv_create.argtypes = [ctypes.POINTER(tgv_layout), ctypes.POINTER(tgv_params), ctypes.c_int, ctypes.c_int,
+                               ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.tgv_load_histograms.argtypes = [vp, vp, i64]
+    lib.tgv_reset.argtypes = [vp]
+    lib.tgv_iterate.argtypes = [vp, i32]
+    lib.tgv_read_u.argtypes = [vp, vp, i64]
+    lib.tgv_read_field.argtypes = [vp, ctypes.c_int, vp, i64]
+    lib.tgv_write_field.argtypes = [vp, ctypes.c_int, vp, i64]
+    lib.tgv_energy.argtypes = [vp, vp]
+    lib.tgv_set_timing.argtypes = [vp, ctypes.c_int]
+    lib.tgv_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
+    lib.tgv_info.argtypes = [vp, ctypes.POINTER(tgv_info_t)]
+    lib.tgv_destroy.argtypes = [vp]
+    lib.tgv_destroy.restype = None
+    lib.tgv_status_string.argtypes = [ctypes.c_int]
+    lib.tgv_status_string.restype = ctypes.c_char_p
+    lib.tgv_last_error.argtypes = [vp]
+    lib.tgv_last_error.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("tgv_destroy", "tgv_status_string", "tgv_last_error"):
+            getattr(lib, name).restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+class TgvError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{lib.tgv_status_string(status).decode()} -- {detail}")
+        self.status = status
+
+
+def _check(rc: int, ctx=None):
+    if rc != TGV_OK:
+        raise TgvError(rc, lib.tgv_last_error(ctx).decode(errors="replace"))
+
+
+def _host_ptr(a, dtype):
+    """Pointer + element count of a C-contiguous host buffer (numpy or torch CPU tensor)."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            assert a.device.type == "cpu" and a.is_contiguous(), "host buffer must be a contiguous CPU tensor"
+            assert a.dtype == {np.uint32: torch.uint32, np.float32: torch.float32}[dtype]
+            return a.data_ptr(), a.numel()
+    except ImportError:  # pragma: no cover
+        pass
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype == dtype, "need a C-contiguous array"
+    return a.ctypes.data, a.size
+
+
+# ---- ABI-named functions -------------------------------------------------------
+def tgv_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.tgv_get_unique_id(buf))
+    return buf.raw
+
+
+def tgv_create(shape, z_begin, z_end, centers, lam, alpha0, alpha1, tau, sigma, rank=0, nranks=1, uid=None,
+               device=0):
+    nx, ny, nz = shape
+    L = tgv_layout(nx, ny, nz, z_begin, z_end, (ctypes.c_int32 * 3)(0, 0, 0))
+    c = (ctypes.c_float * len(centers))(*[float(x) for x in centers])
+    P = tgv_params(len(centers), ctypes.cast(c, ctypes.POINTER(ctypes.c_float)), lam, alpha0, alpha1, tau, sigma)
+    out = ctypes.c_void_p()
+    _check(lib.tgv_create(ctypes.byref(L), ctypes.byref(P), rank, nranks, uid, device, ctypes.byref(out)))
+    return out
+
+
+def tgv_load_histograms(ctx, counts):
+    p, n = _host_ptr(counts, np.uint32)
+    _check(lib.tgv_load_histograms(ctx, p, n), ctx)
+
+
+def tgv_reset(ctx):
+    _check(lib.tgv_reset(ctx), ctx)
+
+
+def tgv_iterate(ctx, n: int):
+    _check(lib.tgv_iterate(ctx, int(n)), ctx)
+
+
+def tgv_read_u(ctx, out):
+    p, n = _host_ptr(out, np.float32)
+    _check(lib.tgv_read_u(ctx, p, n), ctx)
+    return out
+
+
+def tgv_read_field(ctx, field: int, out):
+    p, n = _host_ptr(out, np.float32)
+    _check(lib.tgv_read_field(ctx, int(field), p, n), ctx)
+    return out
+
+
+def tgv_write_field(ctx, field: int, arr):
+    p, n = _host_ptr(arr, np.float32)
+    _check(lib.tgv_write_field(ctx, int(field), p, n), ctx)
+
+
+def tgv_energy(ctx) -> np.ndarray:
+    out = np.zeros(6, dtype=np.float64)
+    _check(lib.tgv_energy(ctx, out.ctypes.data), ctx)
+    return out
+
+
+def tgv_set_timing(ctx, enable: bool):
+    _check(lib.tgv_set_timing(ctx, 1 if enable else 0), ctx)
+
+
+def tgv_get_timing(ctx) -> dict:
+    t = tgv_timing()
+    _check(lib.tgv_get_timing(ctx, ctypes.byref(t)), ctx)
+    return {k: getattr(t, k) for k, _ in tgv_timing._fields_}
+
+
+def tgv_info(ctx) -> dict:
+    t = tgv_info_t()
+    _check(lib.tgv_info(ctx, ctypes.byref(t)), ctx)
+    return {k: getattr(t, k) for k, _ in tgv_info_t._fields_}
+
+
+def tgv_destroy(ctx):
+    lib.tgv_destroy(ctx)
+
+
+# ---- convenience wrapper ---------------------------------------------------------
+class Solver:
+    """One context on one GPU owning z-slab [z_begin, z_end) of an (nx, ny, nz) grid.
+
+    With ``nranks > 1`` pass ``uid`` (from rank 0's ``tgv_get_unique_id``), or
+    call ``Solver.distributed(...)`` which broadcasts it with torch.distributed.
+    """
+
+    def __init__(self, shape, centers, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25, z_begin=0,
+                 z_end=None, rank=0, nranks=1, uid=None, device=0):
+        self.shape = tuple(int(s) for s in shape)
+        self.z_begin = int(z_begin)
+        self.z_end = self.shape[2] if z_end is None else int(z_end)
+        self.nbins = len(centers)
+        self.ctx = tgv_create(self.shape, self.z_begin, self.z_end, centers, lam, alpha0, alpha1, tau, sigma, rank,
+                              nranks, uid, device)
+
+    @classmethod
+    def distributed(cls, shape, centers, z_begin, z_end, device, **kw):
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        uid = None
+        if world > 1:
+            t = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
+            if rank == 0:
+                t.copy_(torch.frombuffer(bytearray(tgv_get_unique_id()), dtype=torch.uint8))
+            dist.broadcast(t, 0)
+            uid = bytes(t.cpu().numpy().tobytes())
+        return cls(shape, centers, z_begin=z_begin, z_end=z_end, rank=rank, nranks=world, uid=uid, device=device, **kw)
+
+    @property
+    def local_shape(self):
+        nx, ny, _ = self.shape
+        return (self.z_end - self.z_begin, ny, nx)
+
+    def load(self, counts):
+        tgv_load_histograms(self.ctx, counts)
+        return self
+
+    def reset(self):
+        tgv_reset(self.ctx)
+
+    def iterate(self, n: int):
+        tgv_iterate(self.ctx, n)
+        return self
+
+    def read_u(self, out=None):
+        out = np.empty(self.local_shape, np.float32) if out is None else out
+        return tgv_read_u(self.ctx, out)
+
+    def get(self, name: str) -> np.ndarray:
+        ids = FIELDS[name]
+        out = np.empty((len(ids),) + self.local_shape, np.float32)
+        for k, f in enumerate(ids):
+            tgv_read_field(self.ctx, f, out[k])
+        return out[0] if len(ids) == 1 else out
+
+    def set(self, name: str, arr):
+        ids = FIELDS[name]
+        arr = np.ascontiguousarray(arr, dtype=np.float32).reshape((len(ids),) + self.local_shape)
+        for k, f in enumerate(ids):
+            tgv_write_field(self.ctx, f, np.ascontiguousarray(arr[k]))
+
+    def energy(self) -> dict:
+        e = tgv_energy(self.ctx)
+        return {"E": e[0], "alpha1": e[1], "alpha0": e[2], "data": e[3], "gap": e[4], "vmax": e[5]}
+
+    def set_timing(self, on: bool):
+        tgv_set_timing(self.ctx, on)
+
+    def timing(self) -> dict:
+        return tgv_get_timing(self.ctx)
+
+    def info(self) -> dict:
+        return tgv_info(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            tgv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,10 @@
+#!/bin/bash
+# One gpurun session: build, GPU tests, smoke, bench, ncu launch list + one full capture.
+# usage (from this container):  gpurun --timeout 1800 -- 'bash scripts/gpu_check.sh [tag]'
+set -x
+TAG=${1:-r1}
+mkdir -p gpurun_out
+nvidia-smi > gpurun_out/nvidia-smi_$TAG.txt 2>&1
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
+timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err

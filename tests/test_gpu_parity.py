@@ -1,0 +1,184 @@
+"""GPU (libtgv.so through the C ABI) vs the fp64 CPU oracle on the same seeded
+inputs (SURVEY.md §8(c) "GPU vs oracle parity"; north_star tolerances):
+
+    max |u_gpu - u_cpu| <= 1e-4   and   |E_gpu - E_cpu| / |E_cpu| <= 1e-5
+
+after the stated iteration count.  Sizes: the C1 workload at its full count,
+ragged grids spanning several 32x8 tiles with partial tiles and size-1 axes,
+a 64^3 window of the C2 workload at C2's full 500 iterations, and the full
+256^3 C2 grid (the bench's launch configuration) at a truncated count plus
+properties that hold at any size at the full count.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+U_TOL = 1e-4
+E_RTOL = 1e-5
+NT = max(1, oracle.max_threads())
+
+
+def solver_cls():
+    from paper_2107_14790_b200 import Solver
+    return Solver
+
+
+def params(wl=None, **kw):
+    p = dict(lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25)
+    if wl is not None:
+        p = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
+    p.update(kw)
+    return p
+
+
+def pair(shape, counts, iters, centers=None, **kw):
+    c = oracle.default_centers(8) if centers is None else np.asarray(centers, np.float64)
+    p = params(**kw)
+    o = oracle.Oracle(shape, centers=c, **p).load(counts).iterate(iters, threads=NT)
+    s = solver_cls()(shape, [float(x) for x in c], **p).load(np.ascontiguousarray(counts, np.uint32)).iterate(iters)
+    return o, s
+
+
+def assert_parity(o, s, u_tol=U_TOL, e_rtol=E_RTOL):
+    du = np.max(np.abs(s.read_u().astype(np.float64) - o.u))
+    eo, es = o.energy(), s.energy()
+    rel = abs(es["E"] - eo["E"]) / max(abs(eo["E"]), 1e-300)
+    assert du <= u_tol, f"max|du| = {du}"
+    assert rel <= e_rtol, f"energy rel diff {rel} (gpu {es['E']}, cpu {eo['E']})"
+    for k in ("alpha1", "alpha0", "data"):
+        assert abs(es[k] - eo[k]) <= 1e-4 * max(1.0, abs(eo["E"])), k
+    return du, rel
+
+
+def test_init_matches():
+    shape = (37, 23, 19)
+    h = synth.random_histograms(shape, 1)
+    o, s = pair(shape, h, 0)
+    np.testing.assert_allclose(s.read_u(), o.u, rtol=0, atol=6e-8)
+    assert np.all(s.get("ubar") == s.read_u())
+    for f in ("v", "vbar", "p", "q"):
+        assert np.all(s.get(f) == 0)
+
+
+@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 16, 5), (1, 1, 9), (33, 1, 4), (2, 70, 3)])
+def test_one_iteration_from_random_state(shape):
+    """Every stencil path (interior, all six boundary faces, projections active) in one step."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(7)
+    h = synth.random_histograms(shape, 2)
+    c = oracle.default_centers(8)
+    o = oracle.Oracle(shape, **params()).load(h)
+    s = solver_cls()(shape, list(c), **params()).load(h)
+    st = {"u": rng.uniform(-1, 1, (nz, ny, nx)), "ubar": rng.uniform(-1.5, 1.5, (nz, ny, nx)),
+          "v": rng.normal(0, 0.5, (3, nz, ny, nx)), "vbar": rng.normal(0, 0.5, (3, nz, ny, nx)),
+          "p": rng.normal(0, 0.7, (3, nz, ny, nx)), "q": rng.normal(0, 1.0, (6, nz, ny, nx))}
+    for k, a in st.items():
+        a32 = a.astype(np.float32)
+        s.set(k, a32)
+        o.set(k, a32.astype(np.float64))
+    o.iterate(1)
+    s.iterate(1)
+    for f in ("p", "q", "u", "ubar", "v", "vbar"):
+        np.testing.assert_allclose(s.get(f), o.get(f), rtol=0, atol=3e-6, err_msg=f)
+
+
+def test_c1_full_count():
+    wl = synth.workload("C1")
+    h = synth.make_histograms("C1")
+    o, s = pair(wl.shape, h, wl.iters, **params(wl))
+    du, rel = assert_parity(o, s)
+    print(f"C1 x{wl.iters}: max|du| = {du:.3e}, rel dE = {rel:.3e}")
+
+
+@pytest.mark.parametrize("shape,seed", [((37, 23, 19), 3), ((1, 1, 40), 4), ((33, 1, 7), 5), ((129, 9, 4), 6),
+                                        ((1, 1, 1), 7), ((5, 64, 3), 8)])
+def test_ragged_shapes(shape, seed):
+    h = synth.random_histograms(shape, seed)
+    o, s = pair(shape, h, 60)
+    assert_parity(o, s)
+
+
+def test_nonuniform_centres_and_16_bins():
+    shape = (21, 13, 11)
+    rng = np.random.default_rng(9)
+    for nb in (3, 16):
+        c = np.sort(rng.uniform(-0.95, 0.95, nb)).astype(np.float32).astype(np.float64)
+        h = rng.integers(0, 5, size=(11, 13, 21, nb)).astype(np.uint32)
+        o, s = pair(shape, h, 40, centers=c)
+        assert_parity(o, s)
+
+
+def test_special_cases_exact():
+    S = solver_cls()
+    c = list(oracle.default_centers(8))
+    s = S((9, 7, 5), c).load(np.zeros((5, 7, 9, 8), np.uint32)).iterate(20)
+    assert np.all(s.read_u() == 0.0)
+    h = np.array([3, 0, 1, 0, 0, 2, 5, 1], np.uint32)
+    s = S((9, 7, 5), c).load(np.broadcast_to(h, (5, 7, 9, 8)).copy()).iterate(5)
+    assert np.all(s.read_u() == 0.375)  # weighted-median limit (tests/test_oracle_scheme.py)
+
+
+def test_c2_window_full_count():
+    """A 64^3 window of the C2 workload (sphere + plane, noise, floaters) at C2's 500 iterations."""
+    wl = synth.workload("C2")
+    h = synth.make_histograms("C2", 118, 182)[:, 96:160, 96:160]
+    h = np.ascontiguousarray(h)
+    o, s = pair((64, 64, 64), h, wl.iters, **params(wl))
+    du, rel = assert_parity(o, s)
+    print(f"C2 window 64^3 x{wl.iters}: max|du| = {du:.3e}, rel dE = {rel:.3e}")
+
+
+def test_c2_full_grid_truncated_count():
+    """Full 256^3 C2 grid in the bench's launch configuration, every voxel compared."""
+    wl = synth.workload("C2")
+    h = synth.make_histograms("C2")
+    o, s = pair(wl.shape, h, 6, **params(wl))
+    assert_parity(o, s)
+
+
+def test_c2_full_count_properties():
+    wl = synth.workload("C2")
+    h = synth.make_histograms("C2")
+    s = solver_cls()(wl.shape, list(wl.centers), **params(wl)).load(h)
+    it, gaps, Es = 0, [], []
+    for ck in (8, 16, 32, 64, 128, 256, wl.iters):
+        s.iterate(ck - it)
+        it = ck
+        e = s.energy()
+        gaps.append(e["gap"])
+        Es.append(e["E"])
+        assert e["vmax"] <= 2.0 and e["gap"] >= -1e-6 * e["E"]
+    u1 = s.read_u()
+    assert np.all(np.abs(u1) <= 1.0)
+    assert Es[-1] <= Es[0]
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(gaps, gaps[1:])), gaps
+    s.reset()
+    s.iterate(wl.iters)
+    assert np.array_equal(s.read_u(), u1)  # deterministic
+
+
+def test_error_paths():
+    from paper_2107_14790_b200 import tgv
+    S = solver_cls()
+    c = list(oracle.default_centers(8))
+    s = S((8, 8, 8), c)
+    with pytest.raises(tgv.TgvError) as ei:
+        s.iterate(1)
+    assert ei.value.status == tgv.TGV_ESTATE
+    with pytest.raises(tgv.TgvError) as ei:
+        s.load(np.zeros((8, 8, 8, 7), np.uint32))
+    assert ei.value.status == tgv.TGV_EINVAL
+    h = np.zeros((8, 8, 8, 8), np.uint32)
+    h[3, 4, 5, 2] = 70000
+    with pytest.raises(tgv.TgvError) as ei:
+        s.load(h)
+    assert ei.value.status == tgv.TGV_ERANGE
+    s.load(np.ones((8, 8, 8, 8), np.uint32))
+    with pytest.raises(tgv.TgvError) as ei:
+        s.iterate(-1)
+    assert ei.value.status == tgv.TGV_EINVAL
+    s.iterate(2)
