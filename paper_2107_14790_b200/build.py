@@ -1,6 +1,6 @@
 """Build the sm_100a shared library libtgv.so (C ABI of include/tgv.h) in-tree.
 
-nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared ... -lnccl
+nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared ... -ldl (NCCL is dlopen'ed at run time)
 The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
 """
 from __future__ import annotations
@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-lnccl"]
+    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

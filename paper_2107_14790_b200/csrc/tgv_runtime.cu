@@ -6,7 +6,6 @@
 // histogram store, a compute stream, CUDA events for kernel timing and, for
 // nranks > 1, an NCCL communicator over NVLink/NVSwitch.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -17,6 +16,7 @@
 #include <vector>
 
 #include "../../include/tgv.h"
+#include "nccl_api.h"
 #include "tgv_kernels.cuh"
 
 using namespace tgvk;
@@ -64,6 +64,7 @@ struct tgv_ctx {
 
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    const NcclApi* nccl = nullptr;  // resolved at create when nranks > 1
 
     bool loaded = false;
     bool poisoned = false;
@@ -100,7 +101,7 @@ int fail(tgv_ctx* c, int code, const char* fmt, ...)
     do {                                                                                           \
         ncclResult_t r_ = (call);                                                                  \
         if (r_ != ncclSuccess)                                                                     \
-            return fail(c, TGV_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(r_)); \
+            return fail(c, TGV_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, nccl->GetErrorString(r_)); \
     } while (0)
 
 inline float* field(tgv_ctx* c, int f) { return c->state + (int64_t)f * c->g.fs; }
@@ -194,23 +195,24 @@ int launch_primal(tgv_ctx* c)
 int halo_exchange(tgv_ctx* c, const HaloPlan& hp)
 {
     if (c->nranks == 1) return TGV_OK;
+    const NcclApi* nccl = c->nccl;
     size_t slot = 0;
     int rc = timer_begin(c, T_HALO, &slot);
     if (rc) return rc;
     const size_t n = (size_t)c->g.plane;
     const int nzl = c->g.nzl;
-    NC(ncclGroupStart());
+    NC(nccl->GroupStart());
     for (int k = 0; k < hp.ndown; ++k) {
-        if (c->rank > 0) NC(ncclSend(plane_ptr(c, hp.down[k], 0), n, ncclFloat, c->rank - 1, c->comm, c->stream));
+        if (c->rank > 0) NC(nccl->Send(plane_ptr(c, hp.down[k], 0), n, ncclFloat, c->rank - 1, c->comm, c->stream));
         if (c->rank < c->nranks - 1)
-            NC(ncclRecv(plane_ptr(c, hp.down[k], nzl), n, ncclFloat, c->rank + 1, c->comm, c->stream));
+            NC(nccl->Recv(plane_ptr(c, hp.down[k], nzl), n, ncclFloat, c->rank + 1, c->comm, c->stream));
     }
     for (int k = 0; k < hp.nup; ++k) {
         if (c->rank < c->nranks - 1)
-            NC(ncclSend(plane_ptr(c, hp.up[k], nzl - 1), n, ncclFloat, c->rank + 1, c->comm, c->stream));
-        if (c->rank > 0) NC(ncclRecv(plane_ptr(c, hp.up[k], -1), n, ncclFloat, c->rank - 1, c->comm, c->stream));
+            NC(nccl->Send(plane_ptr(c, hp.up[k], nzl - 1), n, ncclFloat, c->rank + 1, c->comm, c->stream));
+        if (c->rank > 0) NC(nccl->Recv(plane_ptr(c, hp.up[k], -1), n, ncclFloat, c->rank - 1, c->comm, c->stream));
     }
-    NC(ncclGroupEnd());
+    NC(nccl->GroupEnd());
     return timer_end(c, slot);
 }
 
@@ -218,9 +220,10 @@ int sync_stream(tgv_ctx* c)
 {
     CU(cudaStreamSynchronize(c->stream));
     if (c->comm) {
+        const NcclApi* nccl = c->nccl;
         ncclResult_t ar = ncclSuccess;
-        NC(ncclCommGetAsyncError(c->comm, &ar));
-        if (ar != ncclSuccess) return fail(c, TGV_ENCCL, "NCCL async error: %s", ncclGetErrorString(ar));
+        NC(nccl->CommGetAsyncError(c->comm, &ar));
+        if (ar != ncclSuccess) return fail(c, TGV_ENCCL, "NCCL async error: %s", nccl->GetErrorString(ar));
     }
     return timer_collect(c);
 }
@@ -263,8 +266,10 @@ int tgv_get_unique_id(uint8_t uid[128])
 {
     tgv_ctx* c = nullptr;
     if (!uid) return fail(c, TGV_EINVAL, "uid is NULL");
+    const NcclApi* nccl = nccl_api(g_create_error, sizeof g_create_error);
+    if (!nccl) return TGV_ENCCL;
     ncclUniqueId id;
-    NC(ncclGetUniqueId(&id));
+    NC(nccl->GetUniqueId(&id));
     static_assert(sizeof(id.internal) == 128, "NCCL unique id size");
     memcpy(uid, id.internal, 128);
     return TGV_OK;
@@ -361,12 +366,14 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     }
 
     if (nranks > 1) {
+        const NcclApi* nccl = c->nccl = nccl_api(c->err, sizeof c->err);
+        if (!nccl) return bail(TGV_ENCCL);
         ncclUniqueId id;
         memcpy(id.internal, uid, 128);
-        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+        ncclResult_t r = nccl->CommInitRank(&c->comm, nranks, id, rank);
         if (r != ncclSuccess) {
             c->comm = nullptr;
-            fail(c, TGV_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            fail(c, TGV_ENCCL, "ncclCommInitRank: %s", nccl->GetErrorString(r));
             return bail(TGV_ENCCL);
         }
         // every rank checks that the slabs tile [0, nz) in rank order
@@ -378,12 +385,12 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
         }
         int64_t mine[2] = {L->z_begin, L->z_end};
         cudaMemcpy(d_sl + 2 * rank, mine, sizeof mine, cudaMemcpyHostToDevice);
-        r = ncclAllGather(d_sl + 2 * rank, d_sl, 2, ncclInt64, c->comm, c->stream);
+        r = nccl->AllGather(d_sl + 2 * rank, d_sl, 2, ncclInt64, c->comm, c->stream);
         cudaStreamSynchronize(c->stream);
         cudaMemcpy(sl.data(), d_sl, sizeof(int64_t) * 2 * nranks, cudaMemcpyDeviceToHost);
         cudaFree(d_sl);
         if (r != ncclSuccess) {
-            fail(c, TGV_ENCCL, "slab allgather: %s", ncclGetErrorString(r));
+            fail(c, TGV_ENCCL, "slab allgather: %s", nccl->GetErrorString(r));
             return bail(TGV_ENCCL);
         }
         bool ok = sl[0] == 0 && sl[2 * (nranks - 1) + 1] == L->nz;
@@ -535,8 +542,9 @@ int tgv_energy(tgv_ctx* c, double out[6])
     CU(cudaGetLastError());
     if ((rc = timer_end(c, slot))) return rc;
     if (c->nranks > 1) {
-        NC(ncclAllReduce(c->d_out, c->d_out, 4, ncclFloat64, ncclSum, c->comm, c->stream));
-        NC(ncclAllReduce(c->d_out + 4, c->d_out + 4, 1, ncclFloat64, ncclMax, c->comm, c->stream));
+        const NcclApi* nccl = c->nccl;
+        NC(nccl->AllReduce(c->d_out, c->d_out, 4, ncclFloat64, ncclSum, c->comm, c->stream));
+        NC(nccl->AllReduce(c->d_out + 4, c->d_out + 4, 1, ncclFloat64, ncclMax, c->comm, c->stream));
     }
     double h[EN_TERMS];
     CU(cudaMemcpyAsync(h, c->d_out, sizeof h, cudaMemcpyDeviceToHost, c->stream));
@@ -600,10 +608,11 @@ void tgv_destroy(tgv_ctx* c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm) {
+        const NcclApi* nccl = c->nccl;
         if (c->poisoned)
-            ncclCommAbort(c->comm);
+            nccl->CommAbort(c->comm);
         else
-            ncclCommDestroy(c->comm);
+            nccl->CommDestroy(c->comm);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     cudaFree(c->state);
