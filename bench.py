@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--iters", type=int, default=None, help="iterations per step (default: the workload's)")
+    ap.add_argument("--schedule", default="fused", choices=["fused", "split"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -179,6 +180,7 @@ def run_ours(a):
         s = Solver.distributed(wl.shape, list(wl.centers), z0, z1, local, **kw)
     else:
         s = Solver(wl.shape, list(wl.centers), device=local, **kw)
+    s.set_schedule(a.schedule)
     s.load(counts)
     info = s.info()
     nvox_local = (z1 - z0) * ny * nx
@@ -220,13 +222,16 @@ def run_ours(a):
     ms_max = float(ms_t[0])
     value = wl.nvox * iters / (ms_max * 1e-3)
 
-    # roofline of the dominant kernel (primal: largest bytes and time per launch)
+    # roofline of the dominant kernel: the kernel with the largest device time per step
     peak, peak_src = measured_peaks()
-    k_primal = tm["primal_ms"] / max(1, tm["primal_launches"])
-    k_dual = tm["dual_ms"] / max(1, tm["dual_launches"])
-    dom, kms, bpv = ("primal", k_primal, info["bytes_primal"]) if k_primal >= k_dual else \
-        ("dual", k_dual, info["bytes_dual"])
+    kern = {}
+    for name, bkey in (("fused", "bytes_fused"), ("dual", "bytes_dual"), ("primal", "bytes_primal")):
+        if tm[f"{name}_launches"]:
+            kern[name] = (tm[f"{name}_ms"] / tm[f"{name}_launches"], info[bkey], tm[f"{name}_ms"])
+    dom = max(kern, key=lambda k: kern[k][2])
+    kms, bpv, _ = kern[dom]
     achieved = bpv * nvox_local / (kms * 1e-3) / 1e9
+    bytes_per_it = info["bytes_fused"] if a.schedule == "fused" else info["bytes_dual"] + info["bytes_primal"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -234,8 +239,9 @@ def run_ours(a):
             traffic = json.load(open(tp)).get(a.workload, {}).get(dom)
         except Exception:
             traffic = None
-    step_kernel_ms = tm["primal_ms"] + tm["dual_ms"] + tm["energy_ms"]
-    launches_per_step = (tm["dual_launches"] + tm["primal_launches"]) / a.steps + 3  # + init + 2 energy kernels
+    step_kernel_ms = tm["primal_ms"] + tm["dual_ms"] + tm["fused_ms"] + tm["energy_ms"]
+    # + init + 2 energy kernels (+ the u8 compaction only at load)
+    launches_per_step = (tm["dual_launches"] + tm["primal_launches"] + tm["fused_launches"]) / a.steps + 3
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ------------------
     e2e = None
@@ -276,11 +282,12 @@ def run_ours(a):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "bytes_per_voxel": bpv, "kernel_ms": kms,
-                         "schedule_gbs": (info["bytes_dual"] + info["bytes_primal"]) * wl.nvox * iters
-                         / (ms_max * 1e-3) / 1e9 / world,
+                         "schedule": a.schedule, "bytes_per_voxel_iteration": bytes_per_it,
+                         "count_bytes": info["count_bytes"],
+                         "schedule_gbs": bytes_per_it * wl.nvox * iters / (ms_max * 1e-3) / 1e9 / world,
                          "kernel_share_of_step": step_kernel_ms / a.steps / ms},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches_per_step * a.steps)),
-            "kernel_ms": {"dual": k_dual, "primal": k_primal,
+            "kernel_ms": {**{k: v[0] for k, v in kern.items()},
                           "energy": tm["energy_ms"] / max(1, tm["energy_launches"])},
             "wall_ms_per_step": float(ms_t[1]),
         }

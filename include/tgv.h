@@ -85,21 +85,32 @@ typedef struct {
     float lambda, alpha0, alpha1, tau, sigma;
 } tgv_params;
 
+/* Iteration schedules (same scheme, same results up to fp32 rounding order;
+ * DESIGN.md §5).  FUSED: one single-sweep kernel per iteration (dual, primal and
+ * over-relaxation fused; 136 B per voxel-iteration with u16 counts, 128 B with
+ * u8).  SPLIT: a dual kernel then a primal kernel (188 / 180 B). */
+#define TGV_SCHEDULE_FUSED 0
+#define TGV_SCHEDULE_SPLIT 1
+
 /* Kernel timing (device time from CUDA events on the launching stream). */
 typedef struct {
-    double dual_ms, primal_ms, energy_ms, halo_ms; /* summed device ms since last reset */
-    int64_t dual_launches, primal_launches, energy_launches, halo_exchanges;
+    double dual_ms, primal_ms, fused_ms, energy_ms, halo_ms; /* summed device ms since last enable */
+    int64_t dual_launches, primal_launches, fused_launches, energy_launches, halo_exchanges;
 } tgv_timing;
 
 /* Static facts about a context. */
 typedef struct {
-    int64_t row_pitch;        /* floats per stored row (>= nx, multiple of 32)          */
-    int64_t device_bytes;     /* device memory owned by the context                     */
-    int32_t count_bytes;      /* bytes per stored histogram count (2 = u16)             */
-    int32_t count_slots;      /* histogram slots stored per voxel (8 or 16)             */
-    int64_t bytes_dual;       /* algorithmic HBM bytes per voxel of one dual launch     */
-    int64_t bytes_primal;     /* algorithmic HBM bytes per voxel of one primal launch   */
+    int64_t row_pitch;        /* floats per stored row (>= nx, multiple of 32)             */
+    int64_t device_bytes;     /* device memory owned by the context                        */
+    int32_t count_bytes;      /* bytes per stored histogram count: 1 (u8) or 2 (u16)       */
+    int32_t count_slots;      /* histogram slots stored per voxel (8 or 16)                */
+    int32_t schedule;         /* TGV_SCHEDULE_*                                            */
+    int32_t fused_zc;         /* z-planes per CTA of the fused kernel                      */
+    int64_t bytes_dual;       /* algorithmic HBM bytes per voxel of one SPLIT dual launch  */
+    int64_t bytes_primal;     /* ... of one SPLIT primal launch                            */
+    int64_t bytes_fused;      /* ... of one FUSED launch (one whole iteration)             */
     int32_t nranks, rank;
+    int64_t iteration;        /* iterations since the last load / reset                    */
 } tgv_info_t;
 
 /* Rank 0 creates the NCCL unique id; the caller broadcasts the 128 bytes
@@ -107,9 +118,10 @@ typedef struct {
 int tgv_get_unique_id(uint8_t uid[128]);
 
 /* COLLECTIVE (nranks > 1).  Validates layout and parameters, selects
- * cuda_device, allocates the state (u, v, ubar, vbar, p, q in fp32 SoA planes
- * with one halo plane below and above the slab, 68 B per voxel) and the
- * histogram store, creates streams/events and, if nranks > 1, the NCCL
+ * cuda_device, allocates the state (u and v at the current and two previous
+ * iterates, p and q at two, in fp32 SoA planes with one halo plane below and
+ * above the slab: 120 B per voxel) and the histogram store (16 B per voxel,
+ * plus 8 B when u8 counts are used), creates streams/events and, if nranks > 1, the NCCL
  * communicator from uid (uid must be NULL iff nranks == 1).
  * Errors: TGV_EINVAL for any invalid argument (see tgv_params / tgv_layout;
  * also non-contiguous slabs across ranks), TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL.
@@ -120,7 +132,9 @@ int tgv_create(const tgv_layout* layout, const tgv_params* params, int rank, int
 /* Load this rank's histograms and reset the state.
  *   counts    host, uint32 [z_end - z_begin][ny][nx][nbins] (row-major, bins fastest)
  *   n_counts  number of uint32 elements; must equal (z_end-z_begin)*ny*nx*nbins
- * The counts are copied to the device in chunks and packed to u16.  Then
+ * The counts are copied to the device in chunks and packed to u16, then to u8
+ * when every count is <= 255 (the kernels read 8 instead of 16 B per voxel;
+ * environment TGV_FORCE_U16=1 keeps u16).  Then
  * (R9): u = sum_b h_b c_b / W (0 where W = 0), v = p = q = 0,
  * ubar = u, vbar = 0, iteration counter 0.
  * Errors: TGV_EINVAL (NULL, size mismatch), TGV_ERANGE (a count > 65535; the
@@ -152,7 +166,9 @@ int tgv_read_u(tgv_ctx* ctx, float* u_out, int64_t n_voxels);
 int tgv_read_field(tgv_ctx* ctx, int field, float* out, int64_t n_voxels);
 
 /* Overwrite one state field from the host (test hook; the halo planes are
- * refreshed by the next iterate / energy).  Errors as tgv_read_field. */
+ * refreshed by the next iterate / energy).  TGV_FIELD_UBAR / VBAR set the
+ * previous iterate to 2 x - in, so write U / V before UBAR / VBAR.
+ * Errors as tgv_read_field. */
 int tgv_write_field(tgv_ctx* ctx, int field, const float* in, int64_t n_voxels);
 
 /* COLLECTIVE.  Energy and restricted primal-dual gap of the current state
@@ -166,6 +182,12 @@ int tgv_write_field(tgv_ctx* ctx, int field, const float* in, int64_t n_voxels);
  *   out[5] max_x,k |v_k|  (gap_V >= 0 is guaranteed while this is <= V)
  * Errors: TGV_EINVAL (NULL), TGV_ESTATE, TGV_ECUDA, TGV_ENCCL. */
 int tgv_energy(tgv_ctx* ctx, double out[6]);
+
+/* Select the iteration schedule (TGV_SCHEDULE_FUSED, the default, or
+ * TGV_SCHEDULE_SPLIT; the environment variable TGV_SCHEDULE sets the default at
+ * create).  The state is shared, so switching keeps the current iterate.
+ * Errors: TGV_EINVAL (unknown schedule), TGV_ESTATE. */
+int tgv_set_schedule(tgv_ctx* ctx, int schedule);
 
 /* Enable (1) / disable (0) per-kernel CUDA-event timing inside tgv_iterate
  * and tgv_energy; tgv_get_timing returns the sums since the last enable. */

@@ -1,198 +1,441 @@
 // tgv_kernels.cuh -- sm_100a kernels of the TGV primal-dual hot path.
 //
-// Scheme (include/tgv.h):
-//   dual    p <- P_a1(p + s(grad ubar - vbar)),   q <- P_a0(q + s E(vbar))
-//   primal  u+ = clamp(prox(u + t div p), -1, 1), v+ = v + t(p + div2 q),
-//           ubar = 2u+ - u, vbar = 2v+ - v       (over-relaxation fused)
-// Difference operators (R6), l = coordinate, n = global extent:
+// Scheme (include/tgv.h), iteration k:
+//   ubar_k = 2 u_k - u_{k-1},  vbar_k = 2 v_k - v_{k-1}            (a3, theta = 1)
+//   p_{k+1} = P_a1(p_k + s(grad ubar_k - vbar_k)),  q_{k+1} = P_a0(q_k + s E(vbar_k))   (a1)
+//   u_{k+1} = clamp(prox(u_k + t div p_{k+1}), -1, 1),  v_{k+1} = v_k + t(p_{k+1} + div2 q_{k+1})  (a2)
+// The over-relaxed iterate is formed on the fly from (u_k, u_{k-1}); storing the
+// previous iterate instead of ubar lets the single-sweep kernel write only
+// u, v, p, q (136 B per voxel-iteration, SURVEY.md §8(d) "method minimum").
+//
+// Difference operators (R6), l = coordinate along the axis, n = global extent:
 //   D+ w[l] = w[l+1] - w[l] (l < n-1), 0 at l = n-1
 //   D- w[l] = wt[l] - wt[l-1],  wt[m] = w[m] for 0 <= m < n-1 else 0
+//   grad = D+,  E(v)_kl = (D-_l v_k + D-_k v_l)/2,  div p = sum_k D-_k p_k,
+//   (div2 q)_k = sum_l D+_l q_kl
 //
-// Storage (DESIGN.md §4 "Data layout in HBM"): each of the 17 fp32 fields is
-// an SoA array of (nzl + 2) planes (one halo plane below and above the slab)
-// of ny rows of `px` floats (px = nx rounded up to 32 -> 128-B aligned rows).
-// Histograms: 8 (or 16) u16 counts per voxel, one 16-B (or 2x16-B) vector per
-// voxel, no halo.
+// Storage: every field is an fp32 array of (nzl + 2) planes (one
+// halo plane below and above the slab) of ny rows of px floats (px = nx rounded
+// up to 32: 128-B aligned rows).  Element offsets within a field fit in int32.
+// Histograms: 8 (or 16) counts per voxel, u8 when every count <= 255 else u16,
+// one vector load per voxel, no halo planes.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace tgvk {
 
-enum : int { F_U = 0, F_V = 1, F_UBAR = 4, F_VBAR = 5, F_P = 8, F_Q = 11, NF = 17 };
-// q components: xx=0 yy=1 zz=2 xy=3 xz=4 yz=5
-
 struct Geo {
-    int nx, ny, nzl;   // owned extent (x, y, local z)
-    int nz, z0;        // global nz and global z of local plane 0
-    int64_t px;        // row pitch (floats)
-    int64_t plane;     // px * ny
-    int64_t fs;        // field stride = (nzl + 2) * plane
+    int nx, ny, nzl;  // owned extent (x, y, local z)
+    int nz, z0;       // global nz and global z of local plane 0
+    int px;           // row pitch (floats)
+    int plane;        // px * ny
+    int64_t fs;       // field stride = (nzl + 2) * plane (< 2^31)
 };
 
 struct Centers {
-    float c[16];       // padded with +inf beyond nbins
+    float c[16];  // padded with +inf beyond nbins
 };
 
 struct StepParams {
     float sigma, tau, alpha1, alpha0, tl;  // tl = tau * lambda
 };
 
+constexpr unsigned FULL = 0xffffffffu;
+
+// element offset of local voxel (x, y, z), z in [-1, nzl]
+__device__ __forceinline__ int eoff(const Geo& g, int x, int y, int z) { return (z + 1) * g.plane + y * g.px + x; }
+
 // ---------------------------------------------------------------------------
-// element access: field f, local (x, y, z), z in [-1, nzl]
-__device__ __forceinline__ int64_t vidx(const Geo& g, int x, int y, int z)
+// histograms: raw vector per voxel and exact count extraction
+template <int SLOTS, typename CT>
+struct HistRaw {
+    static constexpr int NW = SLOTS * (int)sizeof(CT) / 4;  // 32-bit words
+    uint32_t w[NW];
+};
+
+template <int SLOTS, typename CT>
+__device__ __forceinline__ HistRaw<SLOTS, CT> load_hist(const void* __restrict__ H, int64_t v)
 {
-    return (int64_t)(z + 1) * g.plane + (int64_t)y * g.px + x;
+    HistRaw<SLOTS, CT> r;
+    constexpr int NW = HistRaw<SLOTS, CT>::NW;
+    if constexpr (NW == 2) {
+        uint2 a = __ldg(reinterpret_cast<const uint2*>(H) + v);
+        r.w[0] = a.x;
+        r.w[1] = a.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < NW / 4; ++k) {
+            uint4 a = __ldg(reinterpret_cast<const uint4*>(H) + v * (NW / 4) + k);
+            r.w[4 * k] = a.x;
+            r.w[4 * k + 1] = a.y;
+            r.w[4 * k + 2] = a.z;
+            r.w[4 * k + 3] = a.w;
+        }
+    }
+    return r;
 }
 
-// exact weighted median of the histogram-L1 prox (DESIGN.md §5 "prox"):
-//   s_j = ut + t (W - 2 C_j), C_j = sum_{b<j} h_b, c_nb = +inf
-//   P = max_j min(s_j, c_j)   (s_j non-increasing, c_j increasing)
-template <int SLOTS>
-__device__ __forceinline__ float hist_prox(float ut, float t, const uint16_t* h, const Centers& C)
+// count b as an exact float: place the byte(s) in the mantissa of 2^23 and subtract 2^23
+template <int SLOTS, typename CT>
+__device__ __forceinline__ float hist_count(const HistRaw<SLOTS, CT>& h, int b)
 {
+    uint32_t bits;
+    if constexpr (sizeof(CT) == 1)
+        bits = __byte_perm(h.w[b >> 2], 0x4B000000u, (b & 3) | 0x4 << 4 | 0x4 << 8 | 0x7 << 12);
+    else
+        bits = __byte_perm(h.w[b >> 1], 0x4B000000u, (2 * (b & 1)) | (2 * (b & 1) + 1) << 4 | 0x4 << 8 | 0x7 << 12);
+    return __uint_as_float(bits) - 8388608.0f;
+}
+
+// Exact histogram-L1 prox, clamped to [-1, 1] (DESIGN.md §5 "prox"):
+//   r_j = W - 2 C_j (C_j = sum_{b<j} h_b, exact in fp32), s_j = ut + t r_j,
+//   P = max_j min(s_j, c_j) with c_nb = +inf   (s_j non-increasing, c_j increasing)
+template <int SLOTS, typename CT>
+__device__ __forceinline__ float hist_prox(float ut, float t, const HistRaw<SLOTS, CT>& h, const Centers& C)
+{
+    float cnt[SLOTS];
     float W = 0.f;
 #pragma unroll
-    for (int b = 0; b < SLOTS; ++b) W += (float)h[b];
+    for (int b = 0; b < SLOTS; ++b) {
+        cnt[b] = hist_count<SLOTS, CT>(h, b);
+        W += cnt[b];
+    }
     float r = W, P = -INFINITY;
 #pragma unroll
     for (int j = 0; j < SLOTS; ++j) {
         P = fmaxf(P, fminf(fmaf(t, r, ut), C.c[j]));
-        r -= 2.f * (float)h[j];
+        r = fmaf(-2.f, cnt[j], r);
     }
     P = fmaxf(P, fmaf(t, r, ut));
     return fminf(fmaxf(P, -1.f), 1.f);
 }
 
-template <int SLOTS>
-__device__ __forceinline__ void load_hist(const uint4* __restrict__ H, int64_t v, uint16_t h[SLOTS])
+// Euclidean projection factor onto the ball of radius a for squared norm n2:
+// min(1, a / |x|)  (n2 = 0 -> 1; a = 0 -> 0 unless n2 = 0)
+__device__ __forceinline__ float proj_scale(float n2, float a) { return fminf(1.f, a * rsqrtf(n2)); }
+
+// ---------------------------------------------------------------------------
+// Field pointers of one iteration (host fills them from the rotating buffers)
+struct IterPtrs {
+    const float* uk;     // u_k
+    const float* um;     // u_{k-1}
+    const float* vk[3];  // v_k
+    const float* vm[3];  // v_{k-1}
+    const float* pk[3];  // p_k
+    const float* qk[6];  // q_k  (xx, yy, zz, xy, xz, yz)
+    float* un;           // u_{k+1}
+    float* vn[3];        // v_{k+1}
+    float* pn[3];        // p_{k+1}
+    float* qn[6];        // q_{k+1}
+    const void* hist;
+};
+
+// ===========================================================================
+// SPLIT schedule: (1) dual kernel, (2) primal kernel with fused over-relaxation
+// bookkeeping.  One voxel per thread, neighbours through L1/L2, all loads issued
+// before any store.  88+16 B and 68+hist B per voxel.
+// ===========================================================================
+__global__ void __launch_bounds__(256) split_dual_kernel(const IterPtrs a, const Geo g, const StepParams sp)
 {
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zg = g.z0 + z;
+    const int i = eoff(g, x, y, z);
+    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
+    const bool xf = x > 0, yf = y > 0, zf = zg > 0;
+    const int sy = g.px, sz = g.plane;
+    auto ubar = [&](int o) { return 2.f * __ldg(a.uk + o) - __ldg(a.um + o); };
+    auto vbar = [&](int k, int o) { return 2.f * __ldg(a.vk[k] + o) - __ldg(a.vm[k] + o); };
+    // ---- loads
+    const float u0 = ubar(i);
+    const float ux = xl ? ubar(i + 1) : 0.f, uy = yl ? ubar(i + sy) : 0.f, uz = zl ? ubar(i + sz) : 0.f;
+    float vb[3], vbx[3], vby[3], vbz[3];
 #pragma unroll
-    for (int k = 0; k < SLOTS / 8; ++k) {
-        uint4 w = __ldg(H + v * (SLOTS / 8) + k);
-        uint32_t a[4] = {w.x, w.y, w.z, w.w};
+    for (int k = 0; k < 3; ++k) {
+        vb[k] = vbar(k, i);
+        vbx[k] = xf ? vbar(k, i - 1) : 0.f;
+        vby[k] = yf ? vbar(k, i - sy) : 0.f;
+        vbz[k] = zf ? vbar(k, i - sz) : 0.f;
+    }
+    float p[3], q[6];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            h[8 * k + 2 * m] = (uint16_t)(a[m] & 0xffffu);
-            h[8 * k + 2 * m + 1] = (uint16_t)(a[m] >> 16);
+    for (int k = 0; k < 3; ++k) p[k] = __ldg(a.pk[k] + i);
+#pragma unroll
+    for (int m = 0; m < 6; ++m) q[m] = __ldg(a.qk[m] + i);
+    // ---- p
+    const float g0 = xl ? ux - u0 : 0.f, g1 = yl ? uy - u0 : 0.f, g2 = zl ? uz - u0 : 0.f;
+    p[0] = fmaf(sp.sigma, g0 - vb[0], p[0]);
+    p[1] = fmaf(sp.sigma, g1 - vb[1], p[1]);
+    p[2] = fmaf(sp.sigma, g2 - vb[2], p[2]);
+    const float sp_ = proj_scale(p[0] * p[0] + p[1] * p[1] + p[2] * p[2], sp.alpha1);
+    // ---- q: D-_x vb_k = (xl ? vb_k : 0) - vbx_k, etc.
+    float dx[3], dy[3], dz[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        dx[k] = (xl ? vb[k] : 0.f) - vbx[k];
+        dy[k] = (yl ? vb[k] : 0.f) - vby[k];
+        dz[k] = (zl ? vb[k] : 0.f) - vbz[k];
+    }
+    const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]), 0.5f * (dz[1] + dy[2])};
+#pragma unroll
+    for (int m = 0; m < 6; ++m) q[m] = fmaf(sp.sigma, e[m], q[m]);
+    const float sq = proj_scale(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + 2.f * (q[3] * q[3] + q[4] * q[4] + q[5] * q[5]),
+                                sp.alpha0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.pn[k][i] = p[k] * sp_;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) a.qn[m][i] = q[m] * sq;
+}
+
+// reads p_{k+1}, q_{k+1} (in a.pk / a.qk), u_k, v_k; writes u_{k+1}, v_{k+1}
+template <int SLOTS, typename CT>
+__global__ void __launch_bounds__(256) split_primal_kernel(const IterPtrs a, const Geo g, const StepParams sp,
+                                                           const Centers C)
+{
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zg = g.z0 + z;
+    const int i = eoff(g, x, y, z);
+    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
+    const bool xf = x > 0, yf = y > 0, zf = zg > 0;
+    const int sy = g.px, sz = g.plane;
+    // ---- loads
+    float p[3], q[6], qx[3], qy[3], qz[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p[k] = __ldg(a.pk[k] + i);
+    const float pxm = xf ? __ldg(a.pk[0] + i - 1) : 0.f;
+    const float pym = yf ? __ldg(a.pk[1] + i - sy) : 0.f;
+    const float pzm = zf ? __ldg(a.pk[2] + i - sz) : 0.f;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) q[m] = __ldg(a.qk[m] + i);
+    // q_kl at +e_l:  x: xx, xy, xz   y: xy, yy, yz   z: xz, yz, zz
+    const int QX[3] = {0, 3, 4}, QY[3] = {3, 1, 5}, QZ[3] = {4, 5, 2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        qx[k] = xl ? __ldg(a.qk[QX[k]] + i + 1) : 0.f;
+        qy[k] = yl ? __ldg(a.qk[QY[k]] + i + sy) : 0.f;
+        qz[k] = zl ? __ldg(a.qk[QZ[k]] + i + sz) : 0.f;
+    }
+    const float uo = __ldg(a.uk + i);
+    float vo[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vo[k] = __ldg(a.vk[k] + i);
+    const auto h = load_hist<SLOTS, CT>(a.hist, (int64_t)z * g.plane + y * g.px + x);
+    // ---- u
+    const float divp = ((xl ? p[0] : 0.f) - pxm) + ((yl ? p[1] : 0.f) - pym) + ((zl ? p[2] : 0.f) - pzm);
+    const float un = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uo), sp.tl, h, C);
+    // ---- v: (div2 q)_k = sum_l D+_l q_kl
+    float w[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        w[k] = (xl ? qx[k] - q[QX[k]] : 0.f) + (yl ? qy[k] - q[QY[k]] : 0.f) + (zl ? qz[k] - q[QZ[k]] : 0.f);
+    a.un[i] = un;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.vn[k][i] = fmaf(sp.tau, p[k] + w[k], vo[k]);
+}
+
+// ===========================================================================
+// FUSED schedule: one single-sweep kernel per iteration (136 B per voxel-iteration
+// with u16 counts, 128 B with u8).
+//
+// CTA = 32 lanes x (TY + 2) rows of threads, one (x, y) column per thread,
+// marching up a z-chunk [zs, ze).  A warp covers 32 consecutive x of which
+// lanes 1..30 are owned and lanes 0 / 31 are the x-halo; rows 1..TY are owned,
+// row 0 (y0-1) and row TY+1 (y0+TY) are the y-halo.  Halos are recomputed
+// redundantly so that no CTA ever needs another CTA's results of the same
+// launch; the inputs are (u_k, u_{k-1}, v_k, v_{k-1}, p_k, q_k) and every output
+// goes to a different buffer (U/V rotate over 3, P/Q over 2), so there is no
+// intra-launch hazard.  Step s computes the dual D(s) (p, q at plane s) and the
+// primal Pm(s-1); x-neighbours come from warp shuffles, y-neighbours from two
+// parity-double-buffered shared planes (one __syncthreads per step), z-neighbours
+// from registers.  Inputs are prefetched one plane ahead.
+// ===========================================================================
+struct FusedArgs {
+    IterPtrs a;
+    Geo g;
+    StepParams sp;
+    Centers C;
+    int z_lo, z_hi, zc;  // local planes [z_lo, z_hi) in chunks of zc, one chunk per blockIdx.z
+};
+
+struct UV {
+    float uk, um, vk[3], vm[3];
+};
+struct PQ {
+    float p[3], q[6];
+};
+
+template <int TY, int SLOTS, typename CT>
+__global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs A)
+{
+    __shared__ float sm_uv[2][4][TY + 2][32];  // ubar, vbar_x, vbar_y, vbar_z of plane s
+    __shared__ float sm_r[2][4][TY + 2][32];   // p_y, q_xy, q_yy, q_yz of D(s)
+    const IterPtrs& a = A.a;
+    const Geo& g = A.g;
+    const StepParams& sp = A.sp;
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int x = blockIdx.x * 30 - 1 + lane, y = blockIdx.y * TY - 1 + ty;
+    const bool vxy = x >= 0 && x < g.nx && y >= 0 && y < g.ny;
+    const bool own = vxy && lane >= 1 && lane <= 30 && ty >= 1 && ty <= TY;
+    const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
+    const bool prow = ty <= TY;       // rows needing p_{k+1} (all but the top halo row)
+    const bool qrow = ty >= 1;        // rows needing q_{k+1} (all but the bottom halo row)
+    const bool mrow = qrow && prow;   // owned rows: primal
+    const int zs = A.z_lo + blockIdx.z * A.zc;
+    const int ze = min(zs + A.zc, A.z_hi);
+    const int rowoff = y * g.px + x;
+
+    auto load_uv = [&](int s) {
+        UV r;
+        const bool ok = vxy && s >= -1 && s <= g.nzl;
+        const int o = (s + 1) * g.plane + rowoff;
+        r.uk = ok ? __ldg(a.uk + o) : 0.f;
+        r.um = ok ? __ldg(a.um + o) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            r.vk[k] = ok ? __ldg(a.vk[k] + o) : 0.f;
+            r.vm[k] = ok ? __ldg(a.vm[k] + o) : 0.f;
         }
+        return r;
+    };
+    auto load_pq = [&](int s) {
+        PQ r;
+        const bool ok = vxy && s >= -1 && s <= g.nzl;
+        const int o = (s + 1) * g.plane + rowoff;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) r.p[k] = (ok && prow) ? __ldg(a.pk[k] + o) : 0.f;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) r.q[m] = (ok && qrow) ? __ldg(a.qk[m] + o) : 0.f;
+        return r;
+    };
+    auto load_h = [&](int s) {
+        HistRaw<SLOTS, CT> h{};
+        if (own && s >= 0 && s < g.nzl) h = load_hist<SLOTS, CT>(a.hist, (int64_t)s * g.plane + rowoff);
+        return h;
+    };
+
+    UV u0 = load_uv(zs - 1), u1 = load_uv(zs);
+    PQ pq0 = load_pq(zs - 1);
+    float vbp[3] = {0.f, 0.f, 0.f};  // vbar(s-1)
+    float uk_p = 0.f, vk_p[3] = {0.f, 0.f, 0.f};
+    HistRaw<SLOTS, CT> h0{};
+    float pn_p[3] = {0.f, 0.f, 0.f}, pz_pp = 0.f, qn_p[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+
+    for (int s = zs - 1; s <= ze; ++s) {
+        // prefetch (consumed next step)
+        const UV u2 = load_uv(s + 2);
+        const PQ pq1 = load_pq(s + 1);
+        const HistRaw<SLOTS, CT> h1 = load_h(s);
+        const int par = s & 1;
+        const int zg = g.z0 + s;
+        const bool zl = zg < g.nz - 1, zf = zg > 0;
+
+        // (a3) over-relaxed iterate at planes s and s+1
+        const float ub = 2.f * u0.uk - u0.um;
+        float vb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) vb[k] = 2.f * u0.vk[k] - u0.vm[k];
+        const float ub1 = 2.f * u1.uk - u1.um;
+        sm_uv[par][0][ty][lane] = ub;
+        sm_uv[par][1][ty][lane] = vb[0];
+        sm_uv[par][2][ty][lane] = vb[1];
+        sm_uv[par][3][ty][lane] = vb[2];
+        __syncthreads();
+
+        // (a1) dual D(s)
+        float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (prow) {
+            const float ux = __shfl_down_sync(FULL, ub, 1);
+            const float uy = sm_uv[par][0][ty + 1][lane];
+            const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
+            pn[0] = fmaf(sp.sigma, g0 - vb[0], pq0.p[0]);
+            pn[1] = fmaf(sp.sigma, g1 - vb[1], pq0.p[1]);
+            pn[2] = fmaf(sp.sigma, g2 - vb[2], pq0.p[2]);
+            const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
+            pn[0] *= f;
+            pn[1] *= f;
+            pn[2] *= f;
+        }
+        if (qrow) {
+            float dx[3], dy[3], dz[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float vx = __shfl_up_sync(FULL, vb[k], 1);
+                const float vy = sm_uv[par][1 + k][ty - 1][lane];
+                dx[k] = (xl ? vb[k] : 0.f) - (xf ? vx : 0.f);
+                dy[k] = (yl ? vb[k] : 0.f) - (yf ? vy : 0.f);
+                dz[k] = (zl ? vb[k] : 0.f) - (zf ? vbp[k] : 0.f);
+            }
+            const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
+                                0.5f * (dz[1] + dy[2])};
+#pragma unroll
+            for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], pq0.q[m]);
+            const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
+                                           2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
+                                       sp.alpha0);
+#pragma unroll
+            for (int m = 0; m < 6; ++m) qn[m] *= f;
+        }
+        sm_r[par][0][ty][lane] = pn[1];
+        sm_r[par][1][ty][lane] = qn[3];
+        sm_r[par][2][ty][lane] = qn[1];
+        sm_r[par][3][ty][lane] = qn[5];
+        if (own && s >= zs && s < ze) {
+            const int o = (s + 1) * g.plane + rowoff;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) a.pn[k][o] = pn[k];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) a.qn[m][o] = qn[m];
+        }
+
+        // (a2) primal Pm(s-1) on owned rows
+        if (mrow && s - 1 >= zs) {
+            const int pr = par ^ 1;
+            const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
+            const float pxm = __shfl_up_sync(FULL, pn_p[0], 1);
+            const float pym = sm_r[pr][0][ty - 1][lane];
+            const float divp = ((xl ? pn_p[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? pn_p[1] : 0.f) - (yf ? pym : 0.f)) +
+                               ((zl1 ? pn_p[2] : 0.f) - (zf1 ? pz_pp : 0.f));
+            const float qxx = __shfl_down_sync(FULL, qn_p[0], 1);
+            const float qxy = __shfl_down_sync(FULL, qn_p[3], 1);
+            const float qxz = __shfl_down_sync(FULL, qn_p[4], 1);
+            const float qyxy = sm_r[pr][1][ty + 1][lane];
+            const float qyyy = sm_r[pr][2][ty + 1][lane];
+            const float qyyz = sm_r[pr][3][ty + 1][lane];
+            // (div2 q)_k = D+_x q_kx + D+_y q_ky + D+_z q_kz at plane s-1; q(s) = qn
+            const float w0 = (xl ? qxx - qn_p[0] : 0.f) + (yl ? qyxy - qn_p[3] : 0.f) + (zl1 ? qn[4] - qn_p[4] : 0.f);
+            const float w1 = (xl ? qxy - qn_p[3] : 0.f) + (yl ? qyyy - qn_p[1] : 0.f) + (zl1 ? qn[5] - qn_p[5] : 0.f);
+            const float w2 = (xl ? qxz - qn_p[4] : 0.f) + (yl ? qyyz - qn_p[5] : 0.f) + (zl1 ? qn[2] - qn_p[2] : 0.f);
+            if (own) {
+                const float un = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uk_p), sp.tl, h0, A.C);
+                const int o = s * g.plane + rowoff;  // plane s-1
+                a.un[o] = un;
+                a.vn[0][o] = fmaf(sp.tau, pn_p[0] + w0, vk_p[0]);
+                a.vn[1][o] = fmaf(sp.tau, pn_p[1] + w1, vk_p[1]);
+                a.vn[2][o] = fmaf(sp.tau, pn_p[2] + w2, vk_p[2]);
+            }
+        }
+
+        // rotate
+        pz_pp = pn_p[2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            pn_p[k] = pn[k];
+            vbp[k] = vb[k];
+            vk_p[k] = u0.vk[k];
+        }
+#pragma unroll
+        for (int m = 0; m < 6; ++m) qn_p[m] = qn[m];
+        uk_p = u0.uk;
+        h0 = h1;
+        u0 = u1;
+        u1 = u2;
+        pq0 = pq1;
     }
 }
 
-// ---------------------------------------------------------------------------
-// (a1) dual kernel, v1: one voxel per thread, neighbours through L1/L2.
-__global__ void __launch_bounds__(256) dual_kernel(float* __restrict__ S, Geo g, StepParams sp)
-{
-    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
-    if (x >= g.nx || y >= g.ny) return;
-    const int zg = g.z0 + z;
-    const int64_t i = vidx(g, x, y, z);
-    const float* __restrict__ ub = S + F_UBAR * g.fs;
-    const float* __restrict__ vb0 = S + (F_VBAR + 0) * g.fs;
-    const float* __restrict__ vb1 = S + (F_VBAR + 1) * g.fs;
-    const float* __restrict__ vb2 = S + (F_VBAR + 2) * g.fs;
-    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
-    const bool xf = x > 0, yf = y > 0, zf = zg > 0;
-    const int64_t sx = 1, sy = g.px, sz = g.plane;
-
-    const float u0 = ub[i];
-    const float gx = xl ? ub[i + sx] - u0 : 0.f;
-    const float gy = yl ? ub[i + sy] - u0 : 0.f;
-    const float gz = zl ? ub[i + sz] - u0 : 0.f;
-    const float vx = vb0[i], vy = vb1[i], vz = vb2[i];
-
-    float* __restrict__ P0 = S + (F_P + 0) * g.fs;
-    float* __restrict__ P1 = S + (F_P + 1) * g.fs;
-    float* __restrict__ P2 = S + (F_P + 2) * g.fs;
-    float p0 = fmaf(sp.sigma, gx - vx, P0[i]);
-    float p1 = fmaf(sp.sigma, gy - vy, P1[i]);
-    float p2 = fmaf(sp.sigma, gz - vz, P2[i]);
-    const float sp_ = fminf(1.f, sp.alpha1 * rsqrtf(p0 * p0 + p1 * p1 + p2 * p2));
-    P0[i] = p0 * sp_;
-    P1[i] = p1 * sp_;
-    P2[i] = p2 * sp_;
-
-    // D- of each vbar component along each axis
-    const float wx = xl ? 1.f : 0.f, wy = yl ? 1.f : 0.f, wz = zl ? 1.f : 0.f;
-    auto dmx = [&](const float* w, float self) { return wx * self - (xf ? w[i - sx] : 0.f); };
-    auto dmy = [&](const float* w, float self) { return wy * self - (yf ? w[i - sy] : 0.f); };
-    auto dmz = [&](const float* w, float self) { return wz * self - (zf ? w[i - sz] : 0.f); };
-    const float exx = dmx(vb0, vx), eyy = dmy(vb1, vy), ezz = dmz(vb2, vz);
-    const float exy = 0.5f * (dmy(vb0, vx) + dmx(vb1, vy));
-    const float exz = 0.5f * (dmz(vb0, vx) + dmx(vb2, vz));
-    const float eyz = 0.5f * (dmz(vb1, vy) + dmy(vb2, vz));
-
-    float* __restrict__ Q = S + F_Q * g.fs;
-    float q[6];
-    const float e[6] = {exx, eyy, ezz, exy, exz, eyz};
-#pragma unroll
-    for (int m = 0; m < 6; ++m) q[m] = fmaf(sp.sigma, e[m], Q[m * g.fs + i]);
-    const float nq2 = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + 2.f * (q[3] * q[3] + q[4] * q[4] + q[5] * q[5]);
-    const float sq = fminf(1.f, sp.alpha0 * rsqrtf(nq2));
-#pragma unroll
-    for (int m = 0; m < 6; ++m) Q[m * g.fs + i] = q[m] * sq;
-}
-
-// (a2)+(a3) primal kernel, v1: one voxel per thread.
-template <int SLOTS>
-__global__ void __launch_bounds__(256)
-    primal_kernel(float* __restrict__ S, const uint4* __restrict__ H, Geo g, StepParams sp, Centers C)
-{
-    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
-    if (x >= g.nx || y >= g.ny) return;
-    const int zg = g.z0 + z;
-    const int64_t i = vidx(g, x, y, z);
-    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
-    const bool xf = x > 0, yf = y > 0, zf = zg > 0;
-    const int64_t sx = 1, sy = g.px, sz = g.plane;
-    const float* __restrict__ P0 = S + (F_P + 0) * g.fs;
-    const float* __restrict__ P1 = S + (F_P + 1) * g.fs;
-    const float* __restrict__ P2 = S + (F_P + 2) * g.fs;
-    const float* __restrict__ Q = S + F_Q * g.fs;
-
-    const float p0 = P0[i], p1 = P1[i], p2 = P2[i];
-    // div p = sum_k D-_k p_k
-    const float divp = ((xl ? p0 : 0.f) - (xf ? P0[i - sx] : 0.f)) + ((yl ? p1 : 0.f) - (yf ? P1[i - sy] : 0.f)) +
-                       ((zl ? p2 : 0.f) - (zf ? P2[i - sz] : 0.f));
-    float* __restrict__ U = S + F_U * g.fs;
-    float* __restrict__ UB = S + F_UBAR * g.fs;
-    const float uo = U[i];
-    uint16_t h[SLOTS];
-    load_hist<SLOTS>(H, (int64_t)z * g.plane + (int64_t)y * g.px + x, h);
-    const float un = hist_prox<SLOTS>(fmaf(sp.tau, divp, uo), sp.tl, h, C);
-    U[i] = un;
-    UB[i] = 2.f * un - uo;
-
-    // (div2 q)_k = sum_l D+_l q_kl
-    const float* qxx = Q + 0 * g.fs;
-    const float* qyy = Q + 1 * g.fs;
-    const float* qzz = Q + 2 * g.fs;
-    const float* qxy = Q + 3 * g.fs;
-    const float* qxz = Q + 4 * g.fs;
-    const float* qyz = Q + 5 * g.fs;
-    const float cxx = qxx[i], cyy = qyy[i], czz = qzz[i], cxy = qxy[i], cxz = qxz[i], cyz = qyz[i];
-    const float w0 = (xl ? qxx[i + sx] - cxx : 0.f) + (yl ? qxy[i + sy] - cxy : 0.f) + (zl ? qxz[i + sz] - cxz : 0.f);
-    const float w1 = (xl ? qxy[i + sx] - cxy : 0.f) + (yl ? qyy[i + sy] - cyy : 0.f) + (zl ? qyz[i + sz] - cyz : 0.f);
-    const float w2 = (xl ? qxz[i + sx] - cxz : 0.f) + (yl ? qyz[i + sy] - cyz : 0.f) + (zl ? qzz[i + sz] - czz : 0.f);
-    float* __restrict__ V0 = S + (F_V + 0) * g.fs;
-    float* __restrict__ V1 = S + (F_V + 1) * g.fs;
-    float* __restrict__ V2 = S + (F_V + 2) * g.fs;
-    float* __restrict__ VB0 = S + (F_VBAR + 0) * g.fs;
-    float* __restrict__ VB1 = S + (F_VBAR + 1) * g.fs;
-    float* __restrict__ VB2 = S + (F_VBAR + 2) * g.fs;
-    const float vo0 = V0[i], vo1 = V1[i], vo2 = V2[i];
-    const float vn0 = fmaf(sp.tau, p0 + w0, vo0);
-    const float vn1 = fmaf(sp.tau, p1 + w1, vo1);
-    const float vn2 = fmaf(sp.tau, p2 + w2, vo2);
-    V0[i] = vn0;
-    V1[i] = vn1;
-    V2[i] = vn2;
-    VB0[i] = 2.f * vn0 - vo0;
-    VB1[i] = 2.f * vn1 - vo1;
-    VB2[i] = 2.f * vn2 - vo2;
-}
-
-// ---------------------------------------------------------------------------
+// ===========================================================================
 // load / reset
 // counts chunk: dense uint32 [nzc][ny][nx][nbins] for local planes [zc0, zc0 + nzc)
 template <int SLOTS>
@@ -213,13 +456,22 @@ __global__ void pack_counts_kernel(const uint32_t* __restrict__ src, int nzc, in
             dst[b] = (uint16_t)min(c, 65535u);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(maxc, m);
 }
 
-// u = sum h c / W (fp64, 0 where W = 0), ubar = u; all other fields are zeroed by the caller.
-template <int SLOTS>
-__global__ void init_state_kernel(float* __restrict__ S, const uint4* __restrict__ H, Geo g, Centers C)
+// u16 -> u8 copy of the whole store (only when every count <= 255)
+__global__ void compact_counts_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t n)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = (uint8_t)src[i];
+}
+
+// u_0 = sum h c / W (fp64, 0 where W = 0) into the current and previous u buffers
+// (ubar_0 = 2 u_0 - u_0 = u_0); every other field is zeroed by the caller.
+template <int SLOTS, typename CT>
+__global__ void init_state_kernel(float* __restrict__ u_cur, float* __restrict__ u_prev, const void* __restrict__ H,
+                                  Geo g, Centers C)
 {
     const int64_t n = (int64_t)g.nzl * g.ny * g.nx;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -227,25 +479,30 @@ __global__ void init_state_kernel(float* __restrict__ S, const uint4* __restrict
         const int64_t r = v / g.nx;
         const int y = (int)(r % g.ny);
         const int z = (int)(r / g.ny);
-        uint16_t h[SLOTS];
-        load_hist<SLOTS>(H, (int64_t)z * g.plane + (int64_t)y * g.px + x, h);
+        const auto h = load_hist<SLOTS, CT>(H, (int64_t)z * g.plane + (int64_t)y * g.px + x);
         double W = 0.0, m = 0.0;
         for (int b = 0; b < SLOTS; ++b) {
-            if (h[b]) {
-                W += (double)h[b];
-                m += (double)h[b] * (double)C.c[b];
+            const double hb = (double)hist_count<SLOTS, CT>(h, b);
+            if (hb != 0.0) {
+                W += hb;
+                m += hb * (double)C.c[b];
             }
         }
         const float u0 = W > 0.0 ? (float)(m / W) : 0.f;
-        const int64_t i = vidx(g, x, y, z);
-        S[F_U * g.fs + i] = u0;
-        S[F_UBAR * g.fs + i] = u0;
+        const int i = eoff(g, x, y, z);
+        u_cur[i] = u0;
+        u_prev[i] = u0;
     }
 }
 
-// ---------------------------------------------------------------------------
+// ===========================================================================
 // (a4) energy and restricted gap, fp64 per-voxel terms, deterministic reduction.
-struct EnergyParams {
+struct EnergyArgs {
+    const float* u;
+    const float* v[3];
+    const float* p[3];
+    const float* q[6];
+    const void* hist;
     double alpha1, alpha0, lambda, V;
     int nbins;
 };
@@ -254,63 +511,62 @@ constexpr int EN_TERMS = 5;  // alpha1, alpha0, data, dual, vmax
 
 __device__ __forceinline__ double warp_sum(double v)
 {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     return v;
 }
 __device__ __forceinline__ double warp_max(double v)
 {
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
     return v;
 }
 
-template <int SLOTS>
+template <int SLOTS, typename CT>
 __global__ void __launch_bounds__(256)
-    energy_partial_kernel(const float* __restrict__ S, const uint4* __restrict__ H, Geo g, EnergyParams ep,
-                          Centers C, double* __restrict__ partials)
+    energy_partial_kernel(const EnergyArgs ea, Geo g, Centers C, double* __restrict__ partials)
 {
     const int64_t n = (int64_t)g.nzl * g.ny * g.nx;
     double t1 = 0, t0 = 0, td = 0, dv = 0, vm = 0;
-    const int64_t sx = 1, sy = g.px, sz = g.plane;
+    const int sy = g.px, sz = g.plane;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int x = (int)(v % g.nx);
         const int64_t r = v / g.nx;
         const int y = (int)(r % g.ny);
         const int z = (int)(r / g.ny);
         const int zg = g.z0 + z;
-        const int64_t i = vidx(g, x, y, z);
+        const int i = eoff(g, x, y, z);
         const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
         const bool xf = x > 0, yf = y > 0, zf = zg > 0;
-        auto F = [&](int f, int64_t off) { return (double)S[f * g.fs + i + off]; };
-        auto dp = [&](int f, bool l, int64_t s) { return l ? F(f, s) - F(f, 0) : 0.0; };
-        auto dm = [&](int f, bool l, bool fst, int64_t s) { return (l ? F(f, 0) : 0.0) - (fst ? F(f, -s) : 0.0); };
-        const double u = F(F_U, 0);
-        const double v0 = F(F_V, 0), v1 = F(F_V + 1, 0), v2 = F(F_V + 2, 0);
-        const double a0 = dp(F_U, xl, sx) - v0, a1 = dp(F_U, yl, sy) - v1, a2 = dp(F_U, zl, sz) - v2;
-        t1 += ep.alpha1 * sqrt(a0 * a0 + a1 * a1 + a2 * a2);
-        const double exx = dm(F_V, xl, xf, sx), eyy = dm(F_V + 1, yl, yf, sy), ezz = dm(F_V + 2, zl, zf, sz);
-        const double exy = 0.5 * (dm(F_V, yl, yf, sy) + dm(F_V + 1, xl, xf, sx));
-        const double exz = 0.5 * (dm(F_V, zl, zf, sz) + dm(F_V + 2, xl, xf, sx));
-        const double eyz = 0.5 * (dm(F_V + 1, zl, zf, sz) + dm(F_V + 2, yl, yf, sy));
-        t0 += ep.alpha0 * sqrt(exx * exx + eyy * eyy + ezz * ezz + 2.0 * (exy * exy + exz * exz + eyz * eyz));
-        uint16_t h[SLOTS];
-        load_hist<SLOTS>(H, (int64_t)z * g.plane + (int64_t)y * g.px + x, h);
+        auto F = [&](const float* f, int off) { return (double)f[i + off]; };
+        auto dp = [&](const float* f, bool l, int s) { return l ? F(f, s) - F(f, 0) : 0.0; };
+        auto dm = [&](const float* f, bool l, bool fst, int s) { return (l ? F(f, 0) : 0.0) - (fst ? F(f, -s) : 0.0); };
+        const double u = F(ea.u, 0);
+        const double v0 = F(ea.v[0], 0), v1 = F(ea.v[1], 0), v2 = F(ea.v[2], 0);
+        const double a0 = dp(ea.u, xl, 1) - v0, a1 = dp(ea.u, yl, sy) - v1, a2 = dp(ea.u, zl, sz) - v2;
+        t1 += ea.alpha1 * sqrt(a0 * a0 + a1 * a1 + a2 * a2);
+        const double exx = dm(ea.v[0], xl, xf, 1), eyy = dm(ea.v[1], yl, yf, sy), ezz = dm(ea.v[2], zl, zf, sz);
+        const double exy = 0.5 * (dm(ea.v[0], yl, yf, sy) + dm(ea.v[1], xl, xf, 1));
+        const double exz = 0.5 * (dm(ea.v[0], zl, zf, sz) + dm(ea.v[2], xl, xf, 1));
+        const double eyz = 0.5 * (dm(ea.v[1], zl, zf, sz) + dm(ea.v[2], yl, yf, sy));
+        t0 += ea.alpha0 * sqrt(exx * exx + eyy * eyy + ezz * ezz + 2.0 * (exy * exy + exz * exz + eyz * eyz));
+        const auto h = load_hist<SLOTS, CT>(ea.hist, (int64_t)z * g.plane + (int64_t)y * g.px + x);
+        double hb[SLOTS];
+        for (int b = 0; b < SLOTS; ++b) hb[b] = (double)hist_count<SLOTS, CT>(h, b);
         double dterm = 0.0;
-        for (int b = 0; b < ep.nbins; ++b) dterm += (double)h[b] * fabs(u - (double)C.c[b]);
-        td += ep.lambda * dterm;
-        const double divp = dm(F_P, xl, xf, sx) + dm(F_P + 1, yl, yf, sy) + dm(F_P + 2, zl, zf, sz);
+        for (int b = 0; b < ea.nbins; ++b) dterm += hb[b] * fabs(u - (double)C.c[b]);
+        td += ea.lambda * dterm;
+        const double divp = dm(ea.p[0], xl, xf, 1) + dm(ea.p[1], yl, yf, sy) + dm(ea.p[2], zl, zf, sz);
         double best = INFINITY;
-        for (int j = -1; j <= ep.nbins; ++j) {
-            const double uu = j < 0 ? -1.0 : (j == ep.nbins ? 1.0 : (double)C.c[j]);
+        for (int j = -1; j <= ea.nbins; ++j) {
+            const double uu = j < 0 ? -1.0 : (j == ea.nbins ? 1.0 : (double)C.c[j]);
             double s = 0.0;
-            for (int b = 0; b < ep.nbins; ++b) s += (double)h[b] * fabs(uu - (double)C.c[b]);
-            best = fmin(best, ep.lambda * s - uu * divp);
+            for (int b = 0; b < ea.nbins; ++b) s += hb[b] * fabs(uu - (double)C.c[b]);
+            best = fmin(best, ea.lambda * s - uu * divp);
         }
-        const int qb = F_Q;  // xx yy zz xy xz yz
-        const double w0 = dp(qb + 0, xl, sx) + dp(qb + 3, yl, sy) + dp(qb + 4, zl, sz);
-        const double w1 = dp(qb + 3, xl, sx) + dp(qb + 1, yl, sy) + dp(qb + 5, zl, sz);
-        const double w2 = dp(qb + 4, xl, sx) + dp(qb + 5, yl, sy) + dp(qb + 2, zl, sz);
-        const double l1 = fabs(F(F_P, 0) + w0) + fabs(F(F_P + 1, 0) + w1) + fabs(F(F_P + 2, 0) + w2);
-        dv += best - ep.V * l1;
+        const double w0 = dp(ea.q[0], xl, 1) + dp(ea.q[3], yl, sy) + dp(ea.q[4], zl, sz);
+        const double w1 = dp(ea.q[3], xl, 1) + dp(ea.q[1], yl, sy) + dp(ea.q[5], zl, sz);
+        const double w2 = dp(ea.q[4], xl, 1) + dp(ea.q[5], yl, sy) + dp(ea.q[2], zl, sz);
+        const double l1 = fabs(F(ea.p[0], 0) + w0) + fabs(F(ea.p[1], 0) + w1) + fabs(F(ea.p[2], 0) + w2);
+        dv += best - ea.V * l1;
         vm = fmax(vm, fmax(fabs(v0), fmax(fabs(v1), fabs(v2))));
     }
     __shared__ double red[EN_TERMS][8];

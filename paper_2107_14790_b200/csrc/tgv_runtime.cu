@@ -1,16 +1,22 @@
 // tgv_runtime.cu -- context, C ABI (include/tgv.h) and NCCL z-slab halo
 // exchange of the B200 TGV solver.
 //
-// One context per (process, GPU).  The context owns the fp32 SoA state
-// (17 fields, each with one halo plane below and above the slab), the u16
+// One context per (process, GPU).  The context owns the fp32 state, the
 // histogram store, a compute stream, CUDA events for kernel timing and, for
-// nranks > 1, an NCCL communicator over NVLink/NVSwitch.
+// nranks > 1, an NCCL communicator over NVLink/NVSwitch (NCCL is dlopen'ed).
+//
+// State representation: iteration k keeps (u_k, u_{k-1}),
+// (v_k, v_{k-1}), p_k, q_k.  u and v rotate over 3 buffers, p and q over 2, so a
+// single-sweep kernel never overwrites anything another CTA of the same launch
+// still reads.  30 field slots of (nzl + 2) planes each (one halo plane below
+// and above the slab).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -25,21 +31,15 @@ namespace {
 
 thread_local char g_create_error[512] = "";
 
-// Halo plan (pinned on CPU by tests/test_slab_gloo.py).
-// "down": this rank's BOTTOM owned plane goes to rank-1 (its top halo).
-// "up":   this rank's TOP owned plane goes to rank+1 (its bottom halo).
-struct HaloPlan {
-    int ndown, nup;
-    int down[4], up[4];
-};
-// before the dual step: grad ubar needs ubar(z+1); E(vbar) needs vbar_k(z-1)
-constexpr HaloPlan HALO_A = {1, 3, {F_UBAR}, {F_VBAR + 0, F_VBAR + 1, F_VBAR + 2}};
-// before the primal step: div p needs p_z(z-1); div2 q needs q_xz, q_yz, q_zz(z+1)
-constexpr HaloPlan HALO_B = {3, 1, {F_Q + 4, F_Q + 5, F_Q + 2}, {F_P + 2}};
-// energy: grad u (u(z+1)), E(v) (v(z-1)), div p, div2 q
-constexpr HaloPlan HALO_E = {4, 4, {F_U, F_Q + 4, F_Q + 5, F_Q + 2}, {F_V + 0, F_V + 1, F_V + 2, F_P + 2}};
+constexpr int NSLOT = 30;
+constexpr int slotU(int b) { return b; }
+constexpr int slotV(int b, int k) { return 3 + 3 * b + k; }
+constexpr int slotP(int b, int k) { return 12 + 3 * b + k; }
+constexpr int slotQ(int b, int m) { return 18 + 6 * b + m; }  // m: xx yy zz xy xz yz
 
-enum TimerKind { T_DUAL = 0, T_PRIMAL, T_ENERGY, T_HALO, T_KINDS };
+constexpr int FUSED_TY = 14;  // fused-kernel tile: 30 x 14 owned voxels, 32 x 16 threads
+
+enum TimerKind { T_DUAL = 0, T_PRIMAL, T_FUSED, T_ENERGY, T_HALO, T_KINDS };
 
 }  // namespace
 
@@ -49,11 +49,15 @@ struct tgv_ctx {
     float centers[16]{};
     float lambda = 0, alpha0 = 0, alpha1 = 0, tau = 0, sigma = 0;
     int rank = 0, nranks = 1, device = 0;
+    int schedule = TGV_SCHEDULE_FUSED;
+    int fused_zc = 0;  // 0 = automatic
 
     Geo g{};
-    int slots = 8;           // histogram slots per voxel
-    float* state = nullptr;  // NF * g.fs floats
-    uint16_t* hist = nullptr;
+    int slots = 8;            // histogram slots per voxel
+    int count_bytes = 2;      // 1 (u8) or 2 (u16), decided per load
+    float* state = nullptr;   // NSLOT * g.fs floats
+    uint16_t* hist16 = nullptr;
+    uint8_t* hist8 = nullptr;
     double* partials = nullptr;
     double* d_out = nullptr;
     unsigned int* d_maxc = nullptr;
@@ -61,6 +65,7 @@ struct tgv_ctx {
     int64_t staging_elems = 0;
     int energy_blocks = 0;
     int64_t device_bytes = 0;
+    int64_t k = 0;  // iteration counter
 
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
@@ -104,9 +109,15 @@ int fail(tgv_ctx* c, int code, const char* fmt, ...)
             return fail(c, TGV_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, nccl->GetErrorString(r_)); \
     } while (0)
 
-inline float* field(tgv_ctx* c, int f) { return c->state + (int64_t)f * c->g.fs; }
-// pointer to local plane z (z in [-1, nzl]) of field f
-inline float* plane_ptr(tgv_ctx* c, int f, int z) { return field(c, f) + (int64_t)(z + 1) * c->g.plane; }
+inline float* slot(tgv_ctx* c, int s) { return c->state + (int64_t)s * c->g.fs; }
+// pointer to local plane z (z in [-1, nzl]) of slot s
+inline float* plane_ptr(tgv_ctx* c, int s, int z) { return slot(c, s) + (int64_t)(z + 1) * c->g.plane; }
+inline const void* hist_ptr(const tgv_ctx* c) { return c->count_bytes == 1 ? (const void*)c->hist8 : c->hist16; }
+
+struct Bufs {
+    int cu, pu, nu, cp, np;
+};
+inline Bufs bufs(int64_t k) { return Bufs{(int)(k % 3), (int)((k + 2) % 3), (int)((k + 1) % 3), (int)(k % 2), (int)((k + 1) % 2)}; }
 
 int check_ready(tgv_ctx* c)
 {
@@ -116,7 +127,7 @@ int check_ready(tgv_ctx* c)
 }
 
 // ---- timing -----------------------------------------------------------------
-int timer_begin(tgv_ctx* c, int kind, size_t* slot)
+int timer_begin(tgv_ctx* c, int kind, size_t* slot_)
 {
     if (!c->timing) return TGV_OK;
     if (c->ev_used + 2 > c->ev_pool.size()) {
@@ -127,19 +138,18 @@ int timer_begin(tgv_ctx* c, int kind, size_t* slot)
             c->ev_pool.push_back(e);
         }
     }
-    *slot = c->ev_used;
+    *slot_ = c->ev_used;
     c->ev_used += 2;
     c->ev_kind.push_back(kind);
-    CU(cudaEventRecord(c->ev_pool[*slot], c->stream));
+    CU(cudaEventRecord(c->ev_pool[*slot_], c->stream));
     return TGV_OK;
 }
-int timer_end(tgv_ctx* c, size_t slot)
+int timer_end(tgv_ctx* c, size_t slot_)
 {
     if (!c->timing) return TGV_OK;
-    CU(cudaEventRecord(c->ev_pool[slot + 1], c->stream));
+    CU(cudaEventRecord(c->ev_pool[slot_ + 1], c->stream));
     return TGV_OK;
 }
-// after a stream sync: fold recorded pairs into the sums
 int timer_collect(tgv_ctx* c)
 {
     if (!c->timing) return TGV_OK;
@@ -166,38 +176,110 @@ Centers centers(const tgv_ctx* c)
     return C;
 }
 
-int launch_dual(tgv_ctx* c)
+// pointers of iteration k: inputs (u_k, u_{k-1}, v_k, v_{k-1}, p_k, q_k), outputs of k+1
+IterPtrs iter_ptrs(tgv_ctx* c, int64_t k)
 {
-    size_t slot = 0;
-    int rc = timer_begin(c, T_DUAL, &slot);
-    if (rc) return rc;
-    dim3 blk(32, 8), grd((c->g.nx + 31) / 32, (c->g.ny + 7) / 8, c->g.nzl);
-    dual_kernel<<<grd, blk, 0, c->stream>>>(c->state, c->g, step_params(c));
-    CU(cudaGetLastError());
-    return timer_end(c, slot);
+    const Bufs b = bufs(k);
+    IterPtrs a{};
+    a.uk = slot(c, slotU(b.cu));
+    a.um = slot(c, slotU(b.pu));
+    a.un = slot(c, slotU(b.nu));
+    for (int d = 0; d < 3; ++d) {
+        a.vk[d] = slot(c, slotV(b.cu, d));
+        a.vm[d] = slot(c, slotV(b.pu, d));
+        a.vn[d] = slot(c, slotV(b.nu, d));
+        a.pk[d] = slot(c, slotP(b.cp, d));
+        a.pn[d] = slot(c, slotP(b.np, d));
+    }
+    for (int m = 0; m < 6; ++m) {
+        a.qk[m] = slot(c, slotQ(b.cp, m));
+        a.qn[m] = slot(c, slotQ(b.np, m));
+    }
+    a.hist = hist_ptr(c);
+    return a;
 }
 
-int launch_primal(tgv_ctx* c)
+template <int SLOTS, typename CT>
+void launch_split_primal_t(tgv_ctx* c, const IterPtrs& a, dim3 grd, dim3 blk)
 {
-    size_t slot = 0;
-    int rc = timer_begin(c, T_PRIMAL, &slot);
+    split_primal_kernel<SLOTS, CT><<<grd, blk, 0, c->stream>>>(a, c->g, step_params(c), centers(c));
+}
+
+int launch_split(tgv_ctx* c, int phase /*0 dual, 1 primal*/)
+{
+    size_t sl = 0;
+    int rc = timer_begin(c, phase == 0 ? T_DUAL : T_PRIMAL, &sl);
     if (rc) return rc;
     dim3 blk(32, 8), grd((c->g.nx + 31) / 32, (c->g.ny + 7) / 8, c->g.nzl);
-    const uint4* H = reinterpret_cast<const uint4*>(c->hist);
-    if (c->slots == 8)
-        primal_kernel<8><<<grd, blk, 0, c->stream>>>(c->state, H, c->g, step_params(c), centers(c));
-    else
-        primal_kernel<16><<<grd, blk, 0, c->stream>>>(c->state, H, c->g, step_params(c), centers(c));
+    IterPtrs a = iter_ptrs(c, c->k);
+    if (phase == 0) {
+        split_dual_kernel<<<grd, blk, 0, c->stream>>>(a, c->g, step_params(c));
+    } else {
+        // the primal reads the dual's outputs p_{k+1}, q_{k+1}
+        for (int d = 0; d < 3; ++d) a.pk[d] = a.pn[d];
+        for (int m = 0; m < 6; ++m) a.qk[m] = a.qn[m];
+        if (c->slots == 8 && c->count_bytes == 1) launch_split_primal_t<8, uint8_t>(c, a, grd, blk);
+        else if (c->slots == 8) launch_split_primal_t<8, uint16_t>(c, a, grd, blk);
+        else if (c->count_bytes == 1) launch_split_primal_t<16, uint8_t>(c, a, grd, blk);
+        else launch_split_primal_t<16, uint16_t>(c, a, grd, blk);
+    }
     CU(cudaGetLastError());
-    return timer_end(c, slot);
+    return timer_end(c, sl);
 }
+
+int fused_zc(const tgv_ctx* c)
+{
+    if (c->fused_zc > 0) return c->fused_zc;
+    const int tiles = ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
+    const int want = 4 * 148;  // about four waves of one CTA per SM
+    int chunks = std::max(1, std::min(c->g.nzl, (want + tiles - 1) / tiles));
+    return std::max(1, (c->g.nzl + chunks - 1) / chunks);
+}
+
+template <int SLOTS, typename CT>
+void launch_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
+{
+    fused_kernel<FUSED_TY, SLOTS, CT><<<grd, dim3(32, FUSED_TY + 2), 0, c->stream>>>(A);
+}
+
+int launch_fused(tgv_ctx* c)
+{
+    size_t sl = 0;
+    int rc = timer_begin(c, T_FUSED, &sl);
+    if (rc) return rc;
+    FusedArgs A{};
+    A.a = iter_ptrs(c, c->k);
+    A.g = c->g;
+    A.sp = step_params(c);
+    A.C = centers(c);
+    A.z_lo = 0;
+    A.z_hi = c->g.nzl;
+    A.zc = fused_zc(c);
+    dim3 grd((c->g.nx + 29) / 30, (c->g.ny + FUSED_TY - 1) / FUSED_TY, (c->g.nzl + A.zc - 1) / A.zc);
+    if (c->slots == 8 && c->count_bytes == 1) launch_fused_t<8, uint8_t>(c, A, grd);
+    else if (c->slots == 8) launch_fused_t<8, uint16_t>(c, A, grd);
+    else if (c->count_bytes == 1) launch_fused_t<16, uint8_t>(c, A, grd);
+    else launch_fused_t<16, uint16_t>(c, A, grd);
+    CU(cudaGetLastError());
+    return timer_end(c, sl);
+}
+
+// ---- halo exchange (plans pinned on CPU by tests/test_slab_gloo.py)
+// "down": this rank's BOTTOM owned plane -> rank-1's top halo plane;
+// "up":   this rank's TOP owned plane    -> rank+1's bottom halo plane.
+struct HaloPlan {
+    int ndown = 0, nup = 0;
+    int down[16], up[16];
+    void add_down(int s) { down[ndown++] = s; }
+    void add_up(int s) { up[nup++] = s; }
+};
 
 int halo_exchange(tgv_ctx* c, const HaloPlan& hp)
 {
     if (c->nranks == 1) return TGV_OK;
     const NcclApi* nccl = c->nccl;
-    size_t slot = 0;
-    int rc = timer_begin(c, T_HALO, &slot);
+    size_t sl = 0;
+    int rc = timer_begin(c, T_HALO, &sl);
     if (rc) return rc;
     const size_t n = (size_t)c->g.plane;
     const int nzl = c->g.nzl;
@@ -213,7 +295,66 @@ int halo_exchange(tgv_ctx* c, const HaloPlan& hp)
         if (c->rank > 0) NC(nccl->Recv(plane_ptr(c, hp.up[k], -1), n, ncclFloat, c->rank - 1, c->comm, c->stream));
     }
     NC(nccl->GroupEnd());
-    return timer_end(c, slot);
+    return timer_end(c, sl);
+}
+
+// split schedule, before the dual: grad ubar needs ubar(z+1) -> (u_k, u_{k-1}) down;
+// E(vbar) needs vbar(z-1) -> (v_k, v_{k-1}) up
+HaloPlan plan_split_a(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_down(slotU(b.cu));
+    h.add_down(slotU(b.pu));
+    for (int d = 0; d < 3; ++d) {
+        h.add_up(slotV(b.cu, d));
+        h.add_up(slotV(b.pu, d));
+    }
+    return h;
+}
+// split schedule, before the primal: div2 q needs q_xz, q_yz, q_zz(z+1) down; div p needs p_z(z-1) up
+HaloPlan plan_split_b(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_down(slotQ(b.np, 4));
+    h.add_down(slotQ(b.np, 5));
+    h.add_down(slotQ(b.np, 2));
+    h.add_up(slotP(b.np, 2));
+    return h;
+}
+// fused schedule, once per iteration: the kernel recomputes the dual on the halo
+// planes (p at plane -1, q at plane nzl), so it needs the full inputs there:
+//   down: u, u_prev, v, v_prev, q (14 planes);  up: u, u_prev, v, v_prev, p (11 planes)
+HaloPlan plan_fused(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    for (int s : {slotU(b.cu), slotU(b.pu)}) {
+        h.add_down(s);
+        h.add_up(s);
+    }
+    for (int d = 0; d < 3; ++d)
+        for (int bb : {b.cu, b.pu}) {
+            h.add_down(slotV(bb, d));
+            h.add_up(slotV(bb, d));
+        }
+    for (int m = 0; m < 6; ++m) h.add_down(slotQ(b.cp, m));
+    for (int d = 0; d < 3; ++d) h.add_up(slotP(b.cp, d));
+    return h;
+}
+// energy: grad u (u(z+1)), div2 q (q_xz, q_yz, q_zz(z+1)) down; E(v) (v(z-1)), div p (p_z(z-1)) up
+HaloPlan plan_energy(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_down(slotU(b.cu));
+    h.add_down(slotQ(b.cp, 4));
+    h.add_down(slotQ(b.cp, 5));
+    h.add_down(slotQ(b.cp, 2));
+    for (int d = 0; d < 3; ++d) h.add_up(slotV(b.cu, d));
+    h.add_up(slotP(b.cp, 2));
+    return h;
 }
 
 int sync_stream(tgv_ctx* c)
@@ -228,17 +369,35 @@ int sync_stream(tgv_ctx* c)
     return timer_collect(c);
 }
 
+template <int SLOTS, typename CT>
+void launch_init_t(tgv_ctx* c)
+{
+    init_state_kernel<SLOTS, CT><<<148 * 8, 256, 0, c->stream>>>(slot(c, slotU(0)), slot(c, slotU(2)), hist_ptr(c),
+                                                                 c->g, centers(c));
+}
+
 int init_from_hist(tgv_ctx* c)
 {
-    CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NF * (size_t)c->g.fs, c->stream));
-    const uint4* H = reinterpret_cast<const uint4*>(c->hist);
-    const int blocks = 148 * 8;
-    if (c->slots == 8)
-        init_state_kernel<8><<<blocks, 256, 0, c->stream>>>(c->state, H, c->g, centers(c));
-    else
-        init_state_kernel<16><<<blocks, 256, 0, c->stream>>>(c->state, H, c->g, centers(c));
+    CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * (size_t)c->g.fs, c->stream));
+    c->k = 0;  // u_0 in U[0], u_{-1} = u_0 in U[2]
+    if (c->slots == 8 && c->count_bytes == 1) launch_init_t<8, uint8_t>(c);
+    else if (c->slots == 8) launch_init_t<8, uint16_t>(c);
+    else if (c->count_bytes == 1) launch_init_t<16, uint8_t>(c);
+    else launch_init_t<16, uint16_t>(c);
     CU(cudaGetLastError());
     return TGV_OK;
+}
+
+template <int SLOTS, typename CT>
+void launch_energy_t(tgv_ctx* c, const EnergyArgs& ea)
+{
+    energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, centers(c), c->partials);
+}
+
+int64_t env_int(const char* name, int64_t dflt)
+{
+    const char* s = getenv(name);
+    return s && *s ? strtoll(s, nullptr, 10) : dflt;
 }
 
 }  // namespace
@@ -284,10 +443,14 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     *out = nullptr;
     if (!L || !P) return fail(c, TGV_EINVAL, "layout or params is NULL");
     if (L->nx < 1 || L->ny < 1 || L->nz < 1) return fail(c, TGV_EINVAL, "grid extents must be >= 1");
-    if (L->nx > (1 << 30) || L->ny > (1 << 30) || L->nz > (1 << 30)) return fail(c, TGV_EINVAL, "grid too large");
     if (L->z_begin < 0 || L->z_end > L->nz || L->z_begin >= L->z_end)
         return fail(c, TGV_EINVAL, "slab [%lld, %lld) outside [0, %lld) or empty", (long long)L->z_begin,
                     (long long)L->z_end, (long long)L->nz);
+    {
+        const int64_t px = (L->nx + 31) / 32 * 32;
+        if (L->nz > (1 << 30) || px * L->ny * (L->z_end - L->z_begin + 2) >= (int64_t(1) << 31))
+            return fail(c, TGV_EINVAL, "slab too large: one field of a slab must hold < 2^31 elements");
+    }
     if (L->brick[0] || L->brick[1] || L->brick[2])
         return fail(c, TGV_EINVAL, "brick layouts are not supported (brick must be {0,0,0})");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TGV_EINVAL, "bad rank %d / nranks %d", rank, nranks);
@@ -327,6 +490,9 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     c->nranks = nranks;
     c->device = dev;
     c->slots = P->nbins <= 8 ? 8 : 16;
+    c->schedule = (int)env_int("TGV_SCHEDULE", TGV_SCHEDULE_FUSED);
+    if (c->schedule != TGV_SCHEDULE_SPLIT) c->schedule = TGV_SCHEDULE_FUSED;
+    c->fused_zc = (int)env_int("TGV_FUSED_ZC", 0);
 
     Geo& g = c->g;
     g.nx = (int)L->nx;
@@ -334,11 +500,10 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     g.nzl = (int)(L->z_end - L->z_begin);
     g.nz = (int)L->nz;
     g.z0 = (int)L->z_begin;
-    g.px = (L->nx + 31) / 32 * 32;
-    g.plane = g.px * L->ny;
+    g.px = (int)((L->nx + 31) / 32 * 32);
+    g.plane = g.px * g.ny;
     g.fs = (int64_t)(g.nzl + 2) * g.plane;
 
-    int rc;
     if (cudaSetDevice(dev) != cudaSuccess) {
         fail(c, TGV_ECUDA, "cudaSetDevice(%d) failed", dev);
         return bail(TGV_ECUDA);
@@ -347,10 +512,10 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
         fail(c, TGV_ECUDA, "stream creation failed");
         return bail(TGV_ECUDA);
     }
-    const size_t state_bytes = sizeof(float) * (size_t)NF * (size_t)g.fs;
+    const size_t state_bytes = sizeof(float) * (size_t)NSLOT * (size_t)g.fs;
     const size_t hist_bytes = sizeof(uint16_t) * (size_t)c->slots * (size_t)g.nzl * (size_t)g.plane;
     c->energy_blocks = 148 * 4;
-    if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->hist, hist_bytes) != cudaSuccess ||
+    if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->hist16, hist_bytes) != cudaSuccess ||
         cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * 8) != cudaSuccess ||
         cudaMalloc(&c->d_maxc, sizeof(unsigned int)) != cudaSuccess) {
@@ -360,7 +525,7 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     }
     c->device_bytes = (int64_t)(state_bytes + hist_bytes);
     if (cudaMemsetAsync(c->state, 0, state_bytes, c->stream) != cudaSuccess ||
-        cudaMemsetAsync(c->hist, 0, hist_bytes, c->stream) != cudaSuccess) {
+        cudaMemsetAsync(c->hist16, 0, hist_bytes, c->stream) != cudaSuccess) {
         fail(c, TGV_ECUDA, "memset failed");
         return bail(TGV_ECUDA);
     }
@@ -404,8 +569,17 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
         fail(c, TGV_ECUDA, "create sync failed");
         return bail(TGV_ECUDA);
     }
-    (void)rc;
     *out = c;
+    return TGV_OK;
+}
+
+int tgv_set_schedule(tgv_ctx* c, int schedule)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT)
+        return fail(c, TGV_EINVAL, "unknown schedule %d", schedule);
+    c->schedule = schedule;  // the state representation is shared: switching keeps the iterate
     return TGV_OK;
 }
 
@@ -420,7 +594,7 @@ int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
         return fail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n_counts, (long long)(per_plane * g.nzl));
     c->loaded = false;
     // staging buffer of whole planes, up to ~256 MB
-    int planes_per_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (64ll << 20) / per_plane));
+    const int planes_per_chunk = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (64ll << 20) / per_plane));
     const int64_t need = per_plane * planes_per_chunk;
     if (c->staging_elems < need) {
         if (c->staging) cudaFree(c->staging);
@@ -439,9 +613,10 @@ int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
                            cudaMemcpyHostToDevice, c->stream));
         const int blocks = 148 * 8;
         if (c->slots == 8)
-            pack_counts_kernel<8><<<blocks, 256, 0, c->stream>>>(c->staging, nzc, z0, g, c->nbins, c->hist, c->d_maxc);
+            pack_counts_kernel<8><<<blocks, 256, 0, c->stream>>>(c->staging, nzc, z0, g, c->nbins, c->hist16,
+                                                                  c->d_maxc);
         else
-            pack_counts_kernel<16><<<blocks, 256, 0, c->stream>>>(c->staging, nzc, z0, g, c->nbins, c->hist,
+            pack_counts_kernel<16><<<blocks, 256, 0, c->stream>>>(c->staging, nzc, z0, g, c->nbins, c->hist16,
                                                                    c->d_maxc);
         CU(cudaGetLastError());
     }
@@ -449,6 +624,20 @@ int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
     CU(cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     if (maxc > 65535u) return fail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc);
+    const bool want8 = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0;
+    if (want8) {
+        const int64_t n = (int64_t)c->slots * g.nzl * g.plane;
+        if (!c->hist8) {
+            if (cudaMalloc(&c->hist8, (size_t)n) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, TGV_ENOMEM, "u8 histogram allocation failed");
+            }
+            c->device_bytes += n;
+        }
+        compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(c->hist16, c->hist8, n);
+        CU(cudaGetLastError());
+    }
+    c->count_bytes = want8 ? 1 : 2;
     rc = init_from_hist(c);
     if (rc) return rc;
     CU(cudaStreamSynchronize(c->stream));
@@ -474,22 +663,47 @@ int tgv_iterate(tgv_ctx* c, int32_t n)
     if (n < 0) return fail(c, TGV_EINVAL, "n < 0");
     if (!c->loaded) return fail(c, TGV_ESTATE, "iterate before load");
     for (int32_t it = 0; it < n; ++it) {
-        if ((rc = halo_exchange(c, HALO_A))) return rc;
-        if ((rc = launch_dual(c))) return rc;
-        if ((rc = halo_exchange(c, HALO_B))) return rc;
-        if ((rc = launch_primal(c))) return rc;
+        if (c->schedule == TGV_SCHEDULE_SPLIT) {
+            if ((rc = halo_exchange(c, plan_split_a(c->k)))) return rc;
+            if ((rc = launch_split(c, 0))) return rc;
+            if ((rc = halo_exchange(c, plan_split_b(c->k)))) return rc;
+            if ((rc = launch_split(c, 1))) return rc;
+        } else {
+            if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
+            if ((rc = launch_fused(c))) return rc;
+        }
+        c->k += 1;
     }
     return sync_stream(c);
 }
 
-static int copy_field_out(tgv_ctx* c, int f, float* out, int64_t n)
+// ---- field access -------------------------------------------------------------
+static int copy_out(tgv_ctx* c, int s, float* out)
 {
     const Geo& g = c->g;
-    CU(cudaMemcpy2DAsync(out, sizeof(float) * g.nx, plane_ptr(c, f, 0), sizeof(float) * g.px, sizeof(float) * g.nx,
+    CU(cudaMemcpy2DAsync(out, sizeof(float) * g.nx, plane_ptr(c, s, 0), sizeof(float) * g.px, sizeof(float) * g.nx,
                          (size_t)g.ny * g.nzl, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    (void)n;
     return TGV_OK;
+}
+static int copy_in(tgv_ctx* c, int s, const float* in)
+{
+    const Geo& g = c->g;
+    CU(cudaMemcpy2DAsync(plane_ptr(c, s, 0), sizeof(float) * g.px, in, sizeof(float) * g.nx, sizeof(float) * g.nx,
+                         (size_t)g.ny * g.nzl, cudaMemcpyHostToDevice, c->stream));
+    return TGV_OK;
+}
+// ABI field id -> (current slot, previous slot or -1)
+static void field_slots(const tgv_ctx* c, int f, int* cur, int* prev)
+{
+    const Bufs b = bufs(c->k);
+    *prev = -1;
+    if (f == TGV_FIELD_U) *cur = slotU(b.cu);
+    else if (f >= TGV_FIELD_V && f < TGV_FIELD_V + 3) *cur = slotV(b.cu, f - TGV_FIELD_V);
+    else if (f == TGV_FIELD_UBAR) *cur = slotU(b.cu), *prev = slotU(b.pu);
+    else if (f >= TGV_FIELD_VBAR && f < TGV_FIELD_VBAR + 3)
+        *cur = slotV(b.cu, f - TGV_FIELD_VBAR), *prev = slotV(b.pu, f - TGV_FIELD_VBAR);
+    else if (f >= TGV_FIELD_P && f < TGV_FIELD_P + 3) *cur = slotP(b.cp, f - TGV_FIELD_P);
+    else *cur = slotQ(b.cp, f - TGV_FIELD_Q);
 }
 
 int tgv_read_field(tgv_ctx* c, int f, float* out, int64_t n)
@@ -497,10 +711,21 @@ int tgv_read_field(tgv_ctx* c, int f, float* out, int64_t n)
     int rc = check_ready(c);
     if (rc) return rc;
     if (!out) return fail(c, TGV_EINVAL, "out is NULL");
-    if (f < 0 || f >= NF) return fail(c, TGV_EINVAL, "bad field id %d", f);
+    if (f < 0 || f >= TGV_NUM_FIELDS) return fail(c, TGV_EINVAL, "bad field id %d", f);
     if (n != (int64_t)c->g.nx * c->g.ny * c->g.nzl) return fail(c, TGV_EINVAL, "n_voxels mismatch");
     if (!c->loaded) return fail(c, TGV_ESTATE, "read before load");
-    return copy_field_out(c, f, out, n);
+    int cur, prev;
+    field_slots(c, f, &cur, &prev);
+    if ((rc = copy_out(c, cur, out))) return rc;
+    if (prev >= 0) {  // over-relaxed iterate: 2 x_k - x_{k-1} (exactly the kernels' rounding)
+        std::vector<float> pv((size_t)n);
+        if ((rc = copy_out(c, prev, pv.data()))) return rc;
+        CU(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < n; ++i) out[i] = 2.f * out[i] - pv[(size_t)i];
+        return TGV_OK;
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
 }
 
 int tgv_read_u(tgv_ctx* c, float* u, int64_t n) { return tgv_read_field(c, TGV_FIELD_U, u, n); }
@@ -510,12 +735,20 @@ int tgv_write_field(tgv_ctx* c, int f, const float* in, int64_t n)
     int rc = check_ready(c);
     if (rc) return rc;
     if (!in) return fail(c, TGV_EINVAL, "in is NULL");
-    if (f < 0 || f >= NF) return fail(c, TGV_EINVAL, "bad field id %d", f);
+    if (f < 0 || f >= TGV_NUM_FIELDS) return fail(c, TGV_EINVAL, "bad field id %d", f);
     if (n != (int64_t)c->g.nx * c->g.ny * c->g.nzl) return fail(c, TGV_EINVAL, "n_voxels mismatch");
     if (!c->loaded) return fail(c, TGV_ESTATE, "write before load");
-    const Geo& g = c->g;
-    CU(cudaMemcpy2DAsync(plane_ptr(c, f, 0), sizeof(float) * g.px, in, sizeof(float) * g.nx, sizeof(float) * g.nx,
-                         (size_t)g.ny * g.nzl, cudaMemcpyHostToDevice, c->stream));
+    int cur, prev;
+    field_slots(c, f, &cur, &prev);
+    if (prev < 0) {
+        if ((rc = copy_in(c, cur, in))) return rc;
+    } else {  // ubar / vbar: set the previous iterate to 2 x_k - in
+        std::vector<float> xk((size_t)n);
+        if ((rc = copy_out(c, cur, xk.data()))) return rc;
+        CU(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < n; ++i) xk[(size_t)i] = 2.f * xk[(size_t)i] - in[i];
+        if ((rc = copy_in(c, prev, xk.data()))) return rc;
+    }
     CU(cudaStreamSynchronize(c->stream));
     return TGV_OK;
 }
@@ -526,21 +759,31 @@ int tgv_energy(tgv_ctx* c, double out[6])
     if (rc) return rc;
     if (!out) return fail(c, TGV_EINVAL, "out is NULL");
     if (!c->loaded) return fail(c, TGV_ESTATE, "energy before load");
-    if ((rc = halo_exchange(c, HALO_E))) return rc;
-    size_t slot = 0;
-    if ((rc = timer_begin(c, T_ENERGY, &slot))) return rc;
-    EnergyParams ep{c->alpha1, c->alpha0, c->lambda, 2.0, c->nbins};
-    const uint4* H = reinterpret_cast<const uint4*>(c->hist);
-    if (c->slots == 8)
-        energy_partial_kernel<8><<<c->energy_blocks, 256, 0, c->stream>>>(c->state, H, c->g, ep, centers(c),
-                                                                          c->partials);
-    else
-        energy_partial_kernel<16><<<c->energy_blocks, 256, 0, c->stream>>>(c->state, H, c->g, ep, centers(c),
-                                                                           c->partials);
+    if ((rc = halo_exchange(c, plan_energy(c->k)))) return rc;
+    size_t sl = 0;
+    if ((rc = timer_begin(c, T_ENERGY, &sl))) return rc;
+    const Bufs b = bufs(c->k);
+    EnergyArgs ea{};
+    ea.u = slot(c, slotU(b.cu));
+    for (int d = 0; d < 3; ++d) {
+        ea.v[d] = slot(c, slotV(b.cu, d));
+        ea.p[d] = slot(c, slotP(b.cp, d));
+    }
+    for (int m = 0; m < 6; ++m) ea.q[m] = slot(c, slotQ(b.cp, m));
+    ea.hist = hist_ptr(c);
+    ea.alpha1 = c->alpha1;
+    ea.alpha0 = c->alpha0;
+    ea.lambda = c->lambda;
+    ea.V = 2.0;
+    ea.nbins = c->nbins;
+    if (c->slots == 8 && c->count_bytes == 1) launch_energy_t<8, uint8_t>(c, ea);
+    else if (c->slots == 8) launch_energy_t<8, uint16_t>(c, ea);
+    else if (c->count_bytes == 1) launch_energy_t<16, uint8_t>(c, ea);
+    else launch_energy_t<16, uint16_t>(c, ea);
     CU(cudaGetLastError());
     energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, c->energy_blocks, c->d_out);
     CU(cudaGetLastError());
-    if ((rc = timer_end(c, slot))) return rc;
+    if ((rc = timer_end(c, sl))) return rc;
     if (c->nranks > 1) {
         const NcclApi* nccl = c->nccl;
         NC(nccl->AllReduce(c->d_out, c->d_out, 4, ncclFloat64, ncclSum, c->comm, c->stream));
@@ -577,10 +820,12 @@ int tgv_get_timing(const tgv_ctx* c, tgv_timing* o)
     if (!c || !o) return TGV_EINVAL;
     o->dual_ms = c->t_ms[T_DUAL];
     o->primal_ms = c->t_ms[T_PRIMAL];
+    o->fused_ms = c->t_ms[T_FUSED];
     o->energy_ms = c->t_ms[T_ENERGY];
     o->halo_ms = c->t_ms[T_HALO];
     o->dual_launches = c->t_n[T_DUAL];
     o->primal_launches = c->t_n[T_PRIMAL];
+    o->fused_launches = c->t_n[T_FUSED];
     o->energy_launches = c->t_n[T_ENERGY];
     o->halo_exchanges = c->t_n[T_HALO];
     return TGV_OK;
@@ -591,14 +836,21 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     if (!c || !o) return TGV_EINVAL;
     o->row_pitch = c->g.px;
     o->device_bytes = c->device_bytes;
-    o->count_bytes = 2;
+    o->count_bytes = c->count_bytes;
     o->count_slots = c->slots;
-    // algorithmic bytes per voxel: dual reads ubar, vbar(3), p(3), q(6) and
-    // writes p, q; primal reads p(3), q(6), u, v(3), histogram and writes u, v, ubar, vbar.
-    o->bytes_dual = 4 * (13 + 9);
-    o->bytes_primal = 4 * (13 + 8) + 2 * c->slots;
+    o->schedule = c->schedule;
+    const int64_t hb = (int64_t)c->count_bytes * c->slots;
+    // algorithmic HBM bytes per voxel of one launch:
+    // split dual: reads u_k, u_{k-1}, v_k, v_{k-1}, p_k, q_k (17 floats), writes p, q (9)
+    o->bytes_dual = 4 * (17 + 9);
+    // split primal: reads p, q (new), u_k, v_k (13 floats) + histogram, writes u, v (4)
+    o->bytes_primal = 4 * (13 + 4) + hb;
+    // fused: reads 17 floats + histogram, writes u, v, p, q (13 floats)
+    o->bytes_fused = 4 * (17 + 13) + hb;
+    o->fused_zc = fused_zc(c);
     o->nranks = c->nranks;
     o->rank = c->rank;
+    o->iteration = c->k;
     return TGV_OK;
 }
 
@@ -616,7 +868,8 @@ void tgv_destroy(tgv_ctx* c)
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     cudaFree(c->state);
-    cudaFree(c->hist);
+    cudaFree(c->hist16);
+    cudaFree(c->hist8);
     cudaFree(c->partials);
     cudaFree(c->d_out);
     cudaFree(c->d_maxc);

@@ -17,12 +17,13 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libtgv.so")
 
 TGV_OK, TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL, TGV_ESTATE, TGV_ERANGE = 0, -1, -2, -3, -4, -5, -6
+SCHEDULE_FUSED, SCHEDULE_SPLIT = 0, 1
 FIELD_U, FIELD_V, FIELD_UBAR, FIELD_VBAR, FIELD_P, FIELD_Q, NUM_FIELDS = 0, 1, 4, 5, 8, 11, 17
 FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 10],
           "q": [11, 12, 13, 14, 15, 16]}
 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
-           "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_timing", "tgv_get_timing", "tgv_info",
+           "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error"]
 
 
@@ -38,16 +39,17 @@ class tgv_params(ctypes.Structure):
 
 
 class tgv_timing(ctypes.Structure):
-    _fields_ = [("dual_ms", ctypes.c_double), ("primal_ms", ctypes.c_double), ("energy_ms", ctypes.c_double),
-                ("halo_ms", ctypes.c_double), ("dual_launches", ctypes.c_int64),
-                ("primal_launches", ctypes.c_int64), ("energy_launches", ctypes.c_int64),
-                ("halo_exchanges", ctypes.c_int64)]
+    _fields_ = [("dual_ms", ctypes.c_double), ("primal_ms", ctypes.c_double), ("fused_ms", ctypes.c_double),
+                ("energy_ms", ctypes.c_double), ("halo_ms", ctypes.c_double), ("dual_launches", ctypes.c_int64),
+                ("primal_launches", ctypes.c_int64), ("fused_launches", ctypes.c_int64),
+                ("energy_launches", ctypes.c_int64), ("halo_exchanges", ctypes.c_int64)]
 
 
 class tgv_info_t(ctypes.Structure):
     _fields_ = [("row_pitch", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32),
-                ("count_slots", ctypes.c_int32), ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64),
-                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32)]
+                ("count_slots", ctypes.c_int32), ("schedule", ctypes.c_int32), ("fused_zc", ctypes.c_int32),
+                ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64), ("bytes_fused", ctypes.c_int64),
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("iteration", ctypes.c_int64)]
 
 
 def _load():
@@ -65,6 +67,7 @@ def _load():
     lib.tgv_read_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_write_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_energy.argtypes = [vp, vp]
+    lib.tgv_set_schedule.argtypes = [vp, ctypes.c_int]
     lib.tgv_set_timing.argtypes = [vp, ctypes.c_int]
     lib.tgv_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
     lib.tgv_info.argtypes = [vp, ctypes.POINTER(tgv_info_t)]
@@ -162,6 +165,10 @@ def tgv_energy(ctx) -> np.ndarray:
     return out
 
 
+def tgv_set_schedule(ctx, schedule: int):
+    _check(lib.tgv_set_schedule(ctx, int(schedule)), ctx)
+
+
 def tgv_set_timing(ctx, enable: bool):
     _check(lib.tgv_set_timing(ctx, 1 if enable else 0), ctx)
 
@@ -249,6 +256,11 @@ class Solver:
     def energy(self) -> dict:
         e = tgv_energy(self.ctx)
         return {"E": e[0], "alpha1": e[1], "alpha0": e[2], "data": e[3], "gap": e[4], "vmax": e[5]}
+
+    def set_schedule(self, schedule):
+        """'fused' (default), 'split', or a TGV_SCHEDULE_* value."""
+        tgv_set_schedule(self.ctx, {"fused": SCHEDULE_FUSED, "split": SCHEDULE_SPLIT}.get(schedule, schedule))
+        return self
 
     def set_timing(self, on: bool):
         tgv_set_timing(self.ctx, on)

@@ -35,11 +35,15 @@ def params(wl=None, **kw):
     return p
 
 
-def pair(shape, counts, iters, centers=None, **kw):
+SCHEDULES = ["fused", "split"]
+
+
+def pair(shape, counts, iters, centers=None, schedule="fused", **kw):
     c = oracle.default_centers(8) if centers is None else np.asarray(centers, np.float64)
     p = params(**kw)
     o = oracle.Oracle(shape, centers=c, **p).load(counts).iterate(iters, threads=NT)
-    s = solver_cls()(shape, [float(x) for x in c], **p).load(np.ascontiguousarray(counts, np.uint32)).iterate(iters)
+    s = solver_cls()(shape, [float(x) for x in c], **p).set_schedule(schedule)
+    s.load(np.ascontiguousarray(counts, np.uint32)).iterate(iters)
     return o, s
 
 
@@ -64,19 +68,21 @@ def test_init_matches():
         assert np.all(s.get(f) == 0)
 
 
-@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 16, 5), (1, 1, 9), (33, 1, 4), (2, 70, 3)])
-def test_one_iteration_from_random_state(shape):
+@pytest.mark.parametrize("schedule", SCHEDULES)
+@pytest.mark.parametrize("shape", [(37, 23, 19), (64, 16, 5), (1, 1, 9), (33, 1, 4), (2, 70, 3), (61, 29, 40)])
+def test_one_iteration_from_random_state(shape, schedule):
     """Every stencil path (interior, all six boundary faces, projections active) in one step."""
     nx, ny, nz = shape
     rng = np.random.default_rng(7)
     h = synth.random_histograms(shape, 2)
     c = oracle.default_centers(8)
     o = oracle.Oracle(shape, **params()).load(h)
-    s = solver_cls()(shape, list(c), **params()).load(h)
+    s = solver_cls()(shape, list(c), **params()).set_schedule(schedule).load(h)
     st = {"u": rng.uniform(-1, 1, (nz, ny, nx)), "ubar": rng.uniform(-1.5, 1.5, (nz, ny, nx)),
           "v": rng.normal(0, 0.5, (3, nz, ny, nx)), "vbar": rng.normal(0, 0.5, (3, nz, ny, nx)),
           "p": rng.normal(0, 0.7, (3, nz, ny, nx)), "q": rng.normal(0, 1.0, (6, nz, ny, nx))}
-    for k, a in st.items():
+    for k in ("u", "ubar", "v", "vbar", "p", "q"):  # u / v before ubar / vbar (tgv_write_field)
+        a = st[k]
         a32 = a.astype(np.float32)
         s.set(k, a32)
         o.set(k, a32.astype(np.float64))
@@ -86,30 +92,74 @@ def test_one_iteration_from_random_state(shape):
         np.testing.assert_allclose(s.get(f), o.get(f), rtol=0, atol=3e-6, err_msg=f)
 
 
-def test_c1_full_count():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_c1_full_count(schedule):
     wl = synth.workload("C1")
     h = synth.make_histograms("C1")
-    o, s = pair(wl.shape, h, wl.iters, **params(wl))
+    o, s = pair(wl.shape, h, wl.iters, schedule=schedule, **params(wl))
     du, rel = assert_parity(o, s)
-    print(f"C1 x{wl.iters}: max|du| = {du:.3e}, rel dE = {rel:.3e}")
+    print(f"C1 x{wl.iters} ({schedule}): max|du| = {du:.3e}, rel dE = {rel:.3e}")
 
 
+@pytest.mark.parametrize("schedule", SCHEDULES)
 @pytest.mark.parametrize("shape,seed", [((37, 23, 19), 3), ((1, 1, 40), 4), ((33, 1, 7), 5), ((129, 9, 4), 6),
-                                        ((1, 1, 1), 7), ((5, 64, 3), 8)])
-def test_ragged_shapes(shape, seed):
+                                        ((1, 1, 1), 7), ((5, 64, 3), 8), ((91, 45, 70), 9)])
+def test_ragged_shapes(shape, seed, schedule):
     h = synth.random_histograms(shape, seed)
-    o, s = pair(shape, h, 60)
+    o, s = pair(shape, h, 60, schedule=schedule)
     assert_parity(o, s)
 
 
-def test_nonuniform_centres_and_16_bins():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_nonuniform_centres_and_16_bins(schedule):
     shape = (21, 13, 11)
     rng = np.random.default_rng(9)
     for nb in (3, 16):
         c = np.sort(rng.uniform(-0.95, 0.95, nb)).astype(np.float32).astype(np.float64)
         h = rng.integers(0, 5, size=(11, 13, 21, nb)).astype(np.uint32)
-        o, s = pair(shape, h, 40, centers=c)
+        o, s = pair(shape, h, 40, centers=c, schedule=schedule)
         assert_parity(o, s)
+
+
+def test_u16_counts_and_large_votes(monkeypatch):
+    """Counts above 255 keep u16 storage; LIDAR-style vote weight 5."""
+    shape = (33, 17, 9)
+    h = synth.random_histograms(shape, 11) * np.uint32(5)
+    h[2, 3, 4, 6] = 300
+    for sched in SCHEDULES:
+        o, s = pair(shape, h, 50, schedule=sched)
+        assert s.info()["count_bytes"] == 2
+        assert_parity(o, s)
+
+
+def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
+    """FUSED and SPLIT evaluate the same fp32 expressions; u8 and u16 counts are the same integers."""
+    shape = (67, 41, 23)
+    h = synth.random_histograms(shape, 12)
+    c = list(oracle.default_centers(8))
+    outs = {}
+    for sched in SCHEDULES:
+        for force16 in ("0", "1"):
+            monkeypatch.setenv("TGV_FORCE_U16", force16)
+            s = solver_cls()(shape, c).set_schedule(sched).load(h).iterate(37)
+            assert s.info()["count_bytes"] == (2 if force16 == "1" else 1)
+            outs[(sched, force16)] = {f: s.get(f) for f in ("u", "v", "p", "q")}
+            s.close()
+    ref = outs[("split", "1")]
+    for key, o in outs.items():
+        for f in ("u", "v", "p", "q"):
+            assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
+
+
+@pytest.mark.parametrize("zc", [1, 3, 7, 64])
+def test_fused_chunk_sizes(monkeypatch, zc):
+    """z-chunk boundaries of the fused kernel (redundant halo planes) do not change the result."""
+    monkeypatch.setenv("TGV_FUSED_ZC", str(zc))
+    shape = (45, 31, 26)
+    h = synth.random_histograms(shape, 13)
+    o, s = pair(shape, h, 30, schedule="fused")
+    assert s.info()["fused_zc"] == zc
+    assert_parity(o, s)
 
 
 def test_special_cases_exact():
@@ -122,12 +172,13 @@ def test_special_cases_exact():
     assert np.all(s.read_u() == 0.375)  # weighted-median limit (tests/test_oracle_scheme.py)
 
 
-def test_c2_window_full_count():
+@pytest.mark.parametrize("schedule", SCHEDULES)
+def test_c2_window_full_count(schedule):
     """A 64^3 window of the C2 workload (sphere + plane, noise, floaters) at C2's 500 iterations."""
     wl = synth.workload("C2")
     h = synth.make_histograms("C2", 118, 182)[:, 96:160, 96:160]
     h = np.ascontiguousarray(h)
-    o, s = pair((64, 64, 64), h, wl.iters, **params(wl))
+    o, s = pair((64, 64, 64), h, wl.iters, schedule=schedule, **params(wl))
     du, rel = assert_parity(o, s)
     print(f"C2 window 64^3 x{wl.iters}: max|du| = {du:.3e}, rel dE = {rel:.3e}")
 
@@ -136,7 +187,11 @@ def test_c2_full_grid_truncated_count():
     """Full 256^3 C2 grid in the bench's launch configuration, every voxel compared."""
     wl = synth.workload("C2")
     h = synth.make_histograms("C2")
-    o, s = pair(wl.shape, h, 6, **params(wl))
+    o, s = pair(wl.shape, h, 6, schedule="fused", **params(wl))
+    assert_parity(o, s)
+    s.set_schedule("split")
+    s.reset()
+    s.iterate(6)
     assert_parity(o, s)
 
 
