@@ -106,6 +106,8 @@ typedef struct {
     int32_t count_slots;      /* histogram slots stored per voxel (8 or 16)                */
     int32_t schedule;         /* TGV_SCHEDULE_*                                            */
     int32_t fused_zc;         /* z-planes per CTA of the fused kernel                      */
+    int32_t fused_tma;        /* 1: the fused kernel stages planes with TMA (default)      */
+    int32_t reserved;
     int64_t bytes_dual;       /* algorithmic HBM bytes per voxel of one SPLIT dual launch  */
     int64_t bytes_primal;     /* ... of one SPLIT primal launch                            */
     int64_t bytes_fused;      /* ... of one FUSED launch (one whole iteration)             */

@@ -1,0 +1,377 @@
+// tgv_fused_tma.cuh -- single-sweep TGV iteration with TMA-staged planes (sm_100a).
+//
+// Same scheme and same fp32 expressions as split_dual_kernel + split_primal_kernel
+// (tgv_kernels.cuh), one launch per iteration, 128 / 136 B per voxel-iteration.
+//
+// CTA = (TY + 3) warps over a 32 x TY owned tile of (x, y), marching up a z-chunk:
+//   warps 0 .. TY+1 : one row each (row 0 = y0-1 and row TY+1 = y0+TY are the
+//                     y-halo), lane = x - x0 (32 owned columns, 128-B aligned)
+//   warp  TY+2      : the x-halo: lanes 0..15 column x0-1 (p only),
+//                     lanes 16..31 column x0+32 (q only), one row per lane
+// Inputs arrive by TMA (cp.async.bulk.tensor) into shared-memory rings, one
+// box of 40 x (TY+2) per field and plane (x0-4 .. x0+35: the +-1 halo; the
+// inner start coordinate must be 16-B aligned), completion signalled on mbarriers; the planes of step s+2 are in
+// flight while step s computes.  Out-of-range boxes (grid and slab edges) are
+// zero-filled by the TMA unit, so there are no per-element guards.  x and y
+// neighbours are exchanged through two small parity-double-buffered planes
+// (over-relaxed inputs, and the dual results); z neighbours stay in registers.
+// Outputs are staged in shared memory and written with TMA bulk tensor stores
+// (which clip at nx, ny).  Two __syncthreads per step.
+#pragma once
+#include <cuda.h>
+
+#include "tgv_kernels.cuh"
+
+namespace tgvk {
+
+// ---- PTX helpers ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// wait for the phase with the given parity; a watchdog traps (kernel error, no hang)
+// if the transaction never completes
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    uint32_t n = 0;
+    while (!mbar_try(bar, parity))
+        if (++n > (1u << 26)) __trap();
+}
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                          int c3)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+        "[%2];" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store4(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3)
+{
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+                 "r"(smem_addr(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+
+// ---- shared memory ---------------------------------------------------------------
+constexpr int TMA_BW = 40;  // input box width: x0-4 .. x0+35 (the inner start must be 16-B aligned)
+constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
+
+// Ring depths: u is read at planes s and s+1, v / p / q / histogram at plane s only;
+// each ring prefetches two planes beyond what step s reads.
+template <int HB>
+struct TmaRings {
+    static constexpr int NU = 4, NV = 3, NPQ = HB <= 16 ? 3 : 2, NH = HB <= 16 ? 3 : 2;
+};
+
+template <int TY, int HB>
+struct alignas(128) TmaSmem {
+    static constexpr int R = TY + 2;
+    using Rg = TmaRings<HB>;
+    float u[Rg::NU][2][R][TMA_BW];    // ring: u_k, u_{k-1}
+    float v[Rg::NV][6][R][TMA_BW];    // ring: v_k(3), v_{k-1}(3)
+    float pq[Rg::NPQ][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
+    float out[13][TY][32];            // staged outputs: u, v(3), p(3), q(6) of iteration k+1
+    uint8_t h[Rg::NH][TY][32 * HB];   // ring: histograms of the owned rows
+    float suv[2][4][R][TMA_CW];       // ubar, vbar(3) of plane s (parity)
+    float sr[2][7][R][TMA_CW];        // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
+    uint64_t bar_u[Rg::NU], bar_v[Rg::NV], bar_pq[Rg::NPQ], bar_h[Rg::NH];
+};
+
+struct TmaArgs {
+    Geo g;
+    StepParams sp;
+    Centers C;
+    int z_lo, z_hi, zc;
+    int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
+    int s_un, s_vn, s_pn, s_qn;              // output slots
+};
+
+template <int TY, int SLOTS, typename CT>
+__global__ void __launch_bounds__(32 * (TY + 3), 1)
+    fused_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
+                     const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_st1,
+                     const __grid_constant__ CUtensorMap m_st3, const __grid_constant__ CUtensorMap m_st6,
+                     const __grid_constant__ CUtensorMap m_h, const TmaArgs A)
+{
+    constexpr int HB = SLOTS * (int)sizeof(CT);
+    constexpr int R = TY + 2;
+    using Smem = TmaSmem<TY, HB>;
+    using Hist = HistRaw<SLOTS, CT>;
+    using Rg = TmaRings<HB>;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);  // dynamic smem starts 128-B aligned (checked below)
+    const Geo& g = A.g;
+    const StepParams& sp = A.sp;
+
+    const int lane = threadIdx.x, w = threadIdx.y;
+    const bool tid0 = lane == 0 && w == 0;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TY;
+    const int zs = A.z_lo + blockIdx.z * A.zc;
+    const int ze = min(zs + A.zc, A.z_hi);
+
+    // ---- this thread's cell
+    const bool halo = w == TY + 2;
+    int r, bc, cc, x;
+    if (!halo) {
+        r = w, bc = lane + 4, cc = lane + 1, x = x0 + lane;
+    } else if (lane < 16) {
+        r = lane, bc = 3, cc = 0, x = x0 - 1;
+    } else {
+        r = lane - 16, bc = 36, cc = TMA_CW - 1, x = x0 + 32;
+    }
+    const int y = y0 - 1 + r;
+    // p is needed on rows 0..TY (row 0 feeds D-_y of row 1) and at column x0-1;
+    // q on rows 1..TY+1 and at column x0+32 (halo lanes: owned rows only)
+    const bool needP = halo ? (lane < 16 && r >= 1 && r <= TY) : r <= TY;
+    const bool needQ = halo ? (lane >= 16 && r >= 1 && r <= TY) : r >= 1;
+    const bool own = !halo && r >= 1 && r <= TY;  // owned row (TMA stores clip at nx, ny)
+    const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
+
+    // Every plane of the chunk's sequence is loaded so that each ring slot is filled in
+    // order (mbarrier phase = fill count); planes past the stored range are clamped to
+    // the nearest stored plane (no box is ever entirely out of bounds) -- those values
+    // only feed results that are never used (p at plane nzl, the primal of planes -1 / nzl).
+    const int j0 = zs - 1;  // relative plane index base: plane s <-> j = s - j0
+    auto zclamp = [&](int s) { return min(max(s + 1, 0), g.nzl + 1); };
+    auto issue_u = [&](int s) {
+        const int st = (s - j0) % Rg::NU;
+        mbar_expect_tx(&S.bar_u[st], 2 * R * TMA_BW * 4);
+        tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
+        tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
+    };
+    auto issue_v = [&](int s) {
+        const int st = (s - j0) % Rg::NV;
+        mbar_expect_tx(&S.bar_v[st], 6 * R * TMA_BW * 4);
+        tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
+        tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
+    };
+    auto issue_pq = [&](int s) {
+        const int st = (s - j0) % Rg::NPQ;
+        mbar_expect_tx(&S.bar_pq[st], 9 * R * TMA_BW * 4);
+        tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
+        tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
+    };
+    auto issue_h = [&](int s) {
+        const int st = (s - j0) % Rg::NH;
+        mbar_expect_tx(&S.bar_h[st], TY * 32 * HB);
+        tma_load3(&S.h[st][0][0], &m_h, &S.bar_h[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
+    };
+
+    if (tid0) {
+        if (smem_addr(smem_raw) & 127) __trap();
+        prefetch_map(&m_ld1);
+        prefetch_map(&m_ld3);
+        prefetch_map(&m_ld6);
+        prefetch_map(&m_h);
+        for (int k = 0; k < Rg::NU; ++k) mbar_init(&S.bar_u[k], 1);
+        for (int k = 0; k < Rg::NV; ++k) mbar_init(&S.bar_v[k], 1);
+        for (int k = 0; k < Rg::NPQ; ++k) mbar_init(&S.bar_pq[k], 1);
+        for (int k = 0; k < Rg::NH; ++k) mbar_init(&S.bar_h[k], 1);
+        fence_mbar_init();
+        // prologue: fill all but one slot of every ring (planes zs-1, zs, ...)
+        for (int t = zs - 1; t < zs - 1 + Rg::NU - 1; ++t) issue_u(t);
+        for (int t = zs - 1; t < zs - 1 + Rg::NV - 1; ++t) issue_v(t);
+        for (int t = zs - 1; t < zs - 1 + Rg::NPQ - 1; ++t) issue_pq(t);
+        for (int t = zs - 1; t < zs - 1 + Rg::NH - 1; ++t) issue_h(t);
+    }
+    __syncthreads();
+    mbar_wait(&S.bar_u[0], 0);
+
+    // carried across steps
+    float vbp[3] = {0.f, 0.f, 0.f};  // vbar(s-1)
+    float uk_p = 0.f, vk_p[3] = {0.f, 0.f, 0.f};
+    Hist h_p{};
+    float pn_p[3] = {0.f, 0.f, 0.f}, pz_pp = 0.f, qn_p[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+
+    for (int s = zs - 1; s <= ze; ++s) {
+        const int j = s - j0;
+        const int par = s & 1, pr = par ^ 1;
+        const int su = j % Rg::NU, su1 = (j + 1) % Rg::NU, sv = j % Rg::NV, spq = j % Rg::NPQ, sh = j % Rg::NH;
+        const int zg = g.z0 + s;
+        const bool zl = zg < g.nz - 1, zf = zg > 0;
+
+        mbar_wait(&S.bar_u[su1], ((j + 1) / Rg::NU) & 1);
+        mbar_wait(&S.bar_v[sv], (j / Rg::NV) & 1);
+        mbar_wait(&S.bar_pq[spq], (j / Rg::NPQ) & 1);
+        mbar_wait(&S.bar_h[sh], (j / Rg::NH) & 1);
+
+        // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
+        const float uk = S.u[su][0][r][bc], um = S.u[su][1][r][bc];
+        float vk[3], vb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            vk[k] = S.v[sv][k][r][bc];
+            vb[k] = 2.f * vk[k] - S.v[sv][3 + k][r][bc];
+        }
+        const float ub = 2.f * uk - um;                                  // (a3) ubar(s)
+        const float ub1 = 2.f * S.u[su1][0][r][bc] - S.u[su1][1][r][bc];  // ubar(s+1)
+        float pk[3], qk[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pk[k] = S.pq[spq][k][r][bc];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) qk[m] = S.pq[spq][3 + m][r][bc];
+        Hist hc{};
+        if (own) {
+            const uint8_t* hp = &S.h[sh][r - 1][lane * HB];
+            if constexpr (HB == 8) {
+                const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
+                hc.w[0] = v2.x;
+                hc.w[1] = v2.y;
+            } else {
+#pragma unroll
+                for (int q4 = 0; q4 < HB / 16; ++q4) {
+                    const uint4 v4 = reinterpret_cast<const uint4*>(hp)[q4];
+                    hc.w[4 * q4] = v4.x;
+                    hc.w[4 * q4 + 1] = v4.y;
+                    hc.w[4 * q4 + 2] = v4.z;
+                    hc.w[4 * q4 + 3] = v4.w;
+                }
+            }
+        }
+        S.suv[par][0][r][cc] = ub;
+        S.suv[par][1][r][cc] = vb[0];
+        S.suv[par][2][r][cc] = vb[1];
+        S.suv[par][3][r][cc] = vb[2];
+        if (tid0) tma_wait_read0();  // the previous step's output staging has been read
+        __syncthreads();             // S1
+        if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
+            if (s + Rg::NU - 1 <= ze + 1) issue_u(s + Rg::NU - 1);
+            if (s + Rg::NV - 1 <= ze) issue_v(s + Rg::NV - 1);
+            if (s + Rg::NPQ - 1 <= ze) issue_pq(s + Rg::NPQ - 1);
+            if (s + Rg::NH - 1 <= ze) issue_h(s + Rg::NH - 1);
+        }
+
+        // ---- phase E: (a1) dual D(s)
+        float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (needP) {
+            const float ux = S.suv[par][0][r][cc + 1];
+            const float uy = S.suv[par][0][r + 1][cc];
+            const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
+            pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
+            pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
+            pn[2] = fmaf(sp.sigma, g2 - vb[2], pk[2]);
+            const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
+            pn[0] *= f;
+            pn[1] *= f;
+            pn[2] *= f;
+        }
+        if (needQ) {
+            float dx[3], dy[3], dz[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float vx = S.suv[par][1 + k][r][cc - 1];
+                const float vy = S.suv[par][1 + k][r - 1][cc];
+                dx[k] = (xl ? vb[k] : 0.f) - (xf ? vx : 0.f);
+                dy[k] = (yl ? vb[k] : 0.f) - (yf ? vy : 0.f);
+                dz[k] = (zl ? vb[k] : 0.f) - (zf ? vbp[k] : 0.f);
+            }
+            const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
+                                0.5f * (dz[1] + dy[2])};
+#pragma unroll
+            for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], qk[m]);
+            const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
+                                           2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
+                                       sp.alpha0);
+#pragma unroll
+            for (int m = 0; m < 6; ++m) qn[m] *= f;
+        }
+        S.sr[par][0][r][cc] = pn[0];
+        S.sr[par][1][r][cc] = pn[1];
+        S.sr[par][2][r][cc] = qn[0];
+        S.sr[par][3][r][cc] = qn[3];
+        S.sr[par][4][r][cc] = qn[4];
+        S.sr[par][5][r][cc] = qn[1];
+        S.sr[par][6][r][cc] = qn[5];
+        if (own) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
+        }
+
+        // ---- phase F: (a2) primal Pm(s-1) on owned rows
+        if (own && s - 1 >= zs) {
+            const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
+            const float pxm = S.sr[pr][0][r][cc - 1];
+            const float pym = S.sr[pr][1][r - 1][cc];
+            const float divp = ((xl ? pn_p[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? pn_p[1] : 0.f) - (yf ? pym : 0.f)) +
+                               ((zl1 ? pn_p[2] : 0.f) - (zf1 ? pz_pp : 0.f));
+            const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
+            const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
+            const float w0 = (xl ? qxx - qn_p[0] : 0.f) + (yl ? qyxy - qn_p[3] : 0.f) + (zl1 ? qn[4] - qn_p[4] : 0.f);
+            const float w1 = (xl ? qxy - qn_p[3] : 0.f) + (yl ? qyyy - qn_p[1] : 0.f) + (zl1 ? qn[5] - qn_p[5] : 0.f);
+            const float w2 = (xl ? qxz - qn_p[4] : 0.f) + (yl ? qyyz - qn_p[5] : 0.f) + (zl1 ? qn[2] - qn_p[2] : 0.f);
+            S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uk_p), sp.tl, h_p, A.C);
+            S.out[1][r - 1][lane] = fmaf(sp.tau, pn_p[0] + w0, vk_p[0]);
+            S.out[2][r - 1][lane] = fmaf(sp.tau, pn_p[1] + w1, vk_p[1]);
+            S.out[3][r - 1][lane] = fmaf(sp.tau, pn_p[2] + w2, vk_p[2]);
+        }
+        fence_proxy_async();
+        __syncthreads();  // S2
+        if (tid0) {
+            if (s >= zs && s < ze) {
+                tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
+                tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
+            }
+            if (s - 1 >= zs) {
+                tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
+                tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
+            }
+            tma_commit();
+        }
+
+        // ---- carry
+        pz_pp = pn_p[2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            pn_p[k] = pn[k];
+            vbp[k] = vb[k];
+            vk_p[k] = vk[k];
+        }
+#pragma unroll
+        for (int m = 0; m < 6; ++m) qn_p[m] = qn[m];
+        uk_p = uk;
+        h_p = hc;
+    }
+    if (tid0) tma_wait0();
+}
+
+}  // namespace tgvk

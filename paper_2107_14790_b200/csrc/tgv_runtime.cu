@@ -23,6 +23,7 @@
 
 #include "../../include/tgv.h"
 #include "nccl_api.h"
+#include "tgv_fused_tma.cuh"
 #include "tgv_kernels.cuh"
 
 using namespace tgvk;
@@ -37,7 +38,12 @@ constexpr int slotV(int b, int k) { return 3 + 3 * b + k; }
 constexpr int slotP(int b, int k) { return 12 + 3 * b + k; }
 constexpr int slotQ(int b, int m) { return 18 + 6 * b + m; }  // m: xx yy zz xy xz yz
 
-constexpr int FUSED_TY = 14;  // fused-kernel tile: 30 x 14 owned voxels, 32 x 16 threads
+constexpr int FUSED_TY = 14;  // register fused kernel: 30 x 14 owned voxels, 32 x 16 threads
+constexpr int TMA_TY = 14;    // TMA fused kernel: 32 x 14 owned voxels, 32 x 17 threads (box rows 16 -> 128-B fields)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 enum TimerKind { T_DUAL = 0, T_PRIMAL, T_FUSED, T_ENERGY, T_HALO, T_KINDS };
 
@@ -50,7 +56,9 @@ struct tgv_ctx {
     float lambda = 0, alpha0 = 0, alpha1 = 0, tau = 0, sigma = 0;
     int rank = 0, nranks = 1, device = 0;
     int schedule = TGV_SCHEDULE_FUSED;
-    int fused_zc = 0;  // 0 = automatic
+    int fused_zc = 0;       // 0 = automatic
+    bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
+    CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
     Geo g{};
     int slots = 8;            // histogram slots per voxel
@@ -230,7 +238,8 @@ int launch_split(tgv_ctx* c, int phase /*0 dual, 1 primal*/)
 int fused_zc(const tgv_ctx* c)
 {
     if (c->fused_zc > 0) return c->fused_zc;
-    const int tiles = ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
+    const int tiles = c->fused_tma ? ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY)
+                                   : ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
     const int want = 4 * 148;  // about four waves of one CTA per SM
     int chunks = std::max(1, std::min(c->g.nzl, (want + tiles - 1) / tiles));
     return std::max(1, (c->g.nzl + chunks - 1) / chunks);
@@ -242,11 +251,124 @@ void launch_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
     fused_kernel<FUSED_TY, SLOTS, CT><<<grd, dim3(32, FUSED_TY + 2), 0, c->stream>>>(A);
 }
 
+// ---- TMA descriptors ------------------------------------------------------------
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// state as a 4-D tensor {x: nx, y: ny, plane: nzl+2 (halo'd), slot: NSLOT}; boxes of nf slots
+int make_state_map(tgv_ctx* c, CUtensorMap* m, int bw, int bh, int nf)
+{
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const Geo& g = c->g;
+    cuuint64_t dims[4] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)(g.nzl + 2), (cuuint64_t)NSLOT};
+    cuuint64_t strides[3] = {(cuuint64_t)g.px * 4, (cuuint64_t)g.plane * 4, (cuuint64_t)g.fs * 4};
+    cuuint32_t box[4] = {(cuuint32_t)bw, (cuuint32_t)bh, 1, (cuuint32_t)nf};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->state, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled(state, box %dx%dx%d) = %d", bw, bh, nf, (int)r);
+    return TGV_OK;
+}
+
+// histogram store as 3-D {8 elements per voxel x nx, ny, nzl}, element = bytes-per-voxel / 8
+int make_hist_map(tgv_ctx* c)
+{
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const Geo& g = c->g;
+    const int e = c->slots * c->count_bytes / 8;
+    const CUtensorMapDataType dt = e == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : e == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+    cuuint64_t dims[3] = {(cuuint64_t)8 * g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nzl};
+    cuuint64_t strides[2] = {(cuuint64_t)8 * g.px * e, (cuuint64_t)8 * g.plane * e};
+    cuuint32_t box[3] = {256, (cuuint32_t)TMA_TY, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&c->m_h, dt, 3, const_cast<void*>(hist_ptr(c)), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled(hist) = %d", (int)r);
+    return TGV_OK;
+}
+
+int make_state_maps(tgv_ctx* c)
+{
+    int rc;
+    if ((rc = make_state_map(c, &c->m_ld1, TMA_BW, TMA_TY + 2, 1))) return rc;
+    if ((rc = make_state_map(c, &c->m_ld3, TMA_BW, TMA_TY + 2, 3))) return rc;
+    if ((rc = make_state_map(c, &c->m_ld6, TMA_BW, TMA_TY + 2, 6))) return rc;
+    if ((rc = make_state_map(c, &c->m_st1, 32, TMA_TY, 1))) return rc;
+    if ((rc = make_state_map(c, &c->m_st3, 32, TMA_TY, 3))) return rc;
+    return make_state_map(c, &c->m_st6, 32, TMA_TY, 6);
+}
+
+template <int SLOTS, typename CT>
+int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
+{
+    constexpr int HB = SLOTS * (int)sizeof(CT);
+    const size_t smem = sizeof(TmaSmem<TMA_TY, HB>) + 128;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        attr_set = true;
+    }
+    fused_tma_kernel<TMA_TY, SLOTS, CT><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
+        c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
+    return TGV_OK;
+}
+
+int launch_fused_tma(tgv_ctx* c)
+{
+    const Bufs b = bufs(c->k);
+    TmaArgs A{};
+    A.g = c->g;
+    A.sp = step_params(c);
+    A.C = centers(c);
+    A.z_lo = 0;
+    A.z_hi = c->g.nzl;
+    A.zc = fused_zc(c);
+    A.s_uk = slotU(b.cu);
+    A.s_um = slotU(b.pu);
+    A.s_vk = slotV(b.cu, 0);
+    A.s_vm = slotV(b.pu, 0);
+    A.s_pk = slotP(b.cp, 0);
+    A.s_qk = slotQ(b.cp, 0);
+    A.s_un = slotU(b.nu);
+    A.s_vn = slotV(b.nu, 0);
+    A.s_pn = slotP(b.np, 0);
+    A.s_qn = slotQ(b.np, 0);
+    dim3 grd((c->g.nx + 31) / 32, (c->g.ny + TMA_TY - 1) / TMA_TY, (c->g.nzl + A.zc - 1) / A.zc);
+    int rc;
+    if (c->slots == 8 && c->count_bytes == 1) rc = launch_fused_tma_t<8, uint8_t>(c, A, grd);
+    else if (c->slots == 8) rc = launch_fused_tma_t<8, uint16_t>(c, A, grd);
+    else if (c->count_bytes == 1) rc = launch_fused_tma_t<16, uint8_t>(c, A, grd);
+    else rc = launch_fused_tma_t<16, uint16_t>(c, A, grd);
+    if (rc) return rc;
+    CU(cudaGetLastError());
+    return TGV_OK;
+}
+
 int launch_fused(tgv_ctx* c)
 {
     size_t sl = 0;
     int rc = timer_begin(c, T_FUSED, &sl);
     if (rc) return rc;
+    if (c->fused_tma) {
+        if ((rc = launch_fused_tma(c))) return rc;
+        return timer_end(c, sl);
+    }
     FusedArgs A{};
     A.a = iter_ptrs(c, c->k);
     A.g = c->g;
@@ -493,6 +615,10 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     c->schedule = (int)env_int("TGV_SCHEDULE", TGV_SCHEDULE_FUSED);
     if (c->schedule != TGV_SCHEDULE_SPLIT) c->schedule = TGV_SCHEDULE_FUSED;
     c->fused_zc = (int)env_int("TGV_FUSED_ZC", 0);
+    {
+        const char* impl = getenv("TGV_FUSED_IMPL");
+        c->fused_tma = !(impl && strcmp(impl, "regs") == 0);
+    }
 
     Geo& g = c->g;
     g.nx = (int)L->nx;
@@ -565,6 +691,7 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
             return bail(TGV_EINVAL);
         }
     }
+    if (make_state_maps(c)) return bail(TGV_ECUDA);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
         fail(c, TGV_ECUDA, "create sync failed");
         return bail(TGV_ECUDA);
@@ -638,6 +765,7 @@ int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
         CU(cudaGetLastError());
     }
     c->count_bytes = want8 ? 1 : 2;
+    if ((rc = make_hist_map(c))) return rc;
     rc = init_from_hist(c);
     if (rc) return rc;
     CU(cudaStreamSynchronize(c->stream));
@@ -848,6 +976,7 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     // fused: reads 17 floats + histogram, writes u, v, p, q (13 floats)
     o->bytes_fused = 4 * (17 + 13) + hb;
     o->fused_zc = fused_zc(c);
+    o->fused_tma = c->fused_tma ? 1 : 0;
     o->nranks = c->nranks;
     o->rank = c->rank;
     o->iteration = c->k;

@@ -48,6 +48,7 @@ class tgv_timing(ctypes.Structure):
 class tgv_info_t(ctypes.Structure):
     _fields_ = [("row_pitch", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32),
                 ("count_slots", ctypes.c_int32), ("schedule", ctypes.c_int32), ("fused_zc", ctypes.c_int32),
+                ("fused_tma", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64), ("bytes_fused", ctypes.c_int64),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("iteration", ctypes.c_int64)]
 

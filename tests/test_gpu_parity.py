@@ -138,23 +138,28 @@ def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
     h = synth.random_histograms(shape, 12)
     c = list(oracle.default_centers(8))
     outs = {}
-    for sched in SCHEDULES:
+    for sched, impl in (("fused", "tma"), ("fused", "regs"), ("split", "-")):
         for force16 in ("0", "1"):
             monkeypatch.setenv("TGV_FORCE_U16", force16)
+            monkeypatch.setenv("TGV_FUSED_IMPL", impl)
             s = solver_cls()(shape, c).set_schedule(sched).load(h).iterate(37)
             assert s.info()["count_bytes"] == (2 if force16 == "1" else 1)
-            outs[(sched, force16)] = {f: s.get(f) for f in ("u", "v", "p", "q")}
+            if sched == "fused":
+                assert s.info()["fused_tma"] == (impl == "tma")
+            outs[(sched, impl, force16)] = {f: s.get(f) for f in ("u", "v", "p", "q")}
             s.close()
-    ref = outs[("split", "1")]
+    ref = outs[("split", "-", "1")]
     for key, o in outs.items():
         for f in ("u", "v", "p", "q"):
             assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
 
 
+@pytest.mark.parametrize("impl", ["tma", "regs"])
 @pytest.mark.parametrize("zc", [1, 3, 7, 64])
-def test_fused_chunk_sizes(monkeypatch, zc):
+def test_fused_chunk_sizes(monkeypatch, zc, impl):
     """z-chunk boundaries of the fused kernel (redundant halo planes) do not change the result."""
     monkeypatch.setenv("TGV_FUSED_ZC", str(zc))
+    monkeypatch.setenv("TGV_FUSED_IMPL", impl)
     shape = (45, 31, 26)
     h = synth.random_histograms(shape, 13)
     o, s = pair(shape, h, 30, schedule="fused")
