@@ -20,6 +20,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "tgv_kernels.cuh"
 
 namespace tgvk {
@@ -215,42 +217,63 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
     __syncthreads();
     mbar_wait(&S.bar_u[0], 0);
 
-    // carried across steps
-    float vbp[3] = {0.f, 0.f, 0.f};  // vbar(s-1)
-    float uk_p = 0.f, vk_p[3] = {0.f, 0.f, 0.f};
-    Hist h_p{};
-    float pn_p[3] = {0.f, 0.f, 0.f}, pz_pp = 0.f, qn_p[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // ring cursors (stage index and mbarrier phase of the plane each ring waits for next)
+    struct Cur {
+        int st;
+        uint32_t ph;
+    };
+    Cur cu1{1 % Rg::NU, 0u}, cv{0, 0u}, cpq{0, 0u}, ch{0, 0u};  // u waits for s+1, the others for s
+    int su = 0;                                                 // stage of u at plane s
+    auto adv = [](Cur& c, int n) {
+        if (++c.st == n) {
+            c.st = 0;
+            c.ph ^= 1u;
+        }
+    };
 
-    for (int s = zs - 1; s <= ze; ++s) {
-        const int j = s - j0;
-        const int par = s & 1, pr = par ^ 1;
-        const int su = j % Rg::NU, su1 = (j + 1) % Rg::NU, sv = j % Rg::NV, spq = j % Rg::NPQ, sh = j % Rg::NH;
+    // carried from step s-1 to step s (double-buffered by the 2x-unrolled loop)
+    struct Carry {
+        float vb[3];       // vbar(s-1)
+        float uk, vk[3];   // u_k, v_k at s-1 (the primal of plane s-1)
+        Hist h;            // histogram of s-1
+        float pn[3], pz;   // p_{k+1}(s-1), p_z{k+1}(s-2)
+        float qn[6];       // q_{k+1}(s-1)
+    };
+    Carry ca{}, cb{};
+
+    auto step = [&](auto PAR, int s, const Carry& in, Carry& o) {
+        constexpr int par = decltype(PAR)::value, pr = par ^ 1;
         const int zg = g.z0 + s;
         const bool zl = zg < g.nz - 1, zf = zg > 0;
 
-        mbar_wait(&S.bar_u[su1], ((j + 1) / Rg::NU) & 1);
-        mbar_wait(&S.bar_v[sv], (j / Rg::NV) & 1);
-        mbar_wait(&S.bar_pq[spq], (j / Rg::NPQ) & 1);
-        mbar_wait(&S.bar_h[sh], (j / Rg::NH) & 1);
+        mbar_wait(&S.bar_u[cu1.st], cu1.ph);
+        mbar_wait(&S.bar_v[cv.st], cv.ph);
+        mbar_wait(&S.bar_pq[cpq.st], cpq.ph);
+        mbar_wait(&S.bar_h[ch.st], ch.ph);
 
         // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
-        const float uk = S.u[su][0][r][bc], um = S.u[su][1][r][bc];
+        const float* U0 = &S.u[su][0][r][bc];
+        const float* U1 = &S.u[cu1.st][0][r][bc];
+        const float* V0 = &S.v[cv.st][0][r][bc];
+        const float* PQ = &S.pq[cpq.st][0][r][bc];
+        constexpr int F = R * TMA_BW;  // field stride in a ring slot
+        const float uk = U0[0], um = U0[F];
         float vk[3], vb[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            vk[k] = S.v[sv][k][r][bc];
-            vb[k] = 2.f * vk[k] - S.v[sv][3 + k][r][bc];
+            vk[k] = V0[k * F];
+            vb[k] = 2.f * vk[k] - V0[(3 + k) * F];
         }
-        const float ub = 2.f * uk - um;                                  // (a3) ubar(s)
-        const float ub1 = 2.f * S.u[su1][0][r][bc] - S.u[su1][1][r][bc];  // ubar(s+1)
+        const float ub = 2.f * uk - um;          // (a3) ubar(s)
+        const float ub1 = 2.f * U1[0] - U1[F];   // ubar(s+1)
         float pk[3], qk[6];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) pk[k] = S.pq[spq][k][r][bc];
+        for (int k = 0; k < 3; ++k) pk[k] = PQ[k * F];
 #pragma unroll
-        for (int m = 0; m < 6; ++m) qk[m] = S.pq[spq][3 + m][r][bc];
+        for (int m = 0; m < 6; ++m) qk[m] = PQ[(3 + m) * F];
         Hist hc{};
         if (own) {
-            const uint8_t* hp = &S.h[sh][r - 1][lane * HB];
+            const uint8_t* hp = &S.h[ch.st][r - 1][lane * HB];
             if constexpr (HB == 8) {
                 const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
                 hc.w[0] = v2.x;
@@ -278,6 +301,11 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             if (s + Rg::NPQ - 1 <= ze) issue_pq(s + Rg::NPQ - 1);
             if (s + Rg::NH - 1 <= ze) issue_h(s + Rg::NH - 1);
         }
+        su = cu1.st;
+        adv(cu1, Rg::NU);
+        adv(cv, Rg::NV);
+        adv(cpq, Rg::NPQ);
+        adv(ch, Rg::NH);
 
         // ---- phase E: (a1) dual D(s)
         float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -294,14 +322,16 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             pn[2] *= f;
         }
         if (needQ) {
+            // vbar is exactly 0 outside the grid (TMA zero fill, zero halo planes at the
+            // global z ends), so the "l > 0" guards of D- are implicit
             float dx[3], dy[3], dz[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const float vx = S.suv[par][1 + k][r][cc - 1];
                 const float vy = S.suv[par][1 + k][r - 1][cc];
-                dx[k] = (xl ? vb[k] : 0.f) - (xf ? vx : 0.f);
-                dy[k] = (yl ? vb[k] : 0.f) - (yf ? vy : 0.f);
-                dz[k] = (zl ? vb[k] : 0.f) - (zf ? vbp[k] : 0.f);
+                dx[k] = (xl ? vb[k] : 0.f) - vx;
+                dy[k] = (yl ? vb[k] : 0.f) - vy;
+                dz[k] = (zl ? vb[k] : 0.f) - in.vb[k];
             }
             const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
                                 0.5f * (dz[1] + dy[2])};
@@ -332,17 +362,17 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
             const float pxm = S.sr[pr][0][r][cc - 1];
             const float pym = S.sr[pr][1][r - 1][cc];
-            const float divp = ((xl ? pn_p[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? pn_p[1] : 0.f) - (yf ? pym : 0.f)) +
-                               ((zl1 ? pn_p[2] : 0.f) - (zf1 ? pz_pp : 0.f));
+            const float divp = ((xl ? in.pn[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? in.pn[1] : 0.f) - (yf ? pym : 0.f)) +
+                               ((zl1 ? in.pn[2] : 0.f) - (zf1 ? in.pz : 0.f));
             const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
             const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
-            const float w0 = (xl ? qxx - qn_p[0] : 0.f) + (yl ? qyxy - qn_p[3] : 0.f) + (zl1 ? qn[4] - qn_p[4] : 0.f);
-            const float w1 = (xl ? qxy - qn_p[3] : 0.f) + (yl ? qyyy - qn_p[1] : 0.f) + (zl1 ? qn[5] - qn_p[5] : 0.f);
-            const float w2 = (xl ? qxz - qn_p[4] : 0.f) + (yl ? qyyz - qn_p[5] : 0.f) + (zl1 ? qn[2] - qn_p[2] : 0.f);
-            S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uk_p), sp.tl, h_p, A.C);
-            S.out[1][r - 1][lane] = fmaf(sp.tau, pn_p[0] + w0, vk_p[0]);
-            S.out[2][r - 1][lane] = fmaf(sp.tau, pn_p[1] + w1, vk_p[1]);
-            S.out[3][r - 1][lane] = fmaf(sp.tau, pn_p[2] + w2, vk_p[2]);
+            const float w0 = (xl ? qxx - in.qn[0] : 0.f) + (yl ? qyxy - in.qn[3] : 0.f) + (zl1 ? qn[4] - in.qn[4] : 0.f);
+            const float w1 = (xl ? qxy - in.qn[3] : 0.f) + (yl ? qyyy - in.qn[1] : 0.f) + (zl1 ? qn[5] - in.qn[5] : 0.f);
+            const float w2 = (xl ? qxz - in.qn[4] : 0.f) + (yl ? qyyz - in.qn[5] : 0.f) + (zl1 ? qn[2] - in.qn[2] : 0.f);
+            S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
+            S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
+            S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
+            S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
         }
         fence_proxy_async();
         __syncthreads();  // S2
@@ -358,18 +388,25 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             tma_commit();
         }
 
-        // ---- carry
-        pz_pp = pn_p[2];
+        // ---- carry to step s+1
+        o.pz = in.pn[2];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            pn_p[k] = pn[k];
-            vbp[k] = vb[k];
-            vk_p[k] = vk[k];
+            o.pn[k] = pn[k];
+            o.vb[k] = vb[k];
+            o.vk[k] = vk[k];
         }
 #pragma unroll
-        for (int m = 0; m < 6; ++m) qn_p[m] = qn[m];
-        uk_p = uk;
-        h_p = hc;
+        for (int m = 0; m < 6; ++m) o.qn[m] = qn[m];
+        o.uk = uk;
+        o.h = hc;
+    };
+
+    // steps s = zs-1 .. ze; the shared exchange planes alternate with the step's parity
+    for (int s = zs - 1; s <= ze; s += 2) {
+        step(std::integral_constant<int, 0>{}, s, ca, cb);
+        if (s + 1 > ze) break;
+        step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
     }
     if (tid0) tma_wait0();
 }
