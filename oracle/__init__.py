@@ -51,6 +51,7 @@ def _lib():
     lib.oracle_dual.argtypes = [vp, ctypes.c_int]
     lib.oracle_primal.argtypes = [vp, ctypes.c_int]
     lib.oracle_iterate.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+    lib.oracle_dual_halo.argtypes = [vp]
     lib.oracle_energy.argtypes = [vp, dbl, vp]
     for fn in ("oracle_get", "oracle_set"):
         getattr(lib, fn).argtypes = [vp, ctypes.c_int, vp]
@@ -150,6 +151,10 @@ class Oracle:
 
     def dual(self, threads=1):
         _lib().oracle_dual(self._ptr, threads)
+
+    def dual_halo(self):
+        """Slab mode: recompute p on the bottom halo plane and q on the top one."""
+        _lib().oracle_dual_halo(self._ptr)
 
     def primal(self, threads=1):
         _lib().oracle_primal(self._ptr, threads)

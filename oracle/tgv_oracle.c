@@ -305,6 +305,49 @@ void oracle_primal(oracle_state* s, int threads)
             }
 }
 
+/* Slab mode, single-sweep multi-GPU plan: with the neighbours'
+ * ubar, vbar and p (bottom halo plane zb-1) and ubar, vbar and q (top halo plane
+ * ze) received, recompute the dual step ON the halo planes -- p at zb-1 and q at
+ * ze, the only halo values the primal step reads -- instead of receiving them
+ * after the dual.  The arithmetic is the per-voxel dual of oracle_dual. */
+void oracle_dual_halo(oracle_state* s)
+{
+    const grid_t* g = &s->g;
+    double* vbar[3] = {s->f[F_VBAR0], s->f[F_VBAR0 + 1], s->f[F_VBAR0 + 2]};
+    double* p[3] = {s->f[F_P0], s->f[F_P0 + 1], s->f[F_P0 + 2]};
+    double* q[6];
+    for (int k = 0; k < 6; ++k) q[k] = s->f[F_Q0 + k];
+    if (g->zb > 0) { /* p at plane zb-1 */
+        const int64_t z = g->zb - 1;
+        for (int64_t y = 0; y < g->ny; ++y)
+            for (int64_t x = 0; x < g->nx; ++x) {
+                int64_t i = idx(g, x, y, z);
+                double gu[3], pn[3];
+                grad_at(g, s->f[F_UBAR], x, y, z, gu);
+                for (int k = 0; k < 3; ++k) pn[k] = p[k][i] + s->sigma * (gu[k] - vbar[k][i]);
+                double np = sqrt(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2]);
+                double sp = (np > s->alpha1) ? s->alpha1 / np : 1.0;
+                for (int k = 0; k < 3; ++k) p[k][i] = pn[k] * sp;
+            }
+    }
+    if (g->ze < g->nz) { /* q at plane ze */
+        const int64_t z = g->ze;
+        for (int64_t y = 0; y < g->ny; ++y)
+            for (int64_t x = 0; x < g->nx; ++x) {
+                int64_t i = idx(g, x, y, z);
+                double e[6], qn[6];
+                symgrad_at(g, vbar, x, y, z, e);
+                for (int m = 0; m < 6; ++m) qn[m] = q[m][i] + s->sigma * e[m];
+                double nq2 = 0.0;
+                for (int k = 0; k < 3; ++k)
+                    for (int l = 0; l < 3; ++l) nq2 += qn[QIDX[k][l]] * qn[QIDX[k][l]];
+                double nq = sqrt(nq2);
+                double sq = (nq > s->alpha0) ? s->alpha0 / nq : 1.0;
+                for (int m = 0; m < 6; ++m) q[m][i] = qn[m] * sq;
+            }
+    }
+}
+
 void oracle_iterate(oracle_state* s, int n, int threads)
 {
     for (int it = 0; it < n; ++it) {

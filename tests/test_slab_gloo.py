@@ -1,17 +1,18 @@
-"""Multi-process z-slab decomposition of the scheme on CPU (gloo), world size 2
-and 3 (reading R12, §"Multi-GPU").
+"""Multi-process z-slab decomposition of the scheme on CPU (gloo), world sizes 2
+and 4 with even and uneven cuts (reading R12, §6).
 
 Each rank runs the oracle on its slab [zb, ze) of the global grid, exchanging
-only the minimal one-plane halos of the exchange plan below (all other halo
-components are poisoned with NaN), and the gathered result must equal the
-monolithic run BITWISE.  This pins the halo plan the CUDA runtime implements
-(paper_2107_14790_b200/csrc/tgv_runtime.cu, HALO_* tables):
+only the one-plane halos of an exchange plan (every other halo plane is
+poisoned with NaN), and the gathered result must equal the monolithic run
+BITWISE.  This pins the halo plans the CUDA runtime implements
+(paper_2107_14790_b200/csrc/tgv_runtime.cu, plan_split_a/b, plan_fused,
+plan_energy; in the runtime's representation ubar travels as (u_k, u_{k-1})):
 
-  phase A (before the dual step):  ubar   bottom plane -> rank r-1 (its top halo)
-                                   vbar_k top plane    -> rank r+1 (its bottom halo), k = x, y, z
-  phase B (before the primal step): q_xz, q_yz, q_zz bottom plane -> rank r-1
-                                   p_z   top plane     -> rank r+1
-  energy:                          u, q_xz, q_yz, q_zz bottom -> r-1;  v_k, p_z top -> r+1
+  SPLIT, before the dual:   ubar bottom plane -> rank r-1;  vbar(3) top plane -> rank r+1
+  SPLIT, before the primal: q_xz, q_yz, q_zz bottom -> r-1;  p_z top -> r+1
+  FUSED, once per iteration: ubar, vbar(3), q(6) bottom -> r-1;  ubar, vbar(3), p(3) top -> r+1,
+                             then the dual is recomputed on the halo planes (p below, q above)
+  energy:                   u, q_xz, q_yz, q_zz bottom -> r-1;  v(3), p_z top -> r+1
 """
 import os
 import socket
@@ -25,8 +26,13 @@ import torch.multiprocessing as mp
 import oracle
 import synth
 
+# SPLIT plan: two exchanges per iteration
 PHASE_A = {"down": [("ubar", 0)], "up": [("vbar", 0), ("vbar", 1), ("vbar", 2)]}
 PHASE_B = {"down": [("q", 4), ("q", 5), ("q", 2)], "up": [("p", 2)]}
+# FUSED plan: one exchange per iteration; the dual is then recomputed on the halo planes
+# (p at the bottom halo, q at the top halo), as the single-sweep kernel does
+FUSED = {"down": [("ubar", 0), ("vbar", 0), ("vbar", 1), ("vbar", 2)] + [("q", m) for m in range(6)],
+         "up": [("ubar", 0), ("vbar", 0), ("vbar", 1), ("vbar", 2), ("p", 0), ("p", 1), ("p", 2)]}
 ENERGY = {"down": [("u", 0), ("q", 4), ("q", 5), ("q", 2)], "up": [("v", 0), ("v", 1), ("v", 2), ("p", 2)]}
 
 
@@ -72,7 +78,7 @@ def poison_halos(o):
             o.set_plane(name, comp, o.ze, nan)
 
 
-def _worker(rank, world, port, shape, cuts, iters, outdir):
+def _worker(rank, world, port, shape, cuts, iters, outdir, plan="split"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -81,10 +87,16 @@ def _worker(rank, world, port, shape, cuts, iters, outdir):
     o = oracle.Oracle(shape, zb=zb, ze=ze).load(h)
     poison_halos(o)
     for _ in range(iters):
-        exchange(o, PHASE_A, rank, world)
-        o.dual()
-        exchange(o, PHASE_B, rank, world)
-        o.primal()
+        if plan == "split":
+            exchange(o, PHASE_A, rank, world)
+            o.dual()
+            exchange(o, PHASE_B, rank, world)
+            o.primal()
+        else:
+            exchange(o, FUSED, rank, world)
+            o.dual()
+            o.dual_halo()
+            o.primal()
     exchange(o, ENERGY, rank, world)
     e = o.energy()
     sums = torch.tensor([e["alpha1"], e["alpha0"], e["data"], e["dual"]], dtype=torch.float64)
@@ -97,11 +109,12 @@ def _worker(rank, world, port, shape, cuts, iters, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cuts", [[0, 8, 16], [0, 4, 8, 12, 16], [0, 1, 5, 6, 16]][:3])
-def test_slab_equals_monolithic_bitwise(tmp_path, cuts):
+@pytest.mark.parametrize("plan", ["split", "fused"])
+@pytest.mark.parametrize("cuts", [[0, 8, 16], [0, 4, 8, 12, 16], [0, 1, 5, 6, 16]])
+def test_slab_equals_monolithic_bitwise(tmp_path, cuts, plan):
     shape, iters = (7, 6, 16), 25
     world = len(cuts) - 1
-    mp.spawn(_worker, args=(world, _free_port(), shape, cuts, iters, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), shape, cuts, iters, str(tmp_path), plan), nprocs=world, join=True)
     ref = oracle.Oracle(shape).load(synth.random_histograms(shape, 3)).iterate(iters)
     parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
     for name in ("u", "v", "p", "q"):
