@@ -185,6 +185,27 @@ int tgv_write_field(tgv_ctx* ctx, int field, const float* in, int64_t n_voxels);
  * Errors: TGV_EINVAL (NULL), TGV_ESTATE, TGV_ECUDA, TGV_ENCCL. */
 int tgv_energy(tgv_ctx* ctx, double out[6]);
 
+/* In-process slab group: n contexts for the z-slabs layouts[0..n-1] of ONE grid
+ * (same nx, ny, nz; slabs tile [0, nz) in order), created in this process on
+ * devices[0..n-1] (several slabs may share a device).  Members exchange their
+ * one-plane halos by device-to-device copies (peer copies over NVLink between
+ * GPUs), with the same halo plans as the NCCL path; the result is
+ * bitwise equal to one context over the whole grid.  out receives n contexts.
+ * Per-member calls (load, reset, read, write, info, timing, schedule) work as
+ * usual; iterate and energy go through tgv_group_iterate / tgv_group_energy
+ * (tgv_iterate / tgv_energy on a member return TGV_ESTATE).
+ * Errors: TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA. */
+int tgv_create_group(const tgv_layout* layouts, const tgv_params* params, int n, const int* devices,
+                     tgv_ctx** out);
+
+/* n >= 0 iterations of every member of a group (members passed in rank order,
+ * all loaded, same schedule and iteration count).  Blocks until done. */
+int tgv_group_iterate(tgv_ctx* const* members, int n, int32_t iterations);
+
+/* Energy of the whole grid of a group (same out[6] as tgv_energy), members'
+ * partial sums added on the host in rank order. */
+int tgv_group_energy(tgv_ctx* const* members, int n, double out[6]);
+
 /* Select the iteration schedule (TGV_SCHEDULE_FUSED, the default, or
  * TGV_SCHEDULE_SPLIT; the environment variable TGV_SCHEDULE sets the default at
  * create).  The state is shared, so switching keeps the current iterate.

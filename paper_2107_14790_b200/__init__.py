@@ -6,6 +6,6 @@ binding.  Importing this package raises if the library is not built: there is
 no CPU fallback.
 """
 from . import tgv  # noqa: F401  (loads lib/libtgv.so or raises)
-from .tgv import Solver, TgvError  # noqa: F401
+from .tgv import Group, Solver, TgvError  # noqa: F401
 
-__all__ = ["tgv", "Solver", "TgvError"]
+__all__ = ["tgv", "Solver", "Group", "TgvError"]

@@ -77,6 +77,9 @@ struct tgv_ctx {
 
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    // in-process slab group (tgv_create_group): members exchange halos by device copies
+    std::vector<tgv_ctx*>* group = nullptr;  // shared by the members, owned by the last one destroyed
+    cudaEvent_t ev_step = nullptr;           // recorded after each of this member's sweeps
     const NcclApi* nccl = nullptr;  // resolved at create when nranks > 1
 
     bool loaded = false;
@@ -556,8 +559,8 @@ int tgv_get_unique_id(uint8_t uid[128])
     return TGV_OK;
 }
 
-int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, const uint8_t* uid, int dev,
-               tgv_ctx** out)
+static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int nranks, const uint8_t* uid, int dev,
+                       bool grouped, tgv_ctx** out)
 {
     tgv_ctx* c = nullptr;
     g_create_error[0] = 0;
@@ -576,7 +579,7 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     if (L->brick[0] || L->brick[1] || L->brick[2])
         return fail(c, TGV_EINVAL, "brick layouts are not supported (brick must be {0,0,0})");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TGV_EINVAL, "bad rank %d / nranks %d", rank, nranks);
-    if ((nranks == 1) != (uid == nullptr)) return fail(c, TGV_EINVAL, "uid must be NULL iff nranks == 1");
+    if (!grouped && (nranks == 1) != (uid == nullptr)) return fail(c, TGV_EINVAL, "uid must be NULL iff nranks == 1");
     if (nranks == 1 && (L->z_begin != 0 || L->z_end != L->nz))
         return fail(c, TGV_EINVAL, "single rank must own the whole grid");
     if (P->nbins < 1 || P->nbins > 16) return fail(c, TGV_EINVAL, "nbins must be in [1, 16]");
@@ -656,7 +659,7 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
         return bail(TGV_ECUDA);
     }
 
-    if (nranks > 1) {
+    if (nranks > 1 && !grouped) {
         const NcclApi* nccl = c->nccl = nccl_api(c->err, sizeof c->err);
         if (!nccl) return bail(TGV_ENCCL);
         ncclUniqueId id;
@@ -692,12 +695,22 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
         }
     }
     if (make_state_maps(c)) return bail(TGV_ECUDA);
+    if (cudaEventCreateWithFlags(&c->ev_step, cudaEventDisableTiming) != cudaSuccess) {
+        fail(c, TGV_ECUDA, "event creation failed");
+        return bail(TGV_ECUDA);
+    }
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
         fail(c, TGV_ECUDA, "create sync failed");
         return bail(TGV_ECUDA);
     }
     *out = c;
     return TGV_OK;
+}
+
+int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, const uint8_t* uid, int dev,
+               tgv_ctx** out)
+{
+    return create_impl(L, P, rank, nranks, uid, dev, false, out);
 }
 
 int tgv_set_schedule(tgv_ctx* c, int schedule)
@@ -790,6 +803,7 @@ int tgv_iterate(tgv_ctx* c, int32_t n)
     if (rc) return rc;
     if (n < 0) return fail(c, TGV_EINVAL, "n < 0");
     if (!c->loaded) return fail(c, TGV_ESTATE, "iterate before load");
+    if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_iterate");
     for (int32_t it = 0; it < n; ++it) {
         if (c->schedule == TGV_SCHEDULE_SPLIT) {
             if ((rc = halo_exchange(c, plan_split_a(c->k)))) return rc;
@@ -881,13 +895,9 @@ int tgv_write_field(tgv_ctx* c, int f, const float* in, int64_t n)
     return TGV_OK;
 }
 
-int tgv_energy(tgv_ctx* c, double out[6])
+static int energy_launch(tgv_ctx* c)
 {
-    int rc = check_ready(c);
-    if (rc) return rc;
-    if (!out) return fail(c, TGV_EINVAL, "out is NULL");
-    if (!c->loaded) return fail(c, TGV_ESTATE, "energy before load");
-    if ((rc = halo_exchange(c, plan_energy(c->k)))) return rc;
+    int rc;
     size_t sl = 0;
     if ((rc = timer_begin(c, T_ENERGY, &sl))) return rc;
     const Bufs b = bufs(c->k);
@@ -911,7 +921,30 @@ int tgv_energy(tgv_ctx* c, double out[6])
     CU(cudaGetLastError());
     energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, c->energy_blocks, c->d_out);
     CU(cudaGetLastError());
-    if ((rc = timer_end(c, sl))) return rc;
+    return timer_end(c, sl);
+}
+
+// {alpha1, alpha0, data, dual, vmax} sums -> ABI out[6]
+static void energy_out(const double h[EN_TERMS], double out[6])
+{
+    const double E = h[0] + h[1] + h[2];
+    out[0] = E;
+    out[1] = h[0];
+    out[2] = h[1];
+    out[3] = h[2];
+    out[4] = E - h[3];
+    out[5] = h[4];
+}
+
+int tgv_energy(tgv_ctx* c, double out[6])
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!out) return fail(c, TGV_EINVAL, "out is NULL");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "energy before load");
+    if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_energy");
+    if ((rc = halo_exchange(c, plan_energy(c->k)))) return rc;
+    if ((rc = energy_launch(c))) return rc;
     if (c->nranks > 1) {
         const NcclApi* nccl = c->nccl;
         NC(nccl->AllReduce(c->d_out, c->d_out, 4, ncclFloat64, ncclSum, c->comm, c->stream));
@@ -920,13 +953,173 @@ int tgv_energy(tgv_ctx* c, double out[6])
     double h[EN_TERMS];
     CU(cudaMemcpyAsync(h, c->d_out, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     if ((rc = sync_stream(c))) return rc;
-    const double E = h[0] + h[1] + h[2];
-    out[0] = E;
-    out[1] = h[0];
-    out[2] = h[1];
-    out[3] = h[2];
-    out[4] = E - h[3];
-    out[5] = h[4];
+    energy_out(h, out);
+    return TGV_OK;
+}
+
+// ============================================================================
+// in-process slab groups
+// ============================================================================
+// every member waits for its neighbours' last recorded step, then copies the
+// neighbours' boundary planes of the plan's slots into its halo planes
+static int group_exchange(tgv_ctx* const* m, int n, const HaloPlan& hp)
+{
+    for (int r = 0; r < n; ++r) {
+        tgv_ctx* c = m[r];
+        CU(cudaSetDevice(c->device));
+        size_t sl = 0;
+        int rc = timer_begin(c, T_HALO, &sl);
+        if (rc) return rc;
+        const size_t bytes = sizeof(float) * (size_t)c->g.plane;
+        if (r + 1 < n) {  // top halo <- bottom plane of r+1
+            tgv_ctx* o = m[r + 1];
+            CU(cudaStreamWaitEvent(c->stream, o->ev_step, 0));
+            for (int k = 0; k < hp.ndown; ++k)
+                CU(cudaMemcpyPeerAsync(plane_ptr(c, hp.down[k], c->g.nzl), c->device, plane_ptr(o, hp.down[k], 0),
+                                       o->device, bytes, c->stream));
+        }
+        if (r > 0) {  // bottom halo <- top plane of r-1
+            tgv_ctx* o = m[r - 1];
+            CU(cudaStreamWaitEvent(c->stream, o->ev_step, 0));
+            for (int k = 0; k < hp.nup; ++k)
+                CU(cudaMemcpyPeerAsync(plane_ptr(c, hp.up[k], -1), c->device, plane_ptr(o, hp.up[k], o->g.nzl - 1),
+                                       o->device, bytes, c->stream));
+        }
+        if ((rc = timer_end(c, sl))) return rc;
+    }
+    return TGV_OK;
+}
+
+static int group_record(tgv_ctx* const* m, int n)
+{
+    for (int r = 0; r < n; ++r) {
+        tgv_ctx* c = m[r];
+        CU(cudaSetDevice(c->device));
+        CU(cudaEventRecord(c->ev_step, c->stream));
+    }
+    return TGV_OK;
+}
+
+static int group_check(tgv_ctx* const* m, int n)
+{
+    if (!m || n < 1) return TGV_EINVAL;
+    for (int r = 0; r < n; ++r) {
+        int rc = check_ready(m[r]);
+        if (rc) return rc;
+        tgv_ctx* c = m[r];
+        if (!c->group || (int)c->group->size() != n || (*c->group)[r] != c)
+            return fail(c, TGV_EINVAL, "contexts are not the members of one group, in rank order");
+        if (!c->loaded) return fail(c, TGV_ESTATE, "group member %d not loaded", r);
+        if (c->k != m[0]->k || c->schedule != m[0]->schedule)
+            return fail(c, TGV_ESTATE, "group members at different iterations or schedules");
+    }
+    return TGV_OK;
+}
+
+int tgv_create_group(const tgv_layout* layouts, const tgv_params* P, int n, const int* devices, tgv_ctx** out)
+{
+    tgv_ctx* c = nullptr;
+    g_create_error[0] = 0;
+    if (!layouts || !out || !devices || n < 1) return fail(c, TGV_EINVAL, "NULL argument or n < 1");
+    for (int r = 0; r < n; ++r) out[r] = nullptr;
+    for (int r = 0; r < n; ++r) {
+        const tgv_layout& L = layouts[r];
+        if (L.nx != layouts[0].nx || L.ny != layouts[0].ny || L.nz != layouts[0].nz)
+            return fail(c, TGV_EINVAL, "group members must share nx, ny, nz");
+        if ((r == 0 && L.z_begin != 0) || (r > 0 && L.z_begin != layouts[r - 1].z_end) ||
+            (r == n - 1 && L.z_end != L.nz))
+            return fail(c, TGV_EINVAL, "group slabs must tile [0, nz) in order");
+    }
+    auto* grp = new (std::nothrow) std::vector<tgv_ctx*>((size_t)n, nullptr);
+    if (!grp) return fail(c, TGV_ENOMEM, "host allocation failed");
+    for (int r = 0; r < n; ++r) {
+        int rc = create_impl(&layouts[r], P, r, n, nullptr, devices[r], true, &out[r]);
+        if (rc) {
+            for (int k = 0; k < r; ++k) {
+                out[k]->group = nullptr;
+                tgv_destroy(out[k]);
+                out[k] = nullptr;
+            }
+            delete grp;
+            return rc;
+        }
+        (*grp)[r] = out[r];
+        out[r]->group = grp;
+    }
+    for (int r = 0; r < n; ++r)  // peer access between distinct devices (NVLink copies)
+        for (int o = 0; o < n; ++o)
+            if (devices[r] != devices[o]) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, devices[r], devices[o]);
+                if (can) {
+                    cudaSetDevice(devices[r]);
+                    cudaError_t e = cudaDeviceEnablePeerAccess(devices[o], 0);
+                    if (e != cudaSuccess) cudaGetLastError();  // already enabled
+                }
+            }
+    return TGV_OK;
+}
+
+int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
+{
+    int rc = group_check(m, n);
+    if (rc) return rc;
+    if (iters < 0) return fail(m[0], TGV_EINVAL, "n < 0");
+    tgv_ctx* c = m[0];
+    CU(cudaSetDevice(c->device));
+    if ((rc = group_record(m, n))) return rc;  // the current state is each member's last step
+    for (int32_t it = 0; it < iters; ++it) {
+        const int64_t k = m[0]->k;
+        if (m[0]->schedule == TGV_SCHEDULE_SPLIT) {
+            if ((rc = group_exchange(m, n, plan_split_a(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_split(m[r], 0))) return rc;
+            }
+            if ((rc = group_record(m, n))) return rc;
+            if ((rc = group_exchange(m, n, plan_split_b(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_split(m[r], 1))) return rc;
+            }
+        } else {
+            if ((rc = group_exchange(m, n, plan_fused(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_fused(m[r]))) return rc;
+            }
+        }
+        if ((rc = group_record(m, n))) return rc;
+        for (int r = 0; r < n; ++r) m[r]->k += 1;
+    }
+    for (int r = 0; r < n; ++r) {
+        c = m[r];
+        CU(cudaSetDevice(c->device));
+        if ((rc = sync_stream(c))) return rc;
+    }
+    return TGV_OK;
+}
+
+int tgv_group_energy(tgv_ctx* const* m, int n, double out[6])
+{
+    int rc = group_check(m, n);
+    if (rc) return rc;
+    if (!out) return fail(m[0], TGV_EINVAL, "out is NULL");
+    tgv_ctx* c = m[0];
+    if ((rc = group_record(m, n))) return rc;
+    if ((rc = group_exchange(m, n, plan_energy(m[0]->k)))) return rc;
+    double tot[EN_TERMS] = {0, 0, 0, 0, 0};
+    for (int r = 0; r < n; ++r) {  // fixed rank order: deterministic
+        c = m[r];
+        CU(cudaSetDevice(c->device));
+        if ((rc = energy_launch(c))) return rc;
+        double h[EN_TERMS];
+        CU(cudaMemcpyAsync(h, c->d_out, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+        if ((rc = sync_stream(c))) return rc;
+        for (int t = 0; t < 4; ++t) tot[t] += h[t];
+        tot[4] = std::max(tot[4], h[4]);
+    }
+    energy_out(tot, out);
     return TGV_OK;
 }
 
@@ -988,6 +1181,16 @@ void tgv_destroy(tgv_ctx* c)
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->group) {  // leave the group; the last member frees the member table
+        bool last = true;
+        for (auto& mbr : *c->group) {
+            if (mbr == c) mbr = nullptr;
+            else if (mbr) last = false;
+        }
+        if (last) delete c->group;
+        c->group = nullptr;
+    }
+    if (c->ev_step) cudaEventDestroy(c->ev_step);
     if (c->comm) {
         const NcclApi* nccl = c->nccl;
         if (c->poisoned)

@@ -24,7 +24,8 @@ FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 
 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
            "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_timing", "tgv_get_timing", "tgv_info",
-           "tgv_destroy", "tgv_status_string", "tgv_last_error"]
+           "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
+           "tgv_group_energy"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -72,6 +73,10 @@ def _load():
     lib.tgv_set_timing.argtypes = [vp, ctypes.c_int]
     lib.tgv_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
     lib.tgv_info.argtypes = [vp, ctypes.POINTER(tgv_info_t)]
+    lib.tgv_create_group.argtypes = [ctypes.POINTER(tgv_layout), ctypes.POINTER(tgv_params), ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]
+    lib.tgv_group_iterate.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i32]
+    lib.tgv_group_energy.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp]
     lib.tgv_destroy.argtypes = [vp]
     lib.tgv_destroy.restype = None
     lib.tgv_status_string.argtypes = [ctypes.c_int]
@@ -190,7 +195,96 @@ def tgv_destroy(ctx):
     lib.tgv_destroy(ctx)
 
 
-# ---- convenience wrapper ---------------------------------------------------------
+def _params(centers, lam, alpha0, alpha1, tau, sigma):
+    c = (ctypes.c_float * len(centers))(*[float(x) for x in centers])
+    return tgv_params(len(centers), ctypes.cast(c, ctypes.POINTER(ctypes.c_float)), lam, alpha0, alpha1, tau,
+                      sigma), c
+
+
+def tgv_create_group(shape, cuts, centers, lam, alpha0, alpha1, tau, sigma, devices):
+    nx, ny, nz = shape
+    n = len(cuts) - 1
+    L = (tgv_layout * n)(*[tgv_layout(nx, ny, nz, cuts[r], cuts[r + 1], (ctypes.c_int32 * 3)(0, 0, 0))
+                           for r in range(n)])
+    P, keep = _params(centers, lam, alpha0, alpha1, tau, sigma)
+    dev = (ctypes.c_int * n)(*devices)
+    out = (ctypes.c_void_p * n)()
+    _check(lib.tgv_create_group(L, ctypes.byref(P), n, dev, out))
+    return [ctypes.c_void_p(out[r]) for r in range(n)]
+
+
+def _ctx_array(ctxs):
+    return (ctypes.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+
+
+def tgv_group_iterate(ctxs, n_iter: int):
+    _check(lib.tgv_group_iterate(_ctx_array(ctxs), len(ctxs), int(n_iter)), ctxs[0])
+
+
+def tgv_group_energy(ctxs) -> np.ndarray:
+    out = np.zeros(6, dtype=np.float64)
+    _check(lib.tgv_group_energy(_ctx_array(ctxs), len(ctxs), out.ctypes.data), ctxs[0])
+    return out
+
+
+# ---- convenience wrappers ---------------------------------------------------------
+class Group:
+    """z-slabs [cuts[r], cuts[r+1]) of one grid in this process (tgv_create_group)."""
+
+    def __init__(self, shape, cuts, centers, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25, devices=None):
+        self.shape, self.cuts = tuple(shape), list(cuts)
+        n = len(cuts) - 1
+        self.ctxs = tgv_create_group(shape, cuts, centers, lam, alpha0, alpha1, tau, sigma,
+                                     devices if devices is not None else [0] * n)
+
+    def set_schedule(self, schedule):
+        for c in self.ctxs:
+            tgv_set_schedule(c, {"fused": SCHEDULE_FUSED, "split": SCHEDULE_SPLIT}.get(schedule, schedule))
+        return self
+
+    def load(self, counts):
+        """counts: the WHOLE grid's uint32 [nz, ny, nx, nbins]; each member loads its slab."""
+        for r, c in enumerate(self.ctxs):
+            tgv_load_histograms(c, np.ascontiguousarray(counts[self.cuts[r]:self.cuts[r + 1]]))
+        return self
+
+    def iterate(self, n: int):
+        tgv_group_iterate(self.ctxs, n)
+        return self
+
+    def read_u(self):
+        nx, ny, _ = self.shape
+        parts = []
+        for r, c in enumerate(self.ctxs):
+            out = np.empty((self.cuts[r + 1] - self.cuts[r], ny, nx), np.float32)
+            parts.append(tgv_read_u(c, out))
+        return np.concatenate(parts, axis=0)
+
+    def get(self, name):
+        nx, ny, _ = self.shape
+        ids = FIELDS[name]
+        parts = []
+        for r, c in enumerate(self.ctxs):
+            out = np.empty((len(ids), self.cuts[r + 1] - self.cuts[r], ny, nx), np.float32)
+            for k, f in enumerate(ids):
+                tgv_read_field(c, f, out[k])
+            parts.append(out)
+        res = np.concatenate(parts, axis=1)
+        return res[0] if len(ids) == 1 else res
+
+    def energy(self) -> dict:
+        e = tgv_group_energy(self.ctxs)
+        return {"E": e[0], "alpha1": e[1], "alpha0": e[2], "data": e[3], "gap": e[4], "vmax": e[5]}
+
+    def close(self):
+        for c in getattr(self, "ctxs", []):
+            tgv_destroy(c)
+        self.ctxs = []
+
+    def __del__(self):
+        self.close()
+
+
 class Solver:
     """One context on one GPU owning z-slab [z_begin, z_end) of an (nx, ny, nz) grid.
 
