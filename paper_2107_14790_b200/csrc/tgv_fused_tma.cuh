@@ -122,6 +122,8 @@ struct TmaArgs {
     StepParams sp;
     Centers C;
     int z_lo, z_hi, zc;
+    const int4* sched;      // segments (tile, z_begin, z_end, -) of all CTAs, see tma_schedule()
+    const int* sched_off;   // CTA b owns sched[sched_off[b] .. sched_off[b+1])
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
 };
@@ -145,57 +147,22 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
 
     const int lane = threadIdx.x, w = threadIdx.y;
     const bool tid0 = lane == 0 && w == 0;
-    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * TY;
-    const int zs = A.z_lo + blockIdx.z * A.zc;
-    const int ze = min(zs + A.zc, A.z_hi);
-
-    // ---- this thread's cell
     const bool halo = w == TY + 2;
-    int r, bc, cc, x;
-    if (!halo) {
-        r = w, bc = lane + 4, cc = lane + 1, x = x0 + lane;
-    } else if (lane < 16) {
-        r = lane, bc = 3, cc = 0, x = x0 - 1;
-    } else {
-        r = lane - 16, bc = 36, cc = TMA_CW - 1, x = x0 + 32;
-    }
-    const int y = y0 - 1 + r;
-    // p is needed on rows 0..TY (row 0 feeds D-_y of row 1) and at column x0-1;
-    // q on rows 1..TY+1 and at column x0+32 (halo lanes: owned rows only)
-    const bool needP = halo ? (lane < 16 && r >= 1 && r <= TY) : r <= TY;
-    const bool needQ = halo ? (lane >= 16 && r >= 1 && r <= TY) : r >= 1;
-    const bool own = !halo && r >= 1 && r <= TY;  // owned row (TMA stores clip at nx, ny)
-    const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
 
-    // Every plane of the chunk's sequence is loaded so that each ring slot is filled in
-    // order (mbarrier phase = fill count); planes past the stored range are clamped to
-    // the nearest stored plane (no box is ever entirely out of bounds) -- those values
-    // only feed results that are never used (p at plane nzl, the primal of planes -1 / nzl).
-    const int j0 = zs - 1;  // relative plane index base: plane s <-> j = s - j0
-    auto zclamp = [&](int s) { return min(max(s + 1, 0), g.nzl + 1); };
-    auto issue_u = [&](int s) {
-        const int st = (s - j0) % Rg::NU;
-        mbar_expect_tx(&S.bar_u[st], 2 * R * TMA_BW * 4);
-        tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
-        tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
+    // ring cursors: next slot to fill (issue side) and next slot / phase to wait for.
+    // Fills and waits happen in the same order on every ring, across all segments.
+    struct Cur {
+        int st;
+        uint32_t ph;
     };
-    auto issue_v = [&](int s) {
-        const int st = (s - j0) % Rg::NV;
-        mbar_expect_tx(&S.bar_v[st], 6 * R * TMA_BW * 4);
-        tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
-        tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
+    auto adv = [](Cur& c, int n) {
+        if (++c.st == n) {
+            c.st = 0;
+            c.ph ^= 1u;
+        }
     };
-    auto issue_pq = [&](int s) {
-        const int st = (s - j0) % Rg::NPQ;
-        mbar_expect_tx(&S.bar_pq[st], 9 * R * TMA_BW * 4);
-        tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
-        tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
-    };
-    auto issue_h = [&](int s) {
-        const int st = (s - j0) % Rg::NH;
-        mbar_expect_tx(&S.bar_h[st], TY * 32 * HB);
-        tma_load3(&S.h[st][0][0], &m_h, &S.bar_h[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
-    };
+    Cur iu{0, 0u}, iv{0, 0u}, ipq{0, 0u}, ih{0, 0u};  // issue cursors (tid0 only)
+    Cur cu{0, 0u}, cv{0, 0u}, cpq{0, 0u}, ch{0, 0u};  // wait cursors (all threads)
 
     if (tid0) {
         if (smem_addr(smem_raw) & 127) __trap();
@@ -208,205 +175,258 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         for (int k = 0; k < Rg::NPQ; ++k) mbar_init(&S.bar_pq[k], 1);
         for (int k = 0; k < Rg::NH; ++k) mbar_init(&S.bar_h[k], 1);
         fence_mbar_init();
-        // prologue: fill all but one slot of every ring (planes zs-1, zs, ...)
-        for (int t = zs - 1; t < zs - 1 + Rg::NU - 1; ++t) issue_u(t);
-        for (int t = zs - 1; t < zs - 1 + Rg::NV - 1; ++t) issue_v(t);
-        for (int t = zs - 1; t < zs - 1 + Rg::NPQ - 1; ++t) issue_pq(t);
-        for (int t = zs - 1; t < zs - 1 + Rg::NH - 1; ++t) issue_h(t);
     }
     __syncthreads();
-    mbar_wait(&S.bar_u[0], 0);
 
-    // ring cursors (stage index and mbarrier phase of the plane each ring waits for next)
-    struct Cur {
-        int st;
-        uint32_t ph;
-    };
-    Cur cu1{1 % Rg::NU, 0u}, cv{0, 0u}, cpq{0, 0u}, ch{0, 0u};  // u waits for s+1, the others for s
-    int su = 0;                                                 // stage of u at plane s
-    auto adv = [](Cur& c, int n) {
-        if (++c.st == n) {
-            c.st = 0;
-            c.ph ^= 1u;
+    // Persistent CTA: it runs the segments (one tile over a z-range) the host schedule
+    // assigned to it -- whole z-chunks round-robin over the CTAs, so that all CTAs
+    // advance through the chunks together and neighbouring tiles' halos stay in L2,
+    // and the chunks that do not fill a last round split evenly over all CTAs.
+    const int tiles_x = (g.nx + 31) / 32;
+    for (int sgi = A.sched_off[blockIdx.x]; sgi < A.sched_off[blockIdx.x + 1]; ++sgi) {
+        const int4 sg = A.sched[sgi];
+        const int t = sg.x, zs = sg.y, ze = sg.z;
+        const int x0 = (t % tiles_x) * 32, y0 = (t / tiles_x) * TY;
+
+        // ---- this thread's cell
+        int r, bc, cc, x;
+        if (!halo) {
+            r = w, bc = lane + 4, cc = lane + 1, x = x0 + lane;
+        } else if (lane < 16) {
+            r = lane, bc = 3, cc = 0, x = x0 - 1;
+        } else {
+            r = lane - 16, bc = 36, cc = TMA_CW - 1, x = x0 + 32;
         }
-    };
+        const int y = y0 - 1 + r;
+        // p is needed on rows 0..TY (row 0 feeds D-_y of row 1) and at column x0-1;
+        // q on rows 1..TY+1 and at column x0+32 (halo lanes: owned rows only)
+        const bool needP = halo ? (lane < 16 && r >= 1 && r <= TY) : r <= TY;
+        const bool needQ = halo ? (lane >= 16 && r >= 1 && r <= TY) : r >= 1;
+        const bool own = !halo && r >= 1 && r <= TY;  // owned row (TMA stores clip at nx, ny)
+        const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
 
-    // carried from step s-1 to step s (double-buffered by the 2x-unrolled loop)
-    struct Carry {
-        float vb[3];       // vbar(s-1)
-        float uk, vk[3];   // u_k, v_k at s-1 (the primal of plane s-1)
-        Hist h;            // histogram of s-1
-        float pn[3], pz;   // p_{k+1}(s-1), p_z{k+1}(s-2)
-        float qn[6];       // q_{k+1}(s-1)
-    };
-    Carry ca{}, cb{};
+        // Every plane of the segment's sequence is loaded so that each ring slot is
+        // filled in order (mbarrier phase = fill count); planes past the stored range are
+        // clamped to the nearest stored plane (no box is ever entirely out of bounds) --
+        // those values only feed results that are never used (p at plane nzl, the primal
+        // of planes -1 / nzl).
+        auto zclamp = [&](int s) { return min(max(s + 1, 0), g.nzl + 1); };
+        auto issue_u = [&](int s) {
+            const int st = iu.st;
+            adv(iu, Rg::NU);
+            mbar_expect_tx(&S.bar_u[st], 2 * R * TMA_BW * 4);
+            tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
+            tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
+        };
+        auto issue_v = [&](int s) {
+            const int st = iv.st;
+            adv(iv, Rg::NV);
+            mbar_expect_tx(&S.bar_v[st], 6 * R * TMA_BW * 4);
+            tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
+            tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
+        };
+        auto issue_pq = [&](int s) {
+            const int st = ipq.st;
+            adv(ipq, Rg::NPQ);
+            mbar_expect_tx(&S.bar_pq[st], 9 * R * TMA_BW * 4);
+            tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
+            tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
+        };
+        auto issue_h = [&](int s) {
+            const int st = ih.st;
+            adv(ih, Rg::NH);
+            mbar_expect_tx(&S.bar_h[st], TY * 32 * HB);
+            tma_load3(&S.h[st][0][0], &m_h, &S.bar_h[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
+        };
 
-    auto step = [&](auto PAR, int s, const Carry& in, Carry& o) {
-        constexpr int par = decltype(PAR)::value, pr = par ^ 1;
-        const int zg = g.z0 + s;
-        const bool zl = zg < g.nz - 1, zf = zg > 0;
-
-        mbar_wait(&S.bar_u[cu1.st], cu1.ph);
-        mbar_wait(&S.bar_v[cv.st], cv.ph);
-        mbar_wait(&S.bar_pq[cpq.st], cpq.ph);
-        mbar_wait(&S.bar_h[ch.st], ch.ph);
-
-        // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
-        const float* U0 = &S.u[su][0][r][bc];
-        const float* U1 = &S.u[cu1.st][0][r][bc];
-        const float* V0 = &S.v[cv.st][0][r][bc];
-        const float* PQ = &S.pq[cpq.st][0][r][bc];
-        constexpr int F = R * TMA_BW;  // field stride in a ring slot
-        const float uk = U0[0], um = U0[F];
-        float vk[3], vb[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            vk[k] = V0[k * F];
-            vb[k] = 2.f * vk[k] - V0[(3 + k) * F];
+        if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
+            for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
+            for (int tz = zs - 1; tz < zs - 1 + Rg::NV - 1; ++tz) issue_v(tz);
+            for (int tz = zs - 1; tz < zs - 1 + Rg::NPQ - 1; ++tz) issue_pq(tz);
+            for (int tz = zs - 1; tz < zs - 1 + Rg::NH - 1; ++tz) issue_h(tz);
         }
-        const float ub = 2.f * uk - um;          // (a3) ubar(s)
-        const float ub1 = 2.f * U1[0] - U1[F];   // ubar(s+1)
-        float pk[3], qk[6];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) pk[k] = PQ[k * F];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) qk[m] = PQ[(3 + m) * F];
-        Hist hc{};
-        if (own) {
-            const uint8_t* hp = &S.h[ch.st][r - 1][lane * HB];
-            if constexpr (HB == 8) {
-                const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
-                hc.w[0] = v2.x;
-                hc.w[1] = v2.y;
-            } else {
-#pragma unroll
-                for (int q4 = 0; q4 < HB / 16; ++q4) {
-                    const uint4 v4 = reinterpret_cast<const uint4*>(hp)[q4];
-                    hc.w[4 * q4] = v4.x;
-                    hc.w[4 * q4 + 1] = v4.y;
-                    hc.w[4 * q4 + 2] = v4.z;
-                    hc.w[4 * q4 + 3] = v4.w;
+        mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
+        int su = cu.st;
+        adv(cu, Rg::NU);
+
+        // carried from step s-1 to step s (double-buffered by the 2x-unrolled loop)
+        struct Carry {
+            float vb[3];      // vbar(s-1)
+            float uk, vk[3];  // u_k, v_k at s-1 (the primal of plane s-1)
+            Hist h;           // histogram of s-1
+            float pn[3], pz;  // p_{k+1}(s-1), p_z{k+1}(s-2)
+            float qn[6];      // q_{k+1}(s-1)
+        };
+        Carry ca{}, cb{};
+
+        auto step = [&](auto PAR, int s, const Carry& in, Carry& o) {
+            constexpr int par = decltype(PAR)::value, pr = par ^ 1;
+            const int zg = g.z0 + s;
+            const bool zl = zg < g.nz - 1, zf = zg > 0;
+
+            mbar_wait(&S.bar_u[cu.st], cu.ph);
+            mbar_wait(&S.bar_v[cv.st], cv.ph);
+            mbar_wait(&S.bar_pq[cpq.st], cpq.ph);
+            mbar_wait(&S.bar_h[ch.st], ch.ph);
+
+            // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
+            const float* U0 = &S.u[su][0][r][bc];
+            const float* U1 = &S.u[cu.st][0][r][bc];
+            const float* V0 = &S.v[cv.st][0][r][bc];
+            const float* PQ = &S.pq[cpq.st][0][r][bc];
+            constexpr int F = R * TMA_BW;  // field stride in a ring slot
+            const float uk = U0[0], um = U0[F];
+            float vk[3], vb[3];
+    #pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                vk[k] = V0[k * F];
+                vb[k] = 2.f * vk[k] - V0[(3 + k) * F];
+            }
+            const float ub = 2.f * uk - um;          // (a3) ubar(s)
+            const float ub1 = 2.f * U1[0] - U1[F];   // ubar(s+1)
+            float pk[3], qk[6];
+    #pragma unroll
+            for (int k = 0; k < 3; ++k) pk[k] = PQ[k * F];
+    #pragma unroll
+            for (int m = 0; m < 6; ++m) qk[m] = PQ[(3 + m) * F];
+            Hist hc{};
+            if (own) {
+                const uint8_t* hp = &S.h[ch.st][r - 1][lane * HB];
+                if constexpr (HB == 8) {
+                    const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
+                    hc.w[0] = v2.x;
+                    hc.w[1] = v2.y;
+                } else {
+    #pragma unroll
+                    for (int q4 = 0; q4 < HB / 16; ++q4) {
+                        const uint4 v4 = reinterpret_cast<const uint4*>(hp)[q4];
+                        hc.w[4 * q4] = v4.x;
+                        hc.w[4 * q4 + 1] = v4.y;
+                        hc.w[4 * q4 + 2] = v4.z;
+                        hc.w[4 * q4 + 3] = v4.w;
+                    }
                 }
             }
-        }
-        S.suv[par][0][r][cc] = ub;
-        S.suv[par][1][r][cc] = vb[0];
-        S.suv[par][2][r][cc] = vb[1];
-        S.suv[par][3][r][cc] = vb[2];
-        if (tid0) tma_wait_read0();  // the previous step's output staging has been read
-        __syncthreads();             // S1
-        if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
-            if (s + Rg::NU - 1 <= ze + 1) issue_u(s + Rg::NU - 1);
-            if (s + Rg::NV - 1 <= ze) issue_v(s + Rg::NV - 1);
-            if (s + Rg::NPQ - 1 <= ze) issue_pq(s + Rg::NPQ - 1);
-            if (s + Rg::NH - 1 <= ze) issue_h(s + Rg::NH - 1);
-        }
-        su = cu1.st;
-        adv(cu1, Rg::NU);
-        adv(cv, Rg::NV);
-        adv(cpq, Rg::NPQ);
-        adv(ch, Rg::NH);
+            S.suv[par][0][r][cc] = ub;
+            S.suv[par][1][r][cc] = vb[0];
+            S.suv[par][2][r][cc] = vb[1];
+            S.suv[par][3][r][cc] = vb[2];
+            if (tid0) tma_wait_read0();  // the previous step's output staging has been read
+            __syncthreads();             // S1
+            if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
+                if (s + Rg::NU - 1 <= ze + 1) issue_u(s + Rg::NU - 1);
+                if (s + Rg::NV - 1 <= ze) issue_v(s + Rg::NV - 1);
+                if (s + Rg::NPQ - 1 <= ze) issue_pq(s + Rg::NPQ - 1);
+                if (s + Rg::NH - 1 <= ze) issue_h(s + Rg::NH - 1);
+            }
+            su = cu.st;
+            adv(cu, Rg::NU);
+            adv(cv, Rg::NV);
+            adv(cpq, Rg::NPQ);
+            adv(ch, Rg::NH);
 
-        // ---- phase E: (a1) dual D(s)
-        float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (needP) {
-            const float ux = S.suv[par][0][r][cc + 1];
-            const float uy = S.suv[par][0][r + 1][cc];
-            const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
-            pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
-            pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
-            pn[2] = fmaf(sp.sigma, g2 - vb[2], pk[2]);
-            const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
-            pn[0] *= f;
-            pn[1] *= f;
-            pn[2] *= f;
-        }
-        if (needQ) {
-            // vbar is exactly 0 outside the grid (TMA zero fill, zero halo planes at the
-            // global z ends), so the "l > 0" guards of D- are implicit
-            float dx[3], dy[3], dz[3];
-#pragma unroll
+            // ---- phase E: (a1) dual D(s)
+            float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (needP) {
+                const float ux = S.suv[par][0][r][cc + 1];
+                const float uy = S.suv[par][0][r + 1][cc];
+                const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
+                pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
+                pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
+                pn[2] = fmaf(sp.sigma, g2 - vb[2], pk[2]);
+                const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
+                pn[0] *= f;
+                pn[1] *= f;
+                pn[2] *= f;
+            }
+            if (needQ) {
+                // vbar is exactly 0 outside the grid (TMA zero fill, zero halo planes at the
+                // global z ends), so the "l > 0" guards of D- are implicit
+                float dx[3], dy[3], dz[3];
+    #pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float vx = S.suv[par][1 + k][r][cc - 1];
+                    const float vy = S.suv[par][1 + k][r - 1][cc];
+                    dx[k] = (xl ? vb[k] : 0.f) - vx;
+                    dy[k] = (yl ? vb[k] : 0.f) - vy;
+                    dz[k] = (zl ? vb[k] : 0.f) - in.vb[k];
+                }
+                const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
+                                    0.5f * (dz[1] + dy[2])};
+    #pragma unroll
+                for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], qk[m]);
+                const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
+                                               2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
+                                           sp.alpha0);
+    #pragma unroll
+                for (int m = 0; m < 6; ++m) qn[m] *= f;
+            }
+            S.sr[par][0][r][cc] = pn[0];
+            S.sr[par][1][r][cc] = pn[1];
+            S.sr[par][2][r][cc] = qn[0];
+            S.sr[par][3][r][cc] = qn[3];
+            S.sr[par][4][r][cc] = qn[4];
+            S.sr[par][5][r][cc] = qn[1];
+            S.sr[par][6][r][cc] = qn[5];
+            if (own) {
+    #pragma unroll
+                for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
+    #pragma unroll
+                for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
+            }
+
+            // ---- phase F: (a2) primal Pm(s-1) on owned rows
+            if (own && s - 1 >= zs) {
+                const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
+                const float pxm = S.sr[pr][0][r][cc - 1];
+                const float pym = S.sr[pr][1][r - 1][cc];
+                const float divp = ((xl ? in.pn[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? in.pn[1] : 0.f) - (yf ? pym : 0.f)) +
+                                   ((zl1 ? in.pn[2] : 0.f) - (zf1 ? in.pz : 0.f));
+                const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
+                const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
+                const float w0 = (xl ? qxx - in.qn[0] : 0.f) + (yl ? qyxy - in.qn[3] : 0.f) + (zl1 ? qn[4] - in.qn[4] : 0.f);
+                const float w1 = (xl ? qxy - in.qn[3] : 0.f) + (yl ? qyyy - in.qn[1] : 0.f) + (zl1 ? qn[5] - in.qn[5] : 0.f);
+                const float w2 = (xl ? qxz - in.qn[4] : 0.f) + (yl ? qyyz - in.qn[5] : 0.f) + (zl1 ? qn[2] - in.qn[2] : 0.f);
+                S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
+                S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
+                S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
+                S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
+            }
+            fence_proxy_async();
+            __syncthreads();  // S2
+            if (tid0) {
+                if (s >= zs && s < ze) {
+                    tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
+                    tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
+                }
+                if (s - 1 >= zs) {
+                    tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
+                    tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
+                }
+                tma_commit();
+            }
+
+            // ---- carry to step s+1
+            o.pz = in.pn[2];
+    #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const float vx = S.suv[par][1 + k][r][cc - 1];
-                const float vy = S.suv[par][1 + k][r - 1][cc];
-                dx[k] = (xl ? vb[k] : 0.f) - vx;
-                dy[k] = (yl ? vb[k] : 0.f) - vy;
-                dz[k] = (zl ? vb[k] : 0.f) - in.vb[k];
+                o.pn[k] = pn[k];
+                o.vb[k] = vb[k];
+                o.vk[k] = vk[k];
             }
-            const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
-                                0.5f * (dz[1] + dy[2])};
-#pragma unroll
-            for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], qk[m]);
-            const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
-                                           2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
-                                       sp.alpha0);
-#pragma unroll
-            for (int m = 0; m < 6; ++m) qn[m] *= f;
-        }
-        S.sr[par][0][r][cc] = pn[0];
-        S.sr[par][1][r][cc] = pn[1];
-        S.sr[par][2][r][cc] = qn[0];
-        S.sr[par][3][r][cc] = qn[3];
-        S.sr[par][4][r][cc] = qn[4];
-        S.sr[par][5][r][cc] = qn[1];
-        S.sr[par][6][r][cc] = qn[5];
-        if (own) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
-#pragma unroll
-            for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
-        }
+    #pragma unroll
+            for (int m = 0; m < 6; ++m) o.qn[m] = qn[m];
+            o.uk = uk;
+            o.h = hc;
+        };
 
-        // ---- phase F: (a2) primal Pm(s-1) on owned rows
-        if (own && s - 1 >= zs) {
-            const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
-            const float pxm = S.sr[pr][0][r][cc - 1];
-            const float pym = S.sr[pr][1][r - 1][cc];
-            const float divp = ((xl ? in.pn[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? in.pn[1] : 0.f) - (yf ? pym : 0.f)) +
-                               ((zl1 ? in.pn[2] : 0.f) - (zf1 ? in.pz : 0.f));
-            const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
-            const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
-            const float w0 = (xl ? qxx - in.qn[0] : 0.f) + (yl ? qyxy - in.qn[3] : 0.f) + (zl1 ? qn[4] - in.qn[4] : 0.f);
-            const float w1 = (xl ? qxy - in.qn[3] : 0.f) + (yl ? qyyy - in.qn[1] : 0.f) + (zl1 ? qn[5] - in.qn[5] : 0.f);
-            const float w2 = (xl ? qxz - in.qn[4] : 0.f) + (yl ? qyyz - in.qn[5] : 0.f) + (zl1 ? qn[2] - in.qn[2] : 0.f);
-            S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
-            S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
-            S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
-            S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
-        }
-        fence_proxy_async();
-        __syncthreads();  // S2
-        if (tid0) {
-            if (s >= zs && s < ze) {
-                tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
-                tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
-            }
-            if (s - 1 >= zs) {
-                tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
-                tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
-            }
-            tma_commit();
-        }
 
-        // ---- carry to step s+1
-        o.pz = in.pn[2];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            o.pn[k] = pn[k];
-            o.vb[k] = vb[k];
-            o.vk[k] = vk[k];
+        // steps s = zs-1 .. ze; the shared exchange planes alternate with the step's parity
+        for (int s = zs - 1; s <= ze; s += 2) {
+            step(std::integral_constant<int, 0>{}, s, ca, cb);
+            if (s + 1 > ze) break;
+            step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
         }
-#pragma unroll
-        for (int m = 0; m < 6; ++m) o.qn[m] = qn[m];
-        o.uk = uk;
-        o.h = hc;
-    };
-
-    // steps s = zs-1 .. ze; the shared exchange planes alternate with the step's parity
-    for (int s = zs - 1; s <= ze; s += 2) {
-        step(std::integral_constant<int, 0>{}, s, ca, cb);
-        if (s + 1 > ze) break;
-        step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
     }
     if (tid0) tma_wait0();
 }

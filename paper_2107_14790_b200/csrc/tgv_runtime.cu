@@ -57,6 +57,10 @@ struct tgv_ctx {
     int rank = 0, nranks = 1, device = 0;
     int schedule = TGV_SCHEDULE_FUSED;
     int fused_zc = 0;       // 0 = automatic
+    int num_sms = 148;
+    int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
+    int* d_sched_off = nullptr;
+    int sched_ctas = 0, sched_zc = -1;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
     CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
@@ -241,6 +245,12 @@ int launch_split(tgv_ctx* c, int phase /*0 dual, 1 primal*/)
 int fused_zc(const tgv_ctx* c)
 {
     if (c->fused_zc > 0) return c->fused_zc;
+    if (c->fused_tma) {  // lock-step chunk of the persistent schedule: <= 128 planes, a divisor if possible
+        if (c->g.nzl <= 128) return c->g.nzl;
+        for (int d = 128; d >= 64; --d)
+            if (c->g.nzl % d == 0) return d;
+        return 128;
+    }
     const int tiles = c->fused_tma ? ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY)
                                    : ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
     const int want = 4 * 148;  // about four waves of one CTA per SM
@@ -316,6 +326,77 @@ int make_state_maps(tgv_ctx* c)
     return make_state_map(c, &c->m_st6, 32, TMA_TY, 6);
 }
 
+// Schedule of the persistent fused kernel: items = (z-chunk, tile) in chunk-major
+// order; the first floor(items / G) * G items go round-robin to the G CTAs (each
+// CTA runs whole chunks, all CTAs in lock-step through z); the planes of the
+// remaining items are split evenly over all G CTAs as contiguous segments.
+int build_schedule(tgv_ctx* c, int zc)
+{
+    const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
+    const int nzl = c->g.nzl;
+    const int nch = (nzl + zc - 1) / zc;
+    const int64_t items = (int64_t)tiles * nch;
+    const int64_t planes = (int64_t)tiles * nzl;
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(c->num_sms, (planes + 7) / 8));
+    std::vector<std::vector<int4>> per(G);
+    const int64_t whole = items / G * G;
+    auto item = [&](int64_t i, int* t, int* z0, int* z1) {
+        const int ch = (int)(i / tiles);
+        *t = (int)(i % tiles);
+        *z0 = ch * zc;
+        *z1 = std::min(nzl, *z0 + zc);
+    };
+    for (int64_t i = 0; i < whole; ++i) {
+        int t, z0, z1;
+        item(i, &t, &z0, &z1);
+        per[i % G].push_back(make_int4(t, z0, z1, 0));
+    }
+    // the rest: a contiguous walk over their planes, cut into G equal shares
+    std::vector<int4> rest;
+    int64_t rest_planes = 0;
+    for (int64_t i = whole; i < items; ++i) {
+        int t, z0, z1;
+        item(i, &t, &z0, &z1);
+        rest.push_back(make_int4(t, z0, z1, 0));
+        rest_planes += z1 - z0;
+    }
+    int64_t pos = 0;
+    size_t ri = 0;
+    int zoff = 0;
+    for (int b = 0; b < G && ri < rest.size(); ++b) {
+        int64_t quota = rest_planes * (b + 1) / G - pos;
+        while (quota > 0 && ri < rest.size()) {
+            const int4 it = rest[ri];
+            const int z0 = it.y + zoff, take = (int)std::min<int64_t>(quota, it.z - z0);
+            per[b].push_back(make_int4(it.x, z0, z0 + take, 0));
+            quota -= take;
+            pos += take;
+            zoff += take;
+            if (it.y + zoff >= it.z) {
+                ++ri;
+                zoff = 0;
+            }
+        }
+    }
+    std::vector<int4> flat;
+    std::vector<int> off(1, 0);
+    for (auto& v : per) {
+        flat.insert(flat.end(), v.begin(), v.end());
+        off.push_back((int)flat.size());
+    }
+    cudaFree(c->d_sched);
+    cudaFree(c->d_sched_off);
+    c->d_sched = nullptr;
+    c->d_sched_off = nullptr;
+    CU(cudaMalloc(&c->d_sched, sizeof(int4) * std::max<size_t>(1, flat.size())));
+    CU(cudaMalloc(&c->d_sched_off, sizeof(int) * off.size()));
+    CU(cudaMemcpy(c->d_sched, flat.data(), sizeof(int4) * flat.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_sched_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+    c->sched_ctas = G;
+    c->sched_zc = zc;
+    return TGV_OK;
+}
+
 template <int SLOTS, typename CT>
 int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
@@ -352,8 +433,12 @@ int launch_fused_tma(tgv_ctx* c)
     A.s_vn = slotV(b.nu, 0);
     A.s_pn = slotP(b.np, 0);
     A.s_qn = slotQ(b.np, 0);
-    dim3 grd((c->g.nx + 31) / 32, (c->g.ny + TMA_TY - 1) / TMA_TY, (c->g.nzl + A.zc - 1) / A.zc);
+    // persistent grid: one CTA per SM (the kernel's shared memory allows one)
     int rc;
+    if (c->sched_zc != A.zc && (rc = build_schedule(c, A.zc))) return rc;
+    A.sched = c->d_sched;
+    A.sched_off = c->d_sched_off;
+    dim3 grd(c->sched_ctas, 1, 1);
     if (c->slots == 8 && c->count_bytes == 1) rc = launch_fused_tma_t<8, uint8_t>(c, A, grd);
     else if (c->slots == 8) rc = launch_fused_tma_t<8, uint16_t>(c, A, grd);
     else if (c->count_bytes == 1) rc = launch_fused_tma_t<16, uint8_t>(c, A, grd);
@@ -637,6 +722,7 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
         fail(c, TGV_ECUDA, "cudaSetDevice(%d) failed", dev);
         return bail(TGV_ECUDA);
     }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
         fail(c, TGV_ECUDA, "stream creation failed");
         return bail(TGV_ECUDA);
@@ -1206,6 +1292,8 @@ void tgv_destroy(tgv_ctx* c)
     cudaFree(c->d_out);
     cudaFree(c->d_maxc);
     cudaFree(c->staging);
+    cudaFree(c->d_sched);
+    cudaFree(c->d_sched_off);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
