@@ -148,6 +148,21 @@ int tgv_load_histograms(tgv_ctx* ctx, const uint32_t* counts, int64_t n_counts);
  * without a host copy.  TGV_ESTATE before the first successful load. */
 int tgv_reset(tgv_ctx* ctx);
 
+/* NEXT-1 coarse-to-fine ("coarse-to-fine scheme ... 200 iterations
+ * ... on each level"; :431-433 §4.5; R18-R20).  Both need single-rank
+ * contexts on one device with coarse = ceil(fine / 2) on every axis.
+ *
+ * tgv_restrict_from: this (coarse) context's histograms become the sums of the
+ *   <= 8 children's counts of the loaded fine context; then the state is reset as
+ *   by tgv_load_histograms.  Errors: TGV_EINVAL (not a 2x coarsening), TGV_ESTATE
+ *   (fine not loaded), TGV_ERANGE (a sum > 65535), TGV_ECUDA.
+ * tgv_prolong_from: this (fine, loaded) context's state restarts from the coarse
+ *   solution: u = u_parent, v = v_parent / 2 (per-voxel slope on a grid of half
+ *   spacing), ubar = u, vbar = v, p = q = 0, iteration counter 0.
+ *   Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_restrict_from(tgv_ctx* coarse, const tgv_ctx* fine);
+int tgv_prolong_from(tgv_ctx* fine, const tgv_ctx* coarse);
+
 /* COLLECTIVE.  Run n >= 0 full iterations of the scheme:
  *   p <- P_alpha1(p + sigma (grad ubar - vbar)),  q <- P_alpha0(q + sigma E(vbar))
  *   u+ = clamp(prox_{tau lambda h}(u + tau div p), -1, 1),  v+ = v + tau (p + div2 q)

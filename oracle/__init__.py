@@ -196,3 +196,56 @@ class Oracle:
     @property
     def u(self):
         return self.get("u")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 coarse-to-fine on the dense grid (
+# SURVEY.md §8(f) NEXT-1; readings R18-R20)
+# ---------------------------------------------------------------------------
+def restrict_counts(counts):
+    """Coarse voxel (X, Y, Z) = sum of the counts of its <= 8 children
+    (2X+{0,1}, 2Y+{0,1}, 2Z+{0,1}) inside the fine grid.  [nz,ny,nx,nb] -> ceil halves."""
+    counts = np.asarray(counts, dtype=np.uint64)
+    nz, ny, nx, nb = counts.shape
+    out = np.zeros(((nz + 1) // 2, (ny + 1) // 2, (nx + 1) // 2, nb), dtype=np.uint64)
+    for dz in (0, 1):
+        for dy in (0, 1):
+            for dx in (0, 1):
+                part = counts[dz::2, dy::2, dx::2]
+                out[:part.shape[0], :part.shape[1], :part.shape[2]] += part
+    return out.astype(np.uint32)
+
+
+def prolong_into(fine, coarse):
+    """Restart the fine state from the coarse solution: u = parent u, v = parent v / 2
+    (per-voxel slope on a grid of half the spacing), ubar = u, vbar = v, p = q = 0."""
+    nz, ny, nx = fine.local_shape
+
+    def up(a):
+        return np.repeat(np.repeat(np.repeat(a, 2, axis=-3), 2, axis=-2), 2, axis=-1)[..., :nz, :ny, :nx]
+
+    u = up(coarse.get("u"))
+    v = up(coarse.get("v")) * 0.5
+    fine.set("u", u)
+    fine.set("ubar", u)
+    fine.set("v", v)
+    fine.set("vbar", v)
+    fine.set("p", np.zeros((3, nz, ny, nx)))
+    fine.set("q", np.zeros((6, nz, ny, nx)))
+    return fine
+
+
+def coarse_to_fine(shape, counts, levels, iters, threads=1, **kw):
+    """Solve `levels` levels (coarsest = finest / 2^(levels-1)), `iters` iterations each,
+    initialising each finer level from the coarser solution.  Returns the finest Oracle."""
+    hs = [np.asarray(counts, dtype=np.uint32)]
+    shapes = [tuple(shape)]
+    for _ in range(levels - 1):
+        hs.append(restrict_counts(hs[-1]))
+        shapes.append(tuple((n + 1) // 2 for n in shapes[-1]))
+    o = Oracle(shapes[-1], **kw).load(hs[-1]).iterate(iters, threads=threads)
+    for lev in range(levels - 2, -1, -1):
+        f = Oracle(shapes[lev], **kw).load(hs[lev])
+        prolong_into(f, o)
+        o = f.iterate(iters, threads=threads)
+    return o

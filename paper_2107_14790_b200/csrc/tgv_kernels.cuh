@@ -467,6 +467,71 @@ __global__ void compact_counts_kernel(const uint16_t* __restrict__ src, uint8_t*
         dst[i] = (uint8_t)src[i];
 }
 
+// ---------------------------------------------------------------------------
+// NEXT-1 coarse-to-fine (R18-R20)
+// restriction: coarse voxel (X, Y, Z) sums the u16 counts of its <= 8 children
+// (2X + {0,1}, 2Y + {0,1}, 2Z + {0,1}) inside the fine grid
+template <int SLOTS>
+__global__ void restrict_counts_kernel(const uint16_t* __restrict__ Hf, Geo gf, uint16_t* __restrict__ Hc, Geo gc,
+                                       unsigned int* __restrict__ maxc)
+{
+    const int64_t n = (int64_t)gc.nzl * gc.ny * gc.nx;
+    unsigned int m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int X = (int)(v % gc.nx);
+        const int64_t r = v / gc.nx;
+        const int Y = (int)(r % gc.ny);
+        const int Z = (int)(r / gc.ny);
+        unsigned int acc[SLOTS];
+        for (int b = 0; b < SLOTS; ++b) acc[b] = 0;
+        for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int x = 2 * X + dx, y = 2 * Y + dy, z = 2 * Z + dz;
+                    if (x < gf.nx && y < gf.ny && z < gf.nzl) {
+                        const uint16_t* src = Hf + ((int64_t)z * gf.plane + (int64_t)y * gf.px + x) * SLOTS;
+                        for (int b = 0; b < SLOTS; ++b) acc[b] += src[b];
+                    }
+                }
+        uint16_t* dst = Hc + ((int64_t)Z * gc.plane + (int64_t)Y * gc.px + X) * SLOTS;
+        for (int b = 0; b < SLOTS; ++b) {
+            m = max(m, acc[b]);
+            dst[b] = (uint16_t)min(acc[b], 65535u);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxc, m);
+}
+
+// prolongation: every fine voxel takes its parent's u and v / 2 (v is a per-voxel
+// slope, and a fine voxel is half as wide), as both the current and the previous
+// iterate (restart: ubar = u, vbar = v); p and q are zeroed by the caller
+__global__ void prolong_kernel(const float* __restrict__ uc, const float* __restrict__ vc0,
+                               const float* __restrict__ vc1, const float* __restrict__ vc2, Geo gc,
+                               float* __restrict__ uf, float* __restrict__ uf_prev, float* __restrict__ vf0,
+                               float* __restrict__ vf1, float* __restrict__ vf2, float* __restrict__ vf0_prev,
+                               float* __restrict__ vf1_prev, float* __restrict__ vf2_prev, Geo gf)
+{
+    const int64_t n = (int64_t)gf.nzl * gf.ny * gf.nx;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(v % gf.nx);
+        const int64_t r = v / gf.nx;
+        const int y = (int)(r % gf.ny);
+        const int z = (int)(r / gf.ny);
+        const int ic = eoff(gc, x / 2, y / 2, z / 2), i = eoff(gf, x, y, z);
+        const float u = uc[ic];
+        const float a = 0.5f * vc0[ic], b = 0.5f * vc1[ic], c = 0.5f * vc2[ic];
+        uf[i] = u;
+        uf_prev[i] = u;
+        vf0[i] = a;
+        vf1[i] = b;
+        vf2[i] = c;
+        vf0_prev[i] = a;
+        vf1_prev[i] = b;
+        vf2_prev[i] = c;
+    }
+}
+
 // u_0 = sum h c / W (fp64, 0 where W = 0) into the current and previous u buffers
 // (ubar_0 = 2 u_0 - u_0 = u_0); every other field is zeroed by the caller.
 template <int SLOTS, typename CT>

@@ -809,6 +809,45 @@ int tgv_set_schedule(tgv_ctx* c, int schedule)
     return TGV_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// after the u16 store (hist16) and the running max (d_maxc) are written: range check,
+// u8 compaction when every count fits, TMA map of the chosen store, state init
+int finish_counts(tgv_ctx* c)
+{
+    const Geo& g = c->g;
+    int rc;
+    unsigned int maxc = 0;
+    CU(cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (maxc > 65535u) return fail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc);
+    const bool want8 = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0;
+    if (want8) {
+        const int64_t n = (int64_t)c->slots * g.nzl * g.plane;
+        if (!c->hist8) {
+            if (cudaMalloc(&c->hist8, (size_t)n) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, TGV_ENOMEM, "u8 histogram allocation failed");
+            }
+            c->device_bytes += n;
+        }
+        compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(c->hist16, c->hist8, n);
+        CU(cudaGetLastError());
+    }
+    c->count_bytes = want8 ? 1 : 2;
+    if ((rc = make_hist_map(c))) return rc;
+    rc = init_from_hist(c);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(c->stream));
+    c->loaded = true;
+    return TGV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
 {
     int rc = check_ready(c);
@@ -846,29 +885,55 @@ int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
                                                                    c->d_maxc);
         CU(cudaGetLastError());
     }
-    unsigned int maxc = 0;
-    CU(cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    if (maxc > 65535u) return fail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc);
-    const bool want8 = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0;
-    if (want8) {
-        const int64_t n = (int64_t)c->slots * g.nzl * g.plane;
-        if (!c->hist8) {
-            if (cudaMalloc(&c->hist8, (size_t)n) != cudaSuccess) {
-                cudaGetLastError();
-                return fail(c, TGV_ENOMEM, "u8 histogram allocation failed");
-            }
-            c->device_bytes += n;
-        }
-        compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(c->hist16, c->hist8, n);
-        CU(cudaGetLastError());
-    }
-    c->count_bytes = want8 ? 1 : 2;
-    if ((rc = make_hist_map(c))) return rc;
-    rc = init_from_hist(c);
+    return finish_counts(c);
+}
+
+// ---- NEXT-1 coarse-to-fine -------------------------------------------------------
+static bool coarse_of(const tgv_ctx* coarse, const tgv_ctx* fine)
+{
+    return coarse->g.nx == (fine->g.nx + 1) / 2 && coarse->g.ny == (fine->g.ny + 1) / 2 &&
+           coarse->g.nz == (fine->g.nz + 1) / 2 && coarse->nranks == 1 && fine->nranks == 1 &&
+           coarse->nbins == fine->nbins && coarse->device == fine->device;
+}
+
+int tgv_restrict_from(tgv_ctx* c, const tgv_ctx* fine)
+{
+    int rc = check_ready(c);
     if (rc) return rc;
+    if (!fine || !fine->loaded) return fail(c, TGV_ESTATE, "fine context missing or not loaded");
+    if (!coarse_of(c, fine))
+        return fail(c, TGV_EINVAL, "not a 2x coarsening of the fine grid (single-rank contexts on one device)");
+    c->loaded = false;
+    CU(cudaStreamSynchronize(fine->stream));
+    CU(cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream));
+    if (c->slots == 8)
+        restrict_counts_kernel<8><<<148 * 8, 256, 0, c->stream>>>(fine->hist16, fine->g, c->hist16, c->g, c->d_maxc);
+    else
+        restrict_counts_kernel<16><<<148 * 8, 256, 0, c->stream>>>(fine->hist16, fine->g, c->hist16, c->g,
+                                                                    c->d_maxc);
+    CU(cudaGetLastError());
+    return finish_counts(c);
+}
+
+int tgv_prolong_from(tgv_ctx* c, const tgv_ctx* coarse)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!coarse || !coarse->loaded) return fail(c, TGV_ESTATE, "coarse context missing or not loaded");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "prolong into a context without histograms");
+    if (!coarse_of(coarse, c))
+        return fail(c, TGV_EINVAL, "not a 2x coarsening of this grid (single-rank contexts on one device)");
+    CU(cudaStreamSynchronize(coarse->stream));
+    CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * (size_t)c->g.fs, c->stream));
+    c->k = 0;  // current buffers 0, previous buffers 2
+    tgv_ctx* cc = const_cast<tgv_ctx*>(coarse);
+    const Bufs b = bufs(cc->k);
+    prolong_kernel<<<148 * 8, 256, 0, c->stream>>>(
+        slot(cc, slotU(b.cu)), slot(cc, slotV(b.cu, 0)), slot(cc, slotV(b.cu, 1)), slot(cc, slotV(b.cu, 2)), cc->g,
+        slot(c, slotU(0)), slot(c, slotU(2)), slot(c, slotV(0, 0)), slot(c, slotV(0, 1)), slot(c, slotV(0, 2)),
+        slot(c, slotV(2, 0)), slot(c, slotV(2, 1)), slot(c, slotV(2, 2)), c->g);
+    CU(cudaGetLastError());
     CU(cudaStreamSynchronize(c->stream));
-    c->loaded = true;
     return TGV_OK;
 }
 

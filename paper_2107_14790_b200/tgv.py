@@ -25,7 +25,7 @@ FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
            "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
-           "tgv_group_energy"]
+           "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -77,6 +77,8 @@ def _load():
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]
     lib.tgv_group_iterate.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i32]
     lib.tgv_group_energy.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp]
+    lib.tgv_restrict_from.argtypes = [vp, vp]
+    lib.tgv_prolong_from.argtypes = [vp, vp]
     lib.tgv_destroy.argtypes = [vp]
     lib.tgv_destroy.restype = None
     lib.tgv_status_string.argtypes = [ctypes.c_int]
@@ -193,6 +195,14 @@ def tgv_info(ctx) -> dict:
 
 def tgv_destroy(ctx):
     lib.tgv_destroy(ctx)
+
+
+def tgv_restrict_from(coarse, fine):
+    _check(lib.tgv_restrict_from(coarse, fine), coarse)
+
+
+def tgv_prolong_from(fine, coarse):
+    _check(lib.tgv_prolong_from(fine, coarse), fine)
 
 
 def _params(centers, lam, alpha0, alpha1, tau, sigma):
@@ -355,6 +365,16 @@ class Solver:
     def set_schedule(self, schedule):
         """'fused' (default), 'split', or a TGV_SCHEDULE_* value."""
         tgv_set_schedule(self.ctx, {"fused": SCHEDULE_FUSED, "split": SCHEDULE_SPLIT}.get(schedule, schedule))
+        return self
+
+    def restrict_from(self, fine: "Solver"):
+        """NEXT-1: this coarse solver's histograms = 2x2x2 sums of `fine`'s; state reset."""
+        tgv_restrict_from(self.ctx, fine.ctx)
+        return self
+
+    def prolong_from(self, coarse: "Solver"):
+        """NEXT-1: restart this solver from `coarse`'s solution (u, v / 2; duals zero)."""
+        tgv_prolong_from(self.ctx, coarse.ctx)
         return self
 
     def set_timing(self, on: bool):
