@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--iters", type=int, default=None, help="iterations per step (default: the workload's)")
     ap.add_argument("--schedule", default="fused", choices=["fused", "split"])
+    ap.add_argument("--model", default="tgv", choices=["tgv", "tvl1"], help="tvl1: NEXT-4 (Eq. 1)")
+    ap.add_argument("--levels", type=int, default=1,
+                    help="NEXT-1: coarse-to-fine levels (a step = the whole multilevel solve, iters per level)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -180,18 +183,38 @@ def run_ours(a):
         s = Solver.distributed(wl.shape, list(wl.centers), z0, z1, local, **kw)
     else:
         s = Solver(wl.shape, list(wl.centers), device=local, **kw)
-    s.set_schedule(a.schedule)
+    s.set_schedule(a.schedule).set_model(a.model)
     s.load(counts)
     info = s.info()
     nvox_local = (z1 - z0) * ny * nx
+    # NEXT-1: coarser levels (single GPU), allocated outside the timed region
+    levels = [s]
+    if a.levels > 1:
+        assert world == 1, "--levels needs a single GPU"
+        from paper_2107_14790_b200.multilevel import level_shapes
+        for shp in level_shapes(wl.shape, a.levels)[1:]:
+            levels.append(Solver(shp, list(wl.centers), device=local, **kw).set_schedule(a.schedule)
+                          .set_model(a.model).restrict_from(levels[-1]))
+    vox_its = sum(int(np.prod(lv.shape)) for lv in levels) * iters  # per step, all levels
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def solve():
+        if len(levels) == 1:
+            s.iterate(iters)
+        else:  # restrict down from the resident fine histograms, solve coarse-to-fine
+            for lev in range(1, len(levels)):
+                levels[lev].restrict_from(levels[lev - 1])
+            levels[-1].iterate(iters)
+            for lev in range(len(levels) - 2, -1, -1):
+                levels[lev].prolong_from(levels[lev + 1]).iterate(iters)
+
     def step():
-        s.reset()
-        s.iterate(iters)
+        if len(levels) == 1:
+            s.reset()
+        solve()
         s.energy()
 
     for _ in range(a.warmup):
@@ -220,7 +243,7 @@ def run_ours(a):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t[0])
-    value = wl.nvox * iters / (ms_max * 1e-3)
+    value = vox_its / (ms_max * 1e-3)
 
     # roofline of the dominant kernel: the kernel with the largest device time per step
     peak, peak_src = measured_peaks()
@@ -231,7 +254,8 @@ def run_ours(a):
     dom = max(kern, key=lambda k: kern[k][2])
     kms, bpv, _ = kern[dom]
     achieved = bpv * nvox_local / (kms * 1e-3) / 1e9
-    bytes_per_it = info["bytes_fused"] if a.schedule == "fused" else info["bytes_dual"] + info["bytes_primal"]
+    bytes_per_it = info["bytes_fused"] if (a.schedule == "fused" and a.model == "tgv") else \
+        info["bytes_dual"] + info["bytes_primal"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -254,14 +278,14 @@ def run_ours(a):
         t0 = time.perf_counter()
         for _ in range(a.steps):
             tgv.tgv_load_histograms(s.ctx, hc)
-            s.iterate(iters)
+            solve()
             s.energy()
             tgv.tgv_read_u(s.ctx, hu)
         torch.cuda.synchronize()
         el = torch.tensor([(time.perf_counter() - t0) / a.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        e2e = {"value": wl.nvox * iters / float(el[0]), "unit": UNIT, "h2d_bytes_per_step": int(hc.numel() * 4),
+        e2e = {"value": vox_its / float(el[0]), "unit": UNIT, "h2d_bytes_per_step": int(hc.numel() * 4),
                "d2h_bytes_per_step": int(hu.numel() * 4 + 6 * 8)}
 
     cpu = None
@@ -275,7 +299,9 @@ def run_ours(a):
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "iters_per_step": iters,
-                       "step": "reset + iters x (dual, primal+over-relax) + energy/gap",
+                       "step": ("reset + iters x (dual, primal+over-relax) + energy/gap" if a.levels == 1 else
+                                f"coarse-to-fine: restrict to {a.levels} levels, iters per level, prolong, energy"),
+                       "model": a.model, "schedule": a.schedule, "levels": a.levels,
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                        "l2": f"no flush: resident state+histograms {info['device_bytes'] / 1e9:.2f} GB per GPU "
                              f">> 126 MB L2"},
@@ -284,7 +310,7 @@ def run_ours(a):
                          "bytes_per_voxel": bpv, "kernel_ms": kms,
                          "schedule": a.schedule, "bytes_per_voxel_iteration": bytes_per_it,
                          "count_bytes": info["count_bytes"],
-                         "schedule_gbs": bytes_per_it * wl.nvox * iters / (ms_max * 1e-3) / 1e9 / world,
+                         "schedule_gbs": bytes_per_it * vox_its / (ms_max * 1e-3) / 1e9 / world,
                          "kernel_share_of_step": step_kernel_ms / a.steps / ms},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches_per_step * a.steps)),
             "kernel_ms": {**{k: v[0] for k, v in kern.items()},

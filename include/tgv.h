@@ -92,6 +92,14 @@ typedef struct {
 #define TGV_SCHEDULE_FUSED 0
 #define TGV_SCHEDULE_SPLIT 1
 
+/* Models.  TGV: Eq. 2, the default.  TVL1: Eq. 1
+ * (PAPER.md:135-144), min_u sum alpha1 |grad u| + lambda sum_b h_b |u - c_b|,
+ * the same scheme with v = q = 0 (R21); it
+ * runs as a dual kernel and a primal kernel (60 B per voxel-iteration with u8
+ * counts) and its restricted gap uses V = 0. */
+#define TGV_MODEL_TGV 0
+#define TGV_MODEL_TVL1 1
+
 /* Kernel timing (device time from CUDA events on the launching stream). */
 typedef struct {
     double dual_ms, primal_ms, fused_ms, energy_ms, halo_ms; /* summed device ms since last enable */
@@ -105,9 +113,9 @@ typedef struct {
     int32_t count_bytes;      /* bytes per stored histogram count: 1 (u8) or 2 (u16)       */
     int32_t count_slots;      /* histogram slots stored per voxel (8 or 16)                */
     int32_t schedule;         /* TGV_SCHEDULE_*                                            */
+    int32_t model;            /* TGV_MODEL_*                                               */
     int32_t fused_zc;         /* z-planes per CTA of the fused kernel                      */
     int32_t fused_tma;        /* 1: the fused kernel stages planes with TMA (default)      */
-    int32_t reserved;
     int64_t bytes_dual;       /* algorithmic HBM bytes per voxel of one SPLIT dual launch  */
     int64_t bytes_primal;     /* ... of one SPLIT primal launch                            */
     int64_t bytes_fused;      /* ... of one FUSED launch (one whole iteration)             */
@@ -220,6 +228,10 @@ int tgv_group_iterate(tgv_ctx* const* members, int n, int32_t iterations);
 /* Energy of the whole grid of a group (same out[6] as tgv_energy), members'
  * partial sums added on the host in rank order. */
 int tgv_group_energy(tgv_ctx* const* members, int n, double out[6]);
+
+/* Select the model (TGV_MODEL_TGV, the default, or TGV_MODEL_TVL1).  A loaded
+ * context restarts from the initialisation.  Errors: TGV_EINVAL, TGV_ESTATE. */
+int tgv_set_model(tgv_ctx* ctx, int model);
 
 /* Select the iteration schedule (TGV_SCHEDULE_FUSED, the default, or
  * TGV_SCHEDULE_SPLIT; the environment variable TGV_SCHEDULE sets the default at

@@ -52,6 +52,7 @@ def _lib():
     lib.oracle_primal.argtypes = [vp, ctypes.c_int]
     lib.oracle_iterate.argtypes = [vp, ctypes.c_int, ctypes.c_int]
     lib.oracle_dual_halo.argtypes = [vp]
+    lib.oracle_set_tvl1.argtypes = [vp, ctypes.c_int]
     lib.oracle_energy.argtypes = [vp, dbl, vp]
     for fn in ("oracle_get", "oracle_set"):
         getattr(lib, fn).argtypes = [vp, ctypes.c_int, vp]
@@ -122,7 +123,8 @@ class Oracle:
     shape = (nx, ny, nz) of the GLOBAL grid; the state owns planes [zb, ze).
     """
 
-    def __init__(self, shape, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25, centers=None, zb=0, ze=None):
+    def __init__(self, shape, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25, centers=None, zb=0, ze=None,
+                 model="tgv"):
         nx, ny, nz = shape
         ze = nz if ze is None else ze
         self.shape, self.zb, self.ze = (nx, ny, nz), zb, ze
@@ -132,6 +134,8 @@ class Oracle:
         self._ptr = _lib().oracle_create(nx, ny, nz, zb, ze, len(c), c.ctypes.data, lam, alpha0, alpha1, tau, sigma)
         if not self._ptr:
             raise ValueError("oracle_create: invalid arguments")
+        self.model = model
+        _lib().oracle_set_tvl1(self._ptr, 1 if model == "tvl1" else 0)
 
     def __del__(self):
         if getattr(self, "_ptr", None):
@@ -187,7 +191,10 @@ class Oracle:
         plane = _c(plane)
         assert _lib().oracle_set_plane(self._ptr, FIELDS[name][comp], z, plane.ctypes.data) == 0
 
-    def energy(self, V=2.0):
+    def energy(self, V=None):
+        """TGV: V = 2 bounds v in the restricted dual (reading R14); TV-L1 has no v (V = 0)."""
+        if V is None:
+            V = 0.0 if self.model == "tvl1" else 2.0
         out = np.zeros(7, dtype=np.float64)
         _lib().oracle_energy(self._ptr, V, out.ctypes.data)
         return {"E": out[0], "alpha1": out[1], "alpha0": out[2], "data": out[3], "gap": out[4], "vmax": out[5],

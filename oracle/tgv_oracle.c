@@ -72,6 +72,7 @@ typedef struct oracle_state {
     double lambda, alpha0, alpha1, tau, sigma;
     double* f[F_COUNT]; /* each (ze-zb+2) planes of ny*nx, halo planes at both ends */
     double* h;          /* owned voxels x nbins (no halo) */
+    int tvl1;           /* 1: TV-L1 model of Eq. 1 (v = q = 0 throughout), see oracle_set_tvl1 */
 } oracle_state;
 
 /* ---- indexing ---------------------------------------------------------- */
@@ -241,6 +242,12 @@ void oracle_load(oracle_state* s, const uint32_t* counts)
             }
 }
 
+/* NEXT-4: the TV-L1 functional of Eq. 1,
+ *     min_u sum alpha1 |grad u| + lambda sum_b h_b |u - c_b|,
+ * is the TGV scheme with v fixed at 0 and no q: p <- P_alpha1(p + sigma grad ubar),
+ * u+ = clamp(prox(u + tau div p)).  (reading R21.) */
+void oracle_set_tvl1(oracle_state* s, int on) { s->tvl1 = on ? 1 : 0; }
+
 /* (a1) dual step: p <- P_alpha1(p + sigma(grad ubar - vbar)), q <- P_alpha0(q + sigma E(vbar)) */
 void oracle_dual(oracle_state* s, int threads)
 {
@@ -262,6 +269,7 @@ void oracle_dual(oracle_state* s, int threads)
                 /* Euclidean projection onto {|p| <= alpha1} (reading R5) */
                 double sp = (np > s->alpha1) ? s->alpha1 / np : 1.0;
                 for (int k = 0; k < 3; ++k) p[k][i] = pn[k] * sp;
+                if (s->tvl1) continue; /* TV-L1: no q (vbar stays 0) */
 
                 symgrad_at(g, vbar, x, y, z, e);
                 for (int m = 0; m < 6; ++m) qn[m] = q[m][i] + s->sigma * e[m];
@@ -294,6 +302,7 @@ void oracle_primal(oracle_state* s, int threads)
                 double unew = oracle_prox(uold + s->tau * d, t, s->nbins, hv, s->c);
                 s->f[F_U][i] = unew;
                 s->f[F_UBAR][i] = 2.0 * unew - uold;
+                if (s->tvl1) continue; /* TV-L1: v stays 0 */
                 double w[3];
                 div2_at(g, q, x, y, z, w);
                 for (int k = 0; k < 3; ++k) {

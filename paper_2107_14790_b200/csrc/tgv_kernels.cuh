@@ -236,6 +236,59 @@ __global__ void __launch_bounds__(256) split_primal_kernel(const IterPtrs a, con
 }
 
 // ===========================================================================
+// NEXT-4 TV-L1 model (Eq. 1; R21): v = q = 0,
+//   p_{k+1} = P_a1(p_k + s grad ubar_k),  u_{k+1} = clamp(prox(u_k + t div p_{k+1}), -1, 1)
+// dual: reads u_k, u_{k-1}, p (5 floats), writes p (3): 32 B per voxel
+// primal: reads p (3), u_k (1) + counts, writes u: 20 B + counts
+// ===========================================================================
+__global__ void __launch_bounds__(256) tvl1_dual_kernel(const IterPtrs a, const Geo g, const StepParams sp)
+{
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zg = g.z0 + z;
+    const int i = eoff(g, x, y, z);
+    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
+    const int sy = g.px, sz = g.plane;
+    auto ubar = [&](int o) { return 2.f * __ldg(a.uk + o) - __ldg(a.um + o); };
+    const float u0 = ubar(i);
+    const float ux = xl ? ubar(i + 1) : 0.f, uy = yl ? ubar(i + sy) : 0.f, uz = zl ? ubar(i + sz) : 0.f;
+    float p[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p[k] = __ldg(a.pk[k] + i);
+    const float g0 = xl ? ux - u0 : 0.f, g1 = yl ? uy - u0 : 0.f, g2 = zl ? uz - u0 : 0.f;
+    p[0] = fmaf(sp.sigma, g0, p[0]);
+    p[1] = fmaf(sp.sigma, g1, p[1]);
+    p[2] = fmaf(sp.sigma, g2, p[2]);
+    const float f = proj_scale(p[0] * p[0] + p[1] * p[1] + p[2] * p[2], sp.alpha1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.pn[k][i] = p[k] * f;
+}
+
+// reads p_{k+1} (in a.pk), u_k; writes u_{k+1}
+template <int SLOTS, typename CT>
+__global__ void __launch_bounds__(256) tvl1_primal_kernel(const IterPtrs a, const Geo g, const StepParams sp,
+                                                          const Centers C)
+{
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    if (x >= g.nx || y >= g.ny) return;
+    const int zg = g.z0 + z;
+    const int i = eoff(g, x, y, z);
+    const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
+    const bool xf = x > 0, yf = y > 0, zf = zg > 0;
+    const int sy = g.px, sz = g.plane;
+    float p[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p[k] = __ldg(a.pk[k] + i);
+    const float pxm = xf ? __ldg(a.pk[0] + i - 1) : 0.f;
+    const float pym = yf ? __ldg(a.pk[1] + i - sy) : 0.f;
+    const float pzm = zf ? __ldg(a.pk[2] + i - sz) : 0.f;
+    const float uo = __ldg(a.uk + i);
+    const auto h = load_hist<SLOTS, CT>(a.hist, (int64_t)z * g.plane + y * g.px + x);
+    const float divp = ((xl ? p[0] : 0.f) - pxm) + ((yl ? p[1] : 0.f) - pym) + ((zl ? p[2] : 0.f) - pzm);
+    a.un[i] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uo), sp.tl, h, C);
+}
+
+// ===========================================================================
 // FUSED schedule: one single-sweep kernel per iteration (136 B per voxel-iteration
 // with u16 counts, 128 B with u8).
 //

@@ -56,6 +56,7 @@ struct tgv_ctx {
     float lambda = 0, alpha0 = 0, alpha1 = 0, tau = 0, sigma = 0;
     int rank = 0, nranks = 1, device = 0;
     int schedule = TGV_SCHEDULE_FUSED;
+    int model = TGV_MODEL_TGV;
     int fused_zc = 0;       // 0 = automatic
     int num_sms = 148;
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
@@ -237,6 +238,33 @@ int launch_split(tgv_ctx* c, int phase /*0 dual, 1 primal*/)
         else if (c->slots == 8) launch_split_primal_t<8, uint16_t>(c, a, grd, blk);
         else if (c->count_bytes == 1) launch_split_primal_t<16, uint8_t>(c, a, grd, blk);
         else launch_split_primal_t<16, uint16_t>(c, a, grd, blk);
+    }
+    CU(cudaGetLastError());
+    return timer_end(c, sl);
+}
+
+template <int SLOTS, typename CT>
+void launch_tvl1_primal_t(tgv_ctx* c, const IterPtrs& a, dim3 grd, dim3 blk)
+{
+    tvl1_primal_kernel<SLOTS, CT><<<grd, blk, 0, c->stream>>>(a, c->g, step_params(c), centers(c));
+}
+
+// NEXT-4 TV-L1 (two kernels; v and q stay zero)
+int launch_tvl1(tgv_ctx* c, int phase)
+{
+    size_t sl = 0;
+    int rc = timer_begin(c, phase == 0 ? T_DUAL : T_PRIMAL, &sl);
+    if (rc) return rc;
+    dim3 blk(32, 8), grd((c->g.nx + 31) / 32, (c->g.ny + 7) / 8, c->g.nzl);
+    IterPtrs a = iter_ptrs(c, c->k);
+    if (phase == 0) {
+        tvl1_dual_kernel<<<grd, blk, 0, c->stream>>>(a, c->g, step_params(c));
+    } else {
+        for (int d = 0; d < 3; ++d) a.pk[d] = a.pn[d];
+        if (c->slots == 8 && c->count_bytes == 1) launch_tvl1_primal_t<8, uint8_t>(c, a, grd, blk);
+        else if (c->slots == 8) launch_tvl1_primal_t<8, uint16_t>(c, a, grd, blk);
+        else if (c->count_bytes == 1) launch_tvl1_primal_t<16, uint8_t>(c, a, grd, blk);
+        else launch_tvl1_primal_t<16, uint16_t>(c, a, grd, blk);
     }
     CU(cudaGetLastError());
     return timer_end(c, sl);
@@ -553,6 +581,22 @@ HaloPlan plan_fused(int64_t k)
     for (int d = 0; d < 3; ++d) h.add_up(slotP(b.cp, d));
     return h;
 }
+// TV-L1, before the dual: grad ubar needs (u_k, u_{k-1})(z+1); before the primal: p_z(z-1)
+HaloPlan plan_tvl1_a(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_down(slotU(b.cu));
+    h.add_down(slotU(b.pu));
+    return h;
+}
+HaloPlan plan_tvl1_b(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_up(slotP(b.np, 2));
+    return h;
+}
 // energy: grad u (u(z+1)), div2 q (q_xz, q_yz, q_zz(z+1)) down; E(v) (v(z-1)), div p (p_z(z-1)) up
 HaloPlan plan_energy(int64_t k)
 {
@@ -799,6 +843,19 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     return create_impl(L, P, rank, nranks, uid, dev, false, out);
 }
 
+int tgv_set_model(tgv_ctx* c, int model)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (model != TGV_MODEL_TGV && model != TGV_MODEL_TVL1) return fail(c, TGV_EINVAL, "unknown model %d", model);
+    c->model = model;
+    if (c->loaded) {  // restart from the initialisation (v = q = 0 for both models)
+        if ((rc = init_from_hist(c))) return rc;
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    return TGV_OK;
+}
+
 int tgv_set_schedule(tgv_ctx* c, int schedule)
 {
     int rc = check_ready(c);
@@ -956,7 +1013,12 @@ int tgv_iterate(tgv_ctx* c, int32_t n)
     if (!c->loaded) return fail(c, TGV_ESTATE, "iterate before load");
     if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_iterate");
     for (int32_t it = 0; it < n; ++it) {
-        if (c->schedule == TGV_SCHEDULE_SPLIT) {
+        if (c->model == TGV_MODEL_TVL1) {
+            if ((rc = halo_exchange(c, plan_tvl1_a(c->k)))) return rc;
+            if ((rc = launch_tvl1(c, 0))) return rc;
+            if ((rc = halo_exchange(c, plan_tvl1_b(c->k)))) return rc;
+            if ((rc = launch_tvl1(c, 1))) return rc;
+        } else if (c->schedule == TGV_SCHEDULE_SPLIT) {
             if ((rc = halo_exchange(c, plan_split_a(c->k)))) return rc;
             if ((rc = launch_split(c, 0))) return rc;
             if ((rc = halo_exchange(c, plan_split_b(c->k)))) return rc;
@@ -1063,7 +1125,7 @@ static int energy_launch(tgv_ctx* c)
     ea.alpha1 = c->alpha1;
     ea.alpha0 = c->alpha0;
     ea.lambda = c->lambda;
-    ea.V = 2.0;
+    ea.V = c->model == TGV_MODEL_TVL1 ? 0.0 : 2.0;  // TV-L1 has no v to bound (R14, R21)
     ea.nbins = c->nbins;
     if (c->slots == 8 && c->count_bytes == 1) launch_energy_t<8, uint8_t>(c, ea);
     else if (c->slots == 8) launch_energy_t<8, uint16_t>(c, ea);
@@ -1161,7 +1223,7 @@ static int group_check(tgv_ctx* const* m, int n)
         if (!c->group || (int)c->group->size() != n || (*c->group)[r] != c)
             return fail(c, TGV_EINVAL, "contexts are not the members of one group, in rank order");
         if (!c->loaded) return fail(c, TGV_ESTATE, "group member %d not loaded", r);
-        if (c->k != m[0]->k || c->schedule != m[0]->schedule)
+        if (c->k != m[0]->k || c->schedule != m[0]->schedule || c->model != m[0]->model)
             return fail(c, TGV_ESTATE, "group members at different iterations or schedules");
     }
     return TGV_OK;
@@ -1221,7 +1283,19 @@ int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
     if ((rc = group_record(m, n))) return rc;  // the current state is each member's last step
     for (int32_t it = 0; it < iters; ++it) {
         const int64_t k = m[0]->k;
-        if (m[0]->schedule == TGV_SCHEDULE_SPLIT) {
+        if (m[0]->model == TGV_MODEL_TVL1) {
+            if ((rc = group_exchange(m, n, plan_tvl1_a(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_tvl1(m[r], 0))) return rc;
+            }
+            if ((rc = group_record(m, n))) return rc;
+            if ((rc = group_exchange(m, n, plan_tvl1_b(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_tvl1(m[r], 1))) return rc;
+            }
+        } else if (m[0]->schedule == TGV_SCHEDULE_SPLIT) {
             if ((rc = group_exchange(m, n, plan_split_a(k)))) return rc;
             for (int r = 0; r < n; ++r) {
                 CU(cudaSetDevice(m[r]->device));
@@ -1311,6 +1385,7 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     o->count_bytes = c->count_bytes;
     o->count_slots = c->slots;
     o->schedule = c->schedule;
+    o->model = c->model;
     const int64_t hb = (int64_t)c->count_bytes * c->slots;
     // algorithmic HBM bytes per voxel of one launch:
     // split dual: reads u_k, u_{k-1}, v_k, v_{k-1}, p_k, q_k (17 floats), writes p, q (9)
@@ -1319,6 +1394,11 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     o->bytes_primal = 4 * (13 + 4) + hb;
     // fused: reads 17 floats + histogram, writes u, v, p, q (13 floats)
     o->bytes_fused = 4 * (17 + 13) + hb;
+    if (c->model == TGV_MODEL_TVL1) {  // TV-L1: dual reads u_k, u_{k-1}, p, writes p; primal reads p, u + counts, writes u
+        o->bytes_dual = 4 * (5 + 3);
+        o->bytes_primal = 4 * (4 + 1) + hb;
+        o->bytes_fused = 0;
+    }
     o->fused_zc = fused_zc(c);
     o->fused_tma = c->fused_tma ? 1 : 0;
     o->nranks = c->nranks;

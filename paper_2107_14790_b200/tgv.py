@@ -18,12 +18,13 @@ LIB_PATH = os.path.join(_PKG, "lib", "libtgv.so")
 
 TGV_OK, TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL, TGV_ESTATE, TGV_ERANGE = 0, -1, -2, -3, -4, -5, -6
 SCHEDULE_FUSED, SCHEDULE_SPLIT = 0, 1
+MODEL_TGV, MODEL_TVL1 = 0, 1
 FIELD_U, FIELD_V, FIELD_UBAR, FIELD_VBAR, FIELD_P, FIELD_Q, NUM_FIELDS = 0, 1, 4, 5, 8, 11, 17
 FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 10],
           "q": [11, 12, 13, 14, 15, 16]}
 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
-           "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_timing", "tgv_get_timing", "tgv_info",
+           "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_model", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
            "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from"]
 
@@ -48,8 +49,8 @@ class tgv_timing(ctypes.Structure):
 
 class tgv_info_t(ctypes.Structure):
     _fields_ = [("row_pitch", ctypes.c_int64), ("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32),
-                ("count_slots", ctypes.c_int32), ("schedule", ctypes.c_int32), ("fused_zc", ctypes.c_int32),
-                ("fused_tma", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("count_slots", ctypes.c_int32), ("schedule", ctypes.c_int32), ("model", ctypes.c_int32),
+                ("fused_zc", ctypes.c_int32), ("fused_tma", ctypes.c_int32),
                 ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64), ("bytes_fused", ctypes.c_int64),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("iteration", ctypes.c_int64)]
 
@@ -70,6 +71,7 @@ def _load():
     lib.tgv_write_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_energy.argtypes = [vp, vp]
     lib.tgv_set_schedule.argtypes = [vp, ctypes.c_int]
+    lib.tgv_set_model.argtypes = [vp, ctypes.c_int]
     lib.tgv_set_timing.argtypes = [vp, ctypes.c_int]
     lib.tgv_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
     lib.tgv_info.argtypes = [vp, ctypes.POINTER(tgv_info_t)]
@@ -177,6 +179,10 @@ def tgv_set_schedule(ctx, schedule: int):
     _check(lib.tgv_set_schedule(ctx, int(schedule)), ctx)
 
 
+def tgv_set_model(ctx, model: int):
+    _check(lib.tgv_set_model(ctx, int(model)), ctx)
+
+
 def tgv_set_timing(ctx, enable: bool):
     _check(lib.tgv_set_timing(ctx, 1 if enable else 0), ctx)
 
@@ -246,6 +252,11 @@ class Group:
         n = len(cuts) - 1
         self.ctxs = tgv_create_group(shape, cuts, centers, lam, alpha0, alpha1, tau, sigma,
                                      devices if devices is not None else [0] * n)
+
+    def set_model(self, model):
+        for c in self.ctxs:
+            tgv_set_model(c, {"tgv": MODEL_TGV, "tvl1": MODEL_TVL1}.get(model, model))
+        return self
 
     def set_schedule(self, schedule):
         for c in self.ctxs:
@@ -375,6 +386,11 @@ class Solver:
     def prolong_from(self, coarse: "Solver"):
         """NEXT-1: restart this solver from `coarse`'s solution (u, v / 2; duals zero)."""
         tgv_prolong_from(self.ctx, coarse.ctx)
+        return self
+
+    def set_model(self, model):
+        """'tgv' (default) or 'tvl1' (NEXT-4, Eq. 1); a loaded solver restarts."""
+        tgv_set_model(self.ctx, {"tgv": MODEL_TGV, "tvl1": MODEL_TVL1}.get(model, model))
         return self
 
     def set_timing(self, on: bool):

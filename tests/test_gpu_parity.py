@@ -242,3 +242,30 @@ def test_error_paths():
         s.iterate(-1)
     assert ei.value.status == tgv.TGV_EINVAL
     s.iterate(2)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4 TV-L1 model (Eq. 1; R21)
+@pytest.mark.parametrize("shape,iters", [((37, 23, 19), 60), ((1, 1, 40), 200), ((64, 64, 64), 500)])
+def test_tvl1_matches_oracle(shape, iters):
+    if shape == (64, 64, 64):
+        h = np.ascontiguousarray(synth.make_histograms("C2", 118, 182)[:, 96:160, 96:160])
+    else:
+        h = synth.random_histograms(shape, 31)
+    c = oracle.default_centers(8)
+    o = oracle.Oracle(shape, model="tvl1").load(h).iterate(iters, threads=NT)
+    s = solver_cls()(shape, list(c)).set_model("tvl1").load(h).iterate(iters)
+    assert s.info()["model"] == 1
+    du, rel = assert_parity(o, s)
+    assert np.all(s.get("v") == 0) and np.all(s.get("q") == 0)
+    assert abs(s.energy()["gap"] - o.energy()["gap"]) <= 1e-4 * o.energy()["E"]
+
+
+def test_tvl1_group_equals_single():
+    from paper_2107_14790_b200 import Group
+    shape = (40, 30, 27)
+    h = synth.random_histograms(shape, 32)
+    c = list(oracle.default_centers(8))
+    one = solver_cls()(shape, c).set_model("tvl1").load(h).iterate(25)
+    grp = Group(shape, [0, 9, 20, 27], c).set_model("tvl1").load(h).iterate(25)
+    assert np.array_equal(grp.read_u(), one.read_u())
