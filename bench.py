@@ -223,7 +223,8 @@ def run_ours(a):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    s.set_timing(True)
+    for lv in levels:
+        lv.set_timing(True)
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -237,7 +238,9 @@ def run_ours(a):
     barrier()
     ms = ev0.elapsed_time(ev1) / a.steps
     tm = s.timing()
-    s.set_timing(False)
+    tms = [lv.timing() for lv in levels]
+    for lv in levels:
+        lv.set_timing(False)
     clk = clocks.stop()
     ms_t = torch.tensor([ms, wall * 1e3 / a.steps], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -265,7 +268,8 @@ def run_ours(a):
             traffic = None
     step_kernel_ms = tm["primal_ms"] + tm["dual_ms"] + tm["fused_ms"] + tm["energy_ms"]
     # + init + 2 energy kernels (+ the u8 compaction only at load)
-    launches_per_step = (tm["dual_launches"] + tm["primal_launches"] + tm["fused_launches"]) / a.steps + 3
+    launches_per_step = sum(t["dual_launches"] + t["primal_launches"] + t["fused_launches"] for t in tms) / a.steps \
+        + 3 + 4 * (len(levels) - 1)  # + init, 2 energy kernels; per coarse level restrict + compact + init + prolong
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ------------------
     e2e = None

@@ -156,6 +156,36 @@ int tgv_load_histograms(tgv_ctx* ctx, const uint32_t* counts, int64_t n_counts);
  * without a host copy.  TGV_ESTATE before the first successful load. */
 int tgv_reset(tgv_ctx* ctx);
 
+/* NEXT-2: a pinhole range image for tgv_vote_depth_maps (§3.1).
+ * world_dir = rot * cam_dir (rot row-major, its columns the camera axes);
+ * a camera-frame point (X, Y, Z), Z > 0, lands on pixel (fx X/Z + cx, fy Y/Z + cy);
+ * the depth map holds the camera-frame Z of the surface per pixel, NaN = none
+ * (R4); vote_weight is Alg. 1's depthmap_vote (1, or 5 for LIDAR). */
+typedef struct {
+    double origin[3];
+    double rot[9];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    int32_t vote_weight;
+    int32_t pad;
+} tgv_camera;
+
+/* NEXT-2: compute this slab's histograms on the GPU with Alg. 1 (
+ * DESIGN.md R22) from host depth maps, then reset the state as
+ * tgv_load_histograms does.  Voxel (x, y, z) (z global) has its centre at
+ * grid_origin + voxel_size * (x, y, z) and radius voxel_radius (delta = 6 r,
+ * eta = 18 r).  depths[i] is float [height][width] of camera i,
+ * read during the call only; mipmap pyramids (mean of valid children) are built
+ * on the device.  Needs nbins == 8.  Counts are bit-identical to the CPU
+ * definition (fp64 without contraction).  Errors: TGV_EINVAL, TGV_ENOMEM,
+ * TGV_ERANGE (a count > 65535), TGV_ECUDA. */
+int tgv_vote_depth_maps(tgv_ctx* ctx, const tgv_camera* cams, int ncams, const float* const* depths,
+                        const double grid_origin[3], double voxel_size, double voxel_radius);
+
+/* Copy this slab's histogram counts to the host as uint32
+ * [z_end-z_begin][ny][nx][nbins].  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_read_counts(tgv_ctx* ctx, uint32_t* counts_out, int64_t n_counts);
+
 /* NEXT-1 coarse-to-fine ("coarse-to-fine scheme ... 200 iterations
  * ... on each level"; :431-433 §4.5; R18-R20).  Both need single-rank
  * contexts on one device with coarse = ceil(fine / 2) on every axis.

@@ -63,6 +63,7 @@ def _lib():
     for fn in ("oracle_grad", "oracle_div", "oracle_symgrad", "oracle_div2"):
         getattr(lib, fn).argtypes = [i64, i64, i64, vp, vp]
     lib.oracle_max_threads.restype = ctypes.c_int
+    lib.oracle_alg1_vote.argtypes = [vp, ctypes.c_int, ctypes.POINTER(vp), i64, i64, i64, i64, vp, dbl, dbl, vp]
     return lib
 
 
@@ -256,3 +257,31 @@ def coarse_to_fine(shape, counts, levels, iters, threads=1, **kw):
         prolong_into(f, o)
         o = f.iterate(iters, threads=threads)
     return o
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 histogram voting, Alg. 1
+# ---------------------------------------------------------------------------
+class OracleCamera(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_double * 3), ("rot", ctypes.c_double * 9), ("fx", ctypes.c_double),
+                ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("vote_weight", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+def alg1_vote(cams, depths, nx, ny, z0, z1, origin=(0.0, 0.0, 0.0), voxel_size=1.0, r=0.5):
+    """cams: sequence of dicts (origin, rot 3x3 world<-camera, fx, fy, cx, cy, width, height, vote_weight);
+    depths: float32 [h, w] z-depth maps (NaN = none).  -> uint32 [z1-z0, ny, nx, 8]."""
+    arr = (OracleCamera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i].origin[:] = [float(x) for x in c["origin"]]
+        arr[i].rot[:] = [float(x) for x in np.asarray(c["rot"], dtype=np.float64).reshape(-1)]
+        arr[i].fx, arr[i].fy, arr[i].cx, arr[i].cy = c["fx"], c["fy"], c["cx"], c["cy"]
+        arr[i].width, arr[i].height, arr[i].vote_weight = c["width"], c["height"], c.get("vote_weight", 1)
+    ds = [np.ascontiguousarray(d, dtype=np.float32) for d in depths]
+    ptrs = (ctypes.c_void_p * len(ds))(*[d.ctypes.data for d in ds])
+    out = np.empty((z1 - z0, ny, nx, 8), dtype=np.uint32)
+    o = np.asarray(origin, dtype=np.float64)
+    _lib().oracle_alg1_vote(arr, len(cams), ptrs, nx, ny, z0, z1, o.ctypes.data, float(voxel_size), float(r),
+                            out.ctypes.data)
+    return out

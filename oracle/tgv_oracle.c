@@ -534,3 +534,112 @@ int oracle_max_threads(void)
     return 1;
 #endif
 }
+
+/* ======================================================================== */
+/* NEXT-2: histogram voting, Alg. 1 (§3.4 :236-250)       */
+/* ======================================================================== */
+/* A pinhole camera: world_dir = rot * cam_dir (row-major, columns = camera
+ * axes), pixel (u, v) = (fx X/Z + cx, fy Y/Z + cy) for camera-frame (X, Y, Z);
+ * depth maps hold the camera-frame z-depth, NaN = no depth (reading R4). */
+typedef struct {
+    double origin[3];
+    double rot[9];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    int32_t vote_weight;
+    int32_t pad;
+} oracle_camera;
+
+/* Mipmap level L+1 = mean of the valid children of level L (ceil halves), NaN if
+ * none ("depth map pyramids").  Returns the number
+ * of levels, 1 + floor(log2(max(w, h))). */
+static int pyramid(const float* d0, int w, int h, float** lev, int* lw, int* lh)
+{
+    int m = w > h ? w : h, n = 1;
+    while ((1 << n) <= m) ++n;
+    lev[0] = (float*)d0;
+    lw[0] = w;
+    lh[0] = h;
+    for (int L = 1; L < n; ++L) {
+        lw[L] = (lw[L - 1] + 1) / 2;
+        lh[L] = (lh[L - 1] + 1) / 2;
+        lev[L] = (float*)malloc(sizeof(float) * (size_t)lw[L] * (size_t)lh[L]);
+        for (int y = 0; y < lh[L]; ++y)
+            for (int x = 0; x < lw[L]; ++x) {
+                double sum = 0.0;
+                int cnt = 0;
+                for (int dy = 0; dy < 2; ++dy)
+                    for (int dx = 0; dx < 2; ++dx) {
+                        int xx = 2 * x + dx, yy = 2 * y + dy;
+                        if (xx < lw[L - 1] && yy < lh[L - 1]) {
+                            float v = lev[L - 1][(int64_t)yy * lw[L - 1] + xx];
+                            if (v == v) {
+                                sum += (double)v;
+                                ++cnt;
+                            }
+                        }
+                    }
+                lev[L][(int64_t)y * lw[L] + x] = cnt ? (float)(sum / (double)cnt) : NAN;
+            }
+    }
+    return n;
+}
+
+/* Alg. 1 for every voxel of global planes [z0, z1) of an nx x ny grid and every
+ * camera.  Voxel (x, y, z) has centre origin + voxel_size * (x, y, z) and radius r.
+ *   project: camera-frame centre (X, Y, Z); Z <= 0 or pixel outside -> no vote
+ *   level:   round(log2(projected diameter 2 r fx / Z)), ties up, clamped to the
+ *            pyramid -- evaluated as the number of k >= 0 with diameter >= sqrt(2) 2^k
+ *   depth:   the level's texel floor(u / 2^L), floor(v / 2^L); NaN -> no vote
+ *   a = depth - Z; a < -eta -> no vote; a = clamp(a / delta, -1, 1);
+ *   bin = min(floor((a + 1) / 2 * 8), 7); counts[bin] += vote_weight
+ * with delta = 6 r, eta = 3 delta.  counts: uint32
+ * [z1-z0][ny][nx][8], zeroed here. */
+void oracle_alg1_vote(const oracle_camera* cams, int ncams, const float* const* depths, int64_t nx, int64_t ny,
+                      int64_t z0, int64_t z1, const double origin[3], double voxel_size, double r, uint32_t* counts)
+{
+    const double delta = 6.0 * r, eta = 3.0 * delta;
+    memset(counts, 0, sizeof(uint32_t) * (size_t)((z1 - z0) * ny * nx * 8));
+    for (int c = 0; c < ncams; ++c) {
+        const oracle_camera* C = &cams[c];
+        float* lev[32];
+        int lw[32], lh[32];
+        const int nlev = pyramid(depths[c], C->width, C->height, lev, lw, lh);
+#pragma omp parallel for schedule(static)
+        for (int64_t z = z0; z < z1; ++z)
+            for (int64_t y = 0; y < ny; ++y)
+                for (int64_t x = 0; x < nx; ++x) {
+                    const double pw[3] = {origin[0] + voxel_size * (double)x, origin[1] + voxel_size * (double)y,
+                                          origin[2] + voxel_size * (double)z};
+                    const double d[3] = {pw[0] - C->origin[0], pw[1] - C->origin[1], pw[2] - C->origin[2]};
+                    double pc[3];
+                    for (int k = 0; k < 3; ++k)
+                        pc[k] = C->rot[0 * 3 + k] * d[0] + C->rot[1 * 3 + k] * d[1] + C->rot[2 * 3 + k] * d[2];
+                    if (!(pc[2] > 0.0)) continue;
+                    const double u = C->fx * pc[0] / pc[2] + C->cx, v = C->fy * pc[1] / pc[2] + C->cy;
+                    if (!(u >= 0.0 && u < (double)C->width && v >= 0.0 && v < (double)C->height)) continue;
+                    const double diam = 2.0 * r * C->fx / pc[2];
+                    int L = 0;
+                    double thr = 1.4142135623730951; /* sqrt(2) 2^k */
+                    while (L < nlev - 1 && diam >= thr) {
+                        ++L;
+                        thr *= 2.0;
+                    }
+                    const double sc = (double)(1 << L);
+                    int ix = (int)floor(u / sc), iy = (int)floor(v / sc);
+                    if (ix > lw[L] - 1) ix = lw[L] - 1;
+                    if (iy > lh[L] - 1) iy = lh[L] - 1;
+                    const float dep = lev[L][(int64_t)iy * lw[L] + ix];
+                    if (dep != dep) continue; /* depth = None */
+                    double a = (double)dep - pc[2];
+                    if (a < -eta) continue;
+                    a = a / delta;
+                    if (a < -1.0) a = -1.0;
+                    if (a > 1.0) a = 1.0;
+                    int bin = (int)floor((a + 1.0) / 2.0 * 8.0);
+                    if (bin > 7) bin = 7;
+                    counts[(((z - z0) * ny + y) * nx + x) * 8 + bin] += (uint32_t)C->vote_weight;
+                }
+        for (int L = 1; L < nlev; ++L) free(lev[L]);
+    }
+}

@@ -25,6 +25,7 @@
 #include "nccl_api.h"
 #include "tgv_fused_tma.cuh"
 #include "tgv_kernels.cuh"
+#include "tgv_vote.cuh"
 
 using namespace tgvk;
 
@@ -991,6 +992,113 @@ int tgv_prolong_from(tgv_ctx* c, const tgv_ctx* coarse)
         slot(c, slotV(2, 0)), slot(c, slotV(2, 1)), slot(c, slotV(2, 2)), c->g);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
+}
+
+// ---- NEXT-2 GPU histogram voting ---------------------------------------------------
+int tgv_vote_depth_maps(tgv_ctx* c, const tgv_camera* cams, int ncams, const float* const* depths,
+                        const double grid_origin[3], double voxel_size, double voxel_radius)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!cams || !depths || !grid_origin || ncams < 0) return fail(c, TGV_EINVAL, "NULL argument");
+    if (c->nbins != 8) return fail(c, TGV_EINVAL, "Alg. 1 votes into 8 bins; this context has %d", c->nbins);
+    if (!(voxel_size > 0.0) || !(voxel_radius > 0.0)) return fail(c, TGV_EINVAL, "voxel size and radius must be > 0");
+    std::vector<VoteCam> vc((size_t)ncams);
+    int64_t total = 0;
+    for (int i = 0; i < ncams; ++i) {
+        const tgv_camera& C = cams[i];
+        if (C.width < 1 || C.height < 1 || C.width > (1 << 22) || C.height > (1 << 22) || !depths[i] ||
+            C.vote_weight < 0 || !(C.fx > 0.0) || !(C.fy > 0.0))
+            return fail(c, TGV_EINVAL, "camera %d: bad size, focal, weight or NULL depth map", i);
+        VoteCam& V = vc[(size_t)i];
+        memcpy(V.origin, C.origin, sizeof V.origin);
+        memcpy(V.rot, C.rot, sizeof V.rot);
+        V.fx = C.fx;
+        V.fy = C.fy;
+        V.cx = C.cx;
+        V.cy = C.cy;
+        V.width = C.width;
+        V.height = C.height;
+        V.vote_weight = C.vote_weight;
+        const int mx = std::max(C.width, C.height);
+        int nl = 1;
+        while ((1 << nl) <= mx) ++nl;  // 1 + floor(log2(max(w, h)))
+        V.nlev = nl;
+        int w = C.width, h = C.height;
+        for (int L = 0; L < nl; ++L) {
+            V.lw[L] = w;
+            V.lh[L] = h;
+            V.lev_off[L] = total;
+            total += (int64_t)w * h;
+            w = (w + 1) / 2;
+            h = (h + 1) / 2;
+        }
+    }
+    c->loaded = false;
+    float* d_depth = nullptr;
+    VoteCam* d_cams = nullptr;
+    if (cudaMalloc(&d_depth, sizeof(float) * (size_t)std::max<int64_t>(1, total)) != cudaSuccess ||
+        cudaMalloc(&d_cams, sizeof(VoteCam) * (size_t)std::max(1, ncams)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(d_depth);
+        return fail(c, TGV_ENOMEM, "depth pyramid allocation of %.2f GB failed", total * 4e-9);
+    }
+    auto cleanup = [&]() {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(d_depth);
+        cudaFree(d_cams);
+    };
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < ncams && e == cudaSuccess; ++i) {
+        const VoteCam& V = vc[(size_t)i];
+        e = cudaMemcpyAsync(d_depth + V.lev_off[0], depths[i], sizeof(float) * (size_t)V.lw[0] * V.lh[0],
+                            cudaMemcpyHostToDevice, c->stream);
+        for (int L = 1; L < V.nlev && e == cudaSuccess; ++L) {
+            pyramid_level_kernel<<<148 * 4, 256, 0, c->stream>>>(d_depth + V.lev_off[L - 1], V.lw[L - 1], V.lh[L - 1],
+                                                                  d_depth + V.lev_off[L], V.lw[L], V.lh[L]);
+            e = cudaGetLastError();
+        }
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_cams, vc.data(), sizeof(VoteCam) * (size_t)ncams, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream);
+    if (e == cudaSuccess) {
+        if (c->slots == 8)
+            vote_kernel<8><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth, c->g, grid_origin[0], grid_origin[1],
+                                                           grid_origin[2], voxel_size, voxel_radius, c->hist16,
+                                                           c->d_maxc);
+        else
+            vote_kernel<16><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth, c->g, grid_origin[0],
+                                                            grid_origin[1], grid_origin[2], voxel_size, voxel_radius,
+                                                            c->hist16, c->d_maxc);
+        e = cudaGetLastError();
+    }
+    cleanup();
+    if (e != cudaSuccess) return fail(c, TGV_ECUDA, "voting: %s", cudaGetErrorString(e));
+    return finish_counts(c);
+}
+
+int tgv_read_counts(tgv_ctx* c, uint32_t* out, int64_t n)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!out) return fail(c, TGV_EINVAL, "out is NULL");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "no histograms");
+    const int64_t need = (int64_t)c->g.nzl * c->g.ny * c->g.nx * c->nbins;
+    if (n != need) return fail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n, (long long)need);
+    uint32_t* d = nullptr;
+    if (cudaMalloc(&d, sizeof(uint32_t) * (size_t)need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ENOMEM, "readback buffer");
+    }
+    unpack_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(c->hist16, c->g, c->slots, c->nbins, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, d, sizeof(uint32_t) * (size_t)need, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(c, TGV_ECUDA, "read counts: %s", cudaGetErrorString(e));
     return TGV_OK;
 }
 

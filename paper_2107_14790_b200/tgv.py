@@ -26,7 +26,7 @@ FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
            "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_model", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
-           "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from"]
+           "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -45,6 +45,13 @@ class tgv_timing(ctypes.Structure):
                 ("energy_ms", ctypes.c_double), ("halo_ms", ctypes.c_double), ("dual_launches", ctypes.c_int64),
                 ("primal_launches", ctypes.c_int64), ("fused_launches", ctypes.c_int64),
                 ("energy_launches", ctypes.c_int64), ("halo_exchanges", ctypes.c_int64)]
+
+
+class tgv_camera(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_double * 3), ("rot", ctypes.c_double * 9), ("fx", ctypes.c_double),
+                ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("vote_weight", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
 
 
 class tgv_info_t(ctypes.Structure):
@@ -79,6 +86,9 @@ def _load():
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp)]
     lib.tgv_group_iterate.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i32]
     lib.tgv_group_energy.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp]
+    lib.tgv_vote_depth_maps.argtypes = [vp, ctypes.POINTER(tgv_camera), ctypes.c_int, ctypes.POINTER(vp), vp,
+                                        ctypes.c_double, ctypes.c_double]
+    lib.tgv_read_counts.argtypes = [vp, vp, i64]
     lib.tgv_restrict_from.argtypes = [vp, vp]
     lib.tgv_prolong_from.argtypes = [vp, vp]
     lib.tgv_destroy.argtypes = [vp]
@@ -201,6 +211,28 @@ def tgv_info(ctx) -> dict:
 
 def tgv_destroy(ctx):
     lib.tgv_destroy(ctx)
+
+
+def tgv_vote_depth_maps(ctx, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, voxel_radius=0.5):
+    """cams: dicts (origin, rot 3x3 world<-camera, fx, fy, cx, cy, width, height, vote_weight);
+    depths: float32 [h, w] host arrays (NaN = no depth)."""
+    arr = (tgv_camera * max(1, len(cams)))()
+    for i, c in enumerate(cams):
+        arr[i].origin[:] = [float(x) for x in c["origin"]]
+        arr[i].rot[:] = [float(x) for x in np.asarray(c["rot"], dtype=np.float64).reshape(-1)]
+        arr[i].fx, arr[i].fy, arr[i].cx, arr[i].cy = c["fx"], c["fy"], c["cx"], c["cy"]
+        arr[i].width, arr[i].height, arr[i].vote_weight = c["width"], c["height"], c.get("vote_weight", 1)
+    ds = [np.ascontiguousarray(d, dtype=np.float32) for d in depths]
+    ptrs = (ctypes.c_void_p * max(1, len(ds)))(*[d.ctypes.data for d in ds])
+    o = np.asarray(grid_origin, dtype=np.float64)
+    _check(lib.tgv_vote_depth_maps(ctx, arr, len(cams), ptrs, o.ctypes.data, float(voxel_size), float(voxel_radius)),
+           ctx)
+
+
+def tgv_read_counts(ctx, out):
+    p, n = _host_ptr(out, np.uint32)
+    _check(lib.tgv_read_counts(ctx, p, n), ctx)
+    return out
 
 
 def tgv_restrict_from(coarse, fine):
@@ -377,6 +409,15 @@ class Solver:
         """'fused' (default), 'split', or a TGV_SCHEDULE_* value."""
         tgv_set_schedule(self.ctx, {"fused": SCHEDULE_FUSED, "split": SCHEDULE_SPLIT}.get(schedule, schedule))
         return self
+
+    def vote(self, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, voxel_radius=0.5):
+        """NEXT-2: histograms of this slab from depth maps by Alg. 1 on the GPU; state reset."""
+        tgv_vote_depth_maps(self.ctx, cams, depths, grid_origin, voxel_size, voxel_radius)
+        return self
+
+    def read_counts(self):
+        nz, ny, nx = self.local_shape
+        return tgv_read_counts(self.ctx, np.empty((nz, ny, nx, self.nbins), np.uint32))
 
     def restrict_from(self, fine: "Solver"):
         """NEXT-1: this coarse solver's histograms = 2x2x2 sums of `fine`'s; state reset."""
