@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default=None,
+                    help="default: C2 (BASELINE configs[1]) on 1 GPU, C4 (configs[3], 1024^3 z-slabs) on 2/4/8")
     ap.add_argument("--iters", type=int, default=None, help="iterations per step (default: the workload's)")
     ap.add_argument("--schedule", default="fused", choices=["fused", "split"])
     ap.add_argument("--model", default="tgv", choices=["tgv", "tvl1"], help="tvl1: NEXT-4 (Eq. 1)")
@@ -48,7 +49,46 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
-    return ap.parse_args()
+    ap.add_argument("--vote", action="store_true", help="NEXT-2: measure GPU Alg. 1 voting instead of the solve")
+    a = ap.parse_args()
+    if a.workload is None:
+        a.workload = "C2" if int(os.environ.get("WORLD_SIZE", a.gpus)) == 1 else "C4"
+    return a
+
+
+# workloads whose inputs are voted on the GPU (bit-identical to the CPU generator,
+# tests/test_gpu_vote.py) because a host vote of 10^9 voxels x 64 cameras is slow
+GPU_VOTED = {"C3", "C4"}
+
+
+def cams_of(wl):
+    return [{"origin": c.origin, "rot": c.rot, "fx": c.f, "fy": c.f, "cx": c.width / 2.0, "cy": c.height / 2.0,
+             "width": c.width, "height": c.height, "vote_weight": c.vote_weight} for c in wl.cams]
+
+
+def render_shared(wl, rank, world):
+    """All depth maps of the workload; with several ranks each renders every world-th
+    camera and the maps are exchanged (torch.distributed all_gather_object)."""
+    import synth
+    if world == 1:
+        return synth.render_depths(wl)
+    import copy
+
+    import torch.distributed as dist
+    mine = list(range(rank, len(wl.cams), world))
+    # keep each camera's noise stream: render_depths numbers cameras 0.., so render one at a time
+    out = {}
+    for i in mine:
+        one = copy.copy(wl)
+        one.cams = [wl.cams[i]]
+        d = synth.render_depths_indexed(one, i)
+        out[i] = d
+    gathered = [None] * world
+    dist.all_gather_object(gathered, out)
+    allmaps = {}
+    for g in gathered:
+        allmaps.update(g)
+    return [allmaps[i] for i in range(len(wl.cams))]
 
 
 def slab(nz, rank, world):
@@ -117,14 +157,20 @@ class ClockSampler:
 
 def cpu_oracle_rate(workload: str, target_s: float, steps: int = 0, warmup: int = 0):
     """Time the fp64 oracle (as it stands) on this host on a bounded sample of
-    the workload: the full grid for k iterations, all host threads."""
+    the workload: the full grid (or, above 256^3 voxels, a 16-plane slab of it as
+    its own grid) for k iterations, all host threads."""
     import oracle
     import synth
     wl = synth.workload(workload)
-    h = synth.make_histograms(workload)
+    nx, ny, nz = wl.shape
+    zs = nz if wl.nvox <= 256 ** 3 else 16
+    h = synth.make_histograms(workload, 0, zs)
+    shape = (nx, ny, zs)
     threads = oracle.max_threads()
-    o = oracle.Oracle(wl.shape, lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma,
+    o = oracle.Oracle(shape, lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma,
                       centers=np.asarray(wl.centers)).load(h)
+    nvox = nx * ny * zs
+    what = f"{workload} full grid {wl.shape}" if zs == nz else f"{workload} planes 0..{zs} ({nx}x{ny}x{zs})"
     t0 = time.perf_counter()
     o.iterate(1, threads=threads)
     t1 = time.perf_counter() - t0
@@ -135,12 +181,12 @@ def cpu_oracle_rate(workload: str, target_s: float, steps: int = 0, warmup: int 
         for _ in range(steps):
             o.iterate(1, threads=threads)
         el = time.perf_counter() - t0
-        return wl.nvox * steps / el, threads, f"{workload} full grid {wl.shape}, {steps} timed iterations of 1", el
+        return nvox * steps / el, threads, f"{what}, {steps} timed iterations of 1", el
     k = int(max(1, min(1000, round(target_s / max(t1, 1e-6)))))
     t0 = time.perf_counter()
     o.iterate(k, threads=threads)
     el = time.perf_counter() - t0
-    return wl.nvox * k / el, threads, f"{workload} full grid {wl.shape}, {k} iterations (after 1 warm-up)", el
+    return nvox * k / el, threads, f"{what}, {k} iterations (after 1 warm-up)", el
 
 
 def run_reference(a):
@@ -160,6 +206,39 @@ def run_reference(a):
     }), flush=True)
 
 
+def run_vote(a, s, wl, rank, world, z0, z1, barrier_fn=None):
+    """NEXT-2 measurement: GPU Alg. 1 (H2D of the depth maps, pyramids, votes,
+    u16/u8 packing) per step; metric = voxel-camera votes per second, all ranks."""
+    import torch
+    import torch.distributed as dist
+    cams, depths = cams_of(wl), render_shared(wl, rank, world)
+    nx, ny, _ = wl.shape
+    for _ in range(a.warmup):
+        s.vote(cams, depths, voxel_radius=wl.voxel_radius)
+    if barrier_fn:
+        barrier_fn()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        s.vote(cams, depths, voxel_radius=wl.voxel_radius)
+    torch.cuda.synchronize()
+    el = torch.tensor([(time.perf_counter() - t0) / a.steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    votes = wl.nvox * len(cams)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Alg. 1 voxel-camera lookups/sec (NEXT-2 GPU voting)", "value": votes / float(el[0]),
+            "unit": "lookups/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": float(el[0]) * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "cameras": len(cams),
+                       "step": "H2D depth maps + pyramids + Alg. 1 votes + count packing + state init"},
+        }), flush=True)
+    s.close()
+    return None
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -177,14 +256,20 @@ def run_ours(a):
     iters = a.iters or wl.iters
     nx, ny, nz = wl.shape
     z0, z1 = slab(nz, rank, world)
-    counts = synth.make_histograms(a.workload, z0, z1)
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
     if world > 1:
         s = Solver.distributed(wl.shape, list(wl.centers), z0, z1, local, **kw)
     else:
         s = Solver(wl.shape, list(wl.centers), device=local, **kw)
     s.set_schedule(a.schedule).set_model(a.model)
-    s.load(counts)
+    if a.vote:
+        return run_vote(a, s, wl, rank, world, z0, z1, barrier_fn=(dist.barrier if world > 1 else None))
+    if a.workload in GPU_VOTED:  # NEXT-2 on the GPU: the same counts as synth.make_histograms
+        s.vote(cams_of(wl), render_shared(wl, rank, world), voxel_radius=wl.voxel_radius)
+        counts = s.read_counts() if (z1 - z0) * ny * nx * 32 <= (16 << 30) else None
+    else:
+        counts = synth.make_histograms(a.workload, z0, z1)
+        s.load(counts)
     info = s.info()
     nvox_local = (z1 - z0) * ny * nx
     # NEXT-1: coarser levels (single GPU), allocated outside the timed region
@@ -273,7 +358,7 @@ def run_ours(a):
 
     # ---- e2e: host buffers, H2D + D2H inside the timed region ------------------
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and counts is not None:
         hc = torch.from_numpy(counts).pin_memory()
         hu = torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory()
         from paper_2107_14790_b200 import tgv

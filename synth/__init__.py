@@ -247,6 +247,20 @@ def render_depths(wl: Workload):
     return depths
 
 
+def render_depths_indexed(wl: Workload, cam_id: int):
+    """Depth map of the single camera wl.cams[0], drawn with global camera index cam_id."""
+    lib = _lib()
+    prims = (_Prim * len(wl.prims))()
+    for i, (k, a) in enumerate(wl.prims):
+        prims[i].kind = k
+        prims[i].a[: len(a)] = list(a)
+    cams = _cams_struct(wl.cams)
+    d = np.empty((wl.cams[0].height, wl.cams[0].width), dtype=np.float32)
+    lib.synth_render(prims, len(wl.prims), ctypes.byref(cams[0]), cam_id, wl.seed, wl.noise, wl.floaters,
+                     d.ctypes.data)
+    return d
+
+
 def vote(cams, depths, nx, ny, z0, z1, r):
     """Alg. 1 over global planes [z0, z1) of an nx*ny*? grid -> uint32 [z1-z0, ny, nx, 8]."""
     lib = _lib()
