@@ -91,12 +91,6 @@ def render_shared(wl, rank, world):
     return [allmaps[i] for i in range(len(wl.cams))]
 
 
-def slab(nz, rank, world):
-    base, rem = divmod(nz, world)
-    z0 = rank * base + min(rank, rem)
-    return z0, z0 + base + (1 if rank < rem else 0)
-
-
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -245,6 +239,7 @@ def run_ours(a):
 
     import synth
     from paper_2107_14790_b200 import Solver
+    from paper_2107_14790_b200.tgv import slab
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -275,6 +275,29 @@ def tgv_group_energy(ctxs) -> np.ndarray:
     return out
 
 
+# ---- multi-rank bootstrap -------------------------------------------------------------
+def broadcast_unique_id(device=0):
+    """Rank 0's NCCL unique id (tgv_get_unique_id) on every rank of the default
+    torch.distributed group; None for a single rank."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_world_size() == 1:
+        return None
+    dev = f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if dist.get_rank() == 0:
+        t.copy_(torch.frombuffer(bytearray(tgv_get_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def slab(nz: int, rank: int, world: int):
+    """z-slab [z0, z1) of `rank`: contiguous, in rank order, sizes differing by at most one."""
+    base, rem = divmod(nz, world)
+    z0 = rank * base + min(rank, rem)
+    return z0, z0 + base + (1 if rank < rem else 0)
+
+
 # ---- convenience wrappers ---------------------------------------------------------
 class Group:
     """z-slabs [cuts[r], cuts[r+1]) of one grid in this process (tgv_create_group)."""
@@ -356,16 +379,10 @@ class Solver:
 
     @classmethod
     def distributed(cls, shape, centers, z_begin, z_end, device, **kw):
-        import torch
+        """One rank of a z-slab decomposition: the NCCL unique id is broadcast with torch.distributed."""
         import torch.distributed as dist
         rank, world = dist.get_rank(), dist.get_world_size()
-        uid = None
-        if world > 1:
-            t = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
-            if rank == 0:
-                t.copy_(torch.frombuffer(bytearray(tgv_get_unique_id()), dtype=torch.uint8))
-            dist.broadcast(t, 0)
-            uid = bytes(t.cpu().numpy().tobytes())
+        uid = broadcast_unique_id(device)
         return cls(shape, centers, z_begin=z_begin, z_end=z_end, rank=rank, nranks=world, uid=uid, device=device, **kw)
 
     @property
