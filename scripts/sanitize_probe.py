@@ -1,0 +1,28 @@
+"""Small runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2107_14790_b200 import Group, Solver  # noqa: E402
+from paper_2107_14790_b200.multilevel import coarse_to_fine  # noqa: E402
+
+C8 = [-0.875 + 0.25 * b for b in range(8)]
+shape = (70, 33, 21)
+h = synth.random_histograms(shape, 1)
+for sched in ("fused", "split"):
+    s = Solver(shape, C8).set_schedule(sched).load(h).iterate(3)
+    s.energy()
+    s.close()
+os.environ["TGV_FUSED_IMPL"] = "regs"
+Solver(shape, C8).load(h).iterate(3).close()
+os.environ.pop("TGV_FUSED_IMPL")
+Solver(shape, C8).set_model("tvl1").load(h).iterate(3).close()
+Group(shape, [0, 7, 21], C8).load(h).iterate(3).close()
+coarse_to_fine(shape, h, C8, levels=2, iters=2).close()
+cam = {"origin": (35.0, 16.0, -40.0), "rot": np.eye(3), "fx": 40.0, "fy": 40.0, "cx": 32.0, "cy": 32.0,
+       "width": 64, "height": 64}
+Solver(shape, C8).vote([cam], [np.full((64, 64), 50.0, np.float32)]).iterate(2).close()
+print("sanitize probe done")

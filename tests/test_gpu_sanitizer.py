@@ -1,0 +1,27 @@
+"""compute-sanitizer memcheck / racecheck / synccheck over small runs of every
+kernel: TMA rings, mbarriers, shared-memory exchange planes,
+the split, TV-L1, group, multilevel and voting paths."""
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    res = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                          os.path.join(ROOT, "scripts", "sanitize_probe.py")],
+                         capture_output=True, text=True, timeout=1500)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert "sanitize probe done" in out
+    assert re.search(r"ERROR SUMMARY: 0 errors|SUMMARY: 0 hazards displayed \(0 errors, 0 warnings\)", out), \
+        out[-4000:]
