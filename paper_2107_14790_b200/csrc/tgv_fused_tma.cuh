@@ -98,23 +98,24 @@ constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
 
 // Ring depths: u is read at planes s and s+1, v / p / q / histogram at plane s only;
 // each ring prefetches two planes beyond what step s reads.
+// v, p, q and the histogram of a plane travel together on one ring ("x").
 template <int HB>
 struct TmaRings {
-    static constexpr int NU = 4, NV = 3, NPQ = HB <= 16 ? 3 : 2, NH = HB <= 16 ? 3 : 2;
+    static constexpr int NU = 4, NX = HB <= 16 ? 3 : 2;
 };
 
 template <int TY, int HB>
 struct alignas(128) TmaSmem {
     static constexpr int R = TY + 2;
     using Rg = TmaRings<HB>;
-    float u[Rg::NU][2][R][TMA_BW];    // ring: u_k, u_{k-1}
-    float v[Rg::NV][6][R][TMA_BW];    // ring: v_k(3), v_{k-1}(3)
-    float pq[Rg::NPQ][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
+    float u[Rg::NU][2][R][TMA_BW];   // ring: u_k, u_{k-1}
+    float v[Rg::NX][6][R][TMA_BW];   // ring: v_k(3), v_{k-1}(3)
+    float pq[Rg::NX][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
     float out[13][TY][32];            // staged outputs: u, v(3), p(3), q(6) of iteration k+1
-    uint8_t h[Rg::NH][TY][32 * HB];   // ring: histograms of the owned rows
+    uint8_t h[Rg::NX][TY][32 * HB];  // ring: histograms of the owned rows
     float suv[2][4][R][TMA_CW];       // ubar, vbar(3) of plane s (parity)
     float sr[2][7][R][TMA_CW];        // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
-    uint64_t bar_u[Rg::NU], bar_v[Rg::NV], bar_pq[Rg::NPQ], bar_h[Rg::NH];
+    uint64_t bar_u[Rg::NU], bar_x[Rg::NX];
 };
 
 struct TmaArgs {
@@ -161,8 +162,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             c.ph ^= 1u;
         }
     };
-    Cur iu{0, 0u}, iv{0, 0u}, ipq{0, 0u}, ih{0, 0u};  // issue cursors (tid0 only)
-    Cur cu{0, 0u}, cv{0, 0u}, cpq{0, 0u}, ch{0, 0u};  // wait cursors (all threads)
+    Cur iu{0, 0u}, ix{0, 0u};  // issue cursors (tid0 only)
+    Cur cu{0, 0u}, cx{0, 0u};  // wait cursors (all threads)
 
     if (tid0) {
         if (smem_addr(smem_raw) & 127) __trap();
@@ -171,9 +172,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         prefetch_map(&m_ld6);
         prefetch_map(&m_h);
         for (int k = 0; k < Rg::NU; ++k) mbar_init(&S.bar_u[k], 1);
-        for (int k = 0; k < Rg::NV; ++k) mbar_init(&S.bar_v[k], 1);
-        for (int k = 0; k < Rg::NPQ; ++k) mbar_init(&S.bar_pq[k], 1);
-        for (int k = 0; k < Rg::NH; ++k) mbar_init(&S.bar_h[k], 1);
+        for (int k = 0; k < Rg::NX; ++k) mbar_init(&S.bar_x[k], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -204,6 +203,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         const bool needQ = halo ? (lane >= 16 && r >= 1 && r <= TY) : r >= 1;
         const bool own = !halo && r >= 1 && r <= TY;  // owned row (TMA stores clip at nx, ny)
         const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
+        const float mxl = xl ? 1.f : 0.f, myl = yl ? 1.f : 0.f;
 
         // Every plane of the segment's sequence is loaded so that each ring slot is
         // filled in order (mbarrier phase = fill count); planes past the stored range are
@@ -218,32 +218,20 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
             tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
         };
-        auto issue_v = [&](int s) {
-            const int st = iv.st;
-            adv(iv, Rg::NV);
-            mbar_expect_tx(&S.bar_v[st], 6 * R * TMA_BW * 4);
-            tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
-            tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_v[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
-        };
-        auto issue_pq = [&](int s) {
-            const int st = ipq.st;
-            adv(ipq, Rg::NPQ);
-            mbar_expect_tx(&S.bar_pq[st], 9 * R * TMA_BW * 4);
-            tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
-            tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_pq[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
-        };
-        auto issue_h = [&](int s) {
-            const int st = ih.st;
-            adv(ih, Rg::NH);
-            mbar_expect_tx(&S.bar_h[st], TY * 32 * HB);
-            tma_load3(&S.h[st][0][0], &m_h, &S.bar_h[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
+        auto issue_x = [&](int s) {  // v_k, v_{k-1}, p_k, q_k and the counts of plane s
+            const int st = ix.st;
+            adv(ix, Rg::NX);
+            mbar_expect_tx(&S.bar_x[st], 15 * R * TMA_BW * 4 + TY * 32 * HB);
+            tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
+            tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
+            tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
+            tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
+            tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
         };
 
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
             for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
-            for (int tz = zs - 1; tz < zs - 1 + Rg::NV - 1; ++tz) issue_v(tz);
-            for (int tz = zs - 1; tz < zs - 1 + Rg::NPQ - 1; ++tz) issue_pq(tz);
-            for (int tz = zs - 1; tz < zs - 1 + Rg::NH - 1; ++tz) issue_h(tz);
+            for (int tz = zs - 1; tz < zs - 1 + Rg::NX - 1; ++tz) issue_x(tz);
         }
         mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
         int su = cu.st;
@@ -265,25 +253,23 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             const bool zl = zg < g.nz - 1, zf = zg > 0;
 
             mbar_wait(&S.bar_u[cu.st], cu.ph);
-            mbar_wait(&S.bar_v[cv.st], cv.ph);
-            mbar_wait(&S.bar_pq[cpq.st], cpq.ph);
-            mbar_wait(&S.bar_h[ch.st], ch.ph);
+            mbar_wait(&S.bar_x[cx.st], cx.ph);
 
             // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
             const float* U0 = &S.u[su][0][r][bc];
             const float* U1 = &S.u[cu.st][0][r][bc];
-            const float* V0 = &S.v[cv.st][0][r][bc];
-            const float* PQ = &S.pq[cpq.st][0][r][bc];
+            const float* V0 = &S.v[cx.st][0][r][bc];
+            const float* PQ = &S.pq[cx.st][0][r][bc];
             constexpr int F = R * TMA_BW;  // field stride in a ring slot
             const float uk = U0[0], um = U0[F];
             float vk[3], vb[3];
     #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 vk[k] = V0[k * F];
-                vb[k] = 2.f * vk[k] - V0[(3 + k) * F];
+                vb[k] = fmaf(2.f, vk[k], -V0[(3 + k) * F]);
             }
-            const float ub = 2.f * uk - um;          // (a3) ubar(s)
-            const float ub1 = 2.f * U1[0] - U1[F];   // ubar(s+1)
+            const float ub = fmaf(2.f, uk, -um);           // (a3) ubar(s)
+            const float ub1 = fmaf(2.f, U1[0], -U1[F]);    // ubar(s+1)
             float pk[3], qk[6];
     #pragma unroll
             for (int k = 0; k < 3; ++k) pk[k] = PQ[k * F];
@@ -291,7 +277,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             for (int m = 0; m < 6; ++m) qk[m] = PQ[(3 + m) * F];
             Hist hc{};
             if (own) {
-                const uint8_t* hp = &S.h[ch.st][r - 1][lane * HB];
+                const uint8_t* hp = &S.h[cx.st][r - 1][lane * HB];
                 if constexpr (HB == 8) {
                     const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
                     hc.w[0] = v2.x;
@@ -315,15 +301,11 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             __syncthreads();             // S1
             if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
                 if (s + Rg::NU - 1 <= ze + 1) issue_u(s + Rg::NU - 1);
-                if (s + Rg::NV - 1 <= ze) issue_v(s + Rg::NV - 1);
-                if (s + Rg::NPQ - 1 <= ze) issue_pq(s + Rg::NPQ - 1);
-                if (s + Rg::NH - 1 <= ze) issue_h(s + Rg::NH - 1);
+                if (s + Rg::NX - 1 <= ze) issue_x(s + Rg::NX - 1);
             }
             su = cu.st;
             adv(cu, Rg::NU);
-            adv(cv, Rg::NV);
-            adv(cpq, Rg::NPQ);
-            adv(ch, Rg::NH);
+            adv(cx, Rg::NX);
 
             // ---- phase E: (a1) dual D(s)
             float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -347,9 +329,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 for (int k = 0; k < 3; ++k) {
                     const float vx = S.suv[par][1 + k][r][cc - 1];
                     const float vy = S.suv[par][1 + k][r - 1][cc];
-                    dx[k] = (xl ? vb[k] : 0.f) - vx;
-                    dy[k] = (yl ? vb[k] : 0.f) - vy;
-                    dz[k] = (zl ? vb[k] : 0.f) - in.vb[k];
+                    dx[k] = fmaf(mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
+                    dy[k] = fmaf(myl, vb[k], -vy);
+                    dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
                 }
                 const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
                                     0.5f * (dz[1] + dy[2])};
@@ -380,8 +362,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
                 const float pxm = S.sr[pr][0][r][cc - 1];
                 const float pym = S.sr[pr][1][r - 1][cc];
-                const float divp = ((xl ? in.pn[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? in.pn[1] : 0.f) - (yf ? pym : 0.f)) +
-                                   ((zl1 ? in.pn[2] : 0.f) - (zf1 ? in.pz : 0.f));
+                const float divp = fmaf(mxl, in.pn[0], -(xf ? pxm : 0.f)) + fmaf(myl, in.pn[1], -(yf ? pym : 0.f)) +
+                                   fmaf(zl1 ? 1.f : 0.f, in.pn[2], -(zf1 ? in.pz : 0.f));
                 const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
                 const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
                 const float w0 = (xl ? qxx - in.qn[0] : 0.f) + (yl ? qyxy - in.qn[3] : 0.f) + (zl1 ? qn[4] - in.qn[4] : 0.f);

@@ -97,9 +97,15 @@ __device__ __forceinline__ float hist_prox(float ut, float t, const HistRaw<SLOT
     float cnt[SLOTS];
     float W = 0.f;
 #pragma unroll
-    for (int b = 0; b < SLOTS; ++b) {
-        cnt[b] = hist_count<SLOTS, CT>(h, b);
-        W += cnt[b];
+    for (int b = 0; b < SLOTS; ++b) cnt[b] = hist_count<SLOTS, CT>(h, b);
+    if constexpr (sizeof(CT) == 1) {  // byte sums in the integer pipe (exact), then the same magic conversion
+        unsigned int wsum = 0;
+#pragma unroll
+        for (int k = 0; k < SLOTS / 4; ++k) wsum = __dp4a(h.w[k], 0x01010101u, wsum);
+        W = __uint_as_float(0x4B000000u | wsum) - 8388608.0f;  // W <= 16 * 255 < 2^23
+    } else {
+#pragma unroll
+        for (int b = 0; b < SLOTS; ++b) W += cnt[b];
     }
     float r = W, P = -INFINITY;
 #pragma unroll
@@ -113,7 +119,13 @@ __device__ __forceinline__ float hist_prox(float ut, float t, const HistRaw<SLOT
 
 // Euclidean projection factor onto the ball of radius a for squared norm n2:
 // min(1, a / |x|)  (n2 = 0 -> 1; a = 0 -> 0 unless n2 = 0)
-__device__ __forceinline__ float proj_scale(float n2, float a) { return fminf(1.f, a * rsqrtf(n2)); }
+// (rsqrt.approx.ftz: one MUFU; a squared norm below 2^-126 counts as 0 -> factor 1)
+__device__ __forceinline__ float proj_scale(float n2, float a)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(n2));
+    return fminf(1.f, a * r);
+}
 
 // ---------------------------------------------------------------------------
 // Field pointers of one iteration (host fills them from the rotating buffers)
@@ -145,8 +157,8 @@ __global__ void __launch_bounds__(256) split_dual_kernel(const IterPtrs a, const
     const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
     const bool xf = x > 0, yf = y > 0, zf = zg > 0;
     const int sy = g.px, sz = g.plane;
-    auto ubar = [&](int o) { return 2.f * __ldg(a.uk + o) - __ldg(a.um + o); };
-    auto vbar = [&](int k, int o) { return 2.f * __ldg(a.vk[k] + o) - __ldg(a.vm[k] + o); };
+    auto ubar = [&](int o) { return fmaf(2.f, __ldg(a.uk + o), -__ldg(a.um + o)); };
+    auto vbar = [&](int k, int o) { return fmaf(2.f, __ldg(a.vk[k] + o), -__ldg(a.vm[k] + o)); };
     // ---- loads
     const float u0 = ubar(i);
     const float ux = xl ? ubar(i + 1) : 0.f, uy = yl ? ubar(i + sy) : 0.f, uz = zl ? ubar(i + sz) : 0.f;
@@ -173,9 +185,9 @@ __global__ void __launch_bounds__(256) split_dual_kernel(const IterPtrs a, const
     float dx[3], dy[3], dz[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        dx[k] = (xl ? vb[k] : 0.f) - vbx[k];
-        dy[k] = (yl ? vb[k] : 0.f) - vby[k];
-        dz[k] = (zl ? vb[k] : 0.f) - vbz[k];
+        dx[k] = fmaf(xl ? 1.f : 0.f, vb[k], -vbx[k]);
+        dy[k] = fmaf(yl ? 1.f : 0.f, vb[k], -vby[k]);
+        dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -vbz[k]);
     }
     const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]), 0.5f * (dz[1] + dy[2])};
 #pragma unroll
@@ -223,7 +235,8 @@ __global__ void __launch_bounds__(256) split_primal_kernel(const IterPtrs a, con
     for (int k = 0; k < 3; ++k) vo[k] = __ldg(a.vk[k] + i);
     const auto h = load_hist<SLOTS, CT>(a.hist, (int64_t)z * g.plane + y * g.px + x);
     // ---- u
-    const float divp = ((xl ? p[0] : 0.f) - pxm) + ((yl ? p[1] : 0.f) - pym) + ((zl ? p[2] : 0.f) - pzm);
+    const float divp = fmaf(xl ? 1.f : 0.f, p[0], -pxm) + fmaf(yl ? 1.f : 0.f, p[1], -pym) +
+                       fmaf(zl ? 1.f : 0.f, p[2], -pzm);
     const float un = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uo), sp.tl, h, C);
     // ---- v: (div2 q)_k = sum_l D+_l q_kl
     float w[3];
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(256) tvl1_dual_kernel(const IterPtrs a, const 
     const int i = eoff(g, x, y, z);
     const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
     const int sy = g.px, sz = g.plane;
-    auto ubar = [&](int o) { return 2.f * __ldg(a.uk + o) - __ldg(a.um + o); };
+    auto ubar = [&](int o) { return fmaf(2.f, __ldg(a.uk + o), -__ldg(a.um + o)); };
     const float u0 = ubar(i);
     const float ux = xl ? ubar(i + 1) : 0.f, uy = yl ? ubar(i + sy) : 0.f, uz = zl ? ubar(i + sz) : 0.f;
     float p[3];
@@ -385,11 +398,11 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs
         const bool zl = zg < g.nz - 1, zf = zg > 0;
 
         // (a3) over-relaxed iterate at planes s and s+1
-        const float ub = 2.f * u0.uk - u0.um;
+        const float ub = fmaf(2.f, u0.uk, -u0.um);
         float vb[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) vb[k] = 2.f * u0.vk[k] - u0.vm[k];
-        const float ub1 = 2.f * u1.uk - u1.um;
+        for (int k = 0; k < 3; ++k) vb[k] = fmaf(2.f, u0.vk[k], -u0.vm[k]);
+        const float ub1 = fmaf(2.f, u1.uk, -u1.um);
         sm_uv[par][0][ty][lane] = ub;
         sm_uv[par][1][ty][lane] = vb[0];
         sm_uv[par][2][ty][lane] = vb[1];
@@ -416,9 +429,9 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs
             for (int k = 0; k < 3; ++k) {
                 const float vx = __shfl_up_sync(FULL, vb[k], 1);
                 const float vy = sm_uv[par][1 + k][ty - 1][lane];
-                dx[k] = (xl ? vb[k] : 0.f) - (xf ? vx : 0.f);
-                dy[k] = (yl ? vb[k] : 0.f) - (yf ? vy : 0.f);
-                dz[k] = (zl ? vb[k] : 0.f) - (zf ? vbp[k] : 0.f);
+                dx[k] = fmaf(xl ? 1.f : 0.f, vb[k], -(xf ? vx : 0.f));
+                dy[k] = fmaf(yl ? 1.f : 0.f, vb[k], -(yf ? vy : 0.f));
+                dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -(zf ? vbp[k] : 0.f));
             }
             const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
                                 0.5f * (dz[1] + dy[2])};
@@ -448,8 +461,9 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs
             const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
             const float pxm = __shfl_up_sync(FULL, pn_p[0], 1);
             const float pym = sm_r[pr][0][ty - 1][lane];
-            const float divp = ((xl ? pn_p[0] : 0.f) - (xf ? pxm : 0.f)) + ((yl ? pn_p[1] : 0.f) - (yf ? pym : 0.f)) +
-                               ((zl1 ? pn_p[2] : 0.f) - (zf1 ? pz_pp : 0.f));
+            const float divp = fmaf(xl ? 1.f : 0.f, pn_p[0], -(xf ? pxm : 0.f)) +
+                               fmaf(yl ? 1.f : 0.f, pn_p[1], -(yf ? pym : 0.f)) +
+                               fmaf(zl1 ? 1.f : 0.f, pn_p[2], -(zf1 ? pz_pp : 0.f));
             const float qxx = __shfl_down_sync(FULL, qn_p[0], 1);
             const float qxy = __shfl_down_sync(FULL, qn_p[3], 1);
             const float qxz = __shfl_down_sync(FULL, qn_p[4], 1);
