@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         const int y = y0 - 1 + r;
         // p is needed on rows 0..TY (row 0 feeds D-_y of row 1) and at column x0-1;
         // q on rows 1..TY+1 and at column x0+32 (halo lanes: owned rows only)
-        const bool needP = halo ? (lane < 16 && r >= 1 && r <= TY) : r <= TY;
-        const bool needQ = halo ? (lane >= 16 && r >= 1 && r <= TY) : r >= 1;
         const bool own = !halo && r >= 1 && r <= TY;  // owned row (TMA stores clip at nx, ny)
+        // warp role: 0 owned row, 1 bottom y-halo row (p only), 2 top y-halo row (q only), 3 x-halo
+        const int role = halo ? 3 : (r == 0 ? 1 : (r == TY + 1 ? 2 : 0));
+        // every cell of the tile and its halo is at distance >= 1 from the x and y grid ends
+        const bool tile_int = x0 >= 2 && x0 + 32 <= g.nx - 2 && y0 >= 2 && y0 + TY <= g.ny - 2;
         const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
         const float mxl = xl ? 1.f : 0.f, myl = yl ? 1.f : 0.f;
 
@@ -250,7 +252,6 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         auto step = [&](auto PAR, int s, const Carry& in, Carry& o) {
             constexpr int par = decltype(PAR)::value, pr = par ^ 1;
             const int zg = g.z0 + s;
-            const bool zl = zg < g.nz - 1, zf = zg > 0;
 
             mbar_wait(&S.bar_u[cu.st], cu.ph);
             mbar_wait(&S.bar_x[cx.st], cx.ph);
@@ -307,72 +308,102 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             adv(cu, Rg::NU);
             adv(cx, Rg::NX);
 
-            // ---- phase E: (a1) dual D(s)
+            // ---- phases E (a1: dual D(s)) and F (a2: primal Pm(s-1)), specialised per warp
+            // role and, for the owned rows of interior tiles away from the z ends, without
+            // the boundary masks (all of them are true there)
             float pn[3] = {0.f, 0.f, 0.f}, qn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (needP) {
-                const float ux = S.suv[par][0][r][cc + 1];
-                const float uy = S.suv[par][0][r + 1][cc];
-                const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
-                pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
-                pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
-                pn[2] = fmaf(sp.sigma, g2 - vb[2], pk[2]);
-                const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
-                pn[0] *= f;
-                pn[1] *= f;
-                pn[2] *= f;
-            }
-            if (needQ) {
-                // vbar is exactly 0 outside the grid (TMA zero fill, zero halo planes at the
-                // global z ends), so the "l > 0" guards of D- are implicit
-                float dx[3], dy[3], dz[3];
-    #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const float vx = S.suv[par][1 + k][r][cc - 1];
-                    const float vy = S.suv[par][1 + k][r - 1][cc];
-                    dx[k] = fmaf(mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
-                    dy[k] = fmaf(myl, vb[k], -vy);
-                    dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
+            auto ef = [&](auto ROLEc, auto INTc) {
+                constexpr int ROLE = decltype(ROLEc)::value;
+                constexpr bool INT = decltype(INTc)::value;
+                const bool zl = INT || zg < g.nz - 1;
+                const bool needP = ROLE == 0 || ROLE == 1 || (ROLE == 3 && lane < 16 && r >= 1 && r <= TY);
+                const bool needQ = ROLE == 0 || ROLE == 2 || (ROLE == 3 && lane >= 16 && r >= 1 && r <= TY);
+                const bool xl_ = INT || xl, yl_ = INT || yl, xf_ = INT || xf, yf_ = INT || yf;
+                if (needP) {
+                    const float ux = S.suv[par][0][r][cc + 1];
+                    const float uy = S.suv[par][0][r + 1][cc];
+                    const float g0 = xl_ ? ux - ub : 0.f, g1 = yl_ ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
+                    pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
+                    pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
+                    pn[2] = fmaf(sp.sigma, g2 - vb[2], pk[2]);
+                    const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
+                    pn[0] *= f;
+                    pn[1] *= f;
+                    pn[2] *= f;
                 }
-                const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
-                                    0.5f * (dz[1] + dy[2])};
-    #pragma unroll
-                for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], qk[m]);
-                const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
-                                               2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
-                                           sp.alpha0);
-    #pragma unroll
-                for (int m = 0; m < 6; ++m) qn[m] *= f;
-            }
-            S.sr[par][0][r][cc] = pn[0];
-            S.sr[par][1][r][cc] = pn[1];
-            S.sr[par][2][r][cc] = qn[0];
-            S.sr[par][3][r][cc] = qn[3];
-            S.sr[par][4][r][cc] = qn[4];
-            S.sr[par][5][r][cc] = qn[1];
-            S.sr[par][6][r][cc] = qn[5];
-            if (own) {
-    #pragma unroll
-                for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
-    #pragma unroll
-                for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
-            }
-
-            // ---- phase F: (a2) primal Pm(s-1) on owned rows
-            if (own && s - 1 >= zs) {
-                const bool zl1 = zg - 1 < g.nz - 1, zf1 = zg - 1 > 0;
-                const float pxm = S.sr[pr][0][r][cc - 1];
-                const float pym = S.sr[pr][1][r - 1][cc];
-                const float divp = fmaf(mxl, in.pn[0], -(xf ? pxm : 0.f)) + fmaf(myl, in.pn[1], -(yf ? pym : 0.f)) +
-                                   fmaf(zl1 ? 1.f : 0.f, in.pn[2], -(zf1 ? in.pz : 0.f));
-                const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1], qxz = S.sr[pr][4][r][cc + 1];
-                const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc], qyyz = S.sr[pr][6][r + 1][cc];
-                const float w0 = (xl ? qxx - in.qn[0] : 0.f) + (yl ? qyxy - in.qn[3] : 0.f) + (zl1 ? qn[4] - in.qn[4] : 0.f);
-                const float w1 = (xl ? qxy - in.qn[3] : 0.f) + (yl ? qyyy - in.qn[1] : 0.f) + (zl1 ? qn[5] - in.qn[5] : 0.f);
-                const float w2 = (xl ? qxz - in.qn[4] : 0.f) + (yl ? qyyz - in.qn[5] : 0.f) + (zl1 ? qn[2] - in.qn[2] : 0.f);
-                S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
-                S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
-                S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
-                S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
+                if (needQ) {
+                    // vbar is exactly 0 outside the grid (TMA zero fill, zero halo planes at the
+                    // global z ends), so the "l > 0" guards of D- are implicit
+                    float dx[3], dy[3], dz[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const float vx = S.suv[par][1 + k][r][cc - 1];
+                        const float vy = S.suv[par][1 + k][r - 1][cc];
+                        dx[k] = fmaf(INT ? 1.f : mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
+                        dy[k] = fmaf(INT ? 1.f : myl, vb[k], -vy);
+                        dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
+                    }
+                    const float e[6] = {dx[0], dy[1], dz[2], 0.5f * (dy[0] + dx[1]), 0.5f * (dz[0] + dx[2]),
+                                        0.5f * (dz[1] + dy[2])};
+#pragma unroll
+                    for (int m = 0; m < 6; ++m) qn[m] = fmaf(sp.sigma, e[m], qk[m]);
+                    const float f = proj_scale(qn[0] * qn[0] + qn[1] * qn[1] + qn[2] * qn[2] +
+                                                   2.f * (qn[3] * qn[3] + qn[4] * qn[4] + qn[5] * qn[5]),
+                                               sp.alpha0);
+#pragma unroll
+                    for (int m = 0; m < 6; ++m) qn[m] *= f;
+                }
+                if (ROLE != 2) {  // p_x, p_y (x- and y-neighbours' div p)
+                    S.sr[par][0][r][cc] = pn[0];
+                    S.sr[par][1][r][cc] = pn[1];
+                }
+                if (ROLE != 1) {  // q_xx, q_xy, q_xz (x-neighbour) and q_xy, q_yy, q_yz (y-neighbour of div2 q)
+                    S.sr[par][2][r][cc] = qn[0];
+                    S.sr[par][3][r][cc] = qn[3];
+                    S.sr[par][4][r][cc] = qn[4];
+                    S.sr[par][5][r][cc] = qn[1];
+                    S.sr[par][6][r][cc] = qn[5];
+                }
+                if constexpr (ROLE == 0) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
+#pragma unroll
+                    for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
+                    if (s - 1 >= zs) {  // (a2) primal Pm(s-1)
+                        const bool zl1 = INT || zg - 1 < g.nz - 1, zf1 = INT || zg - 1 > 0;
+                        const float pxm = S.sr[pr][0][r][cc - 1];
+                        const float pym = S.sr[pr][1][r - 1][cc];
+                        const float divp = fmaf(INT ? 1.f : mxl, in.pn[0], -(xf_ ? pxm : 0.f)) +
+                                           fmaf(INT ? 1.f : myl, in.pn[1], -(yf_ ? pym : 0.f)) +
+                                           fmaf(zl1 ? 1.f : 0.f, in.pn[2], -(zf1 ? in.pz : 0.f));
+                        const float qxx = S.sr[pr][2][r][cc + 1], qxy = S.sr[pr][3][r][cc + 1],
+                                    qxz = S.sr[pr][4][r][cc + 1];
+                        const float qyxy = S.sr[pr][3][r + 1][cc], qyyy = S.sr[pr][5][r + 1][cc],
+                                    qyyz = S.sr[pr][6][r + 1][cc];
+                        const float w0 = (xl_ ? qxx - in.qn[0] : 0.f) + (yl_ ? qyxy - in.qn[3] : 0.f) +
+                                         (zl1 ? qn[4] - in.qn[4] : 0.f);
+                        const float w1 = (xl_ ? qxy - in.qn[3] : 0.f) + (yl_ ? qyyy - in.qn[1] : 0.f) +
+                                         (zl1 ? qn[5] - in.qn[5] : 0.f);
+                        const float w2 = (xl_ ? qxz - in.qn[4] : 0.f) + (yl_ ? qyyz - in.qn[5] : 0.f) +
+                                         (zl1 ? qn[2] - in.qn[2] : 0.f);
+                        S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
+                        S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
+                        S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
+                        S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
+                    }
+                }
+            };
+            using F0 = std::false_type;
+            switch (role) {  // warp-uniform
+                case 0:
+                    if (tile_int && zg - 1 > 0 && zg < g.nz - 1)
+                        ef(std::integral_constant<int, 0>{}, std::true_type{});
+                    else
+                        ef(std::integral_constant<int, 0>{}, F0{});
+                    break;
+                case 1: ef(std::integral_constant<int, 1>{}, F0{}); break;
+                case 2: ef(std::integral_constant<int, 2>{}, F0{}); break;
+                default: ef(std::integral_constant<int, 3>{}, F0{}); break;
             }
             fence_proxy_async();
             __syncthreads();  // S2

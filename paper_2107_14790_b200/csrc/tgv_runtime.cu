@@ -274,11 +274,11 @@ int launch_tvl1(tgv_ctx* c, int phase)
 int fused_zc(const tgv_ctx* c)
 {
     if (c->fused_zc > 0) return c->fused_zc;
-    if (c->fused_tma) {  // lock-step chunk of the persistent schedule: <= 128 planes, a divisor if possible
-        if (c->g.nzl <= 128) return c->g.nzl;
-        for (int d = 128; d >= 64; --d)
+    if (c->fused_tma) {  // lock-step chunk of the persistent schedule: <= 256 planes, a divisor if possible
+        if (c->g.nzl <= 256) return c->g.nzl;
+        for (int d = 256; d >= 128; --d)
             if (c->g.nzl % d == 0) return d;
-        return 128;
+        return 256;
     }
     const int tiles = c->fused_tma ? ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY)
                                    : ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
