@@ -100,6 +100,7 @@ def heightfield(base, waves, zmin, zmax):
     for o, (amp, kx, ky, ph) in enumerate(waves):
         a[1 + 4 * o: 5 + 4 * o] = [amp, kx, ky, ph]
     a[21], a[22] = zmin, zmax
+    a[23] = sum(abs(amp) * math.hypot(kx, ky) for amp, kx, ky, _ in waves)  # Lipschitz bound of H
     return (2, a)
 
 

@@ -106,14 +106,22 @@ static double intersect(const synth_prim* p, const double o[3], const double d[3
         } else {
             return INFINITY;
         }
-        double step = 0.25 / dl; /* 0.25 voxel steps along the ray */
+        /* Lipschitz-bounded steps (a[23] bounds |grad H|): along the ray the height gap
+         * f = z - H shrinks at most by (|d_z| + L |d_xy|) per unit t, so stepping by
+         * f / that rate never jumps over the surface; the last bracket is bisected. */
+        const double L = p->a[23] > 0.0 ? p->a[23] : 10.0;
+        const double rate = fabs(d[2]) + L * sqrt(d[0] * d[0] + d[1] * d[1]);
+        const double min_step = 0.05 / dl;
         double prev_t = t, prev_f = o[2] + t * d[2] - hf_height(p, o[0] + t * d[0], o[1] + t * d[1]);
         if (prev_f <= 0.0) return t > 1e-9 ? t : INFINITY;
-        for (t += step; t <= tend + step; t += step) {
+        while (t <= tend) {
+            double step = prev_f / rate;
+            if (step < min_step) step = min_step;
+            t += step;
             double f = o[2] + t * d[2] - hf_height(p, o[0] + t * d[0], o[1] + t * d[1]);
             if (f <= 0.0) {
                 double lo = prev_t, hi = t;
-                for (int it = 0; it < 40; ++it) {
+                for (int it = 0; it < 24; ++it) {
                     double mid = 0.5 * (lo + hi);
                     double fm = o[2] + mid * d[2] - hf_height(p, o[0] + mid * d[0], o[1] + mid * d[1]);
                     if (fm > 0.0) lo = mid; else hi = mid;
