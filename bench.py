@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--model", default="tgv", choices=["tgv", "tvl1"], help="tvl1: NEXT-4 (Eq. 1)")
     ap.add_argument("--levels", type=int, default=1,
                     help="NEXT-1: coarse-to-fine levels (a step = the whole multilevel solve, iters per level)")
+    ap.add_argument("--out-of-core", type=int, default=0, metavar="LEAF_VOXELS",
+                    help="NEXT-3: out-of-core coarse-to-fine over z-slab leaves of <= LEAF_VOXELS voxels "
+                         "(host-resident counts and levels; a step = the whole solve, --levels levels)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -233,6 +236,53 @@ def run_vote(a, s, wl, rank, world, z0, z1, barrier_fn=None):
     return None
 
 
+def run_out_of_core(a):
+    """NEXT-3 measurement: the out-of-core solve (paper_2107_14790_b200.out_of_core)
+    from host counts to host u, v; every leaf's H2D / prolongation / iterations / D2H
+    inside the timed region.  Metric: voxel-iterations of all leaves of all levels per
+    second (host to host, so it is its own end-to-end number)."""
+    import torch
+
+    import synth
+    from paper_2107_14790_b200 import out_of_core
+    from paper_2107_14790_b200.multilevel import level_shapes
+    wl = synth.workload(a.workload)
+    iters = a.iters or 200
+    levels = max(1, a.levels)
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
+    counts = synth.make_histograms(a.workload)
+    vox_its = sum(int(np.prod(sh)) for sh in level_shapes(wl.shape, levels)) * iters
+    run = lambda st=None: out_of_core.solve(wl.shape, counts, list(wl.centers), levels=levels, iters=iters,
+                                            leaf_voxels=a.out_of_core, stats=st, **kw)
+    for _ in range(a.warmup):
+        run()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        st = {}
+        run(st)
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / a.steps
+    clk = clocks.stop()
+    leaves = st["leaves"][::-1]  # finest first
+    h2d = int(counts.nbytes + sum(4 * 4 * np.prod(sh) for sh in level_shapes(wl.shape, levels)[1:]))
+    d2h = int(sum(4 * 4 * np.prod(sh) for sh in level_shapes(wl.shape, levels)))
+    print(json.dumps({
+        "metric": "TGV voxel-iterations/sec (NEXT-3 out-of-core leaves, host to host)", "value": vox_its / el,
+        "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "levels": levels,
+                   "iters_per_level": iters, "leaf_voxels": a.out_of_core, "leaves_per_level_finest_first": leaves,
+                   "step": "per level, per z-slab leaf: H2D fine counts + coarsen, H2D parent u/v + prolong "
+                           "(borders frozen), iters fused iterations, D2H u, v"},
+        "e2e": {"value": vox_its / el, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "clocks": clk,
+    }), flush=True)
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -411,6 +461,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.out_of_core:
+        run_out_of_core(a)
     else:
         run_ours(a)
 

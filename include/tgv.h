@@ -186,6 +186,44 @@ int tgv_vote_depth_maps(tgv_ctx* ctx, const tgv_camera* cams, int ncams, const f
  * [z_end-z_begin][ny][nx][nbins].  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
 int tgv_read_counts(tgv_ctx* ctx, uint32_t* counts_out, int64_t n_counts);
 
+/* NEXT-3 out-of-core leaves with frozen borders (§4.5, Fig. 9:
+ * "we update the indicator for all cubes inside the current leaf's border (set A)
+ * while the indicator for neighboring cubes outside of the border (set B) is
+ * frozen"; R23).  tgv_create_leaf makes a single-GPU context over the
+ * z-slab [z_begin, z_end) of an nx x ny x nz grid (a leaf); its halo planes hold
+ * the B set and are never exchanged.  The primal (u, v) on B is frozen; the dual
+ * variables the leaf's update reads there (p on the plane below, q on the plane
+ * above) keep evolving from the frozen primal exactly as a slab's halo duals do
+ * in the fused schedule.  Leaves run the fused TGV schedule only (set_schedule
+ * SPLIT / set_model TVL1 return TGV_EINVAL).  tgv_set_border writes the border
+ * plane below (side 0, global z_begin - 1) or above (side 1, global z_end):
+ * u, v (3 planes), p (3), q (6), each [ny][nx] floats, NULL = zeros; call it
+ * after tgv_load_histograms / tgv_reset / tgv_prolong_slab (which reset the
+ * state; tgv_prolong_slab also fills the borders from the parents).  A leaf at
+ * the global end has no border on that side.  Errors: TGV_EINVAL, TGV_ESTATE,
+ * TGV_ECUDA. */
+int tgv_create_leaf(const tgv_layout* layout, const tgv_params* params, int cuda_device, tgv_ctx** out);
+int tgv_set_border(tgv_ctx* ctx, int side, const float* u, const float* v, const float* p, const float* q);
+
+/* NEXT-1/3: this context's histograms as sums of factor^3 fine voxels (DESIGN.md
+ * R18) of a finer grid nxf x nyf x nzf with ceil(n_fine / factor) = n on every axis;
+ * fine_counts: host uint32 [fz1-fz0][nyf][nxf][nbins] for the fine planes
+ * [factor * z_begin, min(factor * z_end, nzf)) this slab covers; then the state is
+ * reset as by tgv_load_histograms.  Errors: TGV_EINVAL, TGV_ERANGE, TGV_ENOMEM, TGV_ECUDA. */
+int tgv_load_histograms_coarsened(tgv_ctx* ctx, const uint32_t* fine_counts, int64_t n_fine, int64_t nxf,
+                                  int64_t nyf, int64_t nzf, int factor);
+
+/* NEXT-1/3: restart this (loaded) context from a coarser solution held on the host:
+ * u_c [cnz][cny][cnx] and v_c [3][cnz][cny][cnx] of coarse global planes
+ * [cz0, cz0 + cnz) of the 2x-coarser grid (cnx = ceil(nx/2), cny = ceil(ny/2)).
+ * u = parent u, v = parent v / 2, ubar = u, vbar = v, p = q = 0 (R19); for a leaf
+ * the frozen border planes get their parents' u and v as well (the B set of
+ * "equal to indicator values of their parenting cubes").
+ * The slab must contain every needed parent.  Errors: TGV_EINVAL, TGV_ESTATE,
+ * TGV_ENOMEM, TGV_ECUDA. */
+int tgv_prolong_slab(tgv_ctx* ctx, const float* u_c, const float* v_c, int64_t cnx, int64_t cny, int64_t cz0,
+                     int64_t cnz);
+
 /* NEXT-1 coarse-to-fine ("coarse-to-fine scheme ... 200 iterations
  * ... on each level"; :431-433 §4.5; R18-R20).  Both need single-rank
  * contexts on one device with coarse = ceil(fine / 2) on every axis.

@@ -260,6 +260,82 @@ def coarse_to_fine(shape, counts, levels, iters, threads=1, **kw):
 
 
 # ---------------------------------------------------------------------------
+# NEXT-3 z-slab leaves with frozen borders (§4.5, Fig. 9;
+# SURVEY.md §8(f) NEXT-3; R23)
+# ---------------------------------------------------------------------------
+def leaf_step(o, threads=1):
+    """One iteration of a leaf: the scheme over the cubes of A (the
+    owned planes) while the indicator of B (the halo planes) is frozen.  The duals on
+    the edges between A and B (p on the plane below, q on the plane above) are the
+    ones a slab recomputes for its halo (oracle_dual_halo), from the frozen values."""
+    o.dual(threads)
+    o.dual_halo()
+    o.primal(threads)
+
+
+def leaf_from_parent(shape, zb, ze, counts_slab, parent_u, parent_v, **kw):
+    """Leaf [zb, ze) of a level: histograms `counts_slab`; u = parent u, v = parent v / 2,
+    ubar = u, vbar = v, p = q = 0 on A (R19); on B (planes zb-1, ze inside the grid)
+    the same parent values, frozen ("equal to indicator values of
+    their parenting cubes, which were estimated on the previous level").
+    parent_u [cnz, cny, cnx] / parent_v [3, ...]: the whole parent level."""
+    nx, ny, nz = shape
+    o = Oracle(shape, zb=zb, ze=ze, **kw).load(counts_slab)
+
+    def up(a):
+        return np.repeat(np.repeat(np.repeat(a, 2, axis=-3), 2, axis=-2), 2, axis=-1)[..., :nz, :ny, :nx]
+
+    U_, V_ = up(np.asarray(parent_u, np.float64)), up(np.asarray(parent_v, np.float64)) * 0.5
+    o.set("u", U_[zb:ze])
+    o.set("ubar", U_[zb:ze])
+    o.set("v", V_[:, zb:ze])
+    o.set("vbar", V_[:, zb:ze])
+    o.set("p", np.zeros((3, ze - zb, ny, nx)))
+    o.set("q", np.zeros((6, ze - zb, ny, nx)))
+    for z in (zb - 1, ze):
+        if 0 <= z < nz:
+            o.set_plane("u", 0, z, U_[z])
+            o.set_plane("ubar", 0, z, U_[z])
+            for d in range(3):
+                o.set_plane("v", d, z, V_[d, z])
+                o.set_plane("vbar", d, z, V_[d, z])
+    return o
+
+
+def out_of_core(shape, counts, levels, iters, leaf_voxels, threads=1, **kw):
+    """Coarse-to-fine over z-slab leaves: level by level (coarsest first), leaves of
+    max(1, leaf_voxels // (nx ny)) consecutive planes from z = 0 (a level of at most
+    leaf_voxels voxels is one leaf), each solved for `iters`
+    iterations with frozen borders from the parent level.  The coarsest level must be
+    one leaf.  Returns (u, v) of the finest level, fp64."""
+    hs = [np.asarray(counts, dtype=np.uint32)]
+    shapes = [tuple(shape)]
+    for _ in range(levels - 1):
+        hs.append(restrict_counts(hs[-1]))
+        shapes.append(tuple((n + 1) // 2 for n in shapes[-1]))
+    prev = None
+    for lev in range(levels - 1, -1, -1):
+        nx, ny, nz = shapes[lev]
+        planes = nz if nx * ny * nz <= leaf_voxels else max(1, leaf_voxels // (nx * ny))
+        if prev is None and planes < nz:
+            raise ValueError("the coarsest level must fit in one leaf")
+        u = np.zeros((nz, ny, nx))
+        v = np.zeros((3, nz, ny, nx))
+        for zb in range(0, nz, planes):
+            ze = min(zb + planes, nz)
+            if prev is None:
+                o = Oracle(shapes[lev], zb=zb, ze=ze, **kw).load(hs[lev][zb:ze])
+            else:
+                o = leaf_from_parent(shapes[lev], zb, ze, hs[lev][zb:ze], prev[0], prev[1], **kw)
+            for _ in range(iters):
+                leaf_step(o, threads)
+            u[zb:ze] = o.u
+            v[:, zb:ze] = o.get("v")
+        prev = (u, v)
+    return prev
+
+
+# ---------------------------------------------------------------------------
 # NEXT-2 histogram voting, Alg. 1 (PAPER.md:252-278)
 # ---------------------------------------------------------------------------
 class OracleCamera(ctypes.Structure):

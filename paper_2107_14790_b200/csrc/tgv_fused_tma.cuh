@@ -127,6 +127,7 @@ struct TmaArgs {
     const int* sched_off;   // CTA b owns sched[sched_off[b] .. sched_off[b+1])
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
+    int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
 };
 
 template <int TY, int SLOTS, typename CT>
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             fence_proxy_async();
             __syncthreads();  // S2
             if (tid0) {
-                if (s >= zs && s < ze) {
+                if ((s >= zs && s < ze) || (A.keep_halo_dual && (s == -1 || s == g.nzl))) {
                     tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
                     tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
                 }

@@ -323,6 +323,7 @@ struct FusedArgs {
     StepParams sp;
     Centers C;
     int z_lo, z_hi, zc;  // local planes [z_lo, z_hi) in chunks of zc, one chunk per blockIdx.z
+    int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
 };
 
 struct UV {
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs
         sm_r[par][1][ty][lane] = qn[3];
         sm_r[par][2][ty][lane] = qn[1];
         sm_r[par][3][ty][lane] = qn[5];
-        if (own && s >= zs && s < ze) {
+        if (own && ((s >= zs && s < ze) || (A.keep_halo_dual && (s == -1 || s == g.nzl)))) {
             const int o = (s + 1) * g.plane + rowoff;
 #pragma unroll
             for (int k = 0; k < 3; ++k) a.pn[k][o] = pn[k];
@@ -596,6 +597,74 @@ __global__ void prolong_kernel(const float* __restrict__ uc, const float* __rest
         vf0_prev[i] = a;
         vf1_prev[i] = b;
         vf2_prev[i] = c;
+    }
+}
+
+// NEXT-3 leaves: counts of this context's planes [0, nzc) (chunk starting at local plane zc0)
+// as sums over factor^3 fine voxels of a dense uint32 fine slab [nzf][nyf][nxf][nbins]
+// (fine plane 0 of the slab = fine plane factor * (z0 + zc0))
+template <int SLOTS>
+__global__ void coarsen_counts_kernel(const uint32_t* __restrict__ fine, int nxf, int nyf, int nzf, int factor,
+                                      int nbins, int nzc, int zc0, Geo g, uint16_t* __restrict__ H,
+                                      unsigned int* __restrict__ maxc)
+{
+    const int64_t n = (int64_t)nzc * g.ny * g.nx;
+    unsigned int m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int X = (int)(v % g.nx);
+        const int64_t r = v / g.nx;
+        const int Y = (int)(r % g.ny);
+        const int Zc = (int)(r / g.ny);  // plane within the chunk
+        unsigned int acc[SLOTS];
+        for (int b = 0; b < SLOTS; ++b) acc[b] = 0;
+        for (int dz = 0; dz < factor; ++dz) {
+            const int zf = Zc * factor + dz;
+            if (zf >= nzf) break;
+            for (int dy = 0; dy < factor; ++dy) {
+                const int yf = Y * factor + dy;
+                if (yf >= nyf) break;
+                for (int dx = 0; dx < factor; ++dx) {
+                    const int xf = X * factor + dx;
+                    if (xf >= nxf) break;
+                    const uint32_t* src = fine + (((int64_t)zf * nyf + yf) * nxf + xf) * nbins;
+                    for (int b = 0; b < nbins; ++b) acc[b] += src[b];
+                }
+            }
+        }
+        uint16_t* dst = H + ((int64_t)(Zc + zc0) * g.plane + (int64_t)Y * g.px + X) * SLOTS;
+        for (int b = 0; b < SLOTS; ++b) {
+            m = max(m, acc[b]);
+            dst[b] = (uint16_t)min(acc[b], 65535u);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxc, m);
+}
+
+// NEXT-3 leaves: prolongation from a dense coarse slab [cnz][cny][cnx] (u) / [3][...] (v)
+// whose plane 0 is coarse global plane cz0, into local planes [zlo, zhi) (halo planes
+// included) of this context: u = parent u, v = parent v / 2, in every slot listed.
+__global__ void prolong_slab_kernel(const float* __restrict__ uc, const float* __restrict__ vc, int cnx, int cny,
+                                    int cnz, int cz0, int zlo, int zhi, Geo g, float* const* __restrict__ us,
+                                    int nus, float* const* __restrict__ vs, int nvs)
+{
+    const int64_t n = (int64_t)(zhi - zlo) * g.ny * g.nx;
+    const int64_t cpl = (int64_t)cnx * cny * cnz;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(v % g.nx);
+        const int64_t r = v / g.nx;
+        const int y = (int)(r % g.ny);
+        const int zl = (int)(r / g.ny) + zlo;
+        const int zc = (g.z0 + zl) / 2 - cz0;  // parent plane within the coarse slab
+        if (zc < 0 || zc >= cnz) continue;
+        const int64_t ic = ((int64_t)zc * cny + y / 2) * cnx + x / 2;
+        const int i = eoff(g, x, y, zl);
+        const float u = uc[ic];
+        for (int k = 0; k < nus; ++k) us[k][i] = u;
+        for (int d = 0; d < 3; ++d) {
+            const float a = 0.5f * vc[d * cpl + ic];
+            for (int k = 0; k < nvs; ++k) vs[3 * k + d][i] = a;
+        }
     }
 }
 

@@ -58,6 +58,7 @@ struct tgv_ctx {
     int rank = 0, nranks = 1, device = 0;
     int schedule = TGV_SCHEDULE_FUSED;
     int model = TGV_MODEL_TGV;
+    bool leaf = false;  // NEXT-3: frozen-border leaf (tgv_create_leaf)
     int fused_zc = 0;       // 0 = automatic
     int num_sms = 148;
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
@@ -451,6 +452,7 @@ int launch_fused_tma(tgv_ctx* c)
     A.C = centers(c);
     A.z_lo = 0;
     A.z_hi = c->g.nzl;
+    A.keep_halo_dual = c->leaf ? 1 : 0;
     A.zc = fused_zc(c);
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
@@ -493,6 +495,7 @@ int launch_fused(tgv_ctx* c)
     A.C = centers(c);
     A.z_lo = 0;
     A.z_hi = c->g.nzl;
+    A.keep_halo_dual = c->leaf ? 1 : 0;
     A.zc = fused_zc(c);
     dim3 grd((c->g.nx + 29) / 30, (c->g.ny + FUSED_TY - 1) / FUSED_TY, (c->g.nzl + A.zc - 1) / A.zc);
     if (c->slots == 8 && c->count_bytes == 1) launch_fused_t<8, uint8_t>(c, A, grd);
@@ -658,6 +661,10 @@ int64_t env_int(const char* name, int64_t dflt)
 }  // namespace
 
 // =============================================================================
+namespace {
+int finish_counts(tgv_ctx* c);
+}
+
 extern "C" {
 
 const char* tgv_status_string(int s)
@@ -690,7 +697,7 @@ int tgv_get_unique_id(uint8_t uid[128])
 }
 
 static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int nranks, const uint8_t* uid, int dev,
-                       bool grouped, tgv_ctx** out)
+                       bool grouped, tgv_ctx** out, bool leaf = false)
 {
     tgv_ctx* c = nullptr;
     g_create_error[0] = 0;
@@ -710,7 +717,7 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
         return fail(c, TGV_EINVAL, "brick layouts are not supported (brick must be {0,0,0})");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TGV_EINVAL, "bad rank %d / nranks %d", rank, nranks);
     if (!grouped && (nranks == 1) != (uid == nullptr)) return fail(c, TGV_EINVAL, "uid must be NULL iff nranks == 1");
-    if (nranks == 1 && (L->z_begin != 0 || L->z_end != L->nz))
+    if (nranks == 1 && !leaf && (L->z_begin != 0 || L->z_end != L->nz))
         return fail(c, TGV_EINVAL, "single rank must own the whole grid");
     if (P->nbins < 1 || P->nbins > 16) return fail(c, TGV_EINVAL, "nbins must be in [1, 16]");
     if (!P->bin_centers) return fail(c, TGV_EINVAL, "bin_centers is NULL");
@@ -745,8 +752,9 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
     c->nranks = nranks;
     c->device = dev;
     c->slots = P->nbins <= 8 ? 8 : 16;
+    c->leaf = leaf;
     c->schedule = (int)env_int("TGV_SCHEDULE", TGV_SCHEDULE_FUSED);
-    if (c->schedule != TGV_SCHEDULE_SPLIT) c->schedule = TGV_SCHEDULE_FUSED;
+    if (c->schedule != TGV_SCHEDULE_SPLIT || leaf) c->schedule = TGV_SCHEDULE_FUSED;
     c->fused_zc = (int)env_int("TGV_FUSED_ZC", 0);
     {
         const char* impl = getenv("TGV_FUSED_IMPL");
@@ -844,11 +852,150 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
     return create_impl(L, P, rank, nranks, uid, dev, false, out);
 }
 
+// ---- NEXT-3 frozen-border leaves ------------------------------------------------------
+int tgv_create_leaf(const tgv_layout* L, const tgv_params* P, int dev, tgv_ctx** out)
+{
+    return create_impl(L, P, 0, 1, nullptr, dev, false, out, true);
+}
+
+int tgv_set_border(tgv_ctx* c, int side, const float* u, const float* v, const float* p, const float* q)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!c->leaf) return fail(c, TGV_ESTATE, "borders belong to leaf contexts (tgv_create_leaf)");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "set borders after load / prolong (they reset the state)");
+    if (side != 0 && side != 1) return fail(c, TGV_EINVAL, "side must be 0 (below) or 1 (above)");
+    const Geo& g = c->g;
+    const int z = side == 0 ? -1 : g.nzl;
+    const size_t rowb = sizeof(float) * g.nx, pitchb = sizeof(float) * g.px;
+    const int64_t pl = (int64_t)g.nx * g.ny;
+    auto put = [&](int sl, const float* src) -> int {
+        if (src)
+            CU(cudaMemcpy2DAsync(plane_ptr(c, sl, z), pitchb, src, rowb, rowb, g.ny, cudaMemcpyHostToDevice, c->stream));
+        else
+            CU(cudaMemset2DAsync(plane_ptr(c, sl, z), pitchb, 0, rowb, g.ny, c->stream));
+        return TGV_OK;
+    };
+    // the same frozen values in every rotating buffer: ubar = u, vbar = v on the border
+    for (int b = 0; b < 3; ++b) {
+        if ((rc = put(slotU(b), u))) return rc;
+        for (int k = 0; k < 3; ++k)
+            if ((rc = put(slotV(b, k), v ? v + k * pl : nullptr))) return rc;
+    }
+    for (int b = 0; b < 2; ++b) {
+        for (int k = 0; k < 3; ++k)
+            if ((rc = put(slotP(b, k), p ? p + k * pl : nullptr))) return rc;
+        for (int m = 0; m < 6; ++m)
+            if ((rc = put(slotQ(b, m), q ? q + m * pl : nullptr))) return rc;
+    }
+    CU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
+}
+
+int tgv_load_histograms_coarsened(tgv_ctx* c, const uint32_t* fine, int64_t n_fine, int64_t nxf, int64_t nyf,
+                                  int64_t nzf, int factor)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    const Geo& g = c->g;
+    if (!fine || factor < 1 || factor > 64) return fail(c, TGV_EINVAL, "NULL counts or factor outside [1, 64]");
+    if ((nxf + factor - 1) / factor != g.nx || (nyf + factor - 1) / factor != g.ny ||
+        (nzf + factor - 1) / factor != g.nz)
+        return fail(c, TGV_EINVAL, "grid is not the fine grid coarsened by %d", factor);
+    const int64_t fz0 = (int64_t)g.z0 * factor, fz1 = std::min<int64_t>(nzf, (int64_t)(g.z0 + g.nzl) * factor);
+    const int64_t per_fplane = nxf * nyf * c->nbins;
+    if (n_fine != (fz1 - fz0) * per_fplane)
+        return fail(c, TGV_EINVAL, "n_fine %lld != fine planes [%lld, %lld) x %lld", (long long)n_fine,
+                    (long long)fz0, (long long)fz1, (long long)per_fplane);
+    c->loaded = false;
+    // chunks of whole coarse planes (factor fine planes each), staging up to ~256 MB
+    const int64_t per_cplane = per_fplane * factor;
+    const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (64ll << 20) / per_cplane));
+    const int64_t need = per_cplane * cpc;
+    if (c->staging_elems < need) {
+        if (c->staging) cudaFree(c->staging);
+        c->staging = nullptr;
+        c->staging_elems = 0;
+        if (cudaMalloc(&c->staging, sizeof(uint32_t) * (size_t)need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, TGV_ENOMEM, "staging allocation failed");
+        }
+        c->staging_elems = need;
+    }
+    CU(cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream));
+    for (int z0 = 0; z0 < g.nzl; z0 += cpc) {
+        const int nzc = std::min(cpc, g.nzl - z0);
+        const int64_t f0 = (int64_t)z0 * factor, f1 = std::min<int64_t>(fz1 - fz0, (int64_t)(z0 + nzc) * factor);
+        CU(cudaMemcpyAsync(c->staging, fine + f0 * per_fplane, sizeof(uint32_t) * (size_t)((f1 - f0) * per_fplane),
+                           cudaMemcpyHostToDevice, c->stream));
+        if (c->slots == 8)
+            coarsen_counts_kernel<8><<<148 * 8, 256, 0, c->stream>>>(c->staging, (int)nxf, (int)nyf, (int)(f1 - f0),
+                                                                      factor, c->nbins, nzc, z0, g, c->hist16,
+                                                                      c->d_maxc);
+        else
+            coarsen_counts_kernel<16><<<148 * 8, 256, 0, c->stream>>>(c->staging, (int)nxf, (int)nyf,
+                                                                       (int)(f1 - f0), factor, c->nbins, nzc, z0, g,
+                                                                       c->hist16, c->d_maxc);
+        CU(cudaGetLastError());
+    }
+    return finish_counts(c);
+}
+
+int tgv_prolong_slab(tgv_ctx* c, const float* u_c, const float* v_c, int64_t cnx, int64_t cny, int64_t cz0,
+                     int64_t cnz)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    const Geo& g = c->g;
+    if (!u_c || !v_c) return fail(c, TGV_EINVAL, "NULL coarse fields");
+    if (cnx != (g.nx + 1) / 2 || cny != (g.ny + 1) / 2) return fail(c, TGV_EINVAL, "coarse slab is not nx/2 x ny/2");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "prolong into a context without histograms");
+    // planes to fill: own planes, plus the frozen border planes of a leaf that exist in the grid
+    const int zlo = (c->leaf && g.z0 > 0) ? -1 : 0;
+    const int zhi = (c->leaf && g.z0 + g.nzl < g.nz) ? g.nzl + 1 : g.nzl;
+    const int64_t need_lo = (g.z0 + zlo) / 2, need_hi = (g.z0 + zhi - 1) / 2;
+    if (cz0 > need_lo || cz0 + cnz <= need_hi)
+        return fail(c, TGV_EINVAL, "coarse slab [%lld, %lld) misses parents [%lld, %lld]", (long long)cz0,
+                    (long long)(cz0 + cnz), (long long)need_lo, (long long)need_hi);
+    CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * (size_t)g.fs, c->stream));
+    c->k = 0;
+    const size_t nc = (size_t)(cnx * cny * cnz);
+    // stream-ordered temporaries: no device-wide synchronisation, so another context's
+    // iterations keep running while this leaf is staged
+    float* d = nullptr;
+    float** d_ptrs;
+    if (cudaMallocAsync(&d, sizeof(float) * 4 * nc + sizeof(float*) * 12, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ENOMEM, "coarse slab upload buffer");
+    }
+    d_ptrs = reinterpret_cast<float**>(d + 4 * nc);  // byte offset 16 nc: pointer-aligned
+    // leaves: the border planes are frozen in every rotating slot; otherwise u_0 = u_{-1}
+    float* ptrs[12];
+    const int nus = c->leaf ? 3 : 2;
+    for (int k = 0; k < nus; ++k) ptrs[k] = slot(c, slotU(c->leaf ? k : (k == 0 ? 0 : 2)));
+    for (int k = 0; k < nus; ++k)
+        for (int dd = 0; dd < 3; ++dd) ptrs[3 + 3 * k + dd] = slot(c, slotV(c->leaf ? k : (k == 0 ? 0 : 2), dd));
+    cudaError_t e = cudaMemcpyAsync(d, u_c, sizeof(float) * nc, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d + nc, v_c, sizeof(float) * 3 * nc, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_ptrs, ptrs, sizeof(float*) * 12, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) {
+        prolong_slab_kernel<<<148 * 8, 256, 0, c->stream>>>(d, d + nc, (int)cnx, (int)cny, (int)cnz, (int)cz0, zlo,
+                                                             zhi, g, d_ptrs, nus, d_ptrs + 3, nus);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaFreeAsync(d, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, TGV_ECUDA, "prolong slab: %s", cudaGetErrorString(e));
+    return TGV_OK;
+}
+
 int tgv_set_model(tgv_ctx* c, int model)
 {
     int rc = check_ready(c);
     if (rc) return rc;
     if (model != TGV_MODEL_TGV && model != TGV_MODEL_TVL1) return fail(c, TGV_EINVAL, "unknown model %d", model);
+    if (c->leaf && model != TGV_MODEL_TGV) return fail(c, TGV_EINVAL, "leaves run the TGV model only");
     c->model = model;
     if (c->loaded) {  // restart from the initialisation (v = q = 0 for both models)
         if ((rc = init_from_hist(c))) return rc;
@@ -863,6 +1010,8 @@ int tgv_set_schedule(tgv_ctx* c, int schedule)
     if (rc) return rc;
     if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT)
         return fail(c, TGV_EINVAL, "unknown schedule %d", schedule);
+    if (c->leaf && schedule != TGV_SCHEDULE_FUSED)
+        return fail(c, TGV_EINVAL, "leaves run the fused schedule only (it updates the border duals)");
     c->schedule = schedule;  // the state representation is shared: switching keeps the iterate
     return TGV_OK;
 }
@@ -951,7 +1100,7 @@ static bool coarse_of(const tgv_ctx* coarse, const tgv_ctx* fine)
 {
     return coarse->g.nx == (fine->g.nx + 1) / 2 && coarse->g.ny == (fine->g.ny + 1) / 2 &&
            coarse->g.nz == (fine->g.nz + 1) / 2 && coarse->nranks == 1 && fine->nranks == 1 &&
-           coarse->nbins == fine->nbins && coarse->device == fine->device;
+           coarse->nbins == fine->nbins && coarse->device == fine->device && !coarse->leaf && !fine->leaf;
 }
 
 int tgv_restrict_from(tgv_ctx* c, const tgv_ctx* fine)

@@ -26,7 +26,8 @@ FIELDS = {"u": [0], "v": [1, 2, 3], "ubar": [4], "vbar": [5, 6, 7], "p": [8, 9, 
 EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset", "tgv_iterate", "tgv_read_u",
            "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_model", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
-           "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts"]
+           "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts",
+           "tgv_create_leaf", "tgv_set_border", "tgv_load_histograms_coarsened", "tgv_prolong_slab"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -91,6 +92,11 @@ def _load():
     lib.tgv_read_counts.argtypes = [vp, vp, i64]
     lib.tgv_restrict_from.argtypes = [vp, vp]
     lib.tgv_prolong_from.argtypes = [vp, vp]
+    lib.tgv_create_leaf.argtypes = [ctypes.POINTER(tgv_layout), ctypes.POINTER(tgv_params), ctypes.c_int,
+                                    ctypes.POINTER(vp)]
+    lib.tgv_set_border.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp]
+    lib.tgv_load_histograms_coarsened.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
+    lib.tgv_prolong_slab.argtypes = [vp, vp, vp, i64, i64, i64, i64]
     lib.tgv_destroy.argtypes = [vp]
     lib.tgv_destroy.restype = None
     lib.tgv_status_string.argtypes = [ctypes.c_int]
@@ -243,6 +249,35 @@ def tgv_prolong_from(fine, coarse):
     _check(lib.tgv_prolong_from(fine, coarse), fine)
 
 
+def tgv_create_leaf(shape, z_begin, z_end, centers, lam, alpha0, alpha1, tau, sigma, device=0):
+    nx, ny, nz = shape
+    L = tgv_layout(nx, ny, nz, z_begin, z_end, (ctypes.c_int32 * 3)(0, 0, 0))
+    P, keep = _params(centers, lam, alpha0, alpha1, tau, sigma)
+    out = ctypes.c_void_p()
+    _check(lib.tgv_create_leaf(ctypes.byref(L), ctypes.byref(P), device, ctypes.byref(out)))
+    return out
+
+
+def tgv_set_border(ctx, side: int, u=None, v=None, p=None, q=None):
+    ptr = [None if a is None else _host_ptr(a, np.float32)[0] for a in (u, v, p, q)]
+    _check(lib.tgv_set_border(ctx, int(side), *ptr), ctx)
+
+
+def tgv_load_histograms_coarsened(ctx, fine_counts, fine_shape, factor: int):
+    p, n = _host_ptr(fine_counts, np.uint32)
+    nxf, nyf, nzf = fine_shape
+    _check(lib.tgv_load_histograms_coarsened(ctx, p, n, nxf, nyf, nzf, int(factor)), ctx)
+
+
+def tgv_prolong_slab(ctx, u_c, v_c, cz0: int):
+    """u_c float32 [cnz, cny, cnx], v_c float32 [3, cnz, cny, cnx]: coarse planes [cz0, cz0 + cnz)."""
+    pu, nu = _host_ptr(u_c, np.float32)
+    pv, nv = _host_ptr(v_c, np.float32)
+    cnz, cny, cnx = u_c.shape
+    assert nv == 3 * nu
+    _check(lib.tgv_prolong_slab(ctx, pu, pv, cnx, cny, int(cz0), cnz), ctx)
+
+
 def _params(centers, lam, alpha0, alpha1, tau, sigma):
     c = (ctypes.c_float * len(centers))(*[float(x) for x in centers])
     return tgv_params(len(centers), ctypes.cast(c, ctypes.POINTER(ctypes.c_float)), lam, alpha0, alpha1, tau,
@@ -378,6 +413,16 @@ class Solver:
                               nranks, uid, device)
 
     @classmethod
+    def leaf(cls, shape, centers, z_begin, z_end, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25, device=0):
+        """NEXT-3: a leaf over z-slab [z_begin, z_end) whose border planes are frozen (tgv_create_leaf)."""
+        self = cls.__new__(cls)
+        self.shape = tuple(int(s) for s in shape)
+        self.z_begin, self.z_end, self.nbins = int(z_begin), int(z_end), len(centers)
+        self.ctx = tgv_create_leaf(self.shape, self.z_begin, self.z_end, centers, lam, alpha0, alpha1, tau, sigma,
+                                   device)
+        return self
+
+    @classmethod
     def distributed(cls, shape, centers, z_begin, z_end, device, **kw):
         """One rank of a z-slab decomposition: the NCCL unique id is broadcast with torch.distributed."""
         import torch.distributed as dist
@@ -412,6 +457,16 @@ class Solver:
             tgv_read_field(self.ctx, f, out[k])
         return out[0] if len(ids) == 1 else out
 
+    def get_into(self, name: str, out):
+        """Like get(), into caller-provided float32 arrays (out[k] C-contiguous per component)."""
+        ids = FIELDS[name]
+        if len(ids) == 1:
+            tgv_read_field(self.ctx, ids[0], out)
+        else:
+            for k, f in enumerate(ids):
+                tgv_read_field(self.ctx, f, out[k])
+        return out
+
     def set(self, name: str, arr):
         ids = FIELDS[name]
         arr = np.ascontiguousarray(arr, dtype=np.float32).reshape((len(ids),) + self.local_shape)
@@ -444,6 +499,24 @@ class Solver:
     def prolong_from(self, coarse: "Solver"):
         """NEXT-1: restart this solver from `coarse`'s solution (u, v / 2; duals zero)."""
         tgv_prolong_from(self.ctx, coarse.ctx)
+        return self
+
+    def set_border(self, side: int, u=None, v=None, p=None, q=None):
+        """NEXT-3: frozen values of the plane below (side 0) / above (side 1) a leaf."""
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float32)
+        tgv_set_border(self.ctx, side, f(u), f(v), f(p), f(q))
+        return self
+
+    def load_coarsened(self, fine_counts, fine_shape, factor: int):
+        """NEXT-1/3: histograms = sums of factor^3 fine voxels; fine_counts covers this slab's fine planes."""
+        tgv_load_histograms_coarsened(self.ctx, np.ascontiguousarray(fine_counts, dtype=np.uint32), fine_shape,
+                                      factor)
+        return self
+
+    def prolong_slab(self, u_c, v_c, cz0: int):
+        """NEXT-1/3: restart from host coarse u / v planes [cz0, cz0 + len(u_c)) (borders of a leaf too)."""
+        tgv_prolong_slab(self.ctx, np.ascontiguousarray(u_c, dtype=np.float32),
+                         np.ascontiguousarray(v_c, dtype=np.float32), cz0)
         return self
 
     def set_model(self, model):
