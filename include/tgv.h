@@ -205,13 +205,23 @@ int tgv_read_counts(tgv_ctx* ctx, uint32_t* counts_out, int64_t n_counts);
 int tgv_create_leaf(const tgv_layout* layout, const tgv_params* params, int cuda_device, tgv_ctx** out);
 int tgv_set_border(tgv_ctx* ctx, int side, const float* u, const float* v, const float* p, const float* q);
 
+/* NEXT-3: move a leaf to another z-slab [z_begin, z_end) of the same grid with the
+ * same number of planes, keeping its device memory (a pool of leaves streams a level
+ * without allocating).  The context is unloaded afterwards: load its histograms
+ * next.  Errors: TGV_EINVAL (bad slab / different size), TGV_ESTATE (not a leaf). */
+int tgv_leaf_rebind(tgv_ctx* ctx, int64_t z_begin, int64_t z_end);
+
 /* NEXT-1/3: this context's histograms as sums of factor^3 fine voxels (DESIGN.md
  * R18) of a finer grid nxf x nyf x nzf with ceil(n_fine / factor) = n on every axis;
- * fine_counts: host uint32 [fz1-fz0][nyf][nxf][nbins] for the fine planes
- * [factor * z_begin, min(factor * z_end, nzf)) this slab covers; then the state is
- * reset as by tgv_load_histograms.  Errors: TGV_EINVAL, TGV_ERANGE, TGV_ENOMEM, TGV_ECUDA. */
-int tgv_load_histograms_coarsened(tgv_ctx* ctx, const uint32_t* fine_counts, int64_t n_fine, int64_t nxf,
-                                  int64_t nyf, int64_t nzf, int factor);
+ * fine_counts: host unsigned integers of count_bytes = 1, 2 or 4 bytes each,
+ * [fz1-fz0][nyf][nxf][nbins], for the fine planes [factor * z_begin,
+ * min(factor * z_end, nzf)) this slab covers (n_fine elements); then the state is
+ * reset as by tgv_load_histograms.  Narrow counts cut the host-to-device bytes;
+ * the sums are formed in 32 bits on the device.  Pinned host memory overlaps the
+ * copies with other contexts' work.
+ * Errors: TGV_EINVAL, TGV_ERANGE (a sum > 65535), TGV_ENOMEM, TGV_ECUDA. */
+int tgv_load_histograms_coarsened(tgv_ctx* ctx, const void* fine_counts, int count_bytes, int64_t n_fine,
+                                  int64_t nxf, int64_t nyf, int64_t nzf, int factor);
 
 /* NEXT-1/3: restart this (loaded) context from a coarser solution held on the host:
  * u_c [cnz][cny][cnx] and v_c [3][cnz][cny][cnx] of coarse global planes
@@ -249,6 +259,18 @@ int tgv_prolong_from(tgv_ctx* fine, const tgv_ctx* coarse);
  * half-step.  Blocks until the device work is done.
  * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load / poisoned), TGV_ECUDA, TGV_ENCCL. */
 int tgv_iterate(tgv_ctx* ctx, int32_t n);
+
+/* tgv_iterate without the final wait: returns once the n iterations are enqueued
+ * on the context's CUDA stream, so the host can stage another context meanwhile
+ * (NEXT-3 leaf pipelining).  Launch errors are returned; execution errors surface
+ * at the next synchronising call (tgv_sync, tgv_read_*, tgv_energy, tgv_iterate).
+ * Single-rank contexts without per-kernel timing only.
+ * Errors: as tgv_iterate, plus TGV_ESTATE (timing enabled / nranks > 1). */
+int tgv_iterate_async(tgv_ctx* ctx, int32_t n);
+
+/* Wait for the context's enqueued work; reports asynchronous CUDA / NCCL errors.
+ * Errors: TGV_ECUDA, TGV_ENCCL. */
+int tgv_sync(tgv_ctx* ctx);
 
 /* Copy this rank's u to the host: u_out float [z_end-z_begin][ny][nx];
  * n_voxels must equal (z_end-z_begin)*ny*nx.  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */

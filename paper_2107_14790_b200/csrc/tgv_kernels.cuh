@@ -603,8 +603,8 @@ __global__ void prolong_kernel(const float* __restrict__ uc, const float* __rest
 // NEXT-3 leaves: counts of this context's planes [0, nzc) (chunk starting at local plane zc0)
 // as sums over factor^3 fine voxels of a dense uint32 fine slab [nzf][nyf][nxf][nbins]
 // (fine plane 0 of the slab = fine plane factor * (z0 + zc0))
-template <int SLOTS>
-__global__ void coarsen_counts_kernel(const uint32_t* __restrict__ fine, int nxf, int nyf, int nzf, int factor,
+template <int SLOTS, typename T>
+__global__ void coarsen_counts_kernel(const T* __restrict__ fine, int nxf, int nyf, int nzf, int factor,
                                       int nbins, int nzc, int zc0, Geo g, uint16_t* __restrict__ H,
                                       unsigned int* __restrict__ maxc)
 {
@@ -626,7 +626,7 @@ __global__ void coarsen_counts_kernel(const uint32_t* __restrict__ fine, int nxf
                 for (int dx = 0; dx < factor; ++dx) {
                     const int xf = X * factor + dx;
                     if (xf >= nxf) break;
-                    const uint32_t* src = fine + (((int64_t)zf * nyf + yf) * nxf + xf) * nbins;
+                    const T* src = fine + (((int64_t)zf * nyf + yf) * nxf + xf) * nbins;
                     for (int b = 0; b < nbins; ++b) acc[b] += src[b];
                 }
             }

@@ -77,6 +77,8 @@ struct tgv_ctx {
     double* d_out = nullptr;
     unsigned int* d_maxc = nullptr;
     uint32_t* staging = nullptr;
+    float* upload = nullptr;  // grow-only device buffer for tgv_prolong_slab's coarse fields
+    size_t upload_bytes = 0;
     int64_t staging_elems = 0;
     int energy_blocks = 0;
     int64_t device_bytes = 0;
@@ -665,6 +667,20 @@ namespace {
 int finish_counts(tgv_ctx* c);
 }
 
+template <typename T>
+void launch_coarsen_t(tgv_ctx* c, const void* staging, int nxf, int nyf, int nzf, int factor, int nzc, int z0)
+{
+    if (c->slots == 8)
+        coarsen_counts_kernel<8, T><<<148 * 8, 256, 0, c->stream>>>(static_cast<const T*>(staging), nxf, nyf, nzf,
+                                                                     factor, c->nbins, nzc, z0, c->g, c->hist16,
+                                                                     c->d_maxc);
+    else
+        coarsen_counts_kernel<16, T><<<148 * 8, 256, 0, c->stream>>>(static_cast<const T*>(staging), nxf, nyf, nzf,
+                                                                      factor, c->nbins, nzc, z0, c->g, c->hist16,
+                                                                      c->d_maxc);
+}
+
+
 extern "C" {
 
 const char* tgv_status_string(int s)
@@ -858,6 +874,22 @@ int tgv_create_leaf(const tgv_layout* L, const tgv_params* P, int dev, tgv_ctx**
     return create_impl(L, P, 0, 1, nullptr, dev, false, out, true);
 }
 
+int tgv_leaf_rebind(tgv_ctx* c, int64_t z_begin, int64_t z_end)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!c->leaf) return fail(c, TGV_ESTATE, "rebind applies to leaf contexts (tgv_create_leaf)");
+    if (z_begin < 0 || z_end > c->L.nz || z_end - z_begin != c->g.nzl)
+        return fail(c, TGV_EINVAL, "rebind to [%lld, %lld): the slab must lie in [0, %lld) and keep %d planes",
+                    (long long)z_begin, (long long)z_end, (long long)c->L.nz, c->g.nzl);
+    CU(cudaStreamSynchronize(c->stream));
+    c->L.z_begin = z_begin;
+    c->L.z_end = z_end;
+    c->g.z0 = (int)z_begin;
+    c->loaded = false;  // the counts of the old slab are not this slab's
+    return TGV_OK;
+}
+
 int tgv_set_border(tgv_ctx* c, int side, const float* u, const float* v, const float* p, const float* q)
 {
     int rc = check_ready(c);
@@ -892,13 +924,16 @@ int tgv_set_border(tgv_ctx* c, int side, const float* u, const float* v, const f
     return TGV_OK;
 }
 
-int tgv_load_histograms_coarsened(tgv_ctx* c, const uint32_t* fine, int64_t n_fine, int64_t nxf, int64_t nyf,
-                                  int64_t nzf, int factor)
+int tgv_load_histograms_coarsened(tgv_ctx* c, const void* fine_v, int count_bytes, int64_t n_fine, int64_t nxf,
+                                  int64_t nyf, int64_t nzf, int factor)
 {
     int rc = check_ready(c);
     if (rc) return rc;
     const Geo& g = c->g;
+    const char* fine = static_cast<const char*>(fine_v);
     if (!fine || factor < 1 || factor > 64) return fail(c, TGV_EINVAL, "NULL counts or factor outside [1, 64]");
+    if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4)
+        return fail(c, TGV_EINVAL, "count_bytes must be 1, 2 or 4");
     if ((nxf + factor - 1) / factor != g.nx || (nyf + factor - 1) / factor != g.ny ||
         (nzf + factor - 1) / factor != g.nz)
         return fail(c, TGV_EINVAL, "grid is not the fine grid coarsened by %d", factor);
@@ -910,8 +945,8 @@ int tgv_load_histograms_coarsened(tgv_ctx* c, const uint32_t* fine, int64_t n_fi
     c->loaded = false;
     // chunks of whole coarse planes (factor fine planes each), staging up to ~256 MB
     const int64_t per_cplane = per_fplane * factor;
-    const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (64ll << 20) / per_cplane));
-    const int64_t need = per_cplane * cpc;
+    const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (256ll << 20) / count_bytes / per_cplane));
+    const int64_t need = (per_cplane * cpc * count_bytes + 3) / 4;  // staging is counted in uint32
     if (c->staging_elems < need) {
         if (c->staging) cudaFree(c->staging);
         c->staging = nullptr;
@@ -926,16 +961,14 @@ int tgv_load_histograms_coarsened(tgv_ctx* c, const uint32_t* fine, int64_t n_fi
     for (int z0 = 0; z0 < g.nzl; z0 += cpc) {
         const int nzc = std::min(cpc, g.nzl - z0);
         const int64_t f0 = (int64_t)z0 * factor, f1 = std::min<int64_t>(fz1 - fz0, (int64_t)(z0 + nzc) * factor);
-        CU(cudaMemcpyAsync(c->staging, fine + f0 * per_fplane, sizeof(uint32_t) * (size_t)((f1 - f0) * per_fplane),
-                           cudaMemcpyHostToDevice, c->stream));
-        if (c->slots == 8)
-            coarsen_counts_kernel<8><<<148 * 8, 256, 0, c->stream>>>(c->staging, (int)nxf, (int)nyf, (int)(f1 - f0),
-                                                                      factor, c->nbins, nzc, z0, g, c->hist16,
-                                                                      c->d_maxc);
+        CU(cudaMemcpyAsync(c->staging, fine + f0 * per_fplane * count_bytes,
+                           (size_t)count_bytes * (size_t)((f1 - f0) * per_fplane), cudaMemcpyHostToDevice, c->stream));
+        if (count_bytes == 1)
+            launch_coarsen_t<uint8_t>(c, c->staging, (int)nxf, (int)nyf, (int)(f1 - f0), factor, nzc, z0);
+        else if (count_bytes == 2)
+            launch_coarsen_t<uint16_t>(c, c->staging, (int)nxf, (int)nyf, (int)(f1 - f0), factor, nzc, z0);
         else
-            coarsen_counts_kernel<16><<<148 * 8, 256, 0, c->stream>>>(c->staging, (int)nxf, (int)nyf,
-                                                                       (int)(f1 - f0), factor, c->nbins, nzc, z0, g,
-                                                                       c->hist16, c->d_maxc);
+            launch_coarsen_t<uint32_t>(c, c->staging, (int)nxf, (int)nyf, (int)(f1 - f0), factor, nzc, z0);
         CU(cudaGetLastError());
     }
     return finish_counts(c);
@@ -960,15 +993,22 @@ int tgv_prolong_slab(tgv_ctx* c, const float* u_c, const float* v_c, int64_t cnx
     CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * (size_t)g.fs, c->stream));
     c->k = 0;
     const size_t nc = (size_t)(cnx * cny * cnz);
-    // stream-ordered temporaries: no device-wide synchronisation, so another context's
-    // iterations keep running while this leaf is staged
-    float* d = nullptr;
-    float** d_ptrs;
-    if (cudaMallocAsync(&d, sizeof(float) * 4 * nc + sizeof(float*) * 12, c->stream) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(c, TGV_ENOMEM, "coarse slab upload buffer");
+    // a grow-only buffer: after the first leaf of a size no allocation (and no
+    // device-wide synchronisation) happens here
+    const size_t need = sizeof(float) * 4 * nc + sizeof(float*) * 12;
+    if (c->upload_bytes < need) {
+        CU(cudaStreamSynchronize(c->stream));
+        cudaFree(c->upload);
+        c->upload = nullptr;
+        c->upload_bytes = 0;
+        if (cudaMalloc(&c->upload, need) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, TGV_ENOMEM, "coarse slab upload buffer");
+        }
+        c->upload_bytes = need;
     }
-    d_ptrs = reinterpret_cast<float**>(d + 4 * nc);  // byte offset 16 nc: pointer-aligned
+    float* d = c->upload;
+    float** d_ptrs = reinterpret_cast<float**>(d + 4 * nc);  // byte offset 16 nc: pointer-aligned
     // leaves: the border planes are frozen in every rotating slot; otherwise u_0 = u_{-1}
     float* ptrs[12];
     const int nus = c->leaf ? 3 : 2;
@@ -984,7 +1024,6 @@ int tgv_prolong_slab(tgv_ctx* c, const float* u_c, const float* v_c, int64_t cnx
                                                              zhi, g, d_ptrs, nus, d_ptrs + 3, nus);
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = cudaFreeAsync(d, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) return fail(c, TGV_ECUDA, "prolong slab: %s", cudaGetErrorString(e));
     return TGV_OK;
@@ -1262,7 +1301,32 @@ int tgv_reset(tgv_ctx* c)
     return TGV_OK;
 }
 
+static int iterate_enqueue(tgv_ctx* c, int32_t n);
+
 int tgv_iterate(tgv_ctx* c, int32_t n)
+{
+    int rc = iterate_enqueue(c, n);
+    if (rc) return rc;
+    return sync_stream(c);
+}
+
+int tgv_iterate_async(tgv_ctx* c, int32_t n)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (c->timing) return fail(c, TGV_ESTATE, "per-kernel timing needs the synchronous tgv_iterate");
+    if (c->nranks > 1) return fail(c, TGV_ESTATE, "multi-rank contexts iterate with tgv_iterate");
+    return iterate_enqueue(c, n);
+}
+
+int tgv_sync(tgv_ctx* c)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    return sync_stream(c);
+}
+
+static int iterate_enqueue(tgv_ctx* c, int32_t n)
 {
     int rc = check_ready(c);
     if (rc) return rc;
@@ -1286,7 +1350,7 @@ int tgv_iterate(tgv_ctx* c, int32_t n)
         }
         c->k += 1;
     }
-    return sync_stream(c);
+    return TGV_OK;
 }
 
 // ---- field access -------------------------------------------------------------
@@ -1694,6 +1758,7 @@ void tgv_destroy(tgv_ctx* c)
     cudaFree(c->d_out);
     cudaFree(c->d_maxc);
     cudaFree(c->staging);
+    cudaFree(c->upload);
     cudaFree(c->d_sched);
     cudaFree(c->d_sched_off);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -27,7 +27,8 @@ EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset"
            "tgv_read_field", "tgv_write_field", "tgv_energy", "tgv_set_schedule", "tgv_set_model", "tgv_set_timing", "tgv_get_timing", "tgv_info",
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
            "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts",
-           "tgv_create_leaf", "tgv_set_border", "tgv_load_histograms_coarsened", "tgv_prolong_slab"]
+           "tgv_create_leaf", "tgv_set_border", "tgv_load_histograms_coarsened", "tgv_prolong_slab",
+           "tgv_leaf_rebind", "tgv_iterate_async", "tgv_sync"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -74,6 +75,8 @@ def _load():
     lib.tgv_load_histograms.argtypes = [vp, vp, i64]
     lib.tgv_reset.argtypes = [vp]
     lib.tgv_iterate.argtypes = [vp, i32]
+    lib.tgv_iterate_async.argtypes = [vp, i32]
+    lib.tgv_sync.argtypes = [vp]
     lib.tgv_read_u.argtypes = [vp, vp, i64]
     lib.tgv_read_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_write_field.argtypes = [vp, ctypes.c_int, vp, i64]
@@ -95,8 +98,9 @@ def _load():
     lib.tgv_create_leaf.argtypes = [ctypes.POINTER(tgv_layout), ctypes.POINTER(tgv_params), ctypes.c_int,
                                     ctypes.POINTER(vp)]
     lib.tgv_set_border.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp]
-    lib.tgv_load_histograms_coarsened.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.c_int]
+    lib.tgv_load_histograms_coarsened.argtypes = [vp, vp, ctypes.c_int, i64, i64, i64, i64, ctypes.c_int]
     lib.tgv_prolong_slab.argtypes = [vp, vp, vp, i64, i64, i64, i64]
+    lib.tgv_leaf_rebind.argtypes = [vp, i64, i64]
     lib.tgv_destroy.argtypes = [vp]
     lib.tgv_destroy.restype = None
     lib.tgv_status_string.argtypes = [ctypes.c_int]
@@ -166,6 +170,14 @@ def tgv_reset(ctx):
 
 def tgv_iterate(ctx, n: int):
     _check(lib.tgv_iterate(ctx, int(n)), ctx)
+
+
+def tgv_iterate_async(ctx, n: int):
+    _check(lib.tgv_iterate_async(ctx, int(n)), ctx)
+
+
+def tgv_sync(ctx):
+    _check(lib.tgv_sync(ctx), ctx)
 
 
 def tgv_read_u(ctx, out):
@@ -263,10 +275,17 @@ def tgv_set_border(ctx, side: int, u=None, v=None, p=None, q=None):
     _check(lib.tgv_set_border(ctx, int(side), *ptr), ctx)
 
 
+def tgv_leaf_rebind(ctx, z_begin: int, z_end: int):
+    _check(lib.tgv_leaf_rebind(ctx, int(z_begin), int(z_end)), ctx)
+
+
 def tgv_load_histograms_coarsened(ctx, fine_counts, fine_shape, factor: int):
-    p, n = _host_ptr(fine_counts, np.uint32)
+    """fine_counts: C-contiguous uint8 / uint16 / uint32 numpy array."""
+    a = fine_counts
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype in (np.uint8, np.uint16, np.uint32)
     nxf, nyf, nzf = fine_shape
-    _check(lib.tgv_load_histograms_coarsened(ctx, p, n, nxf, nyf, nzf, int(factor)), ctx)
+    _check(lib.tgv_load_histograms_coarsened(ctx, a.ctypes.data, a.dtype.itemsize, a.size, nxf, nyf, nzf,
+                                             int(factor)), ctx)
 
 
 def tgv_prolong_slab(ctx, u_c, v_c, cz0: int):
@@ -446,6 +465,15 @@ class Solver:
         tgv_iterate(self.ctx, n)
         return self
 
+    def iterate_async(self, n: int):
+        """Enqueue n iterations and return (tgv_iterate_async); sync() or any read waits."""
+        tgv_iterate_async(self.ctx, n)
+        return self
+
+    def sync(self):
+        tgv_sync(self.ctx)
+        return self
+
     def read_u(self, out=None):
         out = np.empty(self.local_shape, np.float32) if out is None else out
         return tgv_read_u(self.ctx, out)
@@ -507,10 +535,18 @@ class Solver:
         tgv_set_border(self.ctx, side, f(u), f(v), f(p), f(q))
         return self
 
+    def rebind(self, z_begin: int, z_end: int):
+        """NEXT-3: move this leaf to slab [z_begin, z_end) (same plane count), keeping its memory."""
+        tgv_leaf_rebind(self.ctx, z_begin, z_end)
+        self.z_begin, self.z_end = int(z_begin), int(z_end)
+        return self
+
     def load_coarsened(self, fine_counts, fine_shape, factor: int):
         """NEXT-1/3: histograms = sums of factor^3 fine voxels; fine_counts covers this slab's fine planes."""
-        tgv_load_histograms_coarsened(self.ctx, np.ascontiguousarray(fine_counts, dtype=np.uint32), fine_shape,
-                                      factor)
+        a = np.asarray(fine_counts)
+        if a.dtype not in (np.uint8, np.uint16, np.uint32):
+            a = a.astype(np.uint32)
+        tgv_load_histograms_coarsened(self.ctx, np.ascontiguousarray(a), fine_shape, factor)
         return self
 
     def prolong_slab(self, u_c, v_c, cz0: int):

@@ -34,6 +34,10 @@ def test_coarsened_load_is_bit_exact():
         z0, z1 = 1, cs[2] - 1
         leaf = Solver.leaf(cs, C8, z0, z1).load_coarsened(h[z0 * factor:z1 * factor], shape, factor)
         assert np.array_equal(leaf.read_counts(), ref[z0:z1])
+        for narrow in (np.uint8, np.uint16):  # narrow host counts, the same sums
+            assert h.max() <= 255
+            leaf.load_coarsened(h[z0 * factor:z1 * factor].astype(narrow), shape, factor)
+            assert np.array_equal(leaf.read_counts(), ref[z0:z1])
 
 
 def test_prolong_slab_equals_prolong_from():
@@ -110,6 +114,22 @@ def test_out_of_core_matches_oracle_out_of_core():
     assert np.max(np.abs(v.astype(np.float64) - vo)) <= 1e-4
 
 
+def test_pooled_leaves_are_reproducible():
+    """Leaves moved between slabs (tgv_leaf_rebind) give the freshly created leaves'
+    result bit for bit, solve after solve."""
+    from paper_2107_14790_b200 import out_of_core
+    shape = (40, 36, 45)
+    h = synth.random_histograms(shape, 9)
+    kw = dict(levels=3, iters=40, leaf_voxels=40 * 36 * 4)
+    ref_u, ref_v = out_of_core.solve(shape, h, C8, **kw)
+    ooc = out_of_core.OutOfCore(shape, C8, keep_pool=True, **kw)
+    assert ooc.leaves == [12, 2, 1]  # 45 planes by 4 and 23 by 16 (ragged last leaves), 12 in one
+    for counts in (h, h.astype(np.uint8)):
+        u, v = ooc.solve(counts)
+        assert np.array_equal(u, ref_u) and np.array_equal(v, ref_v)
+    ooc.close()
+
+
 def test_many_leaves_stay_close_to_in_core():
     from paper_2107_14790_b200 import out_of_core
     from paper_2107_14790_b200.multilevel import coarse_to_fine
@@ -137,10 +157,14 @@ def test_leaf_errors():
     with pytest.raises(tgv.TgvError) as ei:  # parents of planes 3..12 are coarse planes 1..6
         leaf.prolong_slab(np.zeros((3, 8, 8), np.float32), np.zeros((3, 3, 8, 8), np.float32), 2)
     assert ei.value.status == tgv.TGV_EINVAL
+    with pytest.raises(tgv.TgvError) as ei:  # a leaf keeps its plane count
+        leaf.rebind(0, 9)
+    assert ei.value.status == tgv.TGV_EINVAL
     whole = Solver(shape, C8).load(h)
-    with pytest.raises(tgv.TgvError) as ei:
-        whole.set_border(0)
-    assert ei.value.status == tgv.TGV_ESTATE
+    for call in (lambda: whole.set_border(0), lambda: whole.rebind(0, 16)):
+        with pytest.raises(tgv.TgvError) as ei:
+            call()
+        assert ei.value.status == tgv.TGV_ESTATE
     with pytest.raises(tgv.TgvError) as ei:  # leaves do not take part in restrict / prolong_from
         Solver((8, 8, 8), C8).restrict_from(leaf)
     assert ei.value.status == tgv.TGV_EINVAL
