@@ -504,6 +504,121 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) fused_kernel(const FusedArgs
 }
 
 // ===========================================================================
+// NEXT-4 TV-L1, FUSED schedule: one single-sweep kernel per iteration.
+// Reads u_k, u_{k-1}, p_k and the counts, writes p_{k+1}, u_{k+1}:
+// 4 (2 + 3) + counts + 4 (3 + 1) = 44 B per voxel-iteration with u8 counts (60 B split).
+// Same thread layout as fused_kernel: 32 lanes x (TY + 2) rows, lanes 1..30 and
+// rows 1..TY owned; lane 0 / row 0 compute the dual of the x-1 / y-1 neighbours
+// (div p reads p_x(x-1), p_y(y-1)), lane 31 / row TY+1 only supply ubar(x+1),
+// ubar(y+1).  Step s computes the dual D(s) (rows 0..TY) and the primal of plane
+// s-1, whose p_y(y-1) comes from the shared plane written in step s-1, so one
+// __syncthreads per step separates both exchanges (parity double buffers).  The
+// arithmetic is that of tvl1_dual_kernel / tvl1_primal_kernel expression for
+// expression (the two schedules agree bit for bit, tests/test_gpu_parity.py).
+// ===========================================================================
+template <int TY, int SLOTS, typename CT>
+__global__ void __launch_bounds__(32 * (TY + 2)) tvl1_fused_kernel(const FusedArgs A)
+{
+    __shared__ float sm_u[2][TY + 2][32];  // ubar of plane s
+    __shared__ float sm_p[2][TY + 2][32];  // p_y of D(s)
+    const IterPtrs& a = A.a;
+    const Geo& g = A.g;
+    const StepParams& sp = A.sp;
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int x = blockIdx.x * 30 - 1 + lane, y = blockIdx.y * TY - 1 + ty;
+    const bool vxy = x >= 0 && x < g.nx && y >= 0 && y < g.ny;
+    const bool own = vxy && lane >= 1 && lane <= 30 && ty >= 1 && ty <= TY;
+    const bool xl = x < g.nx - 1, xf = x > 0, yl = y < g.ny - 1, yf = y > 0;
+    const bool prow = ty <= TY;  // rows needing p_{k+1}
+    const int zs = A.z_lo + blockIdx.z * A.zc;
+    const int ze = min(zs + A.zc, A.z_hi);
+    const int rowoff = y * g.px + x;
+
+    // Loads use coordinates clamped into the slab (halo planes included): every
+    // address is valid, and a value read for an out-of-grid thread or plane only
+    // ever meets a zero boundary factor (xl, yl, zl, xf, yf, zf), so no predicate or
+    // select is needed per load.
+    const int rowc = min(max(y, 0), g.ny - 1) * g.px + min(max(x, 0), g.nx - 1);
+    auto off = [&](int s) { return (min(max(s, -1), g.nzl) + 1) * g.plane + rowc; };
+    int o0 = off(zs - 1), o1 = off(zs);
+    float uk0 = __ldg(a.uk + o0), um0 = __ldg(a.um + o0);  // plane s
+    float uk1 = __ldg(a.uk + o1), um1 = __ldg(a.um + o1);  // plane s+1
+    float pk0[3];                                          // p_k(s)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) pk0[d] = __ldg(a.pk[d] + o0);
+    HistRaw<SLOTS, CT> h0{};
+    float uk_p = 0.f, pn_p[3] = {0.f, 0.f, 0.f}, pz_pp = 0.f;
+
+    for (int s = zs - 1; s <= ze; ++s) {
+        // prefetch (consumed next step)
+        const int o2 = off(s + 2);
+        const float uk2 = __ldg(a.uk + o2), um2 = __ldg(a.um + o2);
+        float pk1[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) pk1[d] = __ldg(a.pk[d] + o1);
+        HistRaw<SLOTS, CT> h1{};
+        if (own && s >= 0 && s < g.nzl) h1 = load_hist<SLOTS, CT>(a.hist, (int64_t)s * g.plane + rowoff);
+        const int par = s & 1;
+        const int zg = g.z0 + s;
+        const bool zl = zg < g.nz - 1;
+
+        const float ub = fmaf(2.f, uk0, -um0);
+        const float ub1 = fmaf(2.f, uk1, -um1);
+        sm_u[par][ty][lane] = ub;
+        __syncthreads();
+
+        // dual D(s) (tvl1_dual_kernel)
+        float pn[3] = {0.f, 0.f, 0.f};
+        if (prow && s < ze) {
+            const float ux = __shfl_down_sync(FULL, ub, 1);
+            const float uy = sm_u[par][ty + 1][lane];
+            const float g0 = xl ? ux - ub : 0.f, g1 = yl ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
+            pn[0] = fmaf(sp.sigma, g0, pk0[0]);
+            pn[1] = fmaf(sp.sigma, g1, pk0[1]);
+            pn[2] = fmaf(sp.sigma, g2, pk0[2]);
+            const float f = proj_scale(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2], sp.alpha1);
+            pn[0] *= f;
+            pn[1] *= f;
+            pn[2] *= f;
+        }
+        sm_p[par][ty][lane] = pn[1];
+        if (own && s >= zs && s < ze) {
+            const int o = (s + 1) * g.plane + rowoff;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) a.pn[d][o] = pn[d];
+        }
+
+        // primal of plane s-1 (tvl1_primal_kernel)
+        const float pxm_all = __shfl_up_sync(FULL, pn_p[0], 1);
+        if (own && s - 1 >= zs) {
+            const int zg1 = zg - 1;
+            const bool zl1 = zg1 < g.nz - 1, zf1 = zg1 > 0;
+            const float pxm = xf ? pxm_all : 0.f;
+            const float pym = yf ? sm_p[par ^ 1][ty - 1][lane] : 0.f;
+            const float pzm = zf1 ? pz_pp : 0.f;
+            const float divp = ((xl ? pn_p[0] : 0.f) - pxm) + ((yl ? pn_p[1] : 0.f) - pym) +
+                               ((zl1 ? pn_p[2] : 0.f) - pzm);
+            a.un[s * g.plane + rowoff] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, uk_p), sp.tl, h0, A.C);
+        }
+
+        // rotate
+        pz_pp = pn_p[2];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            pn_p[d] = pn[d];
+            pk0[d] = pk1[d];
+        }
+        uk_p = uk0;
+        h0 = h1;
+        uk0 = uk1;
+        um0 = um1;
+        uk1 = uk2;
+        um1 = um2;
+        o1 = o2;
+    }
+}
+
+// ===========================================================================
 // load / reset
 // counts chunk: dense uint32 [nzc][ny][nx][nbins] for local planes [zc0, zc0 + nzc)
 template <int SLOTS>

@@ -274,6 +274,39 @@ int launch_tvl1(tgv_ctx* c, int phase)
     return timer_end(c, sl);
 }
 
+template <int SLOTS, typename CT>
+void launch_tvl1_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
+{
+    tvl1_fused_kernel<FUSED_TY, SLOTS, CT><<<grd, dim3(32, FUSED_TY + 2), 0, c->stream>>>(A);
+}
+
+// NEXT-4 single sweep (44 B per voxel-iteration with u8 counts)
+int launch_tvl1_fused(tgv_ctx* c)
+{
+    size_t sl = 0;
+    int rc = timer_begin(c, T_FUSED, &sl);
+    if (rc) return rc;
+    FusedArgs A;
+    A.a = iter_ptrs(c, c->k);
+    A.g = c->g;
+    A.sp = step_params(c);
+    A.C = centers(c);
+    A.z_lo = 0;
+    A.z_hi = c->g.nzl;
+    A.keep_halo_dual = 0;
+    // z-chunks for about eight CTAs per SM in total (each chunk re-reads about 2 planes)
+    const int tiles = ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
+    const int chunks = std::max(1, std::min(c->g.nzl / 16 + 1, (8 * c->num_sms + tiles - 1) / tiles));
+    A.zc = c->fused_zc > 0 ? c->fused_zc : std::max(1, (c->g.nzl + chunks - 1) / chunks);
+    dim3 grd((c->g.nx + 29) / 30, (c->g.ny + FUSED_TY - 1) / FUSED_TY, (c->g.nzl + A.zc - 1) / A.zc);
+    if (c->slots == 8 && c->count_bytes == 1) launch_tvl1_fused_t<8, uint8_t>(c, A, grd);
+    else if (c->slots == 8) launch_tvl1_fused_t<8, uint16_t>(c, A, grd);
+    else if (c->count_bytes == 1) launch_tvl1_fused_t<16, uint8_t>(c, A, grd);
+    else launch_tvl1_fused_t<16, uint16_t>(c, A, grd);
+    CU(cudaGetLastError());
+    return timer_end(c, sl);
+}
+
 int fused_zc(const tgv_ctx* c)
 {
     if (c->fused_zc > 0) return c->fused_zc;
@@ -594,6 +627,20 @@ HaloPlan plan_tvl1_a(int64_t k)
     HaloPlan h;
     h.add_down(slotU(b.cu));
     h.add_down(slotU(b.pu));
+    return h;
+}
+// TV-L1 single sweep, once per iteration: the kernel recomputes p at plane -1 from
+// (u_k, u_{k-1}, p_k) there and reads ubar at plane nzl
+//   down: u, u_prev (2 planes);  up: u, u_prev, p (5 planes)
+HaloPlan plan_tvl1_fused(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    for (int s : {slotU(b.cu), slotU(b.pu)}) {
+        h.add_down(s);
+        h.add_up(s);
+    }
+    for (int d = 0; d < 3; ++d) h.add_up(slotP(b.cp, d));
     return h;
 }
 HaloPlan plan_tvl1_b(int64_t k)
@@ -1334,7 +1381,10 @@ static int iterate_enqueue(tgv_ctx* c, int32_t n)
     if (!c->loaded) return fail(c, TGV_ESTATE, "iterate before load");
     if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_iterate");
     for (int32_t it = 0; it < n; ++it) {
-        if (c->model == TGV_MODEL_TVL1) {
+        if (c->model == TGV_MODEL_TVL1 && c->schedule == TGV_SCHEDULE_FUSED) {
+            if ((rc = halo_exchange(c, plan_tvl1_fused(c->k)))) return rc;
+            if ((rc = launch_tvl1_fused(c))) return rc;
+        } else if (c->model == TGV_MODEL_TVL1) {
             if ((rc = halo_exchange(c, plan_tvl1_a(c->k)))) return rc;
             if ((rc = launch_tvl1(c, 0))) return rc;
             if ((rc = halo_exchange(c, plan_tvl1_b(c->k)))) return rc;
@@ -1604,7 +1654,13 @@ int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
     if ((rc = group_record(m, n))) return rc;  // the current state is each member's last step
     for (int32_t it = 0; it < iters; ++it) {
         const int64_t k = m[0]->k;
-        if (m[0]->model == TGV_MODEL_TVL1) {
+        if (m[0]->model == TGV_MODEL_TVL1 && m[0]->schedule == TGV_SCHEDULE_FUSED) {
+            if ((rc = group_exchange(m, n, plan_tvl1_fused(k)))) return rc;
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                if ((rc = launch_tvl1_fused(m[r]))) return rc;
+            }
+        } else if (m[0]->model == TGV_MODEL_TVL1) {
             if ((rc = group_exchange(m, n, plan_tvl1_a(k)))) return rc;
             for (int r = 0; r < n; ++r) {
                 CU(cudaSetDevice(m[r]->device));
@@ -1718,7 +1774,7 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     if (c->model == TGV_MODEL_TVL1) {  // TV-L1: dual reads u_k, u_{k-1}, p, writes p; primal reads p, u + counts, writes u
         o->bytes_dual = 4 * (5 + 3);
         o->bytes_primal = 4 * (4 + 1) + hb;
-        o->bytes_fused = 0;
+        o->bytes_fused = 4 * (5 + 4) + hb;
     }
     o->fused_zc = fused_zc(c);
     o->fused_tma = c->fused_tma ? 1 : 0;

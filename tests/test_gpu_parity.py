@@ -246,26 +246,43 @@ def test_error_paths():
 
 # ---------------------------------------------------------------------------
 # NEXT-4 TV-L1 model (Eq. 1; R21)
+@pytest.mark.parametrize("schedule", ["fused", "split"])
 @pytest.mark.parametrize("shape,iters", [((37, 23, 19), 60), ((1, 1, 40), 200), ((64, 64, 64), 500)])
-def test_tvl1_matches_oracle(shape, iters):
+def test_tvl1_matches_oracle(shape, iters, schedule):
     if shape == (64, 64, 64):
         h = np.ascontiguousarray(synth.make_histograms("C2", 118, 182)[:, 96:160, 96:160])
     else:
         h = synth.random_histograms(shape, 31)
     c = oracle.default_centers(8)
     o = oracle.Oracle(shape, model="tvl1").load(h).iterate(iters, threads=NT)
-    s = solver_cls()(shape, list(c)).set_model("tvl1").load(h).iterate(iters)
+    s = solver_cls()(shape, list(c)).set_schedule(schedule).set_model("tvl1").load(h).iterate(iters)
     assert s.info()["model"] == 1
     du, rel = assert_parity(o, s)
     assert np.all(s.get("v") == 0) and np.all(s.get("q") == 0)
     assert abs(s.energy()["gap"] - o.energy()["gap"]) <= 1e-4 * o.energy()["E"]
 
 
-def test_tvl1_group_equals_single():
+@pytest.mark.parametrize("schedule", ["fused", "split"])
+def test_tvl1_group_equals_single(schedule):
     from paper_2107_14790_b200 import Group
     shape = (40, 30, 27)
     h = synth.random_histograms(shape, 32)
     c = list(oracle.default_centers(8))
-    one = solver_cls()(shape, c).set_model("tvl1").load(h).iterate(25)
-    grp = Group(shape, [0, 9, 20, 27], c).set_model("tvl1").load(h).iterate(25)
+    one = solver_cls()(shape, c).set_schedule(schedule).set_model("tvl1").load(h).iterate(25)
+    grp = Group(shape, [0, 9, 10, 20, 27], c).set_schedule(schedule).set_model("tvl1").load(h).iterate(25)
     assert np.array_equal(grp.read_u(), one.read_u())
+    assert np.array_equal(grp.get("p"), one.get("p"))
+
+
+@pytest.mark.parametrize("zc", ["0", "1", "3", "7"])
+def test_tvl1_fused_equals_split_bitwise(zc, monkeypatch):
+    """The NEXT-4 single sweep does the two kernels' arithmetic expression for
+    expression: bitwise equal for any z-chunking, u8 and u16 counts, 3 bins."""
+    monkeypatch.setenv("TGV_FUSED_ZC", zc)
+    for shape, h, c in (((45, 31, 22), synth.random_histograms((45, 31, 22), 33), list(oracle.default_centers(8))),
+                        ((33, 17, 9), synth.random_histograms((33, 17, 9), 34) * 40, list(oracle.default_centers(8))),
+                        ((29, 14, 12), np.ascontiguousarray(synth.random_histograms((29, 14, 12), 35)[..., :3]), [-0.5, 0.1, 0.7])):
+        a = solver_cls()(shape, c).set_schedule("fused").set_model("tvl1").load(h).iterate(17)
+        b = solver_cls()(shape, c).set_schedule("split").set_model("tvl1").load(h).iterate(17)
+        assert np.array_equal(a.read_u(), b.read_u())
+        assert np.array_equal(a.get("p"), b.get("p"))
