@@ -395,6 +395,8 @@ int make_state_maps(tgv_ctx* c)
 // order; the first floor(items / G) * G items go round-robin to the G CTAs (each
 // CTA runs whole chunks, all CTAs in lock-step through z); the planes of the
 // remaining items are split evenly over all G CTAs as contiguous segments.
+int64_t env_int(const char* name, int64_t dflt);
+
 int build_schedule(tgv_ctx* c, int zc)
 {
     const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
@@ -402,7 +404,8 @@ int build_schedule(tgv_ctx* c, int zc)
     const int nch = (nzl + zc - 1) / zc;
     const int64_t items = (int64_t)tiles * nch;
     const int64_t planes = (int64_t)tiles * nzl;
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(c->num_sms, (planes + 7) / 8));
+    const int ctas = (int)std::min<int64_t>(c->num_sms, env_int("TGV_PERSIST_CTAS", c->num_sms));  // dev knob
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, (planes + 7) / 8));
     std::vector<std::vector<int4>> per(G);
     const int64_t whole = items / G * G;
     auto item = [&](int64_t i, int* t, int* z0, int* z1) {
