@@ -271,7 +271,21 @@ def run_out_of_core(a):
     iters = a.iters or 200
     levels = max(1, a.levels)
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
-    counts = synth.make_histograms(a.workload)
+    if a.workload in GPU_VOTED:  # GPU Alg. 1 per 128-plane slab (bit-exact vs the CPU generator), narrowed to u8
+        from paper_2107_14790_b200 import Solver
+        nx, ny, nz = wl.shape
+        cams, depths = cams_of(wl), render_shared(wl, 0, 1)
+        counts = np.empty((nz, ny, nx, 8), np.uint8)
+        for z0 in range(0, nz, 128):
+            z1 = min(nz, z0 + 128)
+            leaf = Solver.leaf(wl.shape, list(wl.centers), z0, z1, **kw).vote(cams, depths,
+                                                                               voxel_radius=wl.voxel_radius)
+            c = leaf.read_counts()
+            assert c.max() <= 255
+            counts[z0:z1] = c
+            leaf.close()
+    else:
+        counts = synth.make_histograms(a.workload)
     vox_its = sum(int(np.prod(sh)) for sh in level_shapes(wl.shape, levels)) * iters
     # the leaf pool and the pinned host level buffers are allocated outside the timed region
     ooc = out_of_core.OutOfCore(wl.shape, list(wl.centers), levels=levels, iters=iters, leaf_voxels=a.out_of_core,

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <atomic>
 #include <vector>
 
 #include "../../include/tgv.h"
@@ -143,6 +144,11 @@ int check_ready(tgv_ctx* c)
 {
     if (!c) return TGV_EINVAL;
     if (c->poisoned) return fail(c, TGV_ESTATE, "context poisoned by an earlier CUDA/NCCL failure");
+    // every call runs on the context's device, whatever the calling thread's current device
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    }
     return TGV_OK;
 }
 
@@ -470,11 +476,13 @@ int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
     const size_t smem = sizeof(TmaSmem<TMA_TY, HB>) + 128;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the attribute is per device: set it once for each device this process launches on
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = 1ull << (c->device & 63);
+    if (!(attr_set.load() & bit)) {
         CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-        attr_set = true;
+        attr_set.fetch_or(bit);
     }
     fused_tma_kernel<TMA_TY, SLOTS, CT><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
         c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
