@@ -264,7 +264,8 @@ void oracle_dual(oracle_state* s, int threads)
                 int64_t i = idx(g, x, y, z);
                 double gu[3], e[6], pn[3], qn[6];
                 grad_at(g, s->f[F_UBAR], x, y, z, gu);
-                for (int k = 0; k < 3; ++k) pn[k] = p[k][i] + s->sigma * (gu[k] - vbar[k][i]);
+                /* TV-L1 (Eq. 1, reading R21) has no v: p + sigma grad ubar, v never read */
+                for (int k = 0; k < 3; ++k) pn[k] = p[k][i] + s->sigma * (s->tvl1 ? gu[k] : gu[k] - vbar[k][i]);
                 double np = sqrt(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2]);
                 /* Euclidean projection onto {|p| <= alpha1} (reading R5) */
                 double sp = (np > s->alpha1) ? s->alpha1 / np : 1.0;
@@ -333,13 +334,13 @@ void oracle_dual_halo(oracle_state* s)
                 int64_t i = idx(g, x, y, z);
                 double gu[3], pn[3];
                 grad_at(g, s->f[F_UBAR], x, y, z, gu);
-                for (int k = 0; k < 3; ++k) pn[k] = p[k][i] + s->sigma * (gu[k] - vbar[k][i]);
+                for (int k = 0; k < 3; ++k) pn[k] = p[k][i] + s->sigma * (s->tvl1 ? gu[k] : gu[k] - vbar[k][i]);
                 double np = sqrt(pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2]);
                 double sp = (np > s->alpha1) ? s->alpha1 / np : 1.0;
                 for (int k = 0; k < 3; ++k) p[k][i] = pn[k] * sp;
             }
     }
-    if (g->ze < g->nz) { /* q at plane ze */
+    if (g->ze < g->nz && !s->tvl1) { /* q at plane ze (TV-L1 has no q) */
         const int64_t z = g->ze;
         for (int64_t y = 0; y < g->ny; ++y)
             for (int64_t x = 0; x < g->nx; ++x) {
@@ -370,6 +371,8 @@ void oracle_iterate(oracle_state* s, int n, int threads)
  *   E   = sum alpha1 |grad u - v|_2 + alpha0 |E v|_F + lambda sum_b h_b |u - c_b|
  *   D_V = sum min_{u in [-1,1]} (lambda sum_b h_b|u - c_b| - u div p) - V |p + div2 q|_1
  * out = {E, alpha1-term, alpha0-term, data-term, gap = E - D_V, max|v|, D_V}.
+ * TV-L1 (Eq. 1, reading R21): E = sum alpha1 |grad u| + data and D = D_0; v and q
+ * are never read (V is ignored).
  * In slab mode only owned voxels contribute (halo planes must hold the
  * neighbours' u, v, p, q); the caller sums partial terms over slabs. */
 void oracle_energy(const oracle_state* s, double V, double out[7])
@@ -389,13 +392,19 @@ void oracle_energy(const oracle_state* s, double V, double out[7])
                 double gu[3], e[6], w[3];
                 grad_at(g, s->f[F_U], x, y, z, gu);
                 double a = 0.0;
-                for (int k = 0; k < 3; ++k) a += (gu[k] - v[k][i]) * (gu[k] - v[k][i]);
+                if (s->tvl1) { /* Eq. 1 (reading R21): alpha1 |grad u| + data, no v, no q */
+                    for (int k = 0; k < 3; ++k) a += gu[k] * gu[k];
+                } else {
+                    for (int k = 0; k < 3; ++k) a += (gu[k] - v[k][i]) * (gu[k] - v[k][i]);
+                }
                 t1 += s->alpha1 * sqrt(a);
-                symgrad_at(g, v, x, y, z, e);
-                double b2 = 0.0;
-                for (int k = 0; k < 3; ++k)
-                    for (int l = 0; l < 3; ++l) b2 += e[QIDX[k][l]] * e[QIDX[k][l]];
-                t0 += s->alpha0 * sqrt(b2);
+                if (!s->tvl1) {
+                    symgrad_at(g, v, x, y, z, e);
+                    double b2 = 0.0;
+                    for (int k = 0; k < 3; ++k)
+                        for (int l = 0; l < 3; ++l) b2 += e[QIDX[k][l]] * e[QIDX[k][l]];
+                    t0 += s->alpha0 * sqrt(b2);
+                }
                 td += data_term(s->nbins, hv, s->c, s->lambda, u);
                 /* dual: the convex piecewise-linear min is attained at -1, 1 or a centre */
                 double d = div_at(g, p, x, y, z);
@@ -404,6 +413,10 @@ void oracle_energy(const oracle_state* s, double V, double out[7])
                     double uu = (j < 0) ? -1.0 : (j == s->nbins ? 1.0 : s->c[j]);
                     double f = data_term(s->nbins, hv, s->c, s->lambda, uu) - uu * d;
                     if (f < best) best = f;
+                }
+                if (s->tvl1) { /* no v to bound: the plain dual D_0 */
+                    dv += best;
+                    continue;
                 }
                 div2_at(g, q, x, y, z, w);
                 double l1 = 0.0;

@@ -674,6 +674,19 @@ HaloPlan plan_energy(int64_t k)
     h.add_up(slotP(b.cp, 2));
     return h;
 }
+// TV-L1 energy: grad u (u(z+1)) down, div p (p_z(z-1)) up; v and q stay zero
+HaloPlan plan_energy_tvl1(int64_t k)
+{
+    const Bufs b = bufs(k);
+    HaloPlan h;
+    h.add_down(slotU(b.cu));
+    h.add_up(slotP(b.cp, 2));
+    return h;
+}
+HaloPlan plan_energy_for(const tgv_ctx* c, int64_t k)
+{
+    return c->model == TGV_MODEL_TVL1 ? plan_energy_tvl1(k) : plan_energy(k);
+}
 
 int sync_stream(tgv_ctx* c)
 {
@@ -1543,7 +1556,7 @@ int tgv_energy(tgv_ctx* c, double out[6])
     if (!out) return fail(c, TGV_EINVAL, "out is NULL");
     if (!c->loaded) return fail(c, TGV_ESTATE, "energy before load");
     if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_energy");
-    if ((rc = halo_exchange(c, plan_energy(c->k)))) return rc;
+    if ((rc = halo_exchange(c, plan_energy_for(c, c->k)))) return rc;
     if ((rc = energy_launch(c))) return rc;
     if (c->nranks > 1) {
         const NcclApi* nccl = c->nccl;
@@ -1725,7 +1738,7 @@ int tgv_group_energy(tgv_ctx* const* m, int n, double out[6])
     if (!out) return fail(m[0], TGV_EINVAL, "out is NULL");
     tgv_ctx* c = m[0];
     if ((rc = group_record(m, n))) return rc;
-    if ((rc = group_exchange(m, n, plan_energy(m[0]->k)))) return rc;
+    if ((rc = group_exchange(m, n, plan_energy_for(m[0], m[0]->k)))) return rc;
     double tot[EN_TERMS] = {0, 0, 0, 0, 0};
     for (int r = 0; r < n; ++r) {  // fixed rank order: deterministic
         c = m[r];

@@ -13,6 +13,9 @@ plan_energy; in the runtime's representation ubar travels as (u_k, u_{k-1})):
   FUSED, once per iteration: ubar, vbar(3), q(6) bottom -> r-1;  ubar, vbar(3), p(3) top -> r+1,
                              then the dual is recomputed on the halo planes (p below, q above)
   energy:                   u, q_xz, q_yz, q_zz bottom -> r-1;  v(3), p_z top -> r+1
+  TV-L1 (plan_tvl1_a/_b, plan_tvl1_fused, plan_energy_tvl1): ubar down / p_z up (split);
+                             ubar down, ubar + p(3) up then p recomputed at the bottom halo (fused);
+                             u down, p_z up (energy) -- no v or q ever travels
 """
 import os
 import socket
@@ -34,6 +37,11 @@ PHASE_B = {"down": [("q", 4), ("q", 5), ("q", 2)], "up": [("p", 2)]}
 FUSED = {"down": [("ubar", 0), ("vbar", 0), ("vbar", 1), ("vbar", 2)] + [("q", m) for m in range(6)],
          "up": [("ubar", 0), ("vbar", 0), ("vbar", 1), ("vbar", 2), ("p", 0), ("p", 1), ("p", 2)]}
 ENERGY = {"down": [("u", 0), ("q", 4), ("q", 5), ("q", 2)], "up": [("v", 0), ("v", 1), ("v", 2), ("p", 2)]}
+# NEXT-4 TV-L1 (plan_tvl1_a / _b / _fused): no v, no q on the wire
+TVL1_A = {"down": [("ubar", 0)], "up": []}
+TVL1_B = {"down": [], "up": [("p", 2)]}
+TVL1_FUSED = {"down": [("ubar", 0)], "up": [("ubar", 0), ("p", 0), ("p", 1), ("p", 2)]}
+TVL1_ENERGY = {"down": [("u", 0)], "up": [("p", 2)]}
 
 
 def _free_port():
@@ -84,10 +92,21 @@ def _worker(rank, world, port, shape, cuts, iters, outdir, plan="split"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     zb, ze = cuts[rank], cuts[rank + 1]
     h = synth.random_histograms(shape, 3)[zb:ze]
-    o = oracle.Oracle(shape, zb=zb, ze=ze).load(h)
+    tv = plan.startswith("tvl1")
+    o = oracle.Oracle(shape, zb=zb, ze=ze, model="tvl1" if tv else "tgv").load(h)
     poison_halos(o)
     for _ in range(iters):
-        if plan == "split":
+        if plan == "tvl1_split":
+            exchange(o, TVL1_A, rank, world)
+            o.dual()
+            exchange(o, TVL1_B, rank, world)
+            o.primal()
+        elif plan == "tvl1_fused":
+            exchange(o, TVL1_FUSED, rank, world)
+            o.dual()
+            o.dual_halo()
+            o.primal()
+        elif plan == "split":
             exchange(o, PHASE_A, rank, world)
             o.dual()
             exchange(o, PHASE_B, rank, world)
@@ -97,7 +116,7 @@ def _worker(rank, world, port, shape, cuts, iters, outdir, plan="split"):
             o.dual()
             o.dual_halo()
             o.primal()
-    exchange(o, ENERGY, rank, world)
+    exchange(o, TVL1_ENERGY if tv else ENERGY, rank, world)
     e = o.energy()
     sums = torch.tensor([e["alpha1"], e["alpha0"], e["data"], e["dual"]], dtype=torch.float64)
     dist.all_reduce(sums)
@@ -109,13 +128,14 @@ def _worker(rank, world, port, shape, cuts, iters, outdir, plan="split"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("plan", ["split", "fused"])
+@pytest.mark.parametrize("plan", ["split", "fused", "tvl1_split", "tvl1_fused"])
 @pytest.mark.parametrize("cuts", [[0, 8, 16], [0, 4, 8, 12, 16], [0, 1, 5, 6, 16]])
 def test_slab_equals_monolithic_bitwise(tmp_path, cuts, plan):
     shape, iters = (7, 6, 16), 25
     world = len(cuts) - 1
     mp.spawn(_worker, args=(world, _free_port(), shape, cuts, iters, str(tmp_path), plan), nprocs=world, join=True)
-    ref = oracle.Oracle(shape).load(synth.random_histograms(shape, 3)).iterate(iters)
+    model = "tvl1" if plan.startswith("tvl1") else "tgv"
+    ref = oracle.Oracle(shape, model=model).load(synth.random_histograms(shape, 3)).iterate(iters)
     parts = [np.load(os.path.join(tmp_path, f"r{r}.npz")) for r in range(world)]
     for name in ("u", "v", "p", "q"):
         got = np.concatenate([p[name] for p in parts], axis=-3)
