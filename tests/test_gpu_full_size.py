@@ -1,6 +1,6 @@
-"""Parity at the largest BASELINE size (C4, 1024^3: the configuration bench.py times on
-2/4/8 GPUs), in the solver's launch configuration, on sampled outputs the oracle can
-compute (DESIGN.md §3 "light cone").
+"""Parity at the full BASELINE sizes C3 (512^3) and C4 (1024^3: the configuration
+bench.py times on 2/4/8 GPUs), in the solver's launch configuration, on sampled outputs
+the oracle can compute (DESIGN.md §3 "light cone").
 
 One iteration of the scheme reads only the 6-neighbourhood of a voxel (the dual reads
 ubar at +1 and vbar at -1, the primal p at -1 and q at +1), so after n iterations
@@ -28,12 +28,23 @@ def _cams(wl):
              "width": c.width, "height": c.height, "vote_weight": c.vote_weight} for c in wl.cams]
 
 
-def test_c4_full_grid_blocks_match_oracle_windows():
+def _blocks(wl):
+    """32^3 blocks (x0, y0, z0) per workload: grid corners (boundary faces) and surface crossings."""
+    nx, ny, nz = wl.shape
+    if wl.name == "C3":  # terrain around z = 200 +- 78, observed from above
+        return [(0, 0, 184), (240, 240, 184), (nx - B, ny - B, 184), (nx - B, ny - B, nz - B)]
+    sph = wl.prims[1][1]  # C4: (cx, cy, cz, r) of the first sphere; ground plane z = 100
+    return [(0, 0, 84), (496, 496, 84), (int(sph[0] + 0.7 * sph[3]) - 16, int(sph[1]) - 16, 84),
+            (nx - B, ny - B, nz - B)]
+
+
+@pytest.mark.parametrize("name,mem_gb", [("C3", 25), ("C4", 170)])
+def test_full_grid_blocks_match_oracle_windows(name, mem_gb):
     import torch
     from paper_2107_14790_b200 import Solver
-    if torch.cuda.get_device_properties(0).total_memory < 170e9:
-        pytest.skip("C4 needs about 155 GB of device memory")
-    wl = synth.workload("C4")
+    if torch.cuda.get_device_properties(0).total_memory < mem_gb * 1e9:
+        pytest.skip(f"{name} needs about {mem_gb} GB of device memory")
+    wl = synth.workload(name)
     nx, ny, nz = wl.shape
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
     depths = synth.render_depths(wl)
@@ -43,18 +54,14 @@ def test_c4_full_grid_blocks_match_oracle_windows():
     e = s.energy()
     s.close()
     assert np.all(np.abs(u) <= 1) and np.isfinite(e["E"]) and e["gap"] >= -1e-9 * e["E"]
-    # blocks (x0, y0, z0): grid corner, ground plane z = 100 under the centre, a sphere
-    # flank, and the top corner (boundary faces on three sides each for the corners)
-    sph = wl.prims[1][1]  # (cx, cy, cz, r) of the first sphere
-    blocks = [(0, 0, 84), (496, 496, 84), (int(sph[0] + 0.7 * sph[3]) - 16, int(sph[1]) - 16, 84),
-              (nx - B, ny - B, nz - B)]
     bands = {}
     worst, observed = 0.0, 0
+    blocks = _blocks(wl)
     for x0, y0, z0 in blocks:
         x0, y0 = min(max(x0, 0), nx - B), min(max(y0, 0), ny - B)
         wz0, wz1 = max(z0 - M, 0), min(z0 + B + M, nz)
         if (wz0, wz1) not in bands:
-            bands[(wz0, wz1)] = synth.make_histograms("C4", wz0, wz1)
+            bands[(wz0, wz1)] = synth.make_histograms(name, wz0, wz1)
         wx0, wx1 = max(x0 - M, 0), min(x0 + B + M, nx)
         wy0, wy1 = max(y0 - M, 0), min(y0 + B + M, ny)
         h = np.ascontiguousarray(bands[(wz0, wz1)][:, wy0:wy1, wx0:wx1])
@@ -67,4 +74,4 @@ def test_c4_full_grid_blocks_match_oracle_windows():
         assert d <= 1e-4, ((x0, y0, z0), d)
         observed += int(np.any(h[z0 - wz0:z0 - wz0 + B, y0 - wy0:y0 - wy0 + B, x0 - wx0:x0 - wx0 + B].sum(-1) > 0))
     assert observed >= 2  # not only unobserved space (the corners may be outside every frustum)
-    print(f"C4 1024^3, {ITERS} iterations: max|du| over {len(blocks)} blocks of {B}^3 = {worst:.3g}")
+    print(f"{name} {wl.shape}, {ITERS} iterations: max|du| over {len(blocks)} blocks of {B}^3 = {worst:.3g}")
