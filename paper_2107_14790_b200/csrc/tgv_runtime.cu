@@ -25,6 +25,7 @@
 #include "../../include/tgv.h"
 #include "nccl_api.h"
 #include "tgv_fused_tma.cuh"
+#include "tgv_tvl1_tma.cuh"
 #include "tgv_kernels.cuh"
 #include "tgv_vote.cuh"
 
@@ -64,7 +65,7 @@ struct tgv_ctx {
     int num_sms = 148;
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
     int* d_sched_off = nullptr;
-    int sched_ctas = 0, sched_zc = -1;
+    int sched_ctas = 0, sched_zc = -1, sched_per_sm = 1;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
     CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
@@ -286,12 +287,66 @@ void launch_tvl1_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
     tvl1_fused_kernel<FUSED_TY, SLOTS, CT><<<grd, dim3(32, FUSED_TY + 2), 0, c->stream>>>(A);
 }
 
-// NEXT-4 single sweep (44 B per voxel-iteration with u8 counts)
+int build_schedule(tgv_ctx* c, int zc, int per_sm = 1);
+int fused_zc(const tgv_ctx* c);
+
+template <int SLOTS, typename CT>
+int launch_tvl1_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
+{
+    constexpr int HB = SLOTS * (int)sizeof(CT);
+    const size_t smem = sizeof(TvSmem<TMA_TY, HB>) + 128;
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = 1ull << (c->device & 63);
+    if (!(attr_set.load() & bit)) {
+        CU(cudaFuncSetAttribute(tvl1_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        attr_set.fetch_or(bit);
+    }
+    tvl1_tma_kernel<TMA_TY, SLOTS, CT><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(c->m_ld1, c->m_ld3, c->m_st1,
+                                                                                        c->m_st3, c->m_h, A);
+    return TGV_OK;
+}
+
+// NEXT-4 single sweep (44 B per voxel-iteration with u8 counts): the TMA kernel on the
+// persistent schedule of the TGV kernel, or (TGV_FUSED_IMPL=regs) the register kernel
 int launch_tvl1_fused(tgv_ctx* c)
 {
     size_t sl = 0;
     int rc = timer_begin(c, T_FUSED, &sl);
     if (rc) return rc;
+    if (c->fused_tma) {
+        const Bufs b = bufs(c->k);
+        TmaArgs A{};
+        A.g = c->g;
+        A.sp = step_params(c);
+        A.C = centers(c);
+        A.z_lo = 0;
+        A.z_hi = c->g.nzl;
+        // lock-step chunks for 2 CTAs per SM: at least as many (tile, chunk) items as CTAs,
+        // so that neighbouring tiles' halo re-reads meet in L2
+        {
+            const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
+            const int nch = std::max((c->g.nzl + 255) / 256, (2 * c->num_sms + tiles - 1) / tiles);
+            A.zc = c->fused_zc > 0 ? c->fused_zc : std::max(1, (c->g.nzl + nch - 1) / nch);
+        }
+        A.s_uk = slotU(b.cu);
+        A.s_um = slotU(b.pu);
+        A.s_pk = slotP(b.cp, 0);
+        A.s_un = slotU(b.nu);
+        A.s_pn = slotP(b.np, 0);
+        // two CTAs per SM: one TV-L1 plane step is short, so a second CTA hides the waits
+        if ((c->sched_zc != A.zc || c->sched_per_sm != 2) && (rc = build_schedule(c, A.zc, 2))) return rc;
+        A.sched = c->d_sched;
+        A.sched_off = c->d_sched_off;
+        dim3 grd(c->sched_ctas, 1, 1);
+        if (c->slots == 8 && c->count_bytes == 1) rc = launch_tvl1_tma_t<8, uint8_t>(c, A, grd);
+        else if (c->slots == 8) rc = launch_tvl1_tma_t<8, uint16_t>(c, A, grd);
+        else if (c->count_bytes == 1) rc = launch_tvl1_tma_t<16, uint8_t>(c, A, grd);
+        else rc = launch_tvl1_tma_t<16, uint16_t>(c, A, grd);
+        if (rc) return rc;
+        CU(cudaGetLastError());
+        return timer_end(c, sl);
+    }
     FusedArgs A;
     A.a = iter_ptrs(c, c->k);
     A.g = c->g;
@@ -403,14 +458,15 @@ int make_state_maps(tgv_ctx* c)
 // remaining items are split evenly over all G CTAs as contiguous segments.
 int64_t env_int(const char* name, int64_t dflt);
 
-int build_schedule(tgv_ctx* c, int zc)
+int build_schedule(tgv_ctx* c, int zc, int per_sm)
 {
     const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
     const int nzl = c->g.nzl;
     const int nch = (nzl + zc - 1) / zc;
     const int64_t items = (int64_t)tiles * nch;
     const int64_t planes = (int64_t)tiles * nzl;
-    const int ctas = (int)std::min<int64_t>(c->num_sms, env_int("TGV_PERSIST_CTAS", c->num_sms));  // dev knob
+    const int ctas = (int)std::min<int64_t>((int64_t)c->num_sms * per_sm,
+                                            env_int("TGV_PERSIST_CTAS", (int64_t)c->num_sms * per_sm));  // dev knob
     const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, (planes + 7) / 8));
     std::vector<std::vector<int4>> per(G);
     const int64_t whole = items / G * G;
@@ -468,6 +524,7 @@ int build_schedule(tgv_ctx* c, int zc)
     CU(cudaMemcpy(c->d_sched_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
     c->sched_ctas = G;
     c->sched_zc = zc;
+    c->sched_per_sm = per_sm;
     return TGV_OK;
 }
 
@@ -512,7 +569,7 @@ int launch_fused_tma(tgv_ctx* c)
     A.s_qn = slotQ(b.np, 0);
     // persistent grid: one CTA per SM (the kernel's shared memory allows one)
     int rc;
-    if (c->sched_zc != A.zc && (rc = build_schedule(c, A.zc))) return rc;
+    if ((c->sched_zc != A.zc || c->sched_per_sm != 1) && (rc = build_schedule(c, A.zc, 1))) return rc;
     A.sched = c->d_sched;
     A.sched_off = c->d_sched_off;
     dim3 grd(c->sched_ctas, 1, 1);

@@ -274,11 +274,15 @@ def test_tvl1_group_equals_single(schedule):
     assert np.array_equal(grp.get("p"), one.get("p"))
 
 
+@pytest.mark.parametrize("impl", ["tma", "regs"])
 @pytest.mark.parametrize("zc", ["0", "1", "3", "7"])
-def test_tvl1_fused_equals_split_bitwise(zc, monkeypatch):
-    """The NEXT-4 single sweep does the two kernels' arithmetic expression for
-    expression: bitwise equal for any z-chunking, u8 and u16 counts, 3 bins."""
+def test_tvl1_fused_equals_split_bitwise(zc, impl, monkeypatch):
+    """The NEXT-4 single sweeps (TMA and register kernels) do the two kernels'
+    arithmetic expression for expression: bitwise equal for any z-chunking, u8 and
+    u16 counts, 3 bins."""
     monkeypatch.setenv("TGV_FUSED_ZC", zc)
+    if impl == "regs":
+        monkeypatch.setenv("TGV_FUSED_IMPL", "regs")
     for shape, h, c in (((45, 31, 22), synth.random_histograms((45, 31, 22), 33), list(oracle.default_centers(8))),
                         ((33, 17, 9), synth.random_histograms((33, 17, 9), 34) * 40, list(oracle.default_centers(8))),
                         ((29, 14, 12), np.ascontiguousarray(synth.random_histograms((29, 14, 12), 35)[..., :3]), [-0.5, 0.1, 0.7])):
