@@ -93,10 +93,10 @@ __global__ void __launch_bounds__(32 * (TY + 3), 2)
         int r, bc, cc, x;
         if (!halo) {
             r = w, bc = lane + 4, cc = lane + 1, x = x0 + lane;
-        } else if (lane < 16) {
-            r = lane, bc = 3, cc = 0, x = x0 - 1;
+        } else if (lane < 16) {  // rows beyond R (TY < 14) duplicate row R-1 exactly: identical writes
+            r = min(lane, R - 1), bc = 3, cc = 0, x = x0 - 1;
         } else {
-            r = lane - 16, bc = 36, cc = TMA_CW - 1, x = x0 + 32;
+            r = min(lane - 16, R - 1), bc = 36, cc = TMA_CW - 1, x = x0 + 32;
         }
         const int y = y0 - 1 + r;
         const bool own = !halo && r >= 1 && r <= TY;
