@@ -435,7 +435,8 @@ def run_ours(a):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(a.workload, {}).get(dom)
+            key = dom if a.model == "tgv" else f"{a.model}_{dom}"
+            traffic = json.load(open(tp)).get(a.workload, {}).get(key)
         except Exception:
             traffic = None
     step_kernel_ms = tm["primal_ms"] + tm["dual_ms"] + tm["fused_ms"] + tm["energy_ms"]
