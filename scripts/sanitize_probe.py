@@ -19,10 +19,21 @@ for sched in ("fused", "split"):
 os.environ["TGV_FUSED_IMPL"] = "regs"
 Solver(shape, C8).load(h).iterate(3).close()
 os.environ.pop("TGV_FUSED_IMPL")
+Solver(shape, C8).set_model("tvl1").load(h).iterate(3).close()  # TMA single sweep
+Solver(shape, C8).set_schedule("split").set_model("tvl1").load(h).iterate(3).close()
+os.environ["TGV_FUSED_IMPL"] = "regs"
 Solver(shape, C8).set_model("tvl1").load(h).iterate(3).close()
+os.environ.pop("TGV_FUSED_IMPL")
 Group(shape, [0, 7, 21], C8).load(h).iterate(3).close()
 coarse_to_fine(shape, h, C8, levels=2, iters=2).close()
 cam = {"origin": (35.0, 16.0, -40.0), "rot": np.eye(3), "fx": 40.0, "fy": 40.0, "cx": 32.0, "cy": 32.0,
        "width": 64, "height": 64}
 Solver(shape, C8).vote([cam], [np.full((64, 64), 50.0, np.float32)]).iterate(2).close()
+# NEXT-3: leaves (border duals stored), device coarsening of narrow counts, slab prolongation
+from paper_2107_14790_b200 import out_of_core  # noqa: E402
+leaf = Solver.leaf(shape, C8, 5, 14).load_coarsened(h[5:14].astype(np.uint8), shape, 1)
+cs = tuple((n + 1) // 2 for n in shape)
+leaf.prolong_slab(np.zeros((6, cs[1], cs[0]), np.float32), np.zeros((3, 6, cs[1], cs[0]), np.float32), 2)
+leaf.iterate(3).close()
+out_of_core.solve(shape, h, C8, levels=2, iters=2, leaf_voxels=70 * 33 * 6)
 print("sanitize probe done")
