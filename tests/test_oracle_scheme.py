@@ -201,3 +201,26 @@ def test_thread_count_invariance_and_range():
     for f in ("u", "v", "p", "q", "ubar", "vbar"):
         assert np.array_equal(a.get(f), b.get(f)), f
     assert np.all(np.abs(a.u) <= 1.0)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 24), (6, 5, 24)])
+def test_opposite_votes_give_a_jump_with_closed_form_energy(shape):
+    """SPEC.md:346 idea ("a slab with strong bin votes at -1 on one side and +1 on the
+    other -> a monotone transition crossing 0; energy at 200 within 1 % of a long run";
+    E(200) <= E(10), :347).  With 3 votes per voxel (data slope lambda * 3 = 1.5 > alpha1)
+    the minimiser is the step u = c_0 below the middle, c_7 above, v = 0, so
+    E* = alpha1 |c_7 - c_0| per column = 1.75 nx ny (TV of one jump, no data cost)."""
+    nx, ny, nz = shape
+    h = np.zeros((nz, ny, nx, 8), np.uint32)
+    h[:nz // 2, ..., 0] = 3
+    h[nz // 2:, ..., 7] = 3
+    energies = {}
+    for n in (10, 200, 5000):
+        o = oracle.Oracle(shape).load(h).iterate(n)
+        energies[n] = o.energy()["E"]
+    u = o.u
+    assert abs(energies[5000] - 1.75 * nx * ny) <= 1e-9 * 1.75 * nx * ny
+    assert np.max(np.abs(u[:nz // 2] + 0.875)) <= 1e-9 and np.max(np.abs(u[nz // 2:] - 0.875)) <= 1e-9
+    assert np.all(np.diff(u, axis=0) >= -1e-12)  # monotone along z, crossing 0 between the halves
+    assert energies[200] <= 1.01 * energies[5000]
+    assert energies[200] <= energies[10]
