@@ -47,7 +47,7 @@ def test_full_grid_blocks_match_oracle_windows(name, mem_gb):
     wl = synth.workload(name)
     nx, ny, nz = wl.shape
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
-    depths = synth.render_depths(wl)
+    depths = synth._depths_cached(name)  # shared with make_histograms below (same maps)
     s = Solver(wl.shape, list(wl.centers), **kw)
     s.vote(_cams(wl), depths, voxel_radius=wl.voxel_radius).iterate(ITERS)
     u = s.read_u()
@@ -75,3 +75,25 @@ def test_full_grid_blocks_match_oracle_windows(name, mem_gb):
         observed += int(np.any(h[z0 - wz0:z0 - wz0 + B, y0 - wy0:y0 - wy0 + B, x0 - wx0:x0 - wx0 + B].sum(-1) > 0))
     assert observed >= 2  # not only unobserved space (the corners may be outside every frustum)
     print(f"{name} {wl.shape}, {ITERS} iterations: max|du| over {len(blocks)} blocks of {B}^3 = {worst:.3g}")
+
+
+def test_c3_slab_group_equals_single_context_bitwise():
+    """the z-slab decomposition equals one GPU bitwise at a BASELINE
+    size -- C3 (512^3) as 4 uneven slabs of an in-process group (the NCCL path's slab
+    geometry, halo plans and kernels; only the transport differs) against one context."""
+    import torch
+    from paper_2107_14790_b200 import Group, Solver
+    if torch.cuda.get_device_properties(0).total_memory < 60e9:
+        pytest.skip("needs about 45 GB of device memory")
+    wl = synth.workload("C3")
+    nx, ny, nz = wl.shape
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
+    depths = synth._depths_cached("C3")
+    one = Solver(wl.shape, list(wl.centers), **kw).vote(_cams(wl), depths, voxel_radius=wl.voxel_radius)
+    counts = one.read_counts()
+    one.iterate(10)
+    cuts = [0, 100, 256, 257, 512]
+    grp = Group(wl.shape, cuts, list(wl.centers), **kw).load(counts).iterate(10)
+    assert np.array_equal(grp.read_u(), one.read_u())
+    eg, e1 = grp.energy(), one.energy()
+    assert abs(eg["E"] - e1["E"]) <= 1e-12 * abs(e1["E"])
