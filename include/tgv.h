@@ -133,6 +133,11 @@ int tgv_get_unique_id(uint8_t uid[128]);
  * above the slab: 120 B per voxel) and the histogram store (16 B per voxel,
  * plus 8 B when u8 counts are used), creates streams/events and, if nranks > 1, the NCCL
  * communicator from uid (uid must be NULL iff nranks == 1).
+ * Peer halo mode (environment TGV_PEER_HALO=1 at create, nranks > 1):
+ * the neighbours' state and hand-over flags are mapped with CUDA IPC (handles
+ * exchanged by an NCCL all-gather) and the fused TGV kernel writes its boundary
+ * planes straight into the neighbours' halo planes; tgv_destroy is then collective
+ * (no rank may free its state while a neighbour's kernel can still write it).
  * Errors: TGV_EINVAL for any invalid argument (see tgv_params / tgv_layout;
  * also non-contiguous slabs across ranks), TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL.
  * On error *out is NULL. */
@@ -307,6 +312,10 @@ int tgv_energy(tgv_ctx* ctx, double out[6]);
  * Per-member calls (load, reset, read, write, info, timing, schedule) work as
  * usual; iterate and energy go through tgv_group_iterate / tgv_group_energy
  * (tgv_iterate / tgv_energy on a member return TGV_ESTATE).
+ * Members run in peer halo mode unless TGV_PEER_HALO=0 (or neighbouring devices
+ * lack peer access): the fused TGV kernel of each member writes its boundary planes
+ * into the neighbours' halo planes, so after the first iteration of a call no halo
+ * copy runs.
  * Errors: TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA. */
 int tgv_create_group(const tgv_layout* layouts, const tgv_params* params, int n, const int* devices,
                      tgv_ctx** out);

@@ -91,6 +91,17 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* m)
 {
     asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 // ---- shared memory ---------------------------------------------------------------
 constexpr int TMA_BW = 40;  // input box width: x0-4 .. x0+35 (the inner start must be 16-B aligned)
@@ -128,6 +139,23 @@ struct TmaArgs {
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
     int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
+    // Peer halo mode: the kernel itself writes the next iterate of its
+    // boundary planes into the neighbours' halo planes (NVLink / same-device stores,
+    // tile by tile as they are computed) -- down: u, v, q of plane 0 into the lower
+    // neighbour's top halo; up: u, v, p of plane nzl-1 into the upper neighbour's bottom
+    // halo -- and hands over with a flag per neighbour: the last CTA to finish publishes
+    // `seq`; the next launch waits until both neighbours published `wait_seq`.
+    float* pdn;            // lower neighbour's state (slot 0), or null
+    int64_t pdn_fs;        // its slot stride (floats)
+    int pdn_top;           // its top halo plane, in slot-plane coordinates (its nzl + 1)
+    float* pup;            // upper neighbour's state, or null (its bottom halo is plane 0)
+    int64_t pup_fs;
+    unsigned long long* done;            // this rank's CTA completion counter (null: no peer mode)
+    unsigned long long* flag_dn_remote;  // the lower neighbour's "from up" flag
+    unsigned long long* flag_up_remote;  // the upper neighbour's "from down" flag
+    const unsigned long long* flag_in_dn;  // written by the lower neighbour
+    const unsigned long long* flag_in_up;  // written by the upper neighbour
+    unsigned long long seq, wait_seq;
 };
 
 template <int TY, int SLOTS, typename CT>
@@ -175,6 +203,13 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         for (int k = 0; k < Rg::NU; ++k) mbar_init(&S.bar_u[k], 1);
         for (int k = 0; k < Rg::NX; ++k) mbar_init(&S.bar_x[k], 1);
         fence_mbar_init();
+        if (A.wait_seq) {  // peer mode: the neighbours' previous launches wrote our halo planes
+            uint32_t n = 0;
+            while ((A.pdn && ld_acquire_sys(A.flag_in_dn) < A.wait_seq) ||
+                   (A.pup && ld_acquire_sys(A.flag_in_up) < A.wait_seq))
+                if (++n > (1u << 28)) __trap();  // watchdog: a kernel error, never a hang
+            fence_proxy_async_all();  // their generic-proxy stores, before our TMA reads
+        }
     }
     __syncthreads();
 
@@ -370,6 +405,18 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
 #pragma unroll
                     for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
+                    const bool inb = x < g.nx && y < g.ny;
+                    const int64_t cell = (int64_t)y * g.px + x;
+                    if (A.pdn && s == 0 && s >= zs && s < ze && inb) {  // q of plane 0 -> lower neighbour's top halo
+                        float* o = A.pdn + (int64_t)A.pdn_top * g.plane + cell;
+#pragma unroll
+                        for (int m = 0; m < 6; ++m) o[(A.s_qn + m) * A.pdn_fs] = qn[m];
+                    }
+                    if (A.pup && s == g.nzl - 1 && s >= zs && s < ze && inb) {  // p of plane nzl-1 -> upper neighbour
+                        float* o = A.pup + cell;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) o[(A.s_pn + k) * A.pup_fs] = pn[k];
+                    }
                     if (s - 1 >= zs) {  // (a2) primal Pm(s-1)
                         const bool zl1 = INT || zg - 1 < g.nz - 1, zf1 = INT || zg - 1 > 0;
                         const float pxm = S.sr[pr][0][r][cc - 1];
@@ -387,10 +434,37 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                                          (zl1 ? qn[5] - in.qn[5] : 0.f);
                         const float w2 = (xl_ ? qxz - in.qn[4] : 0.f) + (yl_ ? qyyz - in.qn[5] : 0.f) +
                                          (zl1 ? qn[2] - in.qn[2] : 0.f);
-                        S.out[0][r - 1][lane] = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
-                        S.out[1][r - 1][lane] = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
-                        S.out[2][r - 1][lane] = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
-                        S.out[3][r - 1][lane] = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
+                        const float un = hist_prox<SLOTS, CT>(fmaf(sp.tau, divp, in.uk), sp.tl, in.h, A.C);
+                        const float v0 = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
+                        const float v1 = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
+                        const float v2 = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
+                        S.out[0][r - 1][lane] = un;
+                        S.out[1][r - 1][lane] = v0;
+                        S.out[2][r - 1][lane] = v1;
+                        S.out[3][r - 1][lane] = v2;
+                        // u, v of a boundary plane -> the neighbour's halo (peer mode)
+                        float* po = nullptr;
+                        int64_t pfs = 0;
+                        if (A.pdn && s - 1 == 0 && inb) {
+                            po = A.pdn + (int64_t)A.pdn_top * g.plane + cell;
+                            pfs = A.pdn_fs;
+                        } else if (A.pup && s - 1 == g.nzl - 1 && inb) {
+                            po = A.pup + cell;
+                            pfs = A.pup_fs;
+                        }
+                        if (po) {
+                            po[A.s_un * pfs] = un;
+                            po[A.s_vn * pfs] = v0;
+                            po[(A.s_vn + 1) * pfs] = v1;
+                            po[(A.s_vn + 2) * pfs] = v2;
+                        }
+                        if (A.pdn && A.pup && s - 1 == 0 && s - 1 == g.nzl - 1 && inb) {  // 1-plane slab: both
+                            float* o2 = A.pup + cell;
+                            o2[A.s_un * A.pup_fs] = un;
+                            o2[A.s_vn * A.pup_fs] = v0;
+                            o2[(A.s_vn + 1) * A.pup_fs] = v1;
+                            o2[(A.s_vn + 2) * A.pup_fs] = v2;
+                        }
                     }
                 }
             };
@@ -440,6 +514,16 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             step(std::integral_constant<int, 0>{}, s, ca, cb);
             if (s + 1 > ze) break;
             step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
+        }
+    }
+    if (A.done) {  // peer mode: publish once every CTA's halo stores are visible system-wide
+        __threadfence_system();
+        __syncthreads();
+        if (tid0 && atomicAdd(A.done, 1ull) == gridDim.x - 1) {
+            atomicExch(A.done, 0ull);
+            __threadfence_system();
+            if (A.flag_dn_remote) st_release_sys(A.flag_dn_remote, A.seq);
+            if (A.flag_up_remote) st_release_sys(A.flag_up_remote, A.seq);
         }
     }
     if (tid0) tma_wait0();

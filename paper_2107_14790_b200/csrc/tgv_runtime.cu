@@ -61,6 +61,19 @@ struct tgv_ctx {
     int schedule = TGV_SCHEDULE_FUSED;
     int model = TGV_MODEL_TGV;
     bool leaf = false;  // NEXT-3: frozen-border leaf (tgv_create_leaf)
+    // peer halo mode: the fused TMA kernel writes the neighbours' halo planes
+    bool peer = false;          // neighbours' state and flags are mapped
+    bool halo_fresh = false;    // our halos hold the current iterate (the neighbours' last launch wrote them)
+    float* pdn = nullptr;       // lower / upper neighbour's state (same-process pointer or CUDA IPC mapping)
+    float* pup = nullptr;
+    int64_t pdn_fs = 0, pup_fs = 0;
+    int pdn_top = 0;
+    unsigned long long* flags = nullptr;  // [0] CTA counter, [1] written by the lower neighbour, [2] by the upper
+    unsigned long long* flag_dn_remote = nullptr;
+    unsigned long long* flag_up_remote = nullptr;
+    unsigned long long seq = 0, peer_wait = 0;
+    bool peer_now = false;      // the next fused launch writes the neighbours' halos
+    void* ipc_open[4] = {nullptr, nullptr, nullptr, nullptr};  // IPC mappings to close at destroy
     int fused_zc = 0;       // 0 = automatic
     int num_sms = 148;
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
@@ -567,6 +580,20 @@ int launch_fused_tma(tgv_ctx* c)
     A.s_vn = slotV(b.nu, 0);
     A.s_pn = slotP(b.np, 0);
     A.s_qn = slotQ(b.np, 0);
+    if (c->peer_now) {  // peer halo mode: write the neighbours' halos, publish / wait for the hand-over flags
+        A.pdn = c->pdn;
+        A.pdn_fs = c->pdn_fs;
+        A.pdn_top = c->pdn_top;
+        A.pup = c->pup;
+        A.pup_fs = c->pup_fs;
+        A.done = c->flags;
+        A.flag_dn_remote = c->flag_dn_remote;
+        A.flag_up_remote = c->flag_up_remote;
+        A.flag_in_dn = c->flags + 1;
+        A.flag_in_up = c->flags + 2;
+        A.seq = ++c->seq;
+        A.wait_seq = c->peer_wait;
+    }
     // persistent grid: one CTA per SM (the kernel's shared memory allows one)
     int rc;
     if ((c->sched_zc != A.zc || c->sched_per_sm != 1) && (rc = build_schedule(c, A.zc, 1))) return rc;
@@ -766,6 +793,7 @@ void launch_init_t(tgv_ctx* c)
 
 int init_from_hist(tgv_ctx* c)
 {
+    c->halo_fresh = false;
     CU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * (size_t)c->g.fs, c->stream));
     c->k = 0;  // u_0 in U[0], u_{-1} = u_0 in U[2]
     if (c->slots == 8 && c->count_bytes == 1) launch_init_t<8, uint8_t>(c);
@@ -837,6 +865,64 @@ int tgv_get_unique_id(uint8_t uid[128])
     NC(nccl->GetUniqueId(&id));
     static_assert(sizeof(id.internal) == 128, "NCCL unique id size");
     memcpy(uid, id.internal, 128);
+    return TGV_OK;
+}
+
+struct IpcRecord {
+    cudaIpcMemHandle_t state, flags;
+    int64_t fs, nzl;
+};
+
+static int map_ipc_neighbours(tgv_ctx* c)
+{
+    const NcclApi* nccl = c->nccl;
+    IpcRecord mine{};
+    if (cudaIpcGetMemHandle(&mine.state, c->state) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine.flags, c->flags) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ECUDA, "cudaIpcGetMemHandle failed");
+    }
+    mine.fs = c->g.fs;
+    mine.nzl = c->g.nzl;
+    std::vector<IpcRecord> all((size_t)c->nranks);
+    char* d = nullptr;
+    if (cudaMalloc(&d, sizeof(IpcRecord) * (size_t)c->nranks) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ENOMEM, "IPC record buffer");
+    }
+    cudaMemcpy(d + sizeof(IpcRecord) * (size_t)c->rank, &mine, sizeof mine, cudaMemcpyHostToDevice);
+    ncclResult_t r = nccl->AllGather(d + sizeof(IpcRecord) * (size_t)c->rank, d, sizeof(IpcRecord), ncclChar,
+                                     c->comm, c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(all.data(), d, sizeof(IpcRecord) * (size_t)c->nranks, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (r != ncclSuccess) return fail(c, TGV_ENCCL, "IPC all-gather: %s", nccl->GetErrorString(r));
+    auto open = [&](const cudaIpcMemHandle_t& h, int slot, void** p) -> int {
+        if (cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, TGV_ECUDA, "cudaIpcOpenMemHandle failed (no peer access between the GPUs?)");
+        }
+        c->ipc_open[slot] = *p;
+        return TGV_OK;
+    };
+    int rc;
+    void *ps = nullptr, *pf = nullptr;
+    if (c->rank > 0) {
+        const IpcRecord& n = all[(size_t)c->rank - 1];
+        if ((rc = open(n.state, 0, &ps)) || (rc = open(n.flags, 1, &pf))) return rc;
+        c->pdn = static_cast<float*>(ps);
+        c->pdn_fs = n.fs;
+        c->pdn_top = (int)n.nzl + 1;
+        c->flag_dn_remote = static_cast<unsigned long long*>(pf) + 2;
+    }
+    if (c->rank + 1 < c->nranks) {
+        const IpcRecord& n = all[(size_t)c->rank + 1];
+        if ((rc = open(n.state, 2, &ps)) || (rc = open(n.flags, 3, &pf))) return rc;
+        c->pup = static_cast<float*>(ps);
+        c->pup_fs = n.fs;
+        c->flag_up_remote = static_cast<unsigned long long*>(pf) + 1;
+    }
+    c->peer = true;
     return TGV_OK;
 }
 
@@ -935,14 +1021,16 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
     if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->hist16, hist_bytes) != cudaSuccess ||
         cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * 8) != cudaSuccess ||
-        cudaMalloc(&c->d_maxc, sizeof(unsigned int)) != cudaSuccess) {
+        cudaMalloc(&c->d_maxc, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&c->flags, 256) != cudaSuccess) {
         cudaGetLastError();
         fail(c, TGV_ENOMEM, "device allocation of %.2f GB failed", (state_bytes + hist_bytes) / 1e9);
         return bail(TGV_ENOMEM);
     }
     c->device_bytes = (int64_t)(state_bytes + hist_bytes);
     if (cudaMemsetAsync(c->state, 0, state_bytes, c->stream) != cudaSuccess ||
-        cudaMemsetAsync(c->hist16, 0, hist_bytes, c->stream) != cudaSuccess) {
+        cudaMemsetAsync(c->hist16, 0, hist_bytes, c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->flags, 0, 256, c->stream) != cudaSuccess) {
         fail(c, TGV_ECUDA, "memset failed");
         return bail(TGV_ECUDA);
     }
@@ -980,6 +1068,13 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
         if (!ok) {
             fail(c, TGV_EINVAL, "slabs do not tile [0, nz) in rank order");
             return bail(TGV_EINVAL);
+        }
+        // peer halo mode across processes (TGV_PEER_HALO=1; off by default: validated in-process
+        // through slab groups, the CUDA IPC mapping itself needs two GPUs): map the neighbours'
+        // state and flags with CUDA IPC, handles exchanged by an NCCL all-gather
+        if (env_int("TGV_PEER_HALO", 0) != 0) {
+            const int prc = map_ipc_neighbours(c);
+            if (prc) return bail(prc);
         }
     }
     if (make_state_maps(c)) return bail(TGV_ECUDA);
@@ -1027,6 +1122,7 @@ int tgv_set_border(tgv_ctx* c, int side, const float* u, const float* v, const f
 {
     int rc = check_ready(c);
     if (rc) return rc;
+    c->halo_fresh = false;  // the state changes outside an iteration
     if (!c->leaf) return fail(c, TGV_ESTATE, "borders belong to leaf contexts (tgv_create_leaf)");
     if (!c->loaded) return fail(c, TGV_ESTATE, "set borders after load / prolong (they reset the state)");
     if (side != 0 && side != 1) return fail(c, TGV_EINVAL, "side must be 0 (below) or 1 (above)");
@@ -1112,6 +1208,7 @@ int tgv_prolong_slab(tgv_ctx* c, const float* u_c, const float* v_c, int64_t cnx
 {
     int rc = check_ready(c);
     if (rc) return rc;
+    c->halo_fresh = false;  // the state changes outside an iteration
     const Geo& g = c->g;
     if (!u_c || !v_c) return fail(c, TGV_EINVAL, "NULL coarse fields");
     if (cnx != (g.nx + 1) / 2 || cny != (g.ny + 1) / 2) return fail(c, TGV_EINVAL, "coarse slab is not nx/2 x ny/2");
@@ -1298,6 +1395,7 @@ int tgv_prolong_from(tgv_ctx* c, const tgv_ctx* coarse)
 {
     int rc = check_ready(c);
     if (rc) return rc;
+    c->halo_fresh = false;  // the state changes outside an iteration
     if (!coarse || !coarse->loaded) return fail(c, TGV_ESTATE, "coarse context missing or not loaded");
     if (!c->loaded) return fail(c, TGV_ESTATE, "prolong into a context without histograms");
     if (!coarse_of(coarse, c))
@@ -1436,6 +1534,12 @@ int tgv_reset(tgv_ctx* c)
 
 static int iterate_enqueue(tgv_ctx* c, int32_t n);
 
+// the fused TMA TGV sweep with mapped neighbours runs in peer halo mode
+static bool peer_ready(const tgv_ctx* c)
+{
+    return c->peer && c->fused_tma && c->model == TGV_MODEL_TGV && c->schedule == TGV_SCHEDULE_FUSED;
+}
+
 int tgv_iterate(tgv_ctx* c, int32_t n)
 {
     int rc = iterate_enqueue(c, n);
@@ -1480,10 +1584,23 @@ static int iterate_enqueue(tgv_ctx* c, int32_t n)
             if ((rc = launch_split(c, 0))) return rc;
             if ((rc = halo_exchange(c, plan_split_b(c->k)))) return rc;
             if ((rc = launch_split(c, 1))) return rc;
+        } else if (peer_ready(c)) {  // peer halo mode: the previous launch already wrote our halos
+            if (c->halo_fresh) {
+                c->peer_wait = c->seq;
+            } else {
+                if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
+                c->peer_wait = 0;
+            }
+            c->peer_now = true;
+            rc = launch_fused(c);
+            c->peer_now = false;
+            if (rc) return rc;
+            c->halo_fresh = true;
         } else {
             if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
             if ((rc = launch_fused(c))) return rc;
         }
+        if (!peer_ready(c)) c->halo_fresh = false;
         c->k += 1;
     }
     return TGV_OK;
@@ -1546,6 +1663,7 @@ int tgv_write_field(tgv_ctx* c, int f, const float* in, int64_t n)
 {
     int rc = check_ready(c);
     if (rc) return rc;
+    c->halo_fresh = false;  // the state changes outside an iteration
     if (!in) return fail(c, TGV_EINVAL, "in is NULL");
     if (f < 0 || f >= TGV_NUM_FIELDS) return fail(c, TGV_EINVAL, "bad field id %d", f);
     if (n != (int64_t)c->g.nx * c->g.ny * c->g.nzl) return fail(c, TGV_EINVAL, "n_voxels mismatch");
@@ -1716,7 +1834,8 @@ int tgv_create_group(const tgv_layout* layouts, const tgv_params* P, int n, cons
         (*grp)[r] = out[r];
         out[r]->group = grp;
     }
-    for (int r = 0; r < n; ++r)  // peer access between distinct devices (NVLink copies)
+    bool all_peer = true;
+    for (int r = 0; r < n; ++r)  // peer access between distinct devices (NVLink copies and stores)
         for (int o = 0; o < n; ++o)
             if (devices[r] != devices[o]) {
                 int can = 0;
@@ -1725,8 +1844,29 @@ int tgv_create_group(const tgv_layout* layouts, const tgv_params* P, int n, cons
                     cudaSetDevice(devices[r]);
                     cudaError_t e = cudaDeviceEnablePeerAccess(devices[o], 0);
                     if (e != cudaSuccess) cudaGetLastError();  // already enabled
+                } else if (o == r - 1 || o == r + 1) {
+                    all_peer = false;
                 }
             }
+    // peer halo mode (TGV_PEER_HALO=0 turns it off): each member maps its neighbours
+    if (all_peer && n > 1 && env_int("TGV_PEER_HALO", 1) != 0)
+        for (int r = 0; r < n; ++r) {
+            tgv_ctx* c = out[r];
+            c->peer = true;
+            if (r > 0) {
+                tgv_ctx* d = out[r - 1];
+                c->pdn = d->state;
+                c->pdn_fs = d->g.fs;
+                c->pdn_top = d->g.nzl + 1;
+                c->flag_dn_remote = d->flags + 2;  // its "from the upper neighbour" flag
+            }
+            if (r + 1 < n) {
+                tgv_ctx* u = out[r + 1];
+                c->pup = u->state;
+                c->pup_fs = u->g.fs;
+                c->flag_up_remote = u->flags + 1;  // its "from the lower neighbour" flag
+            }
+        }
     return TGV_OK;
 }
 
@@ -1770,6 +1910,27 @@ int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
                 CU(cudaSetDevice(m[r]->device));
                 if ((rc = launch_split(m[r], 1))) return rc;
             }
+        } else if (peer_ready(m[0])) {  // peer halo mode (the members share peer, schedule and model)
+            bool fresh = true;
+            for (int r = 0; r < n; ++r) fresh = fresh && m[r]->halo_fresh;
+            if (!fresh) {
+                if ((rc = group_exchange(m, n, plan_fused(k)))) return rc;
+            } else {  // order after the neighbours' previous launches (they wrote our halos, we write theirs)
+                for (int r = 0; r < n; ++r) {
+                    CU(cudaSetDevice(m[r]->device));
+                    if (r > 0) CU(cudaStreamWaitEvent(m[r]->stream, m[r - 1]->ev_step, 0));
+                    if (r + 1 < n) CU(cudaStreamWaitEvent(m[r]->stream, m[r + 1]->ev_step, 0));
+                }
+            }
+            for (int r = 0; r < n; ++r) {
+                CU(cudaSetDevice(m[r]->device));
+                m[r]->peer_wait = fresh ? m[r]->seq : 0;
+                m[r]->peer_now = true;
+                rc = launch_fused(m[r]);
+                m[r]->peer_now = false;
+                if (rc) return rc;
+                m[r]->halo_fresh = true;
+            }
         } else {
             if ((rc = group_exchange(m, n, plan_fused(k)))) return rc;
             for (int r = 0; r < n; ++r) {
@@ -1777,6 +1938,8 @@ int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
                 if ((rc = launch_fused(m[r]))) return rc;
             }
         }
+        if (!peer_ready(m[0]))
+            for (int r = 0; r < n; ++r) m[r]->halo_fresh = false;
         if ((rc = group_record(m, n))) return rc;
         for (int r = 0; r < n; ++r) m[r]->k += 1;
     }
@@ -1893,6 +2056,9 @@ void tgv_destroy(tgv_ctx* c)
             nccl->CommDestroy(c->comm);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (void* p : c->ipc_open)
+        if (p) cudaIpcCloseMemHandle(p);
+    cudaFree(c->flags);
     cudaFree(c->state);
     cudaFree(c->hist16);
     cudaFree(c->hist8);

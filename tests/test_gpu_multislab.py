@@ -56,3 +56,34 @@ def test_group_errors():
         tgv.tgv_iterate(g.ctxs[0], 1)  # members go through tgv_group_iterate
     assert ei.value.status == tgv.TGV_ESTATE
     g.iterate(2)
+
+
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_peer_halo_mode_replaces_the_exchange(peer, monkeypatch):
+    """Peer halo mode: the fused kernel writes its boundary planes into the
+    neighbours' halo planes and hands over with flags, so after the first iteration of a
+    call no halo copy runs; TGV_PEER_HALO=0 keeps the per-iteration exchange.  Both are
+    bitwise equal to one context."""
+    from paper_2107_14790_b200 import Group, Solver, tgv
+    monkeypatch.setenv("TGV_PEER_HALO", peer)
+    shape, cuts, iters = (61, 35, 29), [0, 7, 8, 20, 29], 12
+    h = synth.random_histograms(shape, 21)
+    one = Solver(shape, C8).load(h).iterate(iters)
+    grp = Group(shape, cuts, C8).load(h)
+    for c in grp.ctxs:
+        tgv.tgv_set_timing(c, True)
+    grp.iterate(iters)
+    exchanges = [tgv.tgv_get_timing(c)["halo_exchanges"] for c in grp.ctxs]
+    assert np.array_equal(grp.read_u(), one.read_u())
+    for f in ("v", "p", "q"):
+        assert np.array_equal(grp.get(f), one.get(f)), f
+    assert exchanges == ([1] * 4 if peer == "1" else [iters] * 4), exchanges
+    # a state change outside iterate (reset) falls back to one exchange, then peer writes again
+    for c in grp.ctxs:
+        tgv.tgv_reset(c)
+    grp.iterate(3)
+    one.reset()
+    one.iterate(3)
+    assert np.array_equal(grp.read_u(), one.read_u())
+    e1, eg = one.energy(), grp.energy()
+    assert abs(e1["E"] - eg["E"]) <= 1e-12 * abs(e1["E"])
