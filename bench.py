@@ -253,6 +253,8 @@ def run_vote(a, s, wl, rank, world, z0, z1, barrier_fn=None):
             "config": {"workload": f"{wl.name}: {wl.description}", "shape": list(wl.shape), "cameras": len(cams),
                        "step": "H2D depth maps + pyramids + Alg. 1 votes + count packing + state init"},
         }), flush=True)
+    if barrier_fn:
+        barrier_fn()
     s.close()
     return None
 
@@ -487,7 +489,9 @@ def run_ours(a):
                        "step": ("reset + iters x (dual, primal+over-relax) + energy/gap" if a.levels == 1 else
                                 f"coarse-to-fine: restrict to {a.levels} levels, iters per level, prolong, energy"),
                        "model": a.model, "schedule": a.schedule, "levels": a.levels,
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"z-slab x{world}, halos " + ("written by the kernel into the neighbours "
+                                       "(peer mode)" if info.get("peer_halo") else "by NCCL send/recv"))
+                       if world > 1 else "single GPU",
                        "l2": f"no flush: resident state+histograms {info['device_bytes'] / 1e9:.2f} GB per GPU "
                              f">> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -503,6 +507,7 @@ def run_ours(a):
             "wall_ms_per_step": float(ms_t[1]),
         }
         print(json.dumps(line), flush=True)
+    barrier()  # peer halo mode: no rank frees its state while a neighbour's kernel may still write it
     s.close()
     if world > 1:
         dist.destroy_process_group()

@@ -121,6 +121,8 @@ typedef struct {
     int64_t bytes_fused;      /* ... of one FUSED launch (one whole iteration)             */
     int32_t nranks, rank;
     int64_t iteration;        /* iterations since the last load / reset                    */
+    int32_t peer_halo;        /* 1: peer halo mode (the kernel writes the neighbours' halos) */
+    int32_t pad;
 } tgv_info_t;
 
 /* Rank 0 creates the NCCL unique id; the caller broadcasts the 128 bytes
@@ -133,11 +135,13 @@ int tgv_get_unique_id(uint8_t uid[128]);
  * above the slab: 120 B per voxel) and the histogram store (16 B per voxel,
  * plus 8 B when u8 counts are used), creates streams/events and, if nranks > 1, the NCCL
  * communicator from uid (uid must be NULL iff nranks == 1).
- * Peer halo mode (environment TGV_PEER_HALO=1 at create, nranks > 1):
+ * Peer halo mode (nranks > 1, unless TGV_PEER_HALO=0 at create):
  * the neighbours' state and hand-over flags are mapped with CUDA IPC (handles
  * exchanged by an NCCL all-gather) and the fused TGV kernel writes its boundary
- * planes straight into the neighbours' halo planes; tgv_destroy is then collective
- * (no rank may free its state while a neighbour's kernel can still write it).
+ * planes straight into the neighbours' halo planes; if any rank cannot map its
+ * neighbours, every rank keeps the NCCL halo exchange.  tgv_destroy is then
+ * collective (no rank may free its state while a neighbour's kernel can still
+ * write it: synchronise the ranks, e.g. with a barrier, before destroying).
  * Errors: TGV_EINVAL for any invalid argument (see tgv_params / tgv_layout;
  * also non-contiguous slabs across ranks), TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL.
  * On error *out is NULL. */
@@ -215,6 +219,18 @@ int tgv_set_border(tgv_ctx* ctx, int side, const float* u, const float* v, const
  * without allocating).  The context is unloaded afterwards: load its histograms
  * next.  Errors: TGV_EINVAL (bad slab / different size), TGV_ESTATE (not a leaf). */
 int tgv_leaf_rebind(tgv_ctx* ctx, int64_t z_begin, int64_t z_end);
+
+/* Peer halo mapping for contexts in different processes, the step
+ * tgv_create performs over NCCL when TGV_PEER_HALO=1: tgv_peer_export writes a
+ * 192-byte record (CUDA IPC handles of this context's state and hand-over flags,
+ * its slot stride and plane count); the neighbour passes it to tgv_peer_import with
+ * side 0 if the record's owner is its lower neighbour (slab just below) or 1 if its
+ * upper.  From then on the fused TGV kernel of the importer writes its boundary
+ * planes into that neighbour's halo planes and both hand over through the flags;
+ * both neighbours must map each other, and destroy is then collective.
+ * Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_peer_export(tgv_ctx* ctx, uint8_t rec[192]);
+int tgv_peer_import(tgv_ctx* ctx, int side, const uint8_t rec[192]);
 
 /* NEXT-1/3: this context's histograms as sums of factor^3 fine voxels (DESIGN.md
  * R18) of a finer grid nxf x nyf x nzf with ceil(n_fine / factor) = n on every axis;

@@ -158,7 +158,8 @@ struct TmaArgs {
     unsigned long long seq, wait_seq;
 };
 
-template <int TY, int SLOTS, typename CT>
+// PEER: the peer halo mode instantiation (the single-GPU kernel carries none of its code)
+template <int TY, int SLOTS, typename CT, bool PEER = false>
 __global__ void __launch_bounds__(32 * (TY + 3), 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
                      const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_st1,
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         for (int k = 0; k < Rg::NU; ++k) mbar_init(&S.bar_u[k], 1);
         for (int k = 0; k < Rg::NX; ++k) mbar_init(&S.bar_x[k], 1);
         fence_mbar_init();
-        if (A.wait_seq) {  // peer mode: the neighbours' previous launches wrote our halo planes
+        if (PEER && A.wait_seq) {  // peer mode: the neighbours' previous launches wrote our halo planes
             uint32_t n = 0;
             while ((A.pdn && ld_acquire_sys(A.flag_in_dn) < A.wait_seq) ||
                    (A.pup && ld_acquire_sys(A.flag_in_up) < A.wait_seq))
@@ -405,14 +406,14 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
 #pragma unroll
                     for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
-                    const bool inb = x < g.nx && y < g.ny;
-                    const int64_t cell = (int64_t)y * g.px + x;
-                    if (A.pdn && s == 0 && s >= zs && s < ze && inb) {  // q of plane 0 -> lower neighbour's top halo
+                    [[maybe_unused]] const bool inb = x < g.nx && y < g.ny;
+                    [[maybe_unused]] const int64_t cell = (int64_t)y * g.px + x;
+                    if (PEER && A.pdn && s == 0 && s >= zs && s < ze && inb) {  // q of plane 0 -> lower neighbour's top halo
                         float* o = A.pdn + (int64_t)A.pdn_top * g.plane + cell;
 #pragma unroll
                         for (int m = 0; m < 6; ++m) o[(A.s_qn + m) * A.pdn_fs] = qn[m];
                     }
-                    if (A.pup && s == g.nzl - 1 && s >= zs && s < ze && inb) {  // p of plane nzl-1 -> upper neighbour
+                    if (PEER && A.pup && s == g.nzl - 1 && s >= zs && s < ze && inb) {  // p of plane nzl-1 -> upper neighbour
                         float* o = A.pup + cell;
 #pragma unroll
                         for (int k = 0; k < 3; ++k) o[(A.s_pn + k) * A.pup_fs] = pn[k];
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                         S.out[2][r - 1][lane] = v1;
                         S.out[3][r - 1][lane] = v2;
                         // u, v of a boundary plane -> the neighbour's halo (peer mode)
+                        if constexpr (PEER) {
                         float* po = nullptr;
                         int64_t pfs = 0;
                         if (A.pdn && s - 1 == 0 && inb) {
@@ -464,6 +466,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                             o2[A.s_vn * A.pup_fs] = v0;
                             o2[(A.s_vn + 1) * A.pup_fs] = v1;
                             o2[(A.s_vn + 2) * A.pup_fs] = v2;
+                        }
                         }
                     }
                 }
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
         }
     }
-    if (A.done) {  // peer mode: publish once every CTA's halo stores are visible system-wide
+    if (PEER && A.done) {  // peer mode: publish once every CTA's halo stores are visible system-wide
         __threadfence_system();
         __syncthreads();
         if (tid0 && atomicAdd(A.done, 1ull) == gridDim.x - 1) {

@@ -541,8 +541,8 @@ int build_schedule(tgv_ctx* c, int zc, int per_sm)
     return TGV_OK;
 }
 
-template <int SLOTS, typename CT>
-int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
+template <int SLOTS, typename CT, bool PEER>
+int launch_fused_tma_tp(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
     const size_t smem = sizeof(TmaSmem<TMA_TY, HB>) + 128;
@@ -550,13 +550,18 @@ int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = 1ull << (c->device & 63);
     if (!(attr_set.load() & bit)) {
-        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT, PEER>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set.fetch_or(bit);
     }
-    fused_tma_kernel<TMA_TY, SLOTS, CT><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
+    fused_tma_kernel<TMA_TY, SLOTS, CT, PEER><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
         c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
     return TGV_OK;
+}
+template <int SLOTS, typename CT>
+int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
+{
+    return c->peer_now ? launch_fused_tma_tp<SLOTS, CT, true>(c, A, grd) : launch_fused_tma_tp<SLOTS, CT, false>(c, A, grd);
 }
 
 int launch_fused_tma(tgv_ctx* c)
@@ -872,18 +877,55 @@ struct IpcRecord {
     cudaIpcMemHandle_t state, flags;
     int64_t fs, nzl;
 };
+static_assert(sizeof(IpcRecord) <= 192, "tgv_peer_export record size");
+
+static int peer_export(tgv_ctx* c, IpcRecord* rec)
+{
+    if (cudaIpcGetMemHandle(&rec->state, c->state) != cudaSuccess ||
+        cudaIpcGetMemHandle(&rec->flags, c->flags) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ECUDA, "cudaIpcGetMemHandle failed");
+    }
+    rec->fs = c->g.fs;
+    rec->nzl = c->g.nzl;
+    return TGV_OK;
+}
+
+// side 0: the lower neighbour (its top halo receives our plane 0), 1: the upper neighbour
+static int peer_import(tgv_ctx* c, int side, const IpcRecord& n)
+{
+    void *ps = nullptr, *pf = nullptr;
+    if (cudaIpcOpenMemHandle(&ps, n.state, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ECUDA, "cudaIpcOpenMemHandle(state) failed (no peer access between the GPUs?)");
+    }
+    c->ipc_open[2 * side] = ps;
+    if (cudaIpcOpenMemHandle(&pf, n.flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ECUDA, "cudaIpcOpenMemHandle(flags) failed");
+    }
+    c->ipc_open[2 * side + 1] = pf;
+    if (side == 0) {
+        c->pdn = static_cast<float*>(ps);
+        c->pdn_fs = n.fs;
+        c->pdn_top = (int)n.nzl + 1;
+        c->flag_dn_remote = static_cast<unsigned long long*>(pf) + 2;  // its "from the upper neighbour" flag
+    } else {
+        c->pup = static_cast<float*>(ps);
+        c->pup_fs = n.fs;
+        c->flag_up_remote = static_cast<unsigned long long*>(pf) + 1;  // its "from the lower neighbour" flag
+    }
+    c->peer = true;
+    c->halo_fresh = false;
+    return TGV_OK;
+}
 
 static int map_ipc_neighbours(tgv_ctx* c)
 {
     const NcclApi* nccl = c->nccl;
     IpcRecord mine{};
-    if (cudaIpcGetMemHandle(&mine.state, c->state) != cudaSuccess ||
-        cudaIpcGetMemHandle(&mine.flags, c->flags) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(c, TGV_ECUDA, "cudaIpcGetMemHandle failed");
-    }
-    mine.fs = c->g.fs;
-    mine.nzl = c->g.nzl;
+    int rc = peer_export(c, &mine);
+    if (rc) return rc;
     std::vector<IpcRecord> all((size_t)c->nranks);
     char* d = nullptr;
     if (cudaMalloc(&d, sizeof(IpcRecord) * (size_t)c->nranks) != cudaSuccess) {
@@ -897,32 +939,8 @@ static int map_ipc_neighbours(tgv_ctx* c)
     cudaMemcpy(all.data(), d, sizeof(IpcRecord) * (size_t)c->nranks, cudaMemcpyDeviceToHost);
     cudaFree(d);
     if (r != ncclSuccess) return fail(c, TGV_ENCCL, "IPC all-gather: %s", nccl->GetErrorString(r));
-    auto open = [&](const cudaIpcMemHandle_t& h, int slot, void** p) -> int {
-        if (cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(c, TGV_ECUDA, "cudaIpcOpenMemHandle failed (no peer access between the GPUs?)");
-        }
-        c->ipc_open[slot] = *p;
-        return TGV_OK;
-    };
-    int rc;
-    void *ps = nullptr, *pf = nullptr;
-    if (c->rank > 0) {
-        const IpcRecord& n = all[(size_t)c->rank - 1];
-        if ((rc = open(n.state, 0, &ps)) || (rc = open(n.flags, 1, &pf))) return rc;
-        c->pdn = static_cast<float*>(ps);
-        c->pdn_fs = n.fs;
-        c->pdn_top = (int)n.nzl + 1;
-        c->flag_dn_remote = static_cast<unsigned long long*>(pf) + 2;
-    }
-    if (c->rank + 1 < c->nranks) {
-        const IpcRecord& n = all[(size_t)c->rank + 1];
-        if ((rc = open(n.state, 2, &ps)) || (rc = open(n.flags, 3, &pf))) return rc;
-        c->pup = static_cast<float*>(ps);
-        c->pup_fs = n.fs;
-        c->flag_up_remote = static_cast<unsigned long long*>(pf) + 1;
-    }
-    c->peer = true;
+    if (c->rank > 0 && (rc = peer_import(c, 0, all[(size_t)c->rank - 1]))) return rc;
+    if (c->rank + 1 < c->nranks && (rc = peer_import(c, 1, all[(size_t)c->rank + 1]))) return rc;
     return TGV_OK;
 }
 
@@ -1069,12 +1087,34 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
             fail(c, TGV_EINVAL, "slabs do not tile [0, nz) in rank order");
             return bail(TGV_EINVAL);
         }
-        // peer halo mode across processes (TGV_PEER_HALO=1; off by default: validated in-process
-        // through slab groups, the CUDA IPC mapping itself needs two GPUs): map the neighbours'
-        // state and flags with CUDA IPC, handles exchanged by an NCCL all-gather
-        if (env_int("TGV_PEER_HALO", 0) != 0) {
-            const int prc = map_ipc_neighbours(c);
-            if (prc) return bail(prc);
+        // peer halo mode across processes (default; TGV_PEER_HALO=0 keeps the NCCL exchange):
+        // map the neighbours' state and flags with CUDA IPC, handles exchanged by an NCCL
+        // all-gather.  Every rank must end up in the same mode (a mapped rank waits for its
+        // neighbours' flags), so the outcome is agreed by an all-reduce; on any failure all
+        // ranks fall back to the NCCL halo exchange.
+        if (env_int("TGV_PEER_HALO", 1) != 0) {
+            int ok = map_ipc_neighbours(c) == TGV_OK ? 1 : 0;
+            int* d_ok = nullptr;
+            int all_ok = 0;
+            if (cudaMalloc(&d_ok, sizeof(int)) == cudaSuccess) {
+                cudaMemcpy(d_ok, &ok, sizeof ok, cudaMemcpyHostToDevice);
+                if (nccl->AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, c->stream) == ncclSuccess &&
+                    cudaStreamSynchronize(c->stream) == cudaSuccess)
+                    cudaMemcpy(&all_ok, d_ok, sizeof all_ok, cudaMemcpyDeviceToHost);
+                cudaFree(d_ok);
+            }
+            cudaGetLastError();
+            if (!all_ok) {  // back to the NCCL exchange on every rank
+                for (void*& q : c->ipc_open)
+                    if (q) {
+                        cudaIpcCloseMemHandle(q);
+                        q = nullptr;
+                    }
+                c->peer = false;
+                c->pdn = c->pup = nullptr;
+                c->flag_dn_remote = c->flag_up_remote = nullptr;
+                c->err[0] = 0;
+            }
         }
     }
     if (make_state_maps(c)) return bail(TGV_ECUDA);
@@ -1100,6 +1140,32 @@ int tgv_create(const tgv_layout* L, const tgv_params* P, int rank, int nranks, c
 int tgv_create_leaf(const tgv_layout* L, const tgv_params* P, int dev, tgv_ctx** out)
 {
     return create_impl(L, P, 0, 1, nullptr, dev, false, out, true);
+}
+
+int tgv_peer_export(tgv_ctx* c, uint8_t rec[192])
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!rec) return fail(c, TGV_EINVAL, "rec is NULL");
+    IpcRecord r{};
+    if ((rc = peer_export(c, &r))) return rc;
+    memset(rec, 0, 192);
+    memcpy(rec, &r, sizeof r);
+    return TGV_OK;
+}
+
+int tgv_peer_import(tgv_ctx* c, int side, const uint8_t rec[192])
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!rec || (side != 0 && side != 1)) return fail(c, TGV_EINVAL, "NULL record or side not 0 / 1");
+    if (c->group) return fail(c, TGV_ESTATE, "group members map each other already");
+    if ((side == 0 && c->g.z0 == 0) || (side == 1 && c->g.z0 + c->g.nzl == c->g.nz))
+        return fail(c, TGV_EINVAL, "no neighbour on that side of the grid");
+    if (c->ipc_open[2 * side]) return fail(c, TGV_ESTATE, "that side is mapped already");
+    IpcRecord r;
+    memcpy(&r, rec, sizeof r);
+    return peer_import(c, side, r);
 }
 
 int tgv_leaf_rebind(tgv_ctx* c, int64_t z_begin, int64_t z_end)
@@ -2028,6 +2094,8 @@ int tgv_info(const tgv_ctx* c, tgv_info_t* o)
     o->fused_zc = fused_zc(c);
     o->fused_tma = c->fused_tma ? 1 : 0;
     o->nranks = c->nranks;
+    o->peer_halo = c->peer ? 1 : 0;
+    o->pad = 0;
     o->rank = c->rank;
     o->iteration = c->k;
     return TGV_OK;

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libtgv.so")
+LIB_PATH = os.environ.get("TGV_LIB") or os.path.join(_PKG, "lib", "libtgv.so")  # TGV_LIB: A/B builds (dev)
 
 TGV_OK, TGV_EINVAL, TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL, TGV_ESTATE, TGV_ERANGE = 0, -1, -2, -3, -4, -5, -6
 SCHEDULE_FUSED, SCHEDULE_SPLIT = 0, 1
@@ -28,7 +28,7 @@ EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset"
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
            "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts",
            "tgv_create_leaf", "tgv_set_border", "tgv_load_histograms_coarsened", "tgv_prolong_slab",
-           "tgv_leaf_rebind", "tgv_iterate_async", "tgv_sync"]
+           "tgv_leaf_rebind", "tgv_iterate_async", "tgv_sync", "tgv_peer_export", "tgv_peer_import"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -61,7 +61,8 @@ class tgv_info_t(ctypes.Structure):
                 ("count_slots", ctypes.c_int32), ("schedule", ctypes.c_int32), ("model", ctypes.c_int32),
                 ("fused_zc", ctypes.c_int32), ("fused_tma", ctypes.c_int32),
                 ("bytes_dual", ctypes.c_int64), ("bytes_primal", ctypes.c_int64), ("bytes_fused", ctypes.c_int64),
-                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("iteration", ctypes.c_int64)]
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("iteration", ctypes.c_int64),
+                ("peer_halo", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 def _load():
@@ -101,6 +102,8 @@ def _load():
     lib.tgv_load_histograms_coarsened.argtypes = [vp, vp, ctypes.c_int, i64, i64, i64, i64, ctypes.c_int]
     lib.tgv_prolong_slab.argtypes = [vp, vp, vp, i64, i64, i64, i64]
     lib.tgv_leaf_rebind.argtypes = [vp, i64, i64]
+    lib.tgv_peer_export.argtypes = [vp, ctypes.c_char_p]
+    lib.tgv_peer_import.argtypes = [vp, ctypes.c_int, ctypes.c_char_p]
     lib.tgv_destroy.argtypes = [vp]
     lib.tgv_destroy.restype = None
     lib.tgv_status_string.argtypes = [ctypes.c_int]
@@ -273,6 +276,17 @@ def tgv_create_leaf(shape, z_begin, z_end, centers, lam, alpha0, alpha1, tau, si
 def tgv_set_border(ctx, side: int, u=None, v=None, p=None, q=None):
     ptr = [None if a is None else _host_ptr(a, np.float32)[0] for a in (u, v, p, q)]
     _check(lib.tgv_set_border(ctx, int(side), *ptr), ctx)
+
+
+def tgv_peer_export(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(192)
+    _check(lib.tgv_peer_export(ctx, buf), ctx)
+    return buf.raw
+
+
+def tgv_peer_import(ctx, side: int, rec: bytes):
+    assert len(rec) == 192
+    _check(lib.tgv_peer_import(ctx, int(side), rec), ctx)
 
 
 def tgv_leaf_rebind(ctx, z_begin: int, z_end: int):
