@@ -1,0 +1,279 @@
+"""NEXT-3 block-sparse brick sets -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu legs may import
+this module; it never imports the product and shares no code with it.
+
+What it follows.  The paper solves each level over the cubes of an octree, part by
+part: "we update the indicator for all cubes inside the current leaf's border (set A)
+while the indicator for neighboring cubes outside of the border (set B) is frozen"
+(§4.5, Fig. 9), and cubes reach their neighbours through stored
+neighbour references (§4.2).  DESIGN.md reading R24 turns this into
+a block-sparse level:
+
+  * a level is a list of bricks, edge E voxels, at integer brick coordinates
+    (bx, by, bz); each brick is either solved (set A) or frozen (set B);
+  * the domain Omega is the union of the bricks' voxels; voxels outside Omega do not
+    exist (Neumann / zero flux across the boundary of Omega, reading R11);
+  * the difference operators are those of reading R6 restricted to Omega:
+        D+_k w[x] = w[x + e_k] - w[x]    if x + e_k in Omega, else 0
+        D-_k w[x] = [x + e_k in Omega] w[x] - [x - e_k in Omega] w[x - e_k]
+    so that D-_k = -(D+_k)^T on Omega (pinned by tests/test_oracle_bricks.py); on a
+    box-shaped Omega they are the dense grid's operators;
+  * one iteration is the scheme of oracle/tgv_oracle.c:
+    the dual step on every voxel of Omega, the primal step (prox, clamp, v update,
+    over-relaxation) on the voxels of A only; on B, u and v keep the values they were
+    given (ubar = u, vbar = v), as in reading R23's frozen leaf borders;
+  * the energy is the functional restricted to what the solve changes: the
+    regulariser over every voxel of Omega (terms at B voxels see A's values through
+    the stencil) and the data term over A.  The restricted dual value follows from the
+    saddle-point form sum_Omega [-u div p - v.(p + div2 q)] + G(u_A):
+        D_V = sum_A [min_{u in [-1,1]} (G(u) - u div p) - V |p + div2 q|_1]
+            + sum_B [-u div p - v.(p + div2 q)]
+    and gap = E - D_V >= 0 whenever the minimiser has |v_A| <= V (reading R14).
+
+The state is embedded in the dense bounding box of the bricks (numpy fp64 arrays,
+[z, y, x]); the masks do the rest.  Every array operation is elementwise or a shift by
+one voxel, written out per axis.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import default_centers
+
+AX = {0: 2, 1: 1, 2: 0}  # operator axis k (x, y, z) -> numpy axis of a [z, y, x] array
+QIDX = ((0, 3, 4), (3, 1, 5), (4, 5, 2))  # symmetric tensor storage xx, yy, zz, xy, xz, yz
+
+
+def _next(a, k):
+    """a[x + e_k], zero beyond the box."""
+    ax = AX[k]
+    out = np.zeros_like(a)
+    src = [slice(None)] * a.ndim
+    dst = [slice(None)] * a.ndim
+    src[ax] = slice(1, None)
+    dst[ax] = slice(0, -1)
+    out[tuple(dst)] = a[tuple(src)]
+    return out
+
+
+def _prev(a, k):
+    """a[x - e_k], zero before the box."""
+    ax = AX[k]
+    out = np.zeros_like(a)
+    src = [slice(None)] * a.ndim
+    dst = [slice(None)] * a.ndim
+    src[ax] = slice(0, -1)
+    dst[ax] = slice(1, None)
+    out[tuple(dst)] = a[tuple(src)]
+    return out
+
+
+def edge(om, k):
+    """[x in Omega and x + e_k in Omega]: the forward difference along k exists at x."""
+    return om & _next(om, k)
+
+
+def dplus(w, om, k):
+    m = edge(om, k)
+    return np.where(m, _next(w, k) - w, 0.0)
+
+
+def dminus(w, om, k):
+    m = edge(om, k)
+    a = np.where(m, w, 0.0)
+    return np.where(om, a - _prev(a, k), 0.0)
+
+
+def grad(u, om):
+    return np.stack([dplus(u, om, k) for k in range(3)])
+
+
+def symgrad(v, om):
+    e = np.zeros((6,) + v.shape[1:])
+    for k in range(3):
+        for l in range(k, 3):
+            e[QIDX[k][l]] = 0.5 * (dminus(v[k], om, l) + dminus(v[l], om, k))
+    return e
+
+
+def div(p, om):
+    return dminus(p[0], om, 0) + dminus(p[1], om, 1) + dminus(p[2], om, 2)
+
+
+def div2(q, om):
+    out = np.zeros((3,) + q.shape[1:])
+    for k in range(3):
+        out[k] = dplus(q[QIDX[k][0]], om, 0) + dplus(q[QIDX[k][1]], om, 1) + dplus(q[QIDX[k][2]], om, 2)
+    return out
+
+
+def data_term(h, c, lam, u):
+    """lambda sum_b h_b |u - c_b| (readings R1-R3); h [..., nb]."""
+    return lam * np.sum(h * np.abs(u[..., None] - c), axis=-1)
+
+
+def prox(ut, t, h, c):
+    """argmin_{u in [-1, 1]} 1/2 (u - ut)^2 + t sum_b h_b |u - c_b|, elementwise.
+    Same plain definition as oracle_prox (oracle/tgv_oracle.c): the objective is a
+    convex quadratic on each interval between breakpoints; minimise each piece, clip
+    to its interval, keep the best (first on ties)."""
+    nb = len(c)
+    best_u = np.zeros_like(ut)
+    best_f = np.full_like(ut, np.inf)
+    for j in range(nb + 1):
+        lo = -1.0 if j == 0 else max(c[j - 1], -1.0)
+        hi = 1.0 if j == nb else min(c[j], 1.0)
+        if lo > hi:
+            continue
+        below = h[..., :j].sum(-1)
+        above = h[..., j:].sum(-1)
+        s = np.clip(ut - t * (below - above), lo, hi)
+        f = 0.5 * (s - ut) ** 2 + t * np.sum(h * np.abs(s[..., None] - c), axis=-1)
+        better = f < best_f
+        best_u = np.where(better, s, best_u)
+        best_f = np.where(better, f, best_f)
+    return best_u
+
+
+def proj(x, a, n2):
+    """x / max(1, |x| / a) with |x|^2 = n2 (reading R5)."""
+    n = np.sqrt(n2)
+    return x * np.where(n > a, a / np.where(n > 0, n, 1.0), 1.0)
+
+
+class BrickOracle:
+    """fp64 state of one block-sparse level (R24).
+
+    coords [nbricks, 3] integer brick coordinates (bx, by, bz); frozen [nbricks] bool
+    (True = set B).  Arrays exchanged with the caller are brick-major:
+    u [nbricks, E, E, E] (z, y, x inside a brick), v [nbricks, 3, E, E, E],
+    counts [nbricks, E, E, E, nbins]."""
+
+    def __init__(self, edge_, coords, frozen=None, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25,
+                 centers=None, V=2.0):
+        self.E = int(edge_)
+        self.coords = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
+        nbk = len(self.coords)
+        if len({tuple(c) for c in self.coords}) != nbk:
+            raise ValueError("duplicate brick coordinates")
+        self.frozen = np.zeros(nbk, bool) if frozen is None else np.asarray(frozen, bool).reshape(nbk)
+        self.c = default_centers(8) if centers is None else np.asarray(centers, np.float64)
+        self.lam, self.alpha0, self.alpha1, self.tau, self.sigma, self.V = lam, alpha0, alpha1, tau, sigma, V
+        self.lo = self.coords.min(0)
+        ext = (self.coords.max(0) - self.lo + 1) * self.E  # (x, y, z) extents of the bounding box
+        self.box = (int(ext[2]), int(ext[1]), int(ext[0]))  # [z, y, x]
+        self.om = np.zeros(self.box, bool)
+        self.act = np.zeros(self.box, bool)
+        for b in range(nbk):
+            self.om[self._sl(b)] = True
+            self.act[self._sl(b)] = not self.frozen[b]
+        z = lambda *lead: np.zeros(lead + self.box)  # noqa: E731
+        self.u, self.ubar = z(), z()
+        self.v, self.vbar, self.p, self.q = z(3), z(3), z(3), z(6)
+        self.h = np.zeros(self.box + (len(self.c),))
+
+    def _sl(self, b):
+        o = (self.coords[b] - self.lo) * self.E
+        E = self.E
+        return (slice(o[2], o[2] + E), slice(o[1], o[1] + E), slice(o[0], o[0] + E))
+
+    # ---- brick-major <-> dense box
+    def _scatter(self, dst, src, lead):
+        for b in range(len(self.coords)):
+            dst[(Ellipsis,) + self._sl(b)] = src[b] if lead == 0 else src[b].reshape((lead,) + (self.E,) * 3)
+
+    def _gather(self, src, lead):
+        shp = (len(self.coords),) + ((lead,) if lead else ()) + (self.E,) * 3
+        out = np.zeros(shp)
+        for b in range(len(self.coords)):
+            out[b] = src[(Ellipsis,) + self._sl(b)]
+        return out
+
+    def load(self, counts):
+        """Histograms of the bricks (frozen bricks' entries are ignored) and the
+        initialisation of reading R9 on A; B holds 0 until set_primal."""
+        counts = np.asarray(counts, dtype=np.float64).reshape((len(self.coords),) + (self.E,) * 3 + (len(self.c),))
+        self.h[:] = 0.0
+        for b in range(len(self.coords)):
+            if not self.frozen[b]:
+                self.h[self._sl(b)] = counts[b]
+        W = self.h.sum(-1)
+        m = np.sum(self.h * self.c, axis=-1)
+        u0 = np.where(W > 0, m / np.where(W > 0, W, 1.0), 0.0)
+        self.u = np.where(self.act, u0, 0.0)
+        self.ubar = self.u.copy()
+        self.v[:] = 0.0
+        self.vbar[:] = 0.0
+        self.p[:] = 0.0
+        self.q[:] = 0.0
+        return self
+
+    def set_primal(self, u, v=None):
+        """u, v on every brick (A and B), a restart: ubar = u, vbar = v, p = q = 0
+        (the prolongation restart of reading R19; B keeps these values frozen)."""
+        self._scatter(self.u, np.asarray(u, np.float64), 0)
+        self.v[:] = 0.0
+        if v is not None:
+            self._scatter(self.v, np.asarray(v, np.float64), 3)
+        self.ubar = self.u.copy()
+        self.vbar = self.v.copy()
+        self.p[:] = 0.0
+        self.q[:] = 0.0
+        return self
+
+    def dual(self):
+        """(a1) on every voxel of Omega: p <- P_a1(p + s(grad ubar - vbar)), q <- P_a0(q + s E(vbar))."""
+        om = self.om
+        pn = self.p + self.sigma * (grad(self.ubar, om) - self.vbar)
+        pn = proj(pn, self.alpha1, pn[0] ** 2 + pn[1] ** 2 + pn[2] ** 2)
+        qn = self.q + self.sigma * symgrad(self.vbar, om)
+        n2 = qn[0] ** 2 + qn[1] ** 2 + qn[2] ** 2 + 2.0 * (qn[3] ** 2 + qn[4] ** 2 + qn[5] ** 2)
+        qn = proj(qn, self.alpha0, n2)
+        self.p = np.where(om, pn, 0.0)
+        self.q = np.where(om, qn, 0.0)
+
+    def primal(self):
+        """(a2) + (a3) on A: u+ = clamp(prox(u + t div p)), v+ = v + t(p + div2 q),
+        ubar = 2u+ - u, vbar = 2v+ - v; B unchanged (ubar = u, vbar = v)."""
+        om, A = self.om, self.act
+        un = prox(self.u + self.tau * div(self.p, om), self.tau * self.lam, self.h, self.c)
+        vn = self.v + self.tau * (self.p + div2(self.q, om))
+        un = np.where(A, un, self.u)
+        vn = np.where(A, vn, self.v)
+        self.ubar = 2.0 * un - self.u
+        self.vbar = 2.0 * vn - self.v
+        self.u, self.v = un, vn
+
+    def iterate(self, n):
+        for _ in range(int(n)):
+            self.dual()
+            self.primal()
+        return self
+
+    def get(self, name):
+        a = getattr(self, name)
+        return self._gather(a, 0 if a.ndim == 3 else a.shape[0])
+
+    def energy(self):
+        """{E, alpha1, alpha0, data, gap, vmax, dual}: regulariser over Omega, data
+        over A, restricted dual D_V of the module docstring, vmax over A."""
+        om, A = self.om, self.act
+        a = grad(self.u, om) - self.v
+        t1 = self.alpha1 * np.sqrt(a[0] ** 2 + a[1] ** 2 + a[2] ** 2)
+        e = symgrad(self.v, om)
+        t0 = self.alpha0 * np.sqrt(e[0] ** 2 + e[1] ** 2 + e[2] ** 2 + 2.0 * (e[3] ** 2 + e[4] ** 2 + e[5] ** 2))
+        td = data_term(self.h, self.c, self.lam, self.u)
+        d = div(self.p, om)
+        w = self.p + div2(self.q, om)
+        cand = [-1.0] + list(self.c) + [1.0]
+        best = np.min(np.stack([data_term(self.h, self.c, self.lam, np.full(self.box, uu)) - uu * d for uu in cand]),
+                      axis=0)
+        dA = best - self.V * (np.abs(w[0]) + np.abs(w[1]) + np.abs(w[2]))
+        dB = -self.u * d - (self.v[0] * w[0] + self.v[1] * w[1] + self.v[2] * w[2])
+        T1, T0 = float(np.sum(t1[om])), float(np.sum(t0[om]))
+        TD = float(np.sum(td[A]))
+        D = float(np.sum(dA[A]) + np.sum(dB[om & ~A]))
+        E = T1 + T0 + TD
+        vmax = float(np.max(np.abs(self.v[:, A]))) if A.any() else 0.0
+        return {"E": E, "alpha1": T1, "alpha0": T0, "data": TD, "gap": E - D, "vmax": vmax, "dual": D}
