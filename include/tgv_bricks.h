@@ -1,0 +1,121 @@
+/*
+ * tgv_bricks.h -- C ABI of the block-sparse brick-set solver (SURVEY.md §8(f)
+ * NEXT-3, BASELINE.json configs[4]; same library as tgv.h, libtgv.so).
+ *
+ * The paper minimises each level over the cubes of a sparse octree that reach
+ * their neighbours through stored references (§4.2), part by
+ * part, updating the cubes inside a part's border (set A) while the cubes just
+ * outside it (set B) stay frozen at the values of the previous level
+ * (§4.5, Fig. 9).  A brick set is one level of that,
+ * block-sparse (reading R24):
+ *
+ *   - nbricks bricks of edge E voxels (E = 4, 8, 16 or 32) at integer brick
+ *     coordinates (bx, by, bz), each SOLVED (set A) or FROZEN (set B);
+ *   - the domain Omega is the union of the bricks' voxels; the difference
+ *     operators of tgv.h (R6) are restricted to Omega:
+ *       D+_k w[x] = w[x + e_k] - w[x] if x + e_k is in Omega, else 0
+ *       D-_k w[x] = [x + e_k in Omega] w[x] - [x - e_k in Omega] w[x - e_k]
+ *     (Neumann / zero flux across the boundary of Omega);
+ *   - one iteration is the scheme of tgv.h (dual step on every voxel of Omega,
+ *     primal step and over-relaxation on the voxels of A); u and v of B keep
+ *     the values given by tgv_bricks_set_primal;
+ *   - a box-shaped set of solved bricks is exactly the dense grid of tgv.h.
+ *
+ * Layout of every per-voxel host array: brick-major in the order the bricks were
+ * given, inside a brick z, y, x (x fastest): element (b, z, y, x) is at
+ * ((b * E + z) * E + y) * E + x.  Conventions (status codes, ownership,
+ * poisoning) are those of tgv.h.  One iteration moves 180 B per voxel with u8
+ * counts (188 B with u16): a dual kernel and a primal kernel.
+ */
+#ifndef TGV_BRICKS_H
+#define TGV_BRICKS_H
+
+#include <stdint.h>
+
+#include "tgv.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tgv_bricks tgv_bricks; /* opaque */
+
+/* Brick set of one level.
+ *   edge     brick edge E in voxels: 4, 8, 16 or 32
+ *   nbricks  number of bricks, >= 1, nbricks * E^3 < 2^31
+ *   coords   int32 [nbricks][3] brick coordinates (bx, by, bz), each in [0, 2^20),
+ *            pairwise distinct; copied at create
+ *   frozen   uint8 [nbricks]: 0 = solved (set A), 1 = frozen (set B); NULL = all
+ *            solved; copied at create */
+typedef struct {
+    int32_t edge;
+    int64_t nbricks;
+    const int32_t* coords;
+    const uint8_t* frozen;
+} tgv_brickset;
+
+/* Create a brick-set context on cuda_device with the parameters of tgv.h
+ * (tgv_params, same validity rules).  The neighbour table (6 face neighbours
+ * per brick, or -1) is built here from the coordinates.
+ * Errors: TGV_EINVAL (NULL, bad edge / count / coordinates, duplicate bricks,
+ * invalid parameters), TGV_ENOMEM, TGV_ECUDA.  The reason is in
+ * tgv_last_error(NULL) when *out could not be created. */
+int tgv_bricks_create(const tgv_brickset* set, const tgv_params* params, int cuda_device, tgv_bricks** out);
+
+/* Load the histograms and initialise (R9): counts [nbricks][E^3][nbins]
+ * of unsigned integers of count_bytes bytes (1, 2 or 4), host memory; frozen
+ * bricks' entries are ignored.  On A: u = ubar = vote-weighted mean of the bin
+ * centres (0 where there is no vote); everywhere else and for every other field 0;
+ * the iteration counter goes to 0.
+ * Errors: TGV_EINVAL (NULL, n_counts != nbricks*E^3*nbins, bad count_bytes),
+ * TGV_ERANGE (a count > 65535), TGV_ENOMEM, TGV_ECUDA. */
+int tgv_bricks_load(tgv_bricks* ctx, const void* counts, int count_bytes, int64_t n_counts);
+
+/* Set u and v on every brick (A and B) and restart: ubar = u, vbar = v,
+ * p = q = 0, iteration counter 0 (the prolongation restart of DESIGN.md R19;
+ * the values on B stay frozen from here on).  u float [nbricks][E^3],
+ * v float [3][nbricks][E^3] (component-major) or NULL for v = 0; n_voxels must
+ * be nbricks*E^3.  Requires a previous tgv_bricks_load.
+ * Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_bricks_set_primal(tgv_bricks* ctx, const float* u, const float* v, int64_t n_voxels);
+
+/* Run n >= 0 iterations (a dual kernel then a primal kernel each) and wait.
+ * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load), TGV_ECUDA. */
+int tgv_bricks_iterate(tgv_bricks* ctx, int32_t n);
+
+/* Copy one field (TGV_FIELD_U, V + k, P + k, Q + m of tgv.h) of every brick to
+ * the host: out float [nbricks][E^3]; n_voxels = nbricks*E^3.  The over-relaxed
+ * iterates are formed inside the kernels and not stored (TGV_FIELD_UBAR / VBAR
+ * return TGV_EINVAL).  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
+int tgv_bricks_read(tgv_bricks* ctx, int field, float* out, int64_t n_voxels);
+
+/* Energy and restricted gap (R24, fp64 per-voxel terms, deterministic
+ * reduction): the regulariser over every voxel of Omega, the data term over A,
+ *   out[0] E   out[1] alpha1-term   out[2] alpha0-term   out[3] data-term
+ *   out[4] gap_V = E - D_V with
+ *          D_V = sum_A [min_{u in [-1,1]} (lambda sum_b h_b |u - c_b| - u div p) - V |p + div2 q|_1]
+ *              + sum_B [-u div p - v.(p + div2 q)],   V = 2
+ *   out[5] max |v_k| over A.
+ * Errors: TGV_EINVAL (NULL), TGV_ESTATE, TGV_ECUDA. */
+int tgv_bricks_energy(tgv_bricks* ctx, double out[6]);
+
+/* Per-kernel device timing with CUDA events on the context's stream (dual_ms,
+ * primal_ms, energy_ms and the launch counts of tgv_timing; the other members
+ * are 0).  Enabling resets the sums.  Errors: TGV_EINVAL, TGV_ECUDA. */
+int tgv_bricks_set_timing(tgv_bricks* ctx, int enable);
+int tgv_bricks_get_timing(tgv_bricks* ctx, tgv_timing* out);
+
+/* Device bytes owned by the context and the stored count width (1 or 2). */
+int tgv_bricks_info(const tgv_bricks* ctx, int64_t* device_bytes, int32_t* count_bytes);
+
+/* Detail of the last failure on ctx (or of the last failed create, ctx = NULL). */
+const char* tgv_bricks_last_error(const tgv_bricks* ctx);
+
+/* Free everything the context owns.  NULL-safe. */
+void tgv_bricks_destroy(tgv_bricks* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TGV_BRICKS_H */

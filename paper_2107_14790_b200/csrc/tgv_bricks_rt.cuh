@@ -1,0 +1,556 @@
+// tgv_bricks_rt.cuh -- context and C ABI of the block-sparse brick-set solver
+// (include/tgv_bricks.h; R24).  Included at the end of tgv_runtime.cu
+// (one translation unit: the kernels of tgv_kernels.cuh are shared, not duplicated).
+//
+// The context owns the fp32 state (30 rotating slots of nbricks * E^3 floats, the
+// slot rotation of tgv_runtime.cu), the neighbour table and frozen flags, the
+// counts (u8 when every count <= 255, else u16), a stream and timing events.
+#include <unordered_map>
+
+#include "../../include/tgv_bricks.h"
+#include "tgv_bricks.cuh"
+
+struct tgv_bricks {
+    int device = 0;
+    int LE = 0, E = 0;
+    int64_t nbricks = 0, nvox = 0;
+    int nbins = 0, slots = 8, count_bytes = 0;
+    float centers[16]{};
+    float lambda = 0, alpha0 = 0, alpha1 = 0, tau = 0, sigma = 0;
+
+    float* state = nullptr;     // NSLOT slots of nvox floats
+    int* nbr = nullptr;         // [nbricks][6]
+    uint8_t* frozen = nullptr;  // [nbricks]
+    void* hist = nullptr;       // [nvox][slots] of u8 / u16
+    double* partials = nullptr;
+    double* d_out = nullptr;
+    unsigned int* d_maxc = nullptr;
+    int energy_blocks = 0;
+    int64_t device_bytes = 0;
+
+    int64_t k = 0;
+    bool loaded = false, poisoned = false;
+    cudaStream_t stream = nullptr;
+    char err[512] = "";
+
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+    std::vector<int> ev_kind;     // 0 dual, 1 primal, 2 energy
+    double t_ms[3]{};
+    int64_t t_n[3]{};
+};
+
+namespace {
+
+thread_local char g_bricks_error[512] = "";
+
+int bfail(tgv_bricks* c, int code, const char* fmt, ...)
+{
+    char* dst = c ? c->err : g_bricks_error;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(dst, 512, fmt, ap);
+    va_end(ap);
+    if (c && code == TGV_ECUDA) c->poisoned = true;
+    return code;
+}
+
+#define BCU(call)                                                                                  \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return bfail(c, TGV_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+inline float* bslot(tgv_bricks* c, int s) { return c->state + (int64_t)s * c->nvox; }
+
+int bready(tgv_bricks* c)
+{
+    if (!c) return TGV_EINVAL;
+    if (c->poisoned) return bfail(c, TGV_ESTATE, "context poisoned by an earlier CUDA failure");
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ECUDA, "cudaSetDevice(%d) failed", c->device);
+    }
+    return TGV_OK;
+}
+
+BrickGeo bgeo(const tgv_bricks* c) { return BrickGeo{(int)c->nvox, c->nbr, c->frozen}; }
+
+IterPtrs biter_ptrs(tgv_bricks* c, int64_t k)
+{
+    const Bufs b = bufs(k);
+    IterPtrs a{};
+    a.uk = bslot(c, slotU(b.cu));
+    a.um = bslot(c, slotU(b.pu));
+    a.un = bslot(c, slotU(b.nu));
+    for (int d = 0; d < 3; ++d) {
+        a.vk[d] = bslot(c, slotV(b.cu, d));
+        a.vm[d] = bslot(c, slotV(b.pu, d));
+        a.vn[d] = bslot(c, slotV(b.nu, d));
+        a.pk[d] = bslot(c, slotP(b.cp, d));
+        a.pn[d] = bslot(c, slotP(b.np, d));
+    }
+    for (int m = 0; m < 6; ++m) {
+        a.qk[m] = bslot(c, slotQ(b.cp, m));
+        a.qn[m] = bslot(c, slotQ(b.np, m));
+    }
+    a.hist = c->hist;
+    return a;
+}
+
+Centers bcenters(const tgv_bricks* c)
+{
+    Centers C;
+    for (int b = 0; b < 16; ++b) C.c[b] = b < c->nbins ? c->centers[b] : INFINITY;
+    return C;
+}
+
+int btimer(tgv_bricks* c, int kind, bool end)
+{
+    if (!c->timing) return TGV_OK;
+    if (!end) {
+        cudaEvent_t e[2];
+        BCU(cudaEventCreate(&e[0]));
+        BCU(cudaEventCreate(&e[1]));
+        c->ev.push_back(e[0]);
+        c->ev.push_back(e[1]);
+        c->ev_kind.push_back(kind);
+        BCU(cudaEventRecord(e[0], c->stream));
+    } else {
+        BCU(cudaEventRecord(c->ev.back(), c->stream));
+    }
+    return TGV_OK;
+}
+
+int btimer_collect(tgv_bricks* c)
+{
+    for (size_t j = 0; j < c->ev_kind.size(); ++j) {
+        float ms = 0.f;
+        BCU(cudaEventElapsedTime(&ms, c->ev[2 * j], c->ev[2 * j + 1]));
+        c->t_ms[c->ev_kind[j]] += ms;
+        c->t_n[c->ev_kind[j]] += 1;
+    }
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    c->ev.clear();
+    c->ev_kind.clear();
+    return TGV_OK;
+}
+
+template <int LE>
+void launch_brick_primal_le(tgv_bricks* c, const IterPtrs& a, int blocks, const StepParams& sp)
+{
+    const BrickGeo bg = bgeo(c);
+    const Centers C = bcenters(c);
+    if (c->slots == 8 && c->count_bytes == 1) brick_primal_kernel<LE, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
+    else if (c->slots == 8) brick_primal_kernel<LE, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
+    else if (c->count_bytes == 1) brick_primal_kernel<LE, 16, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
+    else brick_primal_kernel<LE, 16, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
+}
+
+template <int LE>
+void launch_brick_init_le(tgv_bricks* c)
+{
+    const BrickGeo bg = bgeo(c);
+    const Centers C = bcenters(c);
+    float* u0 = bslot(c, slotU(0));
+    float* u2 = bslot(c, slotU(2));  // bufs(0): current 0, previous 2
+    if (c->slots == 8 && c->count_bytes == 1) brick_init_kernel<LE, 8, uint8_t><<<148 * 8, 256, 0, c->stream>>>(u0, u2, c->hist, bg, C);
+    else if (c->slots == 8) brick_init_kernel<LE, 8, uint16_t><<<148 * 8, 256, 0, c->stream>>>(u0, u2, c->hist, bg, C);
+    else if (c->count_bytes == 1) brick_init_kernel<LE, 16, uint8_t><<<148 * 8, 256, 0, c->stream>>>(u0, u2, c->hist, bg, C);
+    else brick_init_kernel<LE, 16, uint16_t><<<148 * 8, 256, 0, c->stream>>>(u0, u2, c->hist, bg, C);
+}
+
+template <int LE>
+void launch_brick_energy_le(tgv_bricks* c, const EnergyArgs& ea)
+{
+    const BrickGeo bg = bgeo(c);
+    const Centers C = bcenters(c);
+    const int nb = c->energy_blocks;
+    if (c->slots == 8 && c->count_bytes == 1) brick_energy_kernel<LE, 8, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
+    else if (c->slots == 8) brick_energy_kernel<LE, 8, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
+    else if (c->count_bytes == 1) brick_energy_kernel<LE, 16, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
+    else brick_energy_kernel<LE, 16, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
+}
+
+#define BRICK_LE_DISPATCH(fn, ...)            \
+    switch (c->LE) {                          \
+        case 2: fn<2>(__VA_ARGS__); break;    \
+        case 3: fn<3>(__VA_ARGS__); break;    \
+        case 4: fn<4>(__VA_ARGS__); break;    \
+        default: fn<5>(__VA_ARGS__); break;   \
+    }
+
+template <int LE>
+void launch_brick_dual_le(tgv_bricks* c, const IterPtrs& a, int blocks, const StepParams& sp)
+{
+    brick_dual_kernel<LE><<<blocks, 256, 0, c->stream>>>(a, bgeo(c), sp);
+}
+
+int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
+{
+    const int blocks = (int)((c->nvox + 255) / 256);
+    const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
+    int rc;
+    for (int32_t it = 0; it < n; ++it) {
+        const IterPtrs a = biter_ptrs(c, c->k);
+        if ((rc = btimer(c, 0, false))) return rc;
+        BRICK_LE_DISPATCH(launch_brick_dual_le, c, a, blocks, sp);
+        BCU(cudaGetLastError());
+        if ((rc = btimer(c, 0, true))) return rc;
+        // the primal reads p_{k+1}, q_{k+1}: the dual's outputs
+        IterPtrs ap = a;
+        for (int d = 0; d < 3; ++d) ap.pk[d] = a.pn[d];
+        for (int m = 0; m < 6; ++m) ap.qk[m] = a.qn[m];
+        if ((rc = btimer(c, 1, false))) return rc;
+        BRICK_LE_DISPATCH(launch_brick_primal_le, c, ap, blocks, sp);
+        BCU(cudaGetLastError());
+        if ((rc = btimer(c, 1, true))) return rc;
+        c->k += 1;
+    }
+    return TGV_OK;
+}
+
+template <typename T>
+void launch_brick_pack(tgv_bricks* c, const void* src, int64_t nv, uint16_t* dst)
+{
+    if (c->slots == 8)
+        brick_pack_kernel<T, 8><<<148 * 8, 256, 0, c->stream>>>((const T*)src, nv, c->nbins, dst, c->d_maxc);
+    else
+        brick_pack_kernel<T, 16><<<148 * 8, 256, 0, c->stream>>>((const T*)src, nv, c->nbins, dst, c->d_maxc);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tgv_bricks_last_error(const tgv_bricks* c) { return c ? c->err : g_bricks_error; }
+
+int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_bricks** out)
+{
+    tgv_bricks* c = nullptr;
+    if (!S || !P || !out) return bfail(c, TGV_EINVAL, "NULL argument");
+    *out = nullptr;
+    int LE = -1;
+    for (int l = 2; l <= 5; ++l)
+        if (S->edge == (1 << l)) LE = l;
+    if (LE < 0) return bfail(c, TGV_EINVAL, "brick edge %d not in {4, 8, 16, 32}", S->edge);
+    if (S->nbricks < 1 || !S->coords) return bfail(c, TGV_EINVAL, "need nbricks >= 1 and coords");
+    const int64_t nvox = S->nbricks << (3 * LE);
+    if (nvox >= (int64_t(1) << 31)) return bfail(c, TGV_EINVAL, "nbricks * E^3 must be < 2^31");
+    if (P->nbins < 1 || P->nbins > 16) return bfail(c, TGV_EINVAL, "nbins must be in [1, 16]");
+    if (!P->bin_centers) return bfail(c, TGV_EINVAL, "bin_centers is NULL");
+    for (int b = 0; b < P->nbins; ++b) {
+        const float cb = P->bin_centers[b];
+        if (!std::isfinite(cb) || cb < -1.f || cb > 1.f) return bfail(c, TGV_EINVAL, "bin centre %d outside [-1,1]", b);
+        if (b > 0 && !(cb > P->bin_centers[b - 1])) return bfail(c, TGV_EINVAL, "bin centres not strictly increasing");
+    }
+    const float vals[5] = {P->lambda, P->alpha0, P->alpha1, P->tau, P->sigma};
+    for (float v : vals)
+        if (!std::isfinite(v) || v < 0.f) return bfail(c, TGV_EINVAL, "parameters must be finite and >= 0");
+    if (!(P->tau > 0.f) || !(P->sigma > 0.f)) return bfail(c, TGV_EINVAL, "tau and sigma must be > 0");
+    if ((double)P->tau * (double)P->sigma * 16.0 > 1.0 + 1e-6)
+        return bfail(c, TGV_EINVAL, "step sizes violate tau*sigma*16 <= 1 (tau=%g sigma=%g)", P->tau, P->sigma);
+
+    // neighbour table from the coordinates
+    const int64_t nb = S->nbricks;
+    std::vector<int> nbr((size_t)nb * 6, -1);
+    {
+        std::unordered_map<uint64_t, int> at;
+        at.reserve((size_t)nb * 2);
+        auto key = [](int64_t x, int64_t y, int64_t z) { return (uint64_t)x | (uint64_t)y << 21 | (uint64_t)z << 42; };
+        for (int64_t b = 0; b < nb; ++b) {
+            const int32_t* q = S->coords + 3 * b;
+            for (int a = 0; a < 3; ++a)
+                if (q[a] < 0 || q[a] >= (1 << 20)) return bfail(c, TGV_EINVAL, "brick %lld coordinate outside [0, 2^20)", (long long)b);
+            if (!at.emplace(key(q[0], q[1], q[2]), (int)b).second)
+                return bfail(c, TGV_EINVAL, "duplicate brick coordinates (%d, %d, %d)", q[0], q[1], q[2]);
+        }
+        for (int64_t b = 0; b < nb; ++b) {
+            const int32_t* q = S->coords + 3 * b;
+            for (int a = 0; a < 3; ++a)
+                for (int d = 0; d < 2; ++d) {
+                    int64_t r[3] = {q[0], q[1], q[2]};
+                    r[a] += d ? 1 : -1;
+                    if (r[a] < 0 || r[a] >= (1 << 20)) continue;
+                    auto it = at.find(key(r[0], r[1], r[2]));
+                    if (it != at.end()) nbr[(size_t)b * 6 + 2 * a + d] = it->second;
+                }
+        }
+    }
+
+    c = new (std::nothrow) tgv_bricks();
+    if (!c) return bfail(nullptr, TGV_ENOMEM, "host allocation failed");
+    auto bail = [&](int code) {
+        snprintf(g_bricks_error, sizeof g_bricks_error, "%s", c->err);
+        tgv_bricks_destroy(c);
+        return code;
+    };
+    c->device = dev;
+    c->LE = LE;
+    c->E = 1 << LE;
+    c->nbricks = nb;
+    c->nvox = nvox;
+    c->nbins = P->nbins;
+    c->slots = P->nbins <= 8 ? 8 : 16;
+    for (int b = 0; b < P->nbins; ++b) c->centers[b] = P->bin_centers[b];
+    c->lambda = P->lambda;
+    c->alpha0 = P->alpha0;
+    c->alpha1 = P->alpha1;
+    c->tau = P->tau;
+    c->sigma = P->sigma;
+    if (cudaSetDevice(dev) != cudaSuccess) {
+        cudaGetLastError();
+        bfail(c, TGV_ECUDA, "cudaSetDevice(%d) failed", dev);
+        return bail(TGV_ECUDA);
+    }
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        bfail(c, TGV_ECUDA, "stream creation failed");
+        return bail(TGV_ECUDA);
+    }
+    c->energy_blocks = 148 * 4;
+    const size_t state_bytes = sizeof(float) * (size_t)NSLOT * (size_t)nvox;
+    if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->nbr, sizeof(int) * 6 * (size_t)nb) != cudaSuccess ||
+        cudaMalloc(&c->frozen, (size_t)nb) != cudaSuccess ||
+        cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
+        cudaMalloc(&c->d_out, sizeof(double) * EN_TERMS) != cudaSuccess ||
+        cudaMalloc(&c->d_maxc, sizeof(unsigned int)) != cudaSuccess) {
+        cudaGetLastError();
+        bfail(c, TGV_ENOMEM, "device allocation failed (%zu B of state)", state_bytes);
+        return bail(TGV_ENOMEM);
+    }
+    c->device_bytes = (int64_t)state_bytes + 7 * nb + (int64_t)sizeof(double) * EN_TERMS * (c->energy_blocks + 1);
+    std::vector<uint8_t> fr((size_t)nb, 0);
+    if (S->frozen)
+        for (int64_t b = 0; b < nb; ++b) fr[(size_t)b] = S->frozen[b] ? 1 : 0;
+    if (cudaMemcpy(c->nbr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->frozen, fr.data(), fr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        bfail(c, TGV_ECUDA, "table upload failed");
+        return bail(TGV_ECUDA);
+    }
+    *out = c;
+    return TGV_OK;
+}
+
+int tgv_bricks_load(tgv_bricks* c, const void* counts, int count_bytes, int64_t n_counts)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!counts) return bfail(c, TGV_EINVAL, "counts is NULL");
+    if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4) return bfail(c, TGV_EINVAL, "count_bytes must be 1, 2 or 4");
+    if (n_counts != c->nvox * c->nbins)
+        return bfail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n_counts, (long long)(c->nvox * c->nbins));
+    c->loaded = false;
+    // u16 store of every count, filled chunk by chunk from a device staging buffer
+    uint16_t* h16 = nullptr;
+    const size_t n16 = (size_t)c->nvox * c->slots;
+    if (cudaMalloc(&h16, sizeof(uint16_t) * n16) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ENOMEM, "u16 count staging allocation failed");
+    }
+    const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (c->nbins * count_bytes));  // voxels per chunk
+    void* stg = nullptr;
+    if (cudaMalloc(&stg, (size_t)std::min(chunk, c->nvox) * c->nbins * count_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(h16);
+        return bfail(c, TGV_ENOMEM, "count staging allocation failed");
+    }
+    auto done = [&](int code) {
+        cudaFree(stg);
+        cudaFree(h16);
+        return code;
+    };
+    if (cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream) != cudaSuccess) return done(bfail(c, TGV_ECUDA, "memset"));
+    for (int64_t v0 = 0; v0 < c->nvox; v0 += chunk) {
+        const int64_t nv = std::min(chunk, c->nvox - v0);
+        const size_t bytes = (size_t)nv * c->nbins * count_bytes;
+        if (cudaMemcpyAsync(stg, (const uint8_t*)counts + (size_t)v0 * c->nbins * count_bytes, bytes, cudaMemcpyHostToDevice,
+                            c->stream) != cudaSuccess)
+            return done(bfail(c, TGV_ECUDA, "count upload failed"));
+        uint16_t* dst = h16 + (size_t)v0 * c->slots;
+        if (count_bytes == 1) launch_brick_pack<uint8_t>(c, stg, nv, dst);
+        else if (count_bytes == 2) launch_brick_pack<uint16_t>(c, stg, nv, dst);
+        else launch_brick_pack<uint32_t>(c, stg, nv, dst);
+        if (cudaGetLastError() != cudaSuccess) return done(bfail(c, TGV_ECUDA, "pack kernel launch failed"));
+    }
+    unsigned int maxc = 0;
+    if (cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return done(bfail(c, TGV_ECUDA, "count upload failed: %s", cudaGetErrorString(cudaGetLastError())));
+    if (maxc > 65535u) return done(bfail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc));
+    const int cb = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0 ? 1 : 2;
+    if (c->hist && cb != c->count_bytes) {
+        cudaFree(c->hist);
+        c->device_bytes -= (int64_t)n16 * c->count_bytes;
+        c->hist = nullptr;
+    }
+    if (!c->hist) {
+        if (cudaMalloc(&c->hist, n16 * cb) != cudaSuccess) {
+            cudaGetLastError();
+            return done(bfail(c, TGV_ENOMEM, "count store allocation failed"));
+        }
+        c->device_bytes += (int64_t)n16 * cb;
+    }
+    c->count_bytes = cb;
+    if (cb == 1) compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(h16, (uint8_t*)c->hist, (int64_t)n16);
+    else if (cudaMemcpyAsync(c->hist, h16, sizeof(uint16_t) * n16, cudaMemcpyDeviceToDevice, c->stream) != cudaSuccess)
+        return done(bfail(c, TGV_ECUDA, "count copy failed"));
+    // initial state (R9): zero every slot, then u_0 into the current and previous u
+    if (cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream) != cudaSuccess)
+        return done(bfail(c, TGV_ECUDA, "state memset failed"));
+    BRICK_LE_DISPATCH(launch_brick_init_le, c);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return done(bfail(c, TGV_ECUDA, "initialisation failed: %s", cudaGetErrorString(cudaGetLastError())));
+    c->k = 0;
+    c->loaded = true;
+    return done(TGV_OK);
+}
+
+int tgv_bricks_set_primal(tgv_bricks* c, const float* u, const float* v, int64_t n)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!u) return bfail(c, TGV_EINVAL, "u is NULL");
+    if (n != c->nvox) return bfail(c, TGV_EINVAL, "n_voxels %lld != %lld", (long long)n, (long long)c->nvox);
+    if (!c->loaded) return bfail(c, TGV_ESTATE, "set_primal before load");
+    const size_t fb = sizeof(float) * (size_t)c->nvox;
+    c->k = 0;
+    const Bufs b = bufs(0);
+    BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
+    for (int s : {b.cu, b.pu}) {
+        BCU(cudaMemcpyAsync(bslot(c, slotU(s)), u, fb, cudaMemcpyHostToDevice, c->stream));
+        if (v)
+            for (int d = 0; d < 3; ++d)
+                BCU(cudaMemcpyAsync(bslot(c, slotV(s, d)), v + (size_t)d * c->nvox, fb, cudaMemcpyHostToDevice, c->stream));
+    }
+    BCU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
+}
+
+int tgv_bricks_iterate(tgv_bricks* c, int32_t n)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (n < 0) return bfail(c, TGV_EINVAL, "n must be >= 0");
+    if (!c->loaded) return bfail(c, TGV_ESTATE, "iterate before load");
+    if ((rc = brick_iterate_enqueue(c, n))) return rc;
+    BCU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
+}
+
+int tgv_bricks_read(tgv_bricks* c, int f, float* out, int64_t n)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!out) return bfail(c, TGV_EINVAL, "out is NULL");
+    if (n != c->nvox) return bfail(c, TGV_EINVAL, "n_voxels %lld != %lld", (long long)n, (long long)c->nvox);
+    if (f < 0 || f >= TGV_NUM_FIELDS) return bfail(c, TGV_EINVAL, "bad field id %d", f);
+    if (!c->loaded) return bfail(c, TGV_ESTATE, "read before load");
+    const Bufs b = bufs(c->k);
+    const size_t fb = sizeof(float) * (size_t)c->nvox;
+    if (f == TGV_FIELD_UBAR || (f >= TGV_FIELD_VBAR && f < TGV_FIELD_VBAR + 3))
+        return bfail(c, TGV_EINVAL, "ubar / vbar are formed inside the kernels, not stored: read u, v");
+    int s;
+    if (f == TGV_FIELD_U) s = slotU(b.cu);
+    else if (f < TGV_FIELD_UBAR) s = slotV(b.cu, f - TGV_FIELD_V);
+    else if (f < TGV_FIELD_Q) s = slotP(b.cp, f - TGV_FIELD_P);
+    else s = slotQ(b.cp, f - TGV_FIELD_Q);
+    BCU(cudaMemcpyAsync(out, bslot(c, s), fb, cudaMemcpyDeviceToHost, c->stream));
+    BCU(cudaStreamSynchronize(c->stream));
+    return TGV_OK;
+}
+
+int tgv_bricks_energy(tgv_bricks* c, double out[6])
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!out) return bfail(c, TGV_EINVAL, "out is NULL");
+    if (!c->loaded) return bfail(c, TGV_ESTATE, "energy before load");
+    const Bufs b = bufs(c->k);
+    EnergyArgs ea{};
+    ea.u = bslot(c, slotU(b.cu));
+    for (int d = 0; d < 3; ++d) {
+        ea.v[d] = bslot(c, slotV(b.cu, d));
+        ea.p[d] = bslot(c, slotP(b.cp, d));
+    }
+    for (int m = 0; m < 6; ++m) ea.q[m] = bslot(c, slotQ(b.cp, m));
+    ea.hist = c->hist;
+    ea.alpha1 = c->alpha1;
+    ea.alpha0 = c->alpha0;
+    ea.lambda = c->lambda;
+    ea.V = 2.0;
+    ea.nbins = c->nbins;
+    if ((rc = btimer(c, 2, false))) return rc;
+    BRICK_LE_DISPATCH(launch_brick_energy_le, c, ea);
+    BCU(cudaGetLastError());
+    energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, c->energy_blocks, c->d_out);
+    BCU(cudaGetLastError());
+    if ((rc = btimer(c, 2, true))) return rc;
+    double h[EN_TERMS];
+    BCU(cudaMemcpyAsync(h, c->d_out, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    BCU(cudaStreamSynchronize(c->stream));
+    energy_out(h, out);
+    return TGV_OK;
+}
+
+int tgv_bricks_set_timing(tgv_bricks* c, int enable)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    BCU(cudaStreamSynchronize(c->stream));
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    c->ev.clear();
+    c->ev_kind.clear();
+    for (int j = 0; j < 3; ++j) {
+        c->t_ms[j] = 0.0;
+        c->t_n[j] = 0;
+    }
+    c->timing = enable != 0;
+    return TGV_OK;
+}
+
+int tgv_bricks_get_timing(tgv_bricks* c, tgv_timing* o)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!o) return bfail(c, TGV_EINVAL, "out is NULL");
+    BCU(cudaStreamSynchronize(c->stream));
+    if ((rc = btimer_collect(c))) return rc;
+    *o = tgv_timing{};
+    o->dual_ms = c->t_ms[0];
+    o->primal_ms = c->t_ms[1];
+    o->energy_ms = c->t_ms[2];
+    o->dual_launches = c->t_n[0];
+    o->primal_launches = c->t_n[1];
+    o->energy_launches = c->t_n[2];
+    return TGV_OK;
+}
+
+int tgv_bricks_info(const tgv_bricks* c, int64_t* device_bytes, int32_t* count_bytes)
+{
+    if (!c) return TGV_EINVAL;
+    if (device_bytes) *device_bytes = c->device_bytes;
+    if (count_bytes) *count_bytes = c->count_bytes;
+    return TGV_OK;
+}
+
+void tgv_bricks_destroy(tgv_bricks* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    cudaFree(c->state);
+    cudaFree(c->nbr);
+    cudaFree(c->frozen);
+    cudaFree(c->hist);
+    cudaFree(c->partials);
+    cudaFree(c->d_out);
+    cudaFree(c->d_maxc);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // extern "C"

@@ -2142,3 +2142,6 @@ void tgv_destroy(tgv_ctx* c)
 }
 
 }  // extern "C"
+
+// NEXT-3 block-sparse brick sets (same translation unit: shares the kernels above)
+#include "tgv_bricks_rt.cuh"

@@ -2,6 +2,7 @@
 every function include/tgv.h declares, and rejects invalid arguments before
 touching a device (no compute calls here)."""
 import ctypes
+import glob
 import os
 import re
 import subprocess
@@ -9,13 +10,15 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "tgv.h")
+HEADERS = sorted(glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(tgv_[a-z_]+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(tgv_[a-z_]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_header_declares_the_north_star_calls():
@@ -31,7 +34,8 @@ def test_library_exports_every_declared_symbol():
     exported = set(re.findall(r" T (tgv_\w+)", out))
     missing = [n for n in declared_functions() if n not in exported]
     assert not missing, missing
-    assert set(tgv.EXPORTS) == set(declared_functions())
+    from paper_2107_14790_b200 import bricks
+    assert set(tgv.EXPORTS) | set(bricks.EXPORTS) == set(declared_functions())
 
 
 def test_library_is_sm100a():
@@ -86,3 +90,22 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "tgv_oracle", "oracle_"):
                     assert bad not in txt, (f, bad)
+
+
+@pytest.mark.parametrize("kw,frag", [
+    (dict(edge=6), "brick edge"),
+    (dict(coords=[(0, 0, 0), (0, 0, 0)]), "duplicate"),
+    (dict(coords=[(-1, 0, 0)]), "outside"),
+    (dict(tau=0.5), "tau*sigma*16"),
+    (dict(centers=[0.5, 0.2]), "increasing"),
+])
+def test_bricks_create_rejects_invalid_arguments(kw, frag):
+    """include/tgv_bricks.h: argument checks happen before any device work."""
+    from paper_2107_14790_b200 import tgv
+    from paper_2107_14790_b200.bricks import BrickSolver
+    args = dict(edge=8, coords=[(0, 0, 0), (1, 0, 0)], tau=0.25, centers=None)
+    args.update(kw)
+    with pytest.raises(tgv.TgvError) as ei:
+        BrickSolver(args["edge"], args["coords"], centers=args["centers"], tau=args["tau"])
+    assert ei.value.status == tgv.TGV_EINVAL
+    assert frag in str(ei.value)
