@@ -71,6 +71,43 @@ int tgv_bricks_create(const tgv_brickset* set, const tgv_params* params, int cud
  * TGV_ERANGE (a count > 65535), TGV_ENOMEM, TGV_ECUDA. */
 int tgv_bricks_load(tgv_bricks* ctx, const void* counts, int count_bytes, int64_t n_counts);
 
+/* NEXT-2 on a brick set: Alg. 1 votes of the depth maps into
+ * every voxel of every brick, then the initialisation of tgv_bricks_load.  The
+ * voxel centre of brick b, offset (x, y, z) is grid_origin + voxel_size * (E *
+ * coords[b] + (x, y, z)); cameras, depth maps, voxel_radius and the arithmetic
+ * (fp64, nearest texel of the mip level chosen by the projected diameter) are
+ * those of tgv_vote_depth_maps (tgv.h), so a brick's counts are bit-identical to
+ * a dense vote of its box.  Requires nbins = 8.
+ * Errors: TGV_EINVAL, TGV_ERANGE, TGV_ENOMEM, TGV_ECUDA. */
+int tgv_bricks_vote_depth_maps(tgv_bricks* ctx, const tgv_camera* cams, int ncams, const float* const* depths,
+                               const double grid_origin[3], double voxel_size, double voxel_radius);
+
+/* Copy the stored counts to the host: counts_out uint32 [nbricks][E^3][nbins];
+ * n_counts = nbricks*E^3*nbins.  Errors: TGV_EINVAL, TGV_ESTATE (no counts), TGV_ECUDA. */
+int tgv_bricks_read_counts(tgv_bricks* ctx, uint32_t* counts_out, int64_t n_counts);
+
+/* Re-initialise the state from the resident counts (as tgv_bricks_load, without
+ * the upload).  Errors: TGV_EINVAL, TGV_ESTATE (no counts), TGV_ECUDA. */
+int tgv_bricks_reset(tgv_bricks* ctx);
+
+/* Refinement of the next finer level (R24, "where the samples are"):
+ * flags uint8 [nbricks][8], flags[b][o] = 1 iff brick b is solved and a voxel of its
+ * octant o = (x >= E/2) + 2 (y >= E/2) + 4 (z >= E/2) holds >= min_votes votes
+ * outside the last (free-space) bin, else 0; octant o of brick (bx, by, bz) is the
+ * finer level's brick (2bx + (o & 1), 2by + (o >> 1 & 1), 2bz + (o >> 2)).
+ * n = 8 * nbricks.  Errors: TGV_EINVAL, TGV_ESTATE (no counts), TGV_ECUDA. */
+int tgv_bricks_refine_flags(tgv_bricks* ctx, int32_t min_votes, uint8_t* flags, int64_t n);
+
+/* Coarse-to-fine on brick sets (NEXT-1 with DESIGN.md R19; PAPER.md:167-168,
+ * :431-433): every brick (bx, by, bz) of `fine` takes u = u and v = v / 2 of the
+ * voxel of brick (bx/2, by/2, bz/2) of `coarse` (same edge E, same device; both
+ * loaded) that contains it, into u, ubar, v and vbar; p = q = 0; the iteration
+ * counter goes to 0.  Frozen bricks of `fine` keep these values from here on (the
+ * borders of PAPER.md:449-453).
+ * Errors: TGV_EINVAL (NULL, edges / devices differ, a brick without a parent),
+ * TGV_ESTATE, TGV_ECUDA. */
+int tgv_bricks_prolong_from(tgv_bricks* fine, const tgv_bricks* coarse);
+
 /* Set u and v on every brick (A and B) and restart: ubar = u, vbar = v,
  * p = q = 0, iteration counter 0 (the prolongation restart of DESIGN.md R19;
  * the values on B stay frozen from here on).  u float [nbricks][E^3],

@@ -277,3 +277,57 @@ class BrickOracle:
         E = T1 + T0 + TD
         vmax = float(np.max(np.abs(self.v[:, A]))) if A.any() else 0.0
         return {"E": E, "alpha1": T1, "alpha0": T0, "data": TD, "gap": E - D, "vmax": vmax, "dual": D}
+
+
+# ---------------------------------------------------------------------------
+# Level companions on brick sets (R24 with R18-R22)
+# ---------------------------------------------------------------------------
+def vote(coords, E, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, r=0.5):
+    """Alg. 1 counts of every brick: the oracle's dense vote of the
+    brick's box, voxel (x, y, z) of brick (bx, by, bz) at grid_origin + h (E b + (x, y, z)).
+    The dense oracle places voxel x at origin + h x, so the brick's box is voted from
+    origin + h E (bx, by, 0) with planes [E bz, E bz + E): identical coordinates whenever
+    those sums are exact in fp64 (the tests use origins and voxel sizes that are)."""
+    from . import alg1_vote
+    out = []
+    for bx, by, bz in np.asarray(coords, np.int64):
+        o = (grid_origin[0] + voxel_size * E * bx, grid_origin[1] + voxel_size * E * by, grid_origin[2])
+        out.append(alg1_vote(cams, depths, E, E, E * bz, E * bz + E, origin=o, voxel_size=voxel_size, r=r))
+    return np.stack(out)
+
+
+def refine_flags(counts, frozen, min_votes):
+    """flags [nbricks, 8]: octant o = (x >= E/2) + 2 (y >= E/2) + 4 (z >= E/2) of a solved
+    brick holds a voxel with >= min_votes votes outside the last (free-space) bin."""
+    c = np.asarray(counts)
+    nb, E = c.shape[0], c.shape[1]
+    surf = c[..., :-1].sum(-1) >= min_votes  # [nb, z, y, x]
+    h = E // 2
+    flags = np.zeros((nb, 8), np.uint8)
+    for o in range(8):
+        ox, oy, oz = o & 1, o >> 1 & 1, o >> 2
+        blk = surf[:, oz * h:(oz + 1) * h, oy * h:(oy + 1) * h, ox * h:(ox + 1) * h]
+        flags[:, o] = blk.reshape(nb, -1).any(1)
+    flags[np.asarray(frozen, bool)] = 0
+    return flags
+
+
+def prolong(coarse, fine_coords):
+    """Reading R19 on brick sets: fine voxel p of brick b takes u and v / 2 of the coarse
+    voxel floor((E b + p) / 2), which lies in coarse brick floor(b / 2).
+    coarse: BrickOracle; returns (u [nb, E, E, E], v [nb, 3, E, E, E]) fp64."""
+    E = coarse.E
+    cu, cv = coarse.get("u"), coarse.get("v")
+    index = {tuple(int(a) for a in c): i for i, c in enumerate(coarse.coords)}
+    fc = np.asarray(fine_coords, np.int64)
+    u = np.zeros((len(fc), E, E, E))
+    v = np.zeros((len(fc), 3, E, E, E))
+    for i, (bx, by, bz) in enumerate(fc):
+        pb = index[(int(bx) // 2, int(by) // 2, int(bz) // 2)]
+        iz = (E * (bz % 2) + np.arange(E)) // 2
+        iy = (E * (by % 2) + np.arange(E)) // 2
+        ix = (E * (bx % 2) + np.arange(E)) // 2
+        u[i] = cu[pb][np.ix_(iz, iy, ix)]
+        for d in range(3):
+            v[i, d] = 0.5 * cv[pb, d][np.ix_(iz, iy, ix)]
+    return u, v

@@ -1,0 +1,121 @@
+"""Block-sparse brick levels, coarse to fine (NEXT-3 + NEXT-1 + NEXT-2 on brick sets;
+BASELINE.json configs[4]; reading R24).
+
+Host logic only (which bricks exist, which are frozen); every arithmetic step -- the
+Alg. 1 votes, the refinement flags, the prolongation, the iterations, the energy --
+runs in libtgv.so through include/tgv_bricks.h.
+
+How a level's bricks are chosen (R24): the paper refines its octree where the depth
+samples are (§4.1) and solves each level over the cubes that exist
+(PAPER.md:431-461).  Here:
+  * the coarsest level is every brick of its grid, all solved;
+  * a level's solved set A is every octant (a finer brick) of the coarser level's
+    solved bricks that holds at least `min_votes` votes outside the free-space bin
+    (tgv_bricks_refine_flags), i.e. where the surface samples of that level are;
+  * its frozen set B is the rest of A's 26-neighbourhood inside the grid: the cubes
+    "outside of the border" whose values come from the parent level
+    (PAPER.md:449-453), by prolongation (R19, tgv_bricks_prolong_from).
+Every brick of a finer level then has a parent brick in the coarser level (the
+parent of a 26-neighbour of a child of A is in A or its 26-neighbourhood).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .bricks import BrickSolver
+
+_OCT = np.array([(o & 1, o >> 1 & 1, o >> 2) for o in range(8)], dtype=np.int64)
+_N26 = np.array([(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)
+                 if (dx, dy, dz) != (0, 0, 0)], dtype=np.int64)
+
+
+def brick_grid(extent, edge, level):
+    """Bricks per axis at `level` (voxel size 2^level) covering extent (x, y, z) voxels."""
+    s = edge << level
+    return tuple((int(n) + s - 1) // s for n in extent)
+
+
+def _key(c):
+    c = np.asarray(c, dtype=np.int64)
+    return c[:, 0] | c[:, 1] << 21 | c[:, 2] << 42
+
+
+def children(coords, flags, grid):
+    """Finer bricks of the flagged octants, inside the finer grid, sorted (z, y, x)."""
+    b, o = np.nonzero(np.asarray(flags))
+    ch = 2 * np.asarray(coords, np.int64)[b] + _OCT[o]
+    ch = ch[np.all(ch < np.asarray(grid), axis=1)]
+    return _sorted(ch)
+
+
+def shell(coords, grid):
+    """The 26-neighbourhood of `coords` inside `grid`, minus `coords`, sorted."""
+    c = np.asarray(coords, np.int64)
+    if len(c) == 0:
+        return c.reshape(0, 3)
+    nb = (c[:, None, :] + _N26[None, :, :]).reshape(-1, 3)
+    nb = nb[np.all((nb >= 0) & (nb < np.asarray(grid)), axis=1)]
+    nb = _sorted(nb)
+    return nb[~np.isin(_key(nb), _key(c))]
+
+
+def _sorted(c):
+    c = np.unique(np.asarray(c, np.int64).reshape(-1, 3), axis=0)
+    return c[np.lexsort((c[:, 0], c[:, 1], c[:, 2]))]
+
+
+class BrickLevels:
+    """Brick sets of `levels` levels (index 0 = finest) built from the depth maps, with
+    their counts resident on the GPU; `solve` runs the coarse-to-fine TGV solve."""
+
+    def __init__(self, extent, cams, depths, levels=3, edge=32, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0,
+                 voxel_radius=0.5, min_votes=2, centers=None, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25,
+                 device=0):
+        kw = dict(centers=centers, lam=lam, alpha0=alpha0, alpha1=alpha1, tau=tau, sigma=sigma, device=device)
+        self.edge, self.levels = edge, levels
+        self.solvers = [None] * levels
+        self.coords = [None] * levels
+        self.frozen = [None] * levels
+        top = levels - 1
+        g = brick_grid(extent, edge, top)
+        allc = _sorted(np.stack(np.meshgrid(*[np.arange(n) for n in g], indexing="ij"), -1).reshape(-1, 3))
+        self._add(top, allc, np.zeros(len(allc), bool), cams, depths, grid_origin, voxel_size, voxel_radius, kw)
+        for lev in range(top - 1, -1, -1):
+            g = brick_grid(extent, edge, lev)
+            up = self.solvers[lev + 1]
+            A = children(self.coords[lev + 1], up.refine_flags(min_votes), g)
+            B = shell(A, g)
+            c = np.concatenate([A, B]).astype(np.int32)
+            fr = np.concatenate([np.zeros(len(A), bool), np.ones(len(B), bool)])
+            self._add(lev, c, fr, cams, depths, grid_origin, voxel_size, voxel_radius, kw)
+
+    def _add(self, lev, coords, frozen, cams, depths, origin, h, r, kw):
+        s = BrickSolver(self.edge, coords, frozen, **kw)
+        s.vote(cams, depths, grid_origin=origin, voxel_size=h * (1 << lev), voxel_radius=r * (1 << lev))
+        self.solvers[lev], self.coords[lev], self.frozen[lev] = s, np.asarray(coords), np.asarray(frozen)
+
+    def bricks(self):
+        """(solved, frozen) brick counts per level, finest first."""
+        return [(int((~f).sum()), int(f.sum())) for f in self.frozen]
+
+    def voxels(self):
+        return [len(c) * self.edge ** 3 for c in self.coords]
+
+    def solve(self, iters):
+        """Coarsest level from its votes (R9), each finer level prolongated from the
+        coarser one (R19) with its frozen bricks held at the parent values; `iters`
+        iterations per level (R20).  Returns the finest level's BrickSolver."""
+        top = self.levels - 1
+        s = self.solvers[top].reset().iterate(iters)
+        for lev in range(top - 1, -1, -1):
+            f = self.solvers[lev]
+            f.prolong_from(s)
+            f.iterate(iters)
+            s = f
+        return s
+
+    def close(self):
+        for s in self.solvers:
+            if s is not None:
+                s.close()
+        self.solvers = []

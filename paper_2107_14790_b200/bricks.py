@@ -16,7 +16,8 @@ from .tgv import _check, lib, tgv_params, tgv_timing
 
 EXPORTS = ["tgv_bricks_create", "tgv_bricks_load", "tgv_bricks_set_primal", "tgv_bricks_iterate", "tgv_bricks_read",
            "tgv_bricks_energy", "tgv_bricks_set_timing", "tgv_bricks_get_timing", "tgv_bricks_info",
-           "tgv_bricks_last_error", "tgv_bricks_destroy"]
+           "tgv_bricks_last_error", "tgv_bricks_destroy", "tgv_bricks_vote_depth_maps", "tgv_bricks_read_counts",
+           "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from"]
 
 
 class tgv_brickset(ctypes.Structure):
@@ -36,6 +37,12 @@ def _setup():
     lib.tgv_bricks_set_timing.argtypes = [vp, ctypes.c_int]
     lib.tgv_bricks_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
     lib.tgv_bricks_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    lib.tgv_bricks_vote_depth_maps.argtypes = [vp, ctypes.POINTER(tgv.tgv_camera), ctypes.c_int, ctypes.POINTER(vp),
+                                               vp, ctypes.c_double, ctypes.c_double]
+    lib.tgv_bricks_read_counts.argtypes = [vp, vp, i64]
+    lib.tgv_bricks_reset.argtypes = [vp]
+    lib.tgv_bricks_refine_flags.argtypes = [vp, i32, vp, i64]
+    lib.tgv_bricks_prolong_from.argtypes = [vp, vp]
     lib.tgv_bricks_last_error.argtypes = [vp]
     lib.tgv_bricks_last_error.restype = ctypes.c_char_p
     lib.tgv_bricks_destroy.argtypes = [vp]
@@ -84,6 +91,32 @@ class BrickSolver:
         if a.dtype not in (np.uint8, np.uint16, np.uint32):
             a = a.astype(np.uint32)
         _bcheck(lib.tgv_bricks_load(self.ctx, a.ctypes.data, a.dtype.itemsize, a.size), self.ctx)
+        return self
+
+    def vote(self, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, voxel_radius=0.5):
+        """cams / depths as tgv.tgv_vote_depth_maps (dicts; float32 [h, w], NaN = no depth)."""
+        arr, ptrs, ds = tgv._camera_args(cams, depths)
+        o = np.asarray(grid_origin, dtype=np.float64)
+        _bcheck(lib.tgv_bricks_vote_depth_maps(self.ctx, arr, len(cams), ptrs, o.ctypes.data, float(voxel_size),
+                                               float(voxel_radius)), self.ctx)
+        return self
+
+    def read_counts(self):
+        out = np.empty((self.nbricks,) + (self.E,) * 3 + (self.nbins,), dtype=np.uint32)
+        _bcheck(lib.tgv_bricks_read_counts(self.ctx, out.ctypes.data, out.size), self.ctx)
+        return out
+
+    def reset(self):
+        _bcheck(lib.tgv_bricks_reset(self.ctx), self.ctx)
+        return self
+
+    def refine_flags(self, min_votes=2):
+        out = np.empty((self.nbricks, 8), dtype=np.uint8)
+        _bcheck(lib.tgv_bricks_refine_flags(self.ctx, int(min_votes), out.ctypes.data, out.size), self.ctx)
+        return out
+
+    def prolong_from(self, coarse: "BrickSolver"):
+        _bcheck(lib.tgv_bricks_prolong_from(self.ctx, coarse.ctx), self.ctx)
         return self
 
     def set_primal(self, u, v=None):

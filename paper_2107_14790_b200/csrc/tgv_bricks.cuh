@@ -278,3 +278,105 @@ __global__ void __launch_bounds__(256)
 }
 
 }  // namespace tgvk
+
+// ---------------------------------------------------------------------------
+// Brick-set companions of the dense helpers: Alg. 1 votes, count read-back,
+// refinement flags, prolongation from the parent level.
+#include "tgv_vote.cuh"
+
+namespace tgvk {
+
+// Alg. 1 (NEXT-2) at every voxel of every brick: the voxel centre is
+// origin + h (E * brick coordinate + in-brick offset); same per-point arithmetic as
+// vote_kernel (vote_point), so a brick's counts equal a dense vote of its box
+template <int LE, int SLOTS>
+__global__ void __launch_bounds__(256) brick_vote_kernel(const VoteCam* __restrict__ cams, int ncams,
+                                                         const float* __restrict__ depth, const int* __restrict__ coords,
+                                                         int nvox, double ox, double oy, double oz, double h, double r,
+                                                         uint16_t* __restrict__ H, unsigned int* __restrict__ maxc)
+{
+    constexpr int E = 1 << LE;
+    const double delta = __dmul_rn(6.0, r), eta = __dmul_rn(3.0, delta);
+    unsigned int m = 0;
+    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < nvox; vi += (int64_t)gridDim.x * blockDim.x) {
+        const BrickIdx<LE> I((int)vi);
+        const int gx = coords[3 * I.b] * E + I.c[0], gy = coords[3 * I.b + 1] * E + I.c[1],
+                  gz = coords[3 * I.b + 2] * E + I.c[2];
+        const double pw0 = __dadd_rn(ox, __dmul_rn(h, (double)gx));
+        const double pw1 = __dadd_rn(oy, __dmul_rn(h, (double)gy));
+        const double pw2 = __dadd_rn(oz, __dmul_rn(h, (double)gz));
+        unsigned int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        vote_point(cams, ncams, depth, pw0, pw1, pw2, r, delta, eta, acc);
+        uint16_t* dst = H + vi * SLOTS;
+#pragma unroll
+        for (int b = 0; b < SLOTS; ++b) {
+            const unsigned int cb = b < 8 ? acc[b] : 0u;
+            m = max(m, cb);
+            dst[b] = (uint16_t)min(cb, 65535u);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxc, m);
+}
+
+// stored counts -> uint32 [nvox][nbins]
+template <typename CT>
+__global__ void brick_unpack_kernel(const CT* __restrict__ H, int64_t nvox, int slots, int nbins,
+                                    uint32_t* __restrict__ out)
+{
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox; v += (int64_t)gridDim.x * blockDim.x)
+        for (int b = 0; b < nbins; ++b) out[v * nbins + b] = H[v * slots + b];
+}
+
+// flags[b * 8 + octant] = 1 if a voxel of solved brick b in that octant has at least
+// min_votes votes outside the last (free-space) bin; the caller zeroes flags
+template <int LE, typename CT>
+__global__ void brick_refine_kernel(const CT* __restrict__ H, const uint8_t* __restrict__ frozen, int nvox, int slots,
+                                    int nbins, int min_votes, uint8_t* __restrict__ flags)
+{
+    constexpr int E = 1 << LE;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox; v += (int64_t)gridDim.x * blockDim.x) {
+        const BrickIdx<LE> I((int)v);
+        if (frozen[I.b]) continue;
+        int s = 0;
+        for (int b = 0; b < nbins - 1; ++b) s += H[v * slots + b];
+        if (s >= min_votes) {
+            const int oct = (I.c[0] >= E / 2) | (I.c[1] >= E / 2) << 1 | (I.c[2] >= E / 2) << 2;
+            flags[I.b * 8 + oct] = 1;  // identical writes only
+        }
+    }
+}
+
+// Prolongation from the parent level (R19 on brick sets): fine voxel
+// (brick b, offset c) lies in parent brick parent[b] at offset (E (coord_b & 1) + c) / 2;
+// u = parent u, v = parent v / 2 into the current and previous slots
+template <int LE>
+__global__ void brick_prolong_kernel(const float* __restrict__ uc, const float* __restrict__ vc0,
+                                     const float* __restrict__ vc1, const float* __restrict__ vc2,
+                                     const int* __restrict__ parent, const int* __restrict__ coords, int nvox,
+                                     float* __restrict__ u_cur, float* __restrict__ u_prev, float* __restrict__ v_cur0,
+                                     float* __restrict__ v_cur1, float* __restrict__ v_cur2, float* __restrict__ v_prev0,
+                                     float* __restrict__ v_prev1, float* __restrict__ v_prev2)
+{
+    constexpr int E = 1 << LE;
+    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < nvox; vi += (int64_t)gridDim.x * blockDim.x) {
+        const BrickIdx<LE> I((int)vi);
+        const int pb = parent[I.b];
+        const int px = ((coords[3 * I.b] & 1) * E + I.c[0]) >> 1;
+        const int py = ((coords[3 * I.b + 1] & 1) * E + I.c[1]) >> 1;
+        const int pz = ((coords[3 * I.b + 2] & 1) * E + I.c[2]) >> 1;
+        const int j = (((pb << LE) + pz) << LE | py) << LE | px;
+        const float u = uc[j];
+        const float v0 = 0.5f * vc0[j], v1 = 0.5f * vc1[j], v2 = 0.5f * vc2[j];
+        u_cur[vi] = u;
+        u_prev[vi] = u;
+        v_cur0[vi] = v0;
+        v_prev0[vi] = v0;
+        v_cur1[vi] = v1;
+        v_prev1[vi] = v1;
+        v_cur2[vi] = v2;
+        v_prev2[vi] = v2;
+    }
+}
+
+}  // namespace tgvk

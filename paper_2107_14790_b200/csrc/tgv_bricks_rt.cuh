@@ -21,6 +21,9 @@ struct tgv_bricks {
     float* state = nullptr;     // NSLOT slots of nvox floats
     int* nbr = nullptr;         // [nbricks][6]
     uint8_t* frozen = nullptr;  // [nbricks]
+    int* d_coords = nullptr;    // [nbricks][3]
+    int* d_parent = nullptr;    // [nbricks]: parent brick index (tgv_bricks_prolong_from)
+    std::vector<int32_t> coords_h;
     void* hist = nullptr;       // [nvox][slots] of u8 / u16
     double* partials = nullptr;
     double* d_out = nullptr;
@@ -220,6 +223,49 @@ void launch_brick_pack(tgv_bricks* c, const void* src, int64_t nv, uint16_t* dst
         brick_pack_kernel<T, 16><<<148 * 8, 256, 0, c->stream>>>((const T*)src, nv, c->nbins, dst, c->d_maxc);
 }
 
+int bricks_init_state(tgv_bricks* c);
+
+// shared tail of tgv_bricks_load / tgv_bricks_vote_depth_maps: range check of the
+// u16 counts in h16 (max in c->d_maxc), u8 narrowing, state initialisation (R9)
+int bricks_finish_counts(tgv_bricks* c, const uint16_t* h16)
+{
+    const size_t n16 = (size_t)c->nvox * c->slots;
+    unsigned int maxc = 0;
+    BCU(cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream));
+    BCU(cudaStreamSynchronize(c->stream));
+    if (maxc > 65535u) return bfail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc);
+    const int cb = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0 ? 1 : 2;
+    if (c->hist && cb != c->count_bytes) {
+        cudaFree(c->hist);
+        c->device_bytes -= (int64_t)n16 * c->count_bytes;
+        c->hist = nullptr;
+    }
+    if (!c->hist) {
+        if (cudaMalloc(&c->hist, n16 * cb) != cudaSuccess) {
+            cudaGetLastError();
+            return bfail(c, TGV_ENOMEM, "count store allocation failed");
+        }
+        c->device_bytes += (int64_t)n16 * cb;
+    }
+    c->count_bytes = cb;
+    if (cb == 1) compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(h16, (uint8_t*)c->hist, (int64_t)n16);
+    else BCU(cudaMemcpyAsync(c->hist, h16, sizeof(uint16_t) * n16, cudaMemcpyDeviceToDevice, c->stream));
+    BCU(cudaGetLastError());
+    return bricks_init_state(c);
+}
+
+// initial state (R9): zero every slot, then u_0 into the current and previous u
+int bricks_init_state(tgv_bricks* c)
+{
+    BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
+    BRICK_LE_DISPATCH(launch_brick_init_le, c);
+    BCU(cudaGetLastError());
+    BCU(cudaStreamSynchronize(c->stream));
+    c->k = 0;
+    c->loaded = true;
+    return TGV_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -324,7 +370,16 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
     std::vector<uint8_t> fr((size_t)nb, 0);
     if (S->frozen)
         for (int64_t b = 0; b < nb; ++b) fr[(size_t)b] = S->frozen[b] ? 1 : 0;
-    if (cudaMemcpy(c->nbr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+    c->coords_h.assign(S->coords, S->coords + 3 * nb);
+    if (cudaMalloc(&c->d_coords, sizeof(int) * 3 * (size_t)nb) != cudaSuccess ||
+        cudaMalloc(&c->d_parent, sizeof(int) * (size_t)nb) != cudaSuccess) {
+        cudaGetLastError();
+        bfail(c, TGV_ENOMEM, "table allocation failed");
+        return bail(TGV_ENOMEM);
+    }
+    c->device_bytes += 16 * nb;
+    if (cudaMemcpy(c->d_coords, S->coords, sizeof(int) * 3 * (size_t)nb, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->nbr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(c->frozen, fr.data(), fr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
         bfail(c, TGV_ECUDA, "table upload failed");
@@ -375,37 +430,7 @@ int tgv_bricks_load(tgv_bricks* c, const void* counts, int count_bytes, int64_t 
         else launch_brick_pack<uint32_t>(c, stg, nv, dst);
         if (cudaGetLastError() != cudaSuccess) return done(bfail(c, TGV_ECUDA, "pack kernel launch failed"));
     }
-    unsigned int maxc = 0;
-    if (cudaMemcpyAsync(&maxc, c->d_maxc, sizeof maxc, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
-        cudaStreamSynchronize(c->stream) != cudaSuccess)
-        return done(bfail(c, TGV_ECUDA, "count upload failed: %s", cudaGetErrorString(cudaGetLastError())));
-    if (maxc > 65535u) return done(bfail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc));
-    const int cb = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0 ? 1 : 2;
-    if (c->hist && cb != c->count_bytes) {
-        cudaFree(c->hist);
-        c->device_bytes -= (int64_t)n16 * c->count_bytes;
-        c->hist = nullptr;
-    }
-    if (!c->hist) {
-        if (cudaMalloc(&c->hist, n16 * cb) != cudaSuccess) {
-            cudaGetLastError();
-            return done(bfail(c, TGV_ENOMEM, "count store allocation failed"));
-        }
-        c->device_bytes += (int64_t)n16 * cb;
-    }
-    c->count_bytes = cb;
-    if (cb == 1) compact_counts_kernel<<<148 * 8, 256, 0, c->stream>>>(h16, (uint8_t*)c->hist, (int64_t)n16);
-    else if (cudaMemcpyAsync(c->hist, h16, sizeof(uint16_t) * n16, cudaMemcpyDeviceToDevice, c->stream) != cudaSuccess)
-        return done(bfail(c, TGV_ECUDA, "count copy failed"));
-    // initial state (R9): zero every slot, then u_0 into the current and previous u
-    if (cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream) != cudaSuccess)
-        return done(bfail(c, TGV_ECUDA, "state memset failed"));
-    BRICK_LE_DISPATCH(launch_brick_init_le, c);
-    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess)
-        return done(bfail(c, TGV_ECUDA, "initialisation failed: %s", cudaGetErrorString(cudaGetLastError())));
-    c->k = 0;
-    c->loaded = true;
-    return done(TGV_OK);
+    return done(bricks_finish_counts(c, h16));
 }
 
 int tgv_bricks_set_primal(tgv_bricks* c, const float* u, const float* v, int64_t n)
@@ -545,6 +570,8 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->state);
     cudaFree(c->nbr);
     cudaFree(c->frozen);
+    cudaFree(c->d_coords);
+    cudaFree(c->d_parent);
     cudaFree(c->hist);
     cudaFree(c->partials);
     cudaFree(c->d_out);
@@ -553,4 +580,193 @@ void tgv_bricks_destroy(tgv_bricks* c)
     delete c;
 }
 
+int tgv_bricks_reset(tgv_bricks* c)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!c->hist) return bfail(c, TGV_ESTATE, "reset before load");
+    return bricks_init_state(c);
+}
+
+int tgv_bricks_vote_depth_maps(tgv_bricks* c, const tgv_camera* cams, int ncams, const float* const* depths,
+                               const double grid_origin[3], double voxel_size, double voxel_radius)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!cams || !depths || !grid_origin || ncams < 0) return bfail(c, TGV_EINVAL, "NULL argument");
+    if (c->nbins != 8) return bfail(c, TGV_EINVAL, "Alg. 1 votes into 8 bins; this context has %d", c->nbins);
+    if (!(voxel_size > 0.0) || !(voxel_radius > 0.0)) return bfail(c, TGV_EINVAL, "voxel size and radius must be > 0");
+    c->loaded = false;
+    float* d_depth = nullptr;
+    VoteCam* d_cams = nullptr;
+    char msg[512];
+    if ((rc = vote_upload(c->stream, cams, ncams, depths, &d_depth, &d_cams, msg))) return bfail(c, rc, "%s", msg);
+    uint16_t* h16 = nullptr;
+    const size_t n16 = (size_t)c->nvox * c->slots;
+    if (cudaMalloc(&h16, sizeof(uint16_t) * n16) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(d_depth);
+        cudaFree(d_cams);
+        return bfail(c, TGV_ENOMEM, "u16 count staging allocation failed");
+    }
+    cudaError_t e = cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream);
+    const int nv = (int)c->nvox;
+    const double ox = grid_origin[0], oy = grid_origin[1], oz = grid_origin[2];
+#define BVOTE(LE_)                                                                                                \
+    (c->slots == 8 ? brick_vote_kernel<LE_, 8><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth, c->d_coords, \
+                                                                             nv, ox, oy, oz, voxel_size,          \
+                                                                             voxel_radius, h16, c->d_maxc)         \
+                   : brick_vote_kernel<LE_, 16><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth,            \
+                                                                              c->d_coords, nv, ox, oy, oz,         \
+                                                                              voxel_size, voxel_radius, h16,       \
+                                                                              c->d_maxc))
+    if (e == cudaSuccess) {
+        switch (c->LE) {
+            case 2: BVOTE(2); break;
+            case 3: BVOTE(3); break;
+            case 4: BVOTE(4); break;
+            default: BVOTE(5); break;
+        }
+#undef BVOTE
+        e = cudaGetLastError();
+    }
+    cudaStreamSynchronize(c->stream);
+    cudaFree(d_depth);
+    cudaFree(d_cams);
+    if (e != cudaSuccess) {
+        cudaFree(h16);
+        return bfail(c, TGV_ECUDA, "voting: %s", cudaGetErrorString(e));
+    }
+    rc = bricks_finish_counts(c, h16);
+    cudaFree(h16);
+    return rc;
+}
+
+int tgv_bricks_read_counts(tgv_bricks* c, uint32_t* out, int64_t n)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!out) return bfail(c, TGV_EINVAL, "out is NULL");
+    if (!c->hist) return bfail(c, TGV_ESTATE, "no counts loaded");
+    if (n != c->nvox * c->nbins)
+        return bfail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n, (long long)(c->nvox * c->nbins));
+    const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / c->nbins);
+    uint32_t* d = nullptr;
+    if (cudaMalloc(&d, sizeof(uint32_t) * (size_t)std::min(chunk, c->nvox) * c->nbins) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ENOMEM, "read-back staging allocation failed");
+    }
+    cudaError_t e = cudaSuccess;
+    for (int64_t v0 = 0; v0 < c->nvox && e == cudaSuccess; v0 += chunk) {
+        const int64_t nv = std::min(chunk, c->nvox - v0);
+        if (c->count_bytes == 1)
+            brick_unpack_kernel<uint8_t><<<148 * 8, 256, 0, c->stream>>>((const uint8_t*)c->hist + v0 * c->slots, nv,
+                                                                         c->slots, c->nbins, d);
+        else
+            brick_unpack_kernel<uint16_t><<<148 * 8, 256, 0, c->stream>>>((const uint16_t*)c->hist + v0 * c->slots,
+                                                                          nv, c->slots, c->nbins, d);
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out + v0 * c->nbins, d, sizeof(uint32_t) * nv * c->nbins, cudaMemcpyDeviceToHost,
+                                c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    }
+    cudaFree(d);
+    if (e != cudaSuccess) return bfail(c, TGV_ECUDA, "count read-back: %s", cudaGetErrorString(e));
+    return TGV_OK;
+}
+
+int tgv_bricks_refine_flags(tgv_bricks* c, int32_t min_votes, uint8_t* flags, int64_t n)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!flags) return bfail(c, TGV_EINVAL, "flags is NULL");
+    if (n != 8 * c->nbricks) return bfail(c, TGV_EINVAL, "n %lld != 8 * nbricks", (long long)n);
+    if (min_votes < 1) return bfail(c, TGV_EINVAL, "min_votes must be >= 1");
+    if (!c->hist) return bfail(c, TGV_ESTATE, "no counts loaded");
+    uint8_t* d = nullptr;
+    if (cudaMalloc(&d, (size_t)n) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ENOMEM, "flag allocation failed");
+    }
+    cudaError_t e = cudaMemsetAsync(d, 0, (size_t)n, c->stream);
+    const int nv = (int)c->nvox;
+#define BREF(LE_)                                                                                                    \
+    (c->count_bytes == 1                                                                                             \
+         ? brick_refine_kernel<LE_, uint8_t><<<148 * 8, 256, 0, c->stream>>>((const uint8_t*)c->hist, c->frozen, nv,  \
+                                                                             c->slots, c->nbins, min_votes, d)        \
+         : brick_refine_kernel<LE_, uint16_t><<<148 * 8, 256, 0, c->stream>>>((const uint16_t*)c->hist, c->frozen,   \
+                                                                              nv, c->slots, c->nbins, min_votes, d))
+    if (e == cudaSuccess) {
+        switch (c->LE) {
+            case 2: BREF(2); break;
+            case 3: BREF(3); break;
+            case 4: BREF(4); break;
+            default: BREF(5); break;
+        }
+#undef BREF
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d, (size_t)n, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return bfail(c, TGV_ECUDA, "refine flags: %s", cudaGetErrorString(e));
+    return TGV_OK;
+}
+
+int tgv_bricks_prolong_from(tgv_bricks* f, const tgv_bricks* pc)
+{
+    tgv_bricks* c = f;
+    int rc = bready(c);
+    if (rc) return rc;
+    if (!pc) return bfail(c, TGV_EINVAL, "coarse context is NULL");
+    if (pc->device != c->device) return bfail(c, TGV_EINVAL, "coarse context on device %d, fine on %d", pc->device, c->device);
+    if (pc->E != c->E) return bfail(c, TGV_EINVAL, "brick edges differ (%d vs %d)", pc->E, c->E);
+    if (!c->loaded || !pc->loaded) return bfail(c, TGV_ESTATE, "both levels must be loaded");
+    if (pc->poisoned) return bfail(c, TGV_ESTATE, "coarse context poisoned");
+    std::unordered_map<uint64_t, int> at;
+    at.reserve((size_t)pc->nbricks * 2);
+    auto key = [](int64_t x, int64_t y, int64_t z) { return (uint64_t)x | (uint64_t)y << 21 | (uint64_t)z << 42; };
+    for (int64_t b = 0; b < pc->nbricks; ++b)
+        at.emplace(key(pc->coords_h[3 * b], pc->coords_h[3 * b + 1], pc->coords_h[3 * b + 2]), (int)b);
+    std::vector<int> parent((size_t)c->nbricks);
+    for (int64_t b = 0; b < c->nbricks; ++b) {
+        const int32_t* q = &c->coords_h[3 * b];
+        auto it = at.find(key(q[0] >> 1, q[1] >> 1, q[2] >> 1));
+        if (it == at.end())
+            return bfail(c, TGV_EINVAL, "brick (%d, %d, %d) has no parent brick in the coarse level", q[0], q[1], q[2]);
+        parent[(size_t)b] = it->second;
+    }
+    // the coarse level's current iterate (its stream is synchronised first: the two
+    // contexts use different streams)
+    if (cudaStreamSynchronize(pc->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ECUDA, "coarse stream synchronisation failed");
+    }
+    const Bufs cb = bufs(pc->k);
+    auto cslot = [&](int s) { return (const float*)(pc->state + (int64_t)s * pc->nvox); };
+    BCU(cudaMemcpyAsync(c->d_parent, parent.data(), sizeof(int) * parent.size(), cudaMemcpyHostToDevice, c->stream));
+    BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
+    const Bufs b = bufs(0);
+    const int nv = (int)c->nvox;
+#define BPRO(LE_)                                                                                                   \
+    brick_prolong_kernel<LE_><<<148 * 8, 256, 0, c->stream>>>(                                                      \
+        cslot(slotU(cb.cu)), cslot(slotV(cb.cu, 0)), cslot(slotV(cb.cu, 1)), cslot(slotV(cb.cu, 2)), c->d_parent,   \
+        c->d_coords, nv, bslot(c, slotU(b.cu)), bslot(c, slotU(b.pu)), bslot(c, slotV(b.cu, 0)),                      \
+        bslot(c, slotV(b.cu, 1)), bslot(c, slotV(b.cu, 2)), bslot(c, slotV(b.pu, 0)), bslot(c, slotV(b.pu, 1)),       \
+        bslot(c, slotV(b.pu, 2)))
+    switch (c->LE) {
+        case 2: BPRO(2); break;
+        case 3: BPRO(3); break;
+        case 4: BPRO(4); break;
+        default: BPRO(5); break;
+    }
+#undef BPRO
+    BCU(cudaGetLastError());
+    BCU(cudaStreamSynchronize(c->stream));
+    c->k = 0;
+    return TGV_OK;
+}
+
 }  // extern "C"
+

@@ -1481,21 +1481,25 @@ int tgv_prolong_from(tgv_ctx* c, const tgv_ctx* coarse)
 }
 
 // ---- NEXT-2 GPU histogram voting ---------------------------------------------------
-int tgv_vote_depth_maps(tgv_ctx* c, const tgv_camera* cams, int ncams, const float* const* depths,
-                        const double grid_origin[3], double voxel_size, double voxel_radius)
+}  // extern "C"
+
+namespace {
+// Alg. 1 inputs on the device: the cameras (VoteCam) and every depth map's mip
+// pyramid (means of the valid children), uploaded / built on stream st.
+// Returns TGV_OK, TGV_EINVAL (bad camera), TGV_ENOMEM or TGV_ECUDA with err set;
+// on success the caller owns *d_depth and *d_cams (free after the vote kernel).
+int vote_upload(cudaStream_t st, const tgv_camera* cams, int ncams, const float* const* depths, float** d_depth_out,
+                VoteCam** d_cams_out, char* err)
 {
-    int rc = check_ready(c);
-    if (rc) return rc;
-    if (!cams || !depths || !grid_origin || ncams < 0) return fail(c, TGV_EINVAL, "NULL argument");
-    if (c->nbins != 8) return fail(c, TGV_EINVAL, "Alg. 1 votes into 8 bins; this context has %d", c->nbins);
-    if (!(voxel_size > 0.0) || !(voxel_radius > 0.0)) return fail(c, TGV_EINVAL, "voxel size and radius must be > 0");
     std::vector<VoteCam> vc((size_t)ncams);
     int64_t total = 0;
     for (int i = 0; i < ncams; ++i) {
         const tgv_camera& C = cams[i];
         if (C.width < 1 || C.height < 1 || C.width > (1 << 22) || C.height > (1 << 22) || !depths[i] ||
-            C.vote_weight < 0 || !(C.fx > 0.0) || !(C.fy > 0.0))
-            return fail(c, TGV_EINVAL, "camera %d: bad size, focal, weight or NULL depth map", i);
+            C.vote_weight < 0 || !(C.fx > 0.0) || !(C.fy > 0.0)) {
+            snprintf(err, 512, "camera %d: bad size, focal, weight or NULL depth map", i);
+            return TGV_EINVAL;
+        }
         VoteCam& V = vc[(size_t)i];
         memcpy(V.origin, C.origin, sizeof V.origin);
         memcpy(V.rot, C.rot, sizeof V.rot);
@@ -1520,34 +1524,59 @@ int tgv_vote_depth_maps(tgv_ctx* c, const tgv_camera* cams, int ncams, const flo
             h = (h + 1) / 2;
         }
     }
-    c->loaded = false;
     float* d_depth = nullptr;
     VoteCam* d_cams = nullptr;
     if (cudaMalloc(&d_depth, sizeof(float) * (size_t)std::max<int64_t>(1, total)) != cudaSuccess ||
         cudaMalloc(&d_cams, sizeof(VoteCam) * (size_t)std::max(1, ncams)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(d_depth);
-        return fail(c, TGV_ENOMEM, "depth pyramid allocation of %.2f GB failed", total * 4e-9);
+        snprintf(err, 512, "depth pyramid allocation of %.2f GB failed", total * 4e-9);
+        return TGV_ENOMEM;
     }
-    auto cleanup = [&]() {
-        cudaStreamSynchronize(c->stream);
-        cudaFree(d_depth);
-        cudaFree(d_cams);
-    };
     cudaError_t e = cudaSuccess;
     for (int i = 0; i < ncams && e == cudaSuccess; ++i) {
         const VoteCam& V = vc[(size_t)i];
         e = cudaMemcpyAsync(d_depth + V.lev_off[0], depths[i], sizeof(float) * (size_t)V.lw[0] * V.lh[0],
-                            cudaMemcpyHostToDevice, c->stream);
+                            cudaMemcpyHostToDevice, st);
         for (int L = 1; L < V.nlev && e == cudaSuccess; ++L) {
-            pyramid_level_kernel<<<148 * 4, 256, 0, c->stream>>>(d_depth + V.lev_off[L - 1], V.lw[L - 1], V.lh[L - 1],
-                                                                  d_depth + V.lev_off[L], V.lw[L], V.lh[L]);
+            pyramid_level_kernel<<<148 * 4, 256, 0, st>>>(d_depth + V.lev_off[L - 1], V.lw[L - 1], V.lh[L - 1],
+                                                           d_depth + V.lev_off[L], V.lw[L], V.lh[L]);
             e = cudaGetLastError();
         }
     }
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(d_cams, vc.data(), sizeof(VoteCam) * (size_t)ncams, cudaMemcpyHostToDevice, c->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream);
+        e = cudaMemcpyAsync(d_cams, vc.data(), sizeof(VoteCam) * (size_t)ncams, cudaMemcpyHostToDevice, st);
+    // the host camera table must stay alive until the copy is done
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        cudaFree(d_depth);
+        cudaFree(d_cams);
+        snprintf(err, 512, "depth upload / pyramids: %s", cudaGetErrorString(e));
+        return TGV_ECUDA;
+    }
+    *d_depth_out = d_depth;
+    *d_cams_out = d_cams;
+    return TGV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int tgv_vote_depth_maps(tgv_ctx* c, const tgv_camera* cams, int ncams, const float* const* depths,
+                        const double grid_origin[3], double voxel_size, double voxel_radius)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!cams || !depths || !grid_origin || ncams < 0) return fail(c, TGV_EINVAL, "NULL argument");
+    if (c->nbins != 8) return fail(c, TGV_EINVAL, "Alg. 1 votes into 8 bins; this context has %d", c->nbins);
+    if (!(voxel_size > 0.0) || !(voxel_radius > 0.0)) return fail(c, TGV_EINVAL, "voxel size and radius must be > 0");
+    c->loaded = false;
+    float* d_depth = nullptr;
+    VoteCam* d_cams = nullptr;
+    char msg[512];
+    if ((rc = vote_upload(c->stream, cams, ncams, depths, &d_depth, &d_cams, msg))) return fail(c, rc, "%s", msg);
+    cudaError_t e = cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream);
     if (e == cudaSuccess) {
         if (c->slots == 8)
             vote_kernel<8><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth, c->g, grid_origin[0], grid_origin[1],
@@ -1559,7 +1588,9 @@ int tgv_vote_depth_maps(tgv_ctx* c, const tgv_camera* cams, int ncams, const flo
                                                             c->hist16, c->d_maxc);
         e = cudaGetLastError();
     }
-    cleanup();
+    cudaStreamSynchronize(c->stream);
+    cudaFree(d_depth);
+    cudaFree(d_cams);
     if (e != cudaSuccess) return fail(c, TGV_ECUDA, "voting: %s", cudaGetErrorString(e));
     return finish_counts(c);
 }

@@ -47,6 +47,46 @@ __global__ void pyramid_level_kernel(const float* __restrict__ src, int sw, int 
     }
 }
 
+// Alg. 1 for one voxel centre pw (world coordinates): every camera's vote into acc[8]
+__device__ __forceinline__ void vote_point(const VoteCam* __restrict__ cams, int ncams,
+                                           const float* __restrict__ depth, double pw0, double pw1, double pw2,
+                                           double r, double delta, double eta, unsigned int (&acc)[8])
+{
+    for (int c = 0; c < ncams; ++c) {
+        const VoteCam& C = cams[c];
+        const double d0 = __dsub_rn(pw0, C.origin[0]), d1 = __dsub_rn(pw1, C.origin[1]),
+                     d2 = __dsub_rn(pw2, C.origin[2]);
+        double pc[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            pc[k] = __dadd_rn(__dadd_rn(__dmul_rn(C.rot[k], d0), __dmul_rn(C.rot[3 + k], d1)),
+                              __dmul_rn(C.rot[6 + k], d2));
+        if (!(pc[2] > 0.0)) continue;
+        const double u = __dadd_rn(__ddiv_rn(__dmul_rn(C.fx, pc[0]), pc[2]), C.cx);
+        const double v = __dadd_rn(__ddiv_rn(__dmul_rn(C.fy, pc[1]), pc[2]), C.cy);
+        if (!(u >= 0.0 && u < (double)C.width && v >= 0.0 && v < (double)C.height)) continue;
+        const double diam = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, r), C.fx), pc[2]);
+        int L = 0;
+        double thr = 1.4142135623730951;  // sqrt(2) 2^k
+        while (L < C.nlev - 1 && diam >= thr) {
+            ++L;
+            thr = __dmul_rn(thr, 2.0);
+        }
+        const double sc = (double)(1 << L);
+        int ix = (int)floor(__ddiv_rn(u, sc)), iy = (int)floor(__ddiv_rn(v, sc));
+        ix = min(ix, C.lw[L] - 1);
+        iy = min(iy, C.lh[L] - 1);
+        const float dep = __ldg(depth + C.lev_off[L] + (int64_t)iy * C.lw[L] + ix);
+        if (dep != dep) continue;  // depth = None
+        double a = __dsub_rn((double)dep, pc[2]);
+        if (a < -eta) continue;  // occluded: no vote
+        a = __ddiv_rn(a, delta);
+        a = fmin(fmax(a, -1.0), 1.0);
+        const int bin = min((int)floor(__dmul_rn(__ddiv_rn(__dadd_rn(a, 1.0), 2.0), 8.0)), 7);
+        acc[bin] += (unsigned)C.vote_weight;
+    }
+}
+
 // counts of local planes [0, nzl) of the slab, u16 store (SLOTS per voxel, bins 0..7
 // used), running maximum for the range check / u8 decision
 template <int SLOTS>
@@ -67,39 +107,7 @@ __global__ void __launch_bounds__(256) vote_kernel(const VoteCam* __restrict__ c
         const double pw1 = __dadd_rn(oy, __dmul_rn(h, (double)y));
         const double pw2 = __dadd_rn(oz, __dmul_rn(h, (double)(g.z0 + zl)));
         unsigned int acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int c = 0; c < ncams; ++c) {
-            const VoteCam& C = cams[c];
-            const double d0 = __dsub_rn(pw0, C.origin[0]), d1 = __dsub_rn(pw1, C.origin[1]),
-                         d2 = __dsub_rn(pw2, C.origin[2]);
-            double pc[3];
-#pragma unroll
-            for (int k = 0; k < 3; ++k)
-                pc[k] = __dadd_rn(__dadd_rn(__dmul_rn(C.rot[k], d0), __dmul_rn(C.rot[3 + k], d1)),
-                                  __dmul_rn(C.rot[6 + k], d2));
-            if (!(pc[2] > 0.0)) continue;
-            const double u = __dadd_rn(__ddiv_rn(__dmul_rn(C.fx, pc[0]), pc[2]), C.cx);
-            const double v = __dadd_rn(__ddiv_rn(__dmul_rn(C.fy, pc[1]), pc[2]), C.cy);
-            if (!(u >= 0.0 && u < (double)C.width && v >= 0.0 && v < (double)C.height)) continue;
-            const double diam = __ddiv_rn(__dmul_rn(__dmul_rn(2.0, r), C.fx), pc[2]);
-            int L = 0;
-            double thr = 1.4142135623730951;  // sqrt(2) 2^k
-            while (L < C.nlev - 1 && diam >= thr) {
-                ++L;
-                thr = __dmul_rn(thr, 2.0);
-            }
-            const double sc = (double)(1 << L);
-            int ix = (int)floor(__ddiv_rn(u, sc)), iy = (int)floor(__ddiv_rn(v, sc));
-            ix = min(ix, C.lw[L] - 1);
-            iy = min(iy, C.lh[L] - 1);
-            const float dep = __ldg(depth + C.lev_off[L] + (int64_t)iy * C.lw[L] + ix);
-            if (dep != dep) continue;  // depth = None
-            double a = __dsub_rn((double)dep, pc[2]);
-            if (a < -eta) continue;  // occluded: no vote
-            a = __ddiv_rn(a, delta);
-            a = fmin(fmax(a, -1.0), 1.0);
-            const int bin = min((int)floor(__dmul_rn(__ddiv_rn(__dadd_rn(a, 1.0), 2.0), 8.0)), 7);
-            acc[bin] += (unsigned)C.vote_weight;
-        }
+        vote_point(cams, ncams, depth, pw0, pw1, pw2, r, delta, eta, acc);
         uint16_t* dst = H + ((int64_t)zl * g.plane + (int64_t)y * g.px + x) * SLOTS;
 #pragma unroll
         for (int b = 0; b < SLOTS; ++b) {

@@ -234,9 +234,8 @@ def tgv_destroy(ctx):
     lib.tgv_destroy(ctx)
 
 
-def tgv_vote_depth_maps(ctx, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, voxel_radius=0.5):
-    """cams: dicts (origin, rot 3x3 world<-camera, fx, fy, cx, cy, width, height, vote_weight);
-    depths: float32 [h, w] host arrays (NaN = no depth)."""
+def _camera_args(cams, depths):
+    """ctypes camera table and depth-map pointers (the arrays are returned to keep them alive)."""
     arr = (tgv_camera * max(1, len(cams)))()
     for i, c in enumerate(cams):
         arr[i].origin[:] = [float(x) for x in c["origin"]]
@@ -245,6 +244,13 @@ def tgv_vote_depth_maps(ctx, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_si
         arr[i].width, arr[i].height, arr[i].vote_weight = c["width"], c["height"], c.get("vote_weight", 1)
     ds = [np.ascontiguousarray(d, dtype=np.float32) for d in depths]
     ptrs = (ctypes.c_void_p * max(1, len(ds)))(*[d.ctypes.data for d in ds])
+    return arr, ptrs, ds
+
+
+def tgv_vote_depth_maps(ctx, cams, depths, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0, voxel_radius=0.5):
+    """cams: dicts (origin, rot 3x3 world<-camera, fx, fy, cx, cy, width, height, vote_weight);
+    depths: float32 [h, w] host arrays (NaN = no depth)."""
+    arr, ptrs, ds = _camera_args(cams, depths)
     o = np.asarray(grid_origin, dtype=np.float64)
     _check(lib.tgv_vote_depth_maps(ctx, arr, len(cams), ptrs, o.ctypes.data, float(voxel_size), float(voxel_radius)),
            ctx)

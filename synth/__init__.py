@@ -104,6 +104,11 @@ def heightfield(base, waves, zmin, zmax):
     return (2, a)
 
 
+def box(lo, hi):
+    """Axis-aligned box (a building of the C5 urban scene)."""
+    return (3, [float(lo[0]), float(lo[1]), float(lo[2]), float(hi[0]), float(hi[1]), float(hi[2])])
+
+
 def fibonacci_sphere(n):
     pts = []
     ga = math.pi * (3.0 - math.sqrt(5.0))
@@ -213,7 +218,39 @@ def _c4() -> Workload:
                     prims=prims, cams=cams)
 
 
-WORKLOADS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4}
+def _c5() -> Workload:
+    """BASELINE configs[4]: a block-sparse brick set of an urban scene, 3 scale levels.
+    The finest level spans 2048 x 2048 x 256 voxels (64 x 64 x 8 bricks of 32^3); which
+    bricks exist is decided by the votes (R24), about 2 x 10^4 over the
+    levels.  120 buildings (boxes, footprints 40-160, heights 30-200) on a ground plane
+    at z = 40, seen by 36 nadir and 28 oblique aerial cameras, 1024 x 1024."""
+    rng = np.random.default_rng(5)
+    ground = 40.0
+    prims = [plane(ground)]
+    for _ in range(120):
+        w, d = float(rng.uniform(40, 160)), float(rng.uniform(40, 160))
+        x0, y0 = float(rng.uniform(64, 1984 - w)), float(rng.uniform(64, 1984 - d))
+        prims.append(box((x0, y0, ground - 5.0), (x0 + w, y0 + d, ground + float(rng.uniform(30, 200)))))
+    cams = []
+    for i in range(6):
+        for j in range(6):
+            x, y = 170.0 + 341.0 * i, 170.0 + 341.0 * j
+            cams.append(look_at((x, y, 2400.0), (x + 1e-3, y, ground), 1024, 1024, 45.0))
+    for h in range(4):
+        hd = (math.cos(h * math.pi / 2 + 0.3), math.sin(h * math.pi / 2 + 0.3))
+        for i in range(7):
+            tx, ty = 300.0 + 240.0 * i, 300.0 + 240.0 * ((i * 3 + h) % 7)
+            dd = 1800.0
+            o = (tx - hd[0] * dd / math.sqrt(2), ty - hd[1] * dd / math.sqrt(2), ground + dd / math.sqrt(2))
+            cams.append(look_at(o, (tx, ty, ground), 1024, 1024, 40.0))
+    return Workload("C5", (2048, 2048, 256), 200, 5, 0.5, 0.0,
+                    "block-sparse brick set of an urban scene (120 buildings on a ground plane), finest level "
+                    "2048x2048x256 in 32^3 bricks selected by the votes, 3 scale levels, 64 aerial depth maps "
+                    "1024x1024, N(0,0.5) noise, 8 bins, 200 iterations per level",
+                    prims=prims, cams=cams)
+
+
+WORKLOADS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5}
 
 
 @functools.lru_cache(maxsize=8)

@@ -30,6 +30,7 @@
 #define PRIM_SPHERE 0
 #define PRIM_PLANE 1      /* horizontal ground plane z = a[0], seen from above */
 #define PRIM_HEIGHTFIELD 2 /* z = a[0] + sum_{o<5} amp_o sin(kx_o x + ky_o y + phi_o) */
+#define PRIM_BOX 3         /* axis-aligned box [a0, a3] x [a1, a4] x [a2, a5] (a building) */
 
 typedef struct {
     int32_t kind;
@@ -94,6 +95,27 @@ static double intersect(const synth_prim* p, const double o[3], const double d[3
         if (d[2] >= 0.0) return INFINITY;
         double t = (p->a[0] - o[2]) / d[2];
         return t > 1e-9 ? t : INFINITY;
+    }
+    if (p->kind == PRIM_BOX) { /* slab test */
+        double t0 = -INFINITY, t1 = INFINITY;
+        for (int k = 0; k < 3; ++k) {
+            if (d[k] == 0.0) {
+                if (o[k] < p->a[k] || o[k] > p->a[3 + k]) return INFINITY;
+                continue;
+            }
+            double ta = (p->a[k] - o[k]) / d[k], tb = (p->a[3 + k] - o[k]) / d[k];
+            if (ta > tb) {
+                double tt = ta;
+                ta = tb;
+                tb = tt;
+            }
+            if (ta > t0) t0 = ta;
+            if (tb < t1) t1 = tb;
+        }
+        if (t0 > t1) return INFINITY;
+        if (t0 > 1e-9) return t0;
+        if (t1 > 1e-9) return t1;
+        return INFINITY;
     }
     if (p->kind == PRIM_HEIGHTFIELD) {
         /* a[21], a[22]: bounds zmin, zmax of the field; march then bisect */
