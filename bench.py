@@ -8,6 +8,7 @@ steps / time, over all ranks.  Inputs are synthetic (synth/, seeded).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--iters I]
   python bench.py --impl reference ...   # the fp64 CPU oracle as the reference arm
+  python bench.py --workload C5          # NEXT-3 block-sparse brick levels (BASELINE configs[4])
 
 Multi-GPU (torchrun, one rank per GPU): the grid is split in z-slabs across
 ranks (strong scaling of the same workload); NCCL halo exchange inside the
@@ -513,12 +514,152 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def run_bricks(a):
+    """NEXT-3 block-sparse brick sets (BASELINE configs[4], workload C5): the brick
+    levels are built once from the GPU votes (brick_levels.BrickLevels); a step is the
+    coarse-to-fine solve (coarsest from its votes, each finer level prolongated with
+    its frozen shell, iters per level) plus the finest level's energy / gap.
+    value = voxel-iterations of the solved voxels per second (value_S: of the voxels
+    whose duals are updated, S = solved + frozen face-adjacent, R24)."""
+    import torch
+
+    import synth
+    from paper_2107_14790_b200.brick_levels import BrickLevels
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
+        return  # single-GPU measurement: the other ranks have no work
+    wl = synth.workload(a.workload)
+    iters = a.iters or wl.iters
+    levels = max(2, a.levels if a.levels > 1 else 3)
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
+    cams, depths = cams_of(wl), render_shared(wl, 0, 1)
+    t_build = time.perf_counter()
+    bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius, **kw)
+    t_build = time.perf_counter() - t_build
+    vox = bl.voxels()
+    infos = [s.info() for s in bl.solvers]
+    solved = [i["solved_voxels"] for i in infos]
+    svox = [i["s_voxels"] for i in infos]
+    vox_its, vox_its_s = sum(solved) * iters, sum(svox) * iters
+
+    def step():
+        bl.solve(iters).energy()
+
+    for _ in range(a.warmup):
+        step()
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.3)
+    for s in bl.solvers:
+        s.set_timing(True)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()  # every library call synchronises its own stream before returning
+    ev1.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / a.steps
+    ms = ev0.elapsed_time(ev1) / a.steps
+    tms = [s.timing() for s in bl.solvers]
+    for s in bl.solvers:
+        s.set_timing(False)
+    clk = clocks.stop()
+    cb = bl.solvers[0].info()["count_bytes"]
+    # algorithmic bytes (DESIGN.md §5): dual on S, 17 reads + 9 writes; primal on the
+    # solved voxels, 13 reads + counts + 4 writes
+    dual_b = sum(svox) * 104 * iters
+    primal_b = sum(solved) * (68 + 8 * cb) * iters
+    dual_ms = sum(t["dual_ms"] for t in tms) / a.steps
+    primal_ms = sum(t["primal_ms"] for t in tms) / a.steps
+    peak, peak_src = measured_peaks()
+    dom, dbytes, dms = ("dual", dual_b, dual_ms) if dual_ms >= primal_ms else ("primal", primal_b, primal_ms)
+    achieved = dbytes / (dms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(a.workload, {}).get(f"brick_{dom}")
+    launches = sum(t["dual_launches"] + t["primal_launches"] + t["energy_launches"] for t in tms) / a.steps \
+        + 2 * levels  # + per level the init / prolongation kernel; + the energy final kernel
+
+    # e2e through the public API: H2D of the depth maps and Alg. 1 votes into every
+    # level's bricks, the coarse-to-fine solve, energy, D2H of the finest u
+    e2e = None
+    if not a.no_e2e:
+        hu = None
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            for lev, s in enumerate(bl.solvers):
+                s.vote(cams, depths, voxel_size=float(1 << lev), voxel_radius=wl.voxel_radius * (1 << lev))
+            f = bl.solve(iters)
+            f.energy()
+            hu = f.read_u()
+        el = (time.perf_counter() - t0) / a.steps
+        h2d = levels * sum(int(d.nbytes) for d in depths)
+        e2e = {"value": vox_its / el, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(hu.nbytes) + 48,
+               "calls": "tgv_bricks_vote_depth_maps per level, tgv_bricks_reset / prolong_from / iterate per level, "
+                        "tgv_bricks_energy, tgv_bricks_read"}
+    cpu = None
+    if not a.no_cpu_baseline:
+        cpu = cpu_brick_oracle_rate(bl, a.cpu_seconds, kw)
+    bricks = bl.bricks()
+    line = {
+        "metric": METRIC + " (NEXT-3 block-sparse brick sets)", "value": vox_its / (ms * 1e-3), "unit": UNIT,
+        "value_S": vox_its_s / (ms * 1e-3), "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{wl.name}: {wl.description}", "extent": list(wl.shape), "edge": 32, "levels": levels,
+                   "iters_per_level": iters,
+                   "bricks_solved_frozen_finest_first": bricks, "bricks_total": int(sum(a_ + b_ for a_, b_ in bricks)),
+                   "voxels_per_level_finest_first": vox, "solved_voxels_per_level": solved,
+                   "s_voxels_per_level": svox, "build_s": t_build,
+                   "step": "coarse-to-fine over the brick levels: reset coarsest, iters; per finer level prolong "
+                           "(frozen shell from the parent), iters; energy/gap of the finest",
+                   "parallelism": "single GPU",
+                   "l2": "no flush: resident brick state >> 126 MB L2"},
+        "roofline": {"bound": "hbm", "kernel": f"brick_{dom}", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_voxel": 104 if dom == "dual" else 68 + 8 * cb, "kernel_ms_per_step": dms,
+                     "schedule_gbs": (dual_b + primal_b) / (ms * 1e-3) / 1e9, "count_bytes": cb,
+                     "kernel_share_of_step": (dual_ms + primal_ms) / ms},
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches * a.steps)),
+        "kernel_ms": {"dual": dual_ms, "primal": primal_ms,
+                      "energy": sum(t["energy_ms"] for t in tms) / a.steps},
+        "wall_ms_per_step": wall * 1e3,
+    }
+    print(json.dumps(line), flush=True)
+    bl.close()
+
+
+def cpu_brick_oracle_rate(bl, target_s, kw):
+    """The brick-set oracle (oracle/bricks.py, numpy fp64) as it stands, on a bounded
+    sample: the first 8 solved bricks of the finest level with their counts."""
+    import oracle.bricks as ob
+    s = bl.solvers[0]
+    sel = np.nonzero(~bl.frozen[0])[0][:8]
+    counts = s.read_counts()[sel]
+    o = ob.BrickOracle(bl.edge, bl.coords[0][sel], **kw).load(counts)
+    t0 = time.perf_counter()
+    o.iterate(1)
+    t1 = time.perf_counter() - t0
+    k = int(max(1, min(1000, round(target_s / max(t1, 1e-6)))))
+    t0 = time.perf_counter()
+    o.iterate(k)
+    el = time.perf_counter() - t0
+    nv = len(sel) * bl.edge ** 3
+    return {"value": nv * k / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"C5 finest level, {len(sel)} solved 32^3 bricks as their own set, {k} iterations (numpy fp64)"}
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
     elif a.out_of_core:
         run_out_of_core(a)
+    elif a.workload == "C5":
+        run_bricks(a)
     else:
         run_ours(a)
 

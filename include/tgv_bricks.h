@@ -16,16 +16,21 @@
  *       D+_k w[x] = w[x + e_k] - w[x] if x + e_k is in Omega, else 0
  *       D-_k w[x] = [x + e_k in Omega] w[x] - [x - e_k in Omega] w[x - e_k]
  *     (Neumann / zero flux across the boundary of Omega);
- *   - one iteration is the scheme of tgv.h (dual step on every voxel of Omega,
- *     primal step and over-relaxation on the voxels of A); u and v of B keep
- *     the values given by tgv_bricks_set_primal;
+ *   - S = A plus the frozen voxels with a face neighbour in A: the terms of the
+ *     functional at any other voxel do not involve A (constants of the solve) and
+ *     the primal step on A reads duals on S only;
+ *   - one iteration is the scheme of tgv.h (dual step on the voxels of S, the
+ *     duals elsewhere staying 0; primal step and over-relaxation on the voxels of
+ *     A); u and v of B keep the values given by tgv_bricks_set_primal /
+ *     tgv_bricks_prolong_from;
  *   - a box-shaped set of solved bricks is exactly the dense grid of tgv.h.
  *
  * Layout of every per-voxel host array: brick-major in the order the bricks were
  * given, inside a brick z, y, x (x fastest): element (b, z, y, x) is at
  * ((b * E + z) * E + y) * E + x.  Conventions (status codes, ownership,
- * poisoning) are those of tgv.h.  One iteration moves 180 B per voxel with u8
- * counts (188 B with u16): a dual kernel and a primal kernel.
+ * poisoning) are those of tgv.h.  One iteration is a dual kernel over S (104 B
+ * per voxel) and a primal kernel over A (76 B per voxel with u8 counts, 84 B with
+ * u16).
  */
 #ifndef TGV_BRICKS_H
 #define TGV_BRICKS_H
@@ -127,7 +132,7 @@ int tgv_bricks_iterate(tgv_bricks* ctx, int32_t n);
 int tgv_bricks_read(tgv_bricks* ctx, int field, float* out, int64_t n_voxels);
 
 /* Energy and restricted gap (R24, fp64 per-voxel terms, deterministic
- * reduction): the regulariser over every voxel of Omega, the data term over A,
+ * reduction): the regulariser over S, the data term over A,
  *   out[0] E   out[1] alpha1-term   out[2] alpha0-term   out[3] data-term
  *   out[4] gap_V = E - D_V with
  *          D_V = sum_A [min_{u in [-1,1]} (lambda sum_b h_b |u - c_b| - u div p) - V |p + div2 q|_1]
@@ -142,8 +147,19 @@ int tgv_bricks_energy(tgv_bricks* ctx, double out[6]);
 int tgv_bricks_set_timing(tgv_bricks* ctx, int enable);
 int tgv_bricks_get_timing(tgv_bricks* ctx, tgv_timing* out);
 
-/* Device bytes owned by the context and the stored count width (1 or 2). */
-int tgv_bricks_info(const tgv_bricks* ctx, int64_t* device_bytes, int32_t* count_bytes);
+/* Static facts about a brick-set context.  S (R24) is the set of voxels
+ * whose duals an iteration updates: the solved voxels and the frozen voxels with a
+ * solved face neighbour; an iteration processes s_voxels in the dual kernel and
+ * solved_voxels in the primal kernel. */
+typedef struct {
+    int64_t device_bytes;   /* device memory owned by the context                 */
+    int32_t count_bytes;    /* stored bytes per count: 1 (u8) or 2 (u16), 0 before load */
+    int32_t edge;           /* E                                                  */
+    int64_t nbricks, nfrozen;
+    int64_t solved_voxels;  /* (nbricks - nfrozen) * E^3                          */
+    int64_t s_voxels;       /* |S|                                                */
+} tgv_bricks_info_t;
+int tgv_bricks_info(const tgv_bricks* ctx, tgv_bricks_info_t* out);
 
 /* Detail of the last failure on ctx (or of the last failed create, ctx = NULL). */
 const char* tgv_bricks_last_error(const tgv_bricks* ctx);

@@ -19,14 +19,19 @@ a block-sparse level:
         D-_k w[x] = [x + e_k in Omega] w[x] - [x - e_k in Omega] w[x - e_k]
     so that D-_k = -(D+_k)^T on Omega (pinned by tests/test_oracle_bricks.py); on a
     box-shaped Omega they are the dense grid's operators;
+  * S = A plus the frozen voxels with a face neighbour in A (dB).  The terms of the
+    functional at a voxel x involve u(x), u(x + e_k), v(x), v(x - e_k) only, so the
+    terms at voxels outside S are constants of the solve, and the only duals the
+    primal step on A reads are those on S (p at x - e_k, q at x + e_l);
   * one iteration is the scheme of oracle/tgv_oracle.c:
-    the dual step on every voxel of Omega, the primal step (prox, clamp, v update,
-    over-relaxation) on the voxels of A only; on B, u and v keep the values they were
-    given (ubar = u, vbar = v), as in reading R23's frozen leaf borders;
+    the dual step on the voxels of S (the duals elsewhere stay 0), the primal step
+    (prox, clamp, v update, over-relaxation) on the voxels of A only; on B, u and v
+    keep the values they were given (ubar = u, vbar = v), as in reading R23's frozen
+    leaf borders (whose recomputed halo duals are exactly dB's);
   * the energy is the functional restricted to what the solve changes: the
-    regulariser over every voxel of Omega (terms at B voxels see A's values through
-    the stencil) and the data term over A.  The restricted dual value follows from the
-    saddle-point form sum_Omega [-u div p - v.(p + div2 q)] + G(u_A):
+    regulariser over S and the data term over A.  The restricted dual value follows
+    from the saddle-point form sum_S [<grad u - v, p> + <E v, q>] + G(u_A) with the
+    duals zero outside S, i.e. sum_Omega [-u div p - v.(p + div2 q)] + G(u_A):
         D_V = sum_A [min_{u in [-1,1]} (G(u) - u div p) - V |p + div2 q|_1]
             + sum_B [-u div p - v.(p + div2 q)]
     and gap = E - D_V >= 0 whenever the minimiser has |v_A| <= V (reading R14).
@@ -168,6 +173,11 @@ class BrickOracle:
         for b in range(nbk):
             self.om[self._sl(b)] = True
             self.act[self._sl(b)] = not self.frozen[b]
+        # S = A + the frozen voxels with a face neighbour in A
+        near = np.zeros(self.box, bool)
+        for k in range(3):
+            near |= _next(self.act, k) | _prev(self.act, k)
+        self.S = self.act | (self.om & near)
         z = lambda *lead: np.zeros(lead + self.box)  # noqa: E731
         self.u, self.ubar = z(), z()
         self.v, self.vbar, self.p, self.q = z(3), z(3), z(3), z(6)
@@ -223,15 +233,16 @@ class BrickOracle:
         return self
 
     def dual(self):
-        """(a1) on every voxel of Omega: p <- P_a1(p + s(grad ubar - vbar)), q <- P_a0(q + s E(vbar))."""
+        """(a1) on the voxels of S: p <- P_a1(p + s(grad ubar - vbar)), q <- P_a0(q + s E(vbar));
+        the operators still see every voxel of Omega (the frozen values around S)."""
         om = self.om
         pn = self.p + self.sigma * (grad(self.ubar, om) - self.vbar)
         pn = proj(pn, self.alpha1, pn[0] ** 2 + pn[1] ** 2 + pn[2] ** 2)
         qn = self.q + self.sigma * symgrad(self.vbar, om)
         n2 = qn[0] ** 2 + qn[1] ** 2 + qn[2] ** 2 + 2.0 * (qn[3] ** 2 + qn[4] ** 2 + qn[5] ** 2)
         qn = proj(qn, self.alpha0, n2)
-        self.p = np.where(om, pn, 0.0)
-        self.q = np.where(om, qn, 0.0)
+        self.p = np.where(self.S, pn, 0.0)
+        self.q = np.where(self.S, qn, 0.0)
 
     def primal(self):
         """(a2) + (a3) on A: u+ = clamp(prox(u + t div p)), v+ = v + t(p + div2 q),
@@ -256,8 +267,8 @@ class BrickOracle:
         return self._gather(a, 0 if a.ndim == 3 else a.shape[0])
 
     def energy(self):
-        """{E, alpha1, alpha0, data, gap, vmax, dual}: regulariser over Omega, data
-        over A, restricted dual D_V of the module docstring, vmax over A."""
+        """{E, alpha1, alpha0, data, gap, vmax, dual}: regulariser over S, data over A,
+        restricted dual D_V of the module docstring, vmax over A."""
         om, A = self.om, self.act
         a = grad(self.u, om) - self.v
         t1 = self.alpha1 * np.sqrt(a[0] ** 2 + a[1] ** 2 + a[2] ** 2)
@@ -271,7 +282,7 @@ class BrickOracle:
                       axis=0)
         dA = best - self.V * (np.abs(w[0]) + np.abs(w[1]) + np.abs(w[2]))
         dB = -self.u * d - (self.v[0] * w[0] + self.v[1] * w[1] + self.v[2] * w[2])
-        T1, T0 = float(np.sum(t1[om])), float(np.sum(t0[om]))
+        T1, T0 = float(np.sum(t1[self.S])), float(np.sum(t0[self.S]))
         TD = float(np.sum(td[A]))
         D = float(np.sum(dA[A]) + np.sum(dB[om & ~A]))
         E = T1 + T0 + TD

@@ -20,6 +20,12 @@ EXPORTS = ["tgv_bricks_create", "tgv_bricks_load", "tgv_bricks_set_primal", "tgv
            "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from"]
 
 
+class tgv_bricks_info_t(ctypes.Structure):
+    _fields_ = [("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32), ("edge", ctypes.c_int32),
+                ("nbricks", ctypes.c_int64), ("nfrozen", ctypes.c_int64), ("solved_voxels", ctypes.c_int64),
+                ("s_voxels", ctypes.c_int64)]
+
+
 class tgv_brickset(ctypes.Structure):
     _fields_ = [("edge", ctypes.c_int32), ("nbricks", ctypes.c_int64), ("coords", ctypes.c_void_p),
                 ("frozen", ctypes.c_void_p)]
@@ -36,7 +42,7 @@ def _setup():
     lib.tgv_bricks_energy.argtypes = [vp, vp]
     lib.tgv_bricks_set_timing.argtypes = [vp, ctypes.c_int]
     lib.tgv_bricks_get_timing.argtypes = [vp, ctypes.POINTER(tgv_timing)]
-    lib.tgv_bricks_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    lib.tgv_bricks_info.argtypes = [vp, ctypes.POINTER(tgv_bricks_info_t)]
     lib.tgv_bricks_vote_depth_maps.argtypes = [vp, ctypes.POINTER(tgv.tgv_camera), ctypes.c_int, ctypes.POINTER(vp),
                                                vp, ctypes.c_double, ctypes.c_double]
     lib.tgv_bricks_read_counts.argtypes = [vp, vp, i64]
@@ -160,6 +166,6 @@ class BrickSolver:
         return {k: getattr(t, k) for k, _ in tgv_timing._fields_}
 
     def info(self):
-        db, cb = ctypes.c_int64(), ctypes.c_int32()
-        _bcheck(lib.tgv_bricks_info(self.ctx, ctypes.byref(db), ctypes.byref(cb)))
-        return {"device_bytes": db.value, "count_bytes": cb.value}
+        t = tgv_bricks_info_t()
+        _bcheck(lib.tgv_bricks_info(self.ctx, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in tgv_bricks_info_t._fields_}

@@ -15,8 +15,8 @@
 // iterates, p, q over 2) are reused as they are.
 //
 // Kernels (one voxel per thread, 256 threads, every load issued before any store):
-//   brick_dual_kernel    p, q at every voxel of Omega            104 B per voxel
-//   brick_primal_kernel  u, v at A (copied through at B)          76 / 84 B per voxel
+//   brick_dual_kernel    p, q at every voxel of S (A + frozen voxels face-adjacent to A)  104 B per voxel
+//   brick_primal_kernel  u, v at A (B skipped)                                        76 / 84 B per voxel
 //   brick_energy_kernel  fp64 terms, block partials (energy_final_kernel sums them)
 #pragma once
 #include "tgv_kernels.cuh"
@@ -27,6 +27,7 @@ struct BrickGeo {
     int nvox;              // nbricks * E^3 (< 2^31, checked at create)
     const int* nbr;        // [nbricks][6]: brick index of the -x, +x, -y, +y, -z, +z neighbour, or -1
     const uint8_t* frozen; // [nbricks]: 1 = set B
+    const uint8_t* aface;  // [nbricks]: bit 2k + d set if the face neighbour along axis k (d = 0: -, 1: +) is solved
 };
 
 // voxel i = ((b * E + z) * E + y) * E + x and its face neighbours (-1: outside Omega)
@@ -40,6 +41,13 @@ struct BrickIdx {
         c[1] = (i >> LE) & (E - 1);
         c[2] = (i >> (2 * LE)) & (E - 1);
         b = i >> (3 * LE);
+    }
+    // a frozen voxel belongs to S (R24) iff a face neighbour is a solved voxel:
+    // it sits on a face of its brick whose neighbour brick across that face is solved
+    __device__ __forceinline__ bool on_solved_face(unsigned int af) const
+    {
+        return ((c[0] == 0) & af) | ((c[0] == E - 1) & (af >> 1)) | ((c[1] == 0) & (af >> 2)) |
+               ((c[1] == E - 1) & (af >> 3)) | ((c[2] == 0) & (af >> 4)) | ((c[2] == E - 1) & (af >> 5));
     }
     __device__ __forceinline__ int fwd(const int* __restrict__ nbr, int k) const
     {
@@ -57,15 +65,41 @@ struct BrickIdx {
     }
 };
 
-// (a1) at every voxel of Omega -- the expressions of split_dual_kernel with the
-// neighbour masks taken from the brick table
-template <int LE>
-__global__ void __launch_bounds__(256) brick_dual_kernel(const IterPtrs a, const BrickGeo bg, const StepParams sp)
+// (a1) at every voxel of S (solved voxels, and frozen voxels face-adjacent to them,
+// which lie on the frozen bricks' faces towards solved bricks; the duals elsewhere
+// stay 0) -- the expressions of split_dual_kernel with the neighbour masks taken
+// from the brick table
+// One body, two index spaces (MODE): 0 = every voxel of the solved bricks of `list`
+// (n = |list| E^3 threads); 1 = the faces of frozen bricks that touch a solved brick,
+// list = (brick, face) pairs, E^2 threads per face (a voxel on two such faces is
+// computed twice, identically: reads and writes use different slots).
+template <int LE, int MODE>
+__device__ __forceinline__ int brick_list_voxel(const int* __restrict__ list, int t)
+{
+    constexpr int E = 1 << LE;
+    if constexpr (MODE == 0) {
+        return (__ldg(list + (t >> (3 * LE))) << (3 * LE)) | (t & (E * E * E - 1));
+    } else {
+        const int j = t >> (2 * LE);
+        const int b = __ldg(list + 2 * j), f = __ldg(list + 2 * j + 1);
+        const int k = f >> 1, side = (f & 1) ? E - 1 : 0;
+        const int a = t & (E - 1), c = (t >> LE) & (E - 1);
+        int x, y, z;  // x fastest where the face allows it (coalesced rows)
+        if (k == 2) x = a, y = c, z = side;
+        else if (k == 1) x = a, y = side, z = c;
+        else x = side, y = a, z = c;
+        return (((b << LE | z) << LE | y) << LE) | x;
+    }
+}
+
+template <int LE, int MODE>
+__global__ void __launch_bounds__(256) brick_dual_kernel(const IterPtrs a, const BrickGeo bg, const StepParams sp,
+                                                         const int* __restrict__ list, int n)
 {
     const int t = blockIdx.x * 256 + threadIdx.x;
-    if (t >= bg.nvox) return;
-    const BrickIdx<LE> I(t);
-    const int i = t;
+    if (t >= n) return;
+    const int i = brick_list_voxel<LE, MODE>(list, t);
+    const BrickIdx<LE> I(i);
     const int fx = I.fwd(bg.nbr, 0), fy = I.fwd(bg.nbr, 1), fz = I.fwd(bg.nbr, 2);
     const int bx = I.bwd(bg.nbr, 0), by = I.bwd(bg.nbr, 1), bz = I.bwd(bg.nbr, 2);
     const bool xl = fx >= 0, yl = fy >= 0, zl = fz >= 0;
@@ -110,22 +144,17 @@ __global__ void __launch_bounds__(256) brick_dual_kernel(const IterPtrs a, const
     for (int m = 0; m < 6; ++m) a.qn[m][i] = q[m] * sq;
 }
 
-// (a2) + (a3) at A -- the expressions of split_primal_kernel; at B (warp-uniform: a
-// brick holds a multiple of 32 voxels) u and v are carried to the next iterate
+// (a2) + (a3) at A -- the expressions of split_primal_kernel; B is skipped (warp-
+// uniform: a brick holds a multiple of 32 voxels): its u and v sit in all three
+// rotating slots (tgv_bricks_set_primal / prolong_from), so ubar = u, vbar = v there
 template <int LE, int SLOTS, typename CT>
 __global__ void __launch_bounds__(256) brick_primal_kernel(const IterPtrs a, const BrickGeo bg, const StepParams sp,
-                                                           const Centers C)
+                                                           const Centers C, const int* __restrict__ list, int n)
 {
     const int t = blockIdx.x * 256 + threadIdx.x;
-    if (t >= bg.nvox) return;
-    const BrickIdx<LE> I(t);
-    const int i = t;
-    if (__ldg(bg.frozen + I.b)) {
-        a.un[i] = __ldg(a.uk + i);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) a.vn[k][i] = __ldg(a.vk[k] + i);
-        return;
-    }
+    if (t >= n) return;
+    const int i = brick_list_voxel<LE, 0>(list, t);  // solved bricks only
+    const BrickIdx<LE> I(i);
     const int fx = I.fwd(bg.nbr, 0), fy = I.fwd(bg.nbr, 1), fz = I.fwd(bg.nbr, 2);
     const int bx = I.bwd(bg.nbr, 0), by = I.bwd(bg.nbr, 1), bz = I.bwd(bg.nbr, 2);
     const bool xl = fx >= 0, yl = fy >= 0, zl = fz >= 0;
@@ -204,9 +233,9 @@ __global__ void brick_init_kernel(float* __restrict__ u_cur, float* __restrict__
     }
 }
 
-// (a4) on a brick set (R24): regulariser over Omega, data and the box
-// term of the dual over A, the frozen primal's saddle term -u div p - v.(p + div2 q)
-// over B; vmax over A.  Partials in the layout of energy_partial_kernel.
+// (a4) on a brick set (R24): regulariser over S, data and the box term of
+// the dual over A, the frozen primal's saddle term -u div p - v.(p + div2 q) over B
+// (duals are 0 outside S); vmax over A.  Partials in the layout of energy_partial_kernel.
 template <int LE, int SLOTS, typename CT>
 __global__ void __launch_bounds__(256)
     brick_energy_kernel(const EnergyArgs ea, const BrickGeo bg, Centers C, double* __restrict__ partials)
@@ -223,13 +252,15 @@ __global__ void __launch_bounds__(256)
         auto dm = [&](const float* f, int k) { return (fw[k] >= 0 ? F(f, i) : 0.0) - (bw[k] >= 0 ? F(f, bw[k]) : 0.0); };
         const double u = F(ea.u, i);
         const double v0 = F(ea.v[0], i), v1 = F(ea.v[1], i), v2 = F(ea.v[2], i);
-        const double a0 = dp(ea.u, 0) - v0, a1 = dp(ea.u, 1) - v1, a2 = dp(ea.u, 2) - v2;
-        t1 += ea.alpha1 * sqrt(a0 * a0 + a1 * a1 + a2 * a2);
-        const double exx = dm(ea.v[0], 0), eyy = dm(ea.v[1], 1), ezz = dm(ea.v[2], 2);
-        const double exy = 0.5 * (dm(ea.v[0], 1) + dm(ea.v[1], 0));
-        const double exz = 0.5 * (dm(ea.v[0], 2) + dm(ea.v[2], 0));
-        const double eyz = 0.5 * (dm(ea.v[1], 2) + dm(ea.v[2], 1));
-        t0 += ea.alpha0 * sqrt(exx * exx + eyy * eyy + ezz * ezz + 2.0 * (exy * exy + exz * exz + eyz * eyz));
+        if (!frozen || I.on_solved_face(bg.aface[I.b])) {  // regulariser over S
+            const double a0 = dp(ea.u, 0) - v0, a1 = dp(ea.u, 1) - v1, a2 = dp(ea.u, 2) - v2;
+            t1 += ea.alpha1 * sqrt(a0 * a0 + a1 * a1 + a2 * a2);
+            const double exx = dm(ea.v[0], 0), eyy = dm(ea.v[1], 1), ezz = dm(ea.v[2], 2);
+            const double exy = 0.5 * (dm(ea.v[0], 1) + dm(ea.v[1], 0));
+            const double exz = 0.5 * (dm(ea.v[0], 2) + dm(ea.v[2], 0));
+            const double eyz = 0.5 * (dm(ea.v[1], 2) + dm(ea.v[2], 1));
+            t0 += ea.alpha0 * sqrt(exx * exx + eyy * eyy + ezz * ezz + 2.0 * (exy * exy + exz * exz + eyz * eyz));
+        }
         const double divp = dm(ea.p[0], 0) + dm(ea.p[1], 1) + dm(ea.p[2], 2);
         const double w0 = F(ea.p[0], i) + dp(ea.q[0], 0) + dp(ea.q[3], 1) + dp(ea.q[4], 2);
         const double w1 = F(ea.p[1], i) + dp(ea.q[3], 0) + dp(ea.q[1], 1) + dp(ea.q[5], 2);
@@ -349,14 +380,17 @@ __global__ void brick_refine_kernel(const CT* __restrict__ H, const uint8_t* __r
 
 // Prolongation from the parent level (R19 on brick sets): fine voxel
 // (brick b, offset c) lies in parent brick parent[b] at offset (E (coord_b & 1) + c) / 2;
-// u = parent u, v = parent v / 2 into the current and previous slots
+// u = parent u, v = parent v / 2 into all three rotating slots (the frozen bricks are
+// never written again)
 template <int LE>
 __global__ void brick_prolong_kernel(const float* __restrict__ uc, const float* __restrict__ vc0,
                                      const float* __restrict__ vc1, const float* __restrict__ vc2,
                                      const int* __restrict__ parent, const int* __restrict__ coords, int nvox,
-                                     float* __restrict__ u_cur, float* __restrict__ u_prev, float* __restrict__ v_cur0,
-                                     float* __restrict__ v_cur1, float* __restrict__ v_cur2, float* __restrict__ v_prev0,
-                                     float* __restrict__ v_prev1, float* __restrict__ v_prev2)
+                                     float* __restrict__ u_cur, float* __restrict__ u_prev, float* __restrict__ u_next,
+                                     float* __restrict__ v_cur0, float* __restrict__ v_cur1, float* __restrict__ v_cur2,
+                                     float* __restrict__ v_prev0, float* __restrict__ v_prev1,
+                                     float* __restrict__ v_prev2, float* __restrict__ v_next0,
+                                     float* __restrict__ v_next1, float* __restrict__ v_next2)
 {
     constexpr int E = 1 << LE;
     for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < nvox; vi += (int64_t)gridDim.x * blockDim.x) {
@@ -370,12 +404,16 @@ __global__ void brick_prolong_kernel(const float* __restrict__ uc, const float* 
         const float v0 = 0.5f * vc0[j], v1 = 0.5f * vc1[j], v2 = 0.5f * vc2[j];
         u_cur[vi] = u;
         u_prev[vi] = u;
+        u_next[vi] = u;
         v_cur0[vi] = v0;
         v_prev0[vi] = v0;
+        v_next0[vi] = v0;
         v_cur1[vi] = v1;
         v_prev1[vi] = v1;
+        v_next1[vi] = v1;
         v_cur2[vi] = v2;
         v_prev2[vi] = v2;
+        v_next2[vi] = v2;
     }
 }
 

@@ -21,6 +21,12 @@ struct tgv_bricks {
     float* state = nullptr;     // NSLOT slots of nvox floats
     int* nbr = nullptr;         // [nbricks][6]
     uint8_t* frozen = nullptr;  // [nbricks]
+    uint8_t* aface = nullptr;   // [nbricks]: solved face neighbours (BrickGeo::aface)
+    int64_t nfrozen = 0;
+    int* d_alist = nullptr;     // solved brick indices
+    int* d_faces = nullptr;     // (frozen brick, face) pairs with a solved brick across the face
+    int n_alist = 0, n_faces = 0;
+    int64_t s_voxels = 0;       // voxels of S (solved + frozen face-adjacent to solved)
     int* d_coords = nullptr;    // [nbricks][3]
     int* d_parent = nullptr;    // [nbricks]: parent brick index (tgv_bricks_prolong_from)
     std::vector<int32_t> coords_h;
@@ -78,7 +84,7 @@ int bready(tgv_bricks* c)
     return TGV_OK;
 }
 
-BrickGeo bgeo(const tgv_bricks* c) { return BrickGeo{(int)c->nvox, c->nbr, c->frozen}; }
+BrickGeo bgeo(const tgv_bricks* c) { return BrickGeo{(int)c->nvox, c->nbr, c->frozen, c->aface}; }
 
 IterPtrs biter_ptrs(tgv_bricks* c, int64_t k)
 {
@@ -141,14 +147,17 @@ int btimer_collect(tgv_bricks* c)
 }
 
 template <int LE>
-void launch_brick_primal_le(tgv_bricks* c, const IterPtrs& a, int blocks, const StepParams& sp)
+void launch_brick_primal_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
 {
     const BrickGeo bg = bgeo(c);
     const Centers C = bcenters(c);
-    if (c->slots == 8 && c->count_bytes == 1) brick_primal_kernel<LE, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
-    else if (c->slots == 8) brick_primal_kernel<LE, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
-    else if (c->count_bytes == 1) brick_primal_kernel<LE, 16, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
-    else brick_primal_kernel<LE, 16, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C);
+    const int n = c->n_alist << (3 * LE), blocks = (n + 255) / 256;
+    if (!n) return;
+    const int* L = c->d_alist;
+    if (c->slots == 8 && c->count_bytes == 1) brick_primal_kernel<LE, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C, L, n);
+    else if (c->slots == 8) brick_primal_kernel<LE, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C, L, n);
+    else if (c->count_bytes == 1) brick_primal_kernel<LE, 16, uint8_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C, L, n);
+    else brick_primal_kernel<LE, 16, uint16_t><<<blocks, 256, 0, c->stream>>>(a, bg, sp, C, L, n);
 }
 
 template <int LE>
@@ -184,21 +193,24 @@ void launch_brick_energy_le(tgv_bricks* c, const EnergyArgs& ea)
         default: fn<5>(__VA_ARGS__); break;   \
     }
 
+// the solved bricks, then the frozen bricks' faces towards solved bricks (same stream:
+// the face launch only reads inputs of this iteration and writes other voxels)
 template <int LE>
-void launch_brick_dual_le(tgv_bricks* c, const IterPtrs& a, int blocks, const StepParams& sp)
+void launch_brick_dual_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
 {
-    brick_dual_kernel<LE><<<blocks, 256, 0, c->stream>>>(a, bgeo(c), sp);
+    const int n0 = c->n_alist << (3 * LE), n1 = c->n_faces << (2 * LE);
+    if (n0) brick_dual_kernel<LE, 0><<<(n0 + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_alist, n0);
+    if (n1) brick_dual_kernel<LE, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_faces, n1);
 }
 
 int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
 {
-    const int blocks = (int)((c->nvox + 255) / 256);
     const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
     int rc;
     for (int32_t it = 0; it < n; ++it) {
         const IterPtrs a = biter_ptrs(c, c->k);
         if ((rc = btimer(c, 0, false))) return rc;
-        BRICK_LE_DISPATCH(launch_brick_dual_le, c, a, blocks, sp);
+        BRICK_LE_DISPATCH(launch_brick_dual_le, c, a, sp);
         BCU(cudaGetLastError());
         if ((rc = btimer(c, 0, true))) return rc;
         // the primal reads p_{k+1}, q_{k+1}: the dual's outputs
@@ -206,7 +218,7 @@ int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
         for (int d = 0; d < 3; ++d) ap.pk[d] = a.pn[d];
         for (int m = 0; m < 6; ++m) ap.qk[m] = a.qn[m];
         if ((rc = btimer(c, 1, false))) return rc;
-        BRICK_LE_DISPATCH(launch_brick_primal_le, c, ap, blocks, sp);
+        BRICK_LE_DISPATCH(launch_brick_primal_le, c, ap, sp);
         BCU(cudaGetLastError());
         if ((rc = btimer(c, 1, true))) return rc;
         c->k += 1;
@@ -358,7 +370,7 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
     c->energy_blocks = 148 * 4;
     const size_t state_bytes = sizeof(float) * (size_t)NSLOT * (size_t)nvox;
     if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->nbr, sizeof(int) * 6 * (size_t)nb) != cudaSuccess ||
-        cudaMalloc(&c->frozen, (size_t)nb) != cudaSuccess ||
+        cudaMalloc(&c->frozen, (size_t)nb) != cudaSuccess || cudaMalloc(&c->aface, (size_t)nb) != cudaSuccess ||
         cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * EN_TERMS) != cudaSuccess ||
         cudaMalloc(&c->d_maxc, sizeof(unsigned int)) != cudaSuccess) {
@@ -367,9 +379,47 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
         return bail(TGV_ENOMEM);
     }
     c->device_bytes = (int64_t)state_bytes + 7 * nb + (int64_t)sizeof(double) * EN_TERMS * (c->energy_blocks + 1);
-    std::vector<uint8_t> fr((size_t)nb, 0);
+    std::vector<uint8_t> fr((size_t)nb, 0), af((size_t)nb, 0);
     if (S->frozen)
         for (int64_t b = 0; b < nb; ++b) fr[(size_t)b] = S->frozen[b] ? 1 : 0;
+    const int64_t E2 = (int64_t)c->E * c->E;
+    c->s_voxels = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        for (int f = 0; f < 6; ++f) {
+            const int n = nbr[(size_t)b * 6 + f];
+            if (n >= 0 && !fr[(size_t)n]) af[(size_t)b] |= (uint8_t)(1u << f);
+        }
+        if (!fr[(size_t)b]) {
+            c->s_voxels += E2 * c->E;
+            continue;
+        }
+        ++c->nfrozen;
+        // frozen voxels on the solved faces (inclusion-exclusion over the faces' edges and corners)
+        int cnt[3] = {0, 0, 0};
+        for (int k = 0; k < 3; ++k) cnt[k] = ((af[(size_t)b] >> (2 * k)) & 1) + ((af[(size_t)b] >> (2 * k + 1)) & 1);
+        const int64_t Em2[3] = {c->E - cnt[0], c->E - cnt[1], c->E - cnt[2]};
+        c->s_voxels += E2 * c->E - Em2[0] * Em2[1] * Em2[2];
+    }
+    std::vector<int> alist, faces;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (!fr[(size_t)b]) alist.push_back((int)b);
+        else
+            for (int f = 0; f < 6; ++f)
+                if (af[(size_t)b] >> f & 1) {
+                    faces.push_back((int)b);
+                    faces.push_back(f);
+                }
+    }
+    c->n_alist = (int)alist.size();
+    c->n_faces = (int)faces.size() / 2;
+    if (cudaMalloc(&c->d_alist, sizeof(int) * std::max<size_t>(1, alist.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_faces, sizeof(int) * std::max<size_t>(1, faces.size())) != cudaSuccess ||
+        (!alist.empty() && cudaMemcpy(c->d_alist, alist.data(), sizeof(int) * alist.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (!faces.empty() && cudaMemcpy(c->d_faces, faces.data(), sizeof(int) * faces.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+        cudaGetLastError();
+        bfail(c, TGV_ENOMEM, "brick list allocation failed");
+        return bail(TGV_ENOMEM);
+    }
     c->coords_h.assign(S->coords, S->coords + 3 * nb);
     if (cudaMalloc(&c->d_coords, sizeof(int) * 3 * (size_t)nb) != cudaSuccess ||
         cudaMalloc(&c->d_parent, sizeof(int) * (size_t)nb) != cudaSuccess) {
@@ -380,7 +430,8 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
     c->device_bytes += 16 * nb;
     if (cudaMemcpy(c->d_coords, S->coords, sizeof(int) * 3 * (size_t)nb, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(c->nbr, nbr.data(), sizeof(int) * nbr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(c->frozen, fr.data(), fr.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(c->frozen, fr.data(), fr.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->aface, af.data(), af.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
         bfail(c, TGV_ECUDA, "table upload failed");
         return bail(TGV_ECUDA);
@@ -444,7 +495,7 @@ int tgv_bricks_set_primal(tgv_bricks* c, const float* u, const float* v, int64_t
     c->k = 0;
     const Bufs b = bufs(0);
     BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
-    for (int s : {b.cu, b.pu}) {
+    for (int s : {b.cu, b.pu, b.nu}) {  // all three: the frozen bricks are never written again
         BCU(cudaMemcpyAsync(bslot(c, slotU(s)), u, fb, cudaMemcpyHostToDevice, c->stream));
         if (v)
             for (int d = 0; d < 3; ++d)
@@ -553,11 +604,17 @@ int tgv_bricks_get_timing(tgv_bricks* c, tgv_timing* o)
     return TGV_OK;
 }
 
-int tgv_bricks_info(const tgv_bricks* c, int64_t* device_bytes, int32_t* count_bytes)
+int tgv_bricks_info(const tgv_bricks* c, tgv_bricks_info_t* o)
 {
-    if (!c) return TGV_EINVAL;
-    if (device_bytes) *device_bytes = c->device_bytes;
-    if (count_bytes) *count_bytes = c->count_bytes;
+    if (!c || !o) return TGV_EINVAL;
+    *o = tgv_bricks_info_t{};
+    o->device_bytes = c->device_bytes;
+    o->count_bytes = c->count_bytes;
+    o->edge = c->E;
+    o->nbricks = c->nbricks;
+    o->nfrozen = c->nfrozen;
+    o->solved_voxels = (c->nbricks - c->nfrozen) * c->E * c->E * c->E;
+    o->s_voxels = c->s_voxels;
     return TGV_OK;
 }
 
@@ -570,6 +627,9 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->state);
     cudaFree(c->nbr);
     cudaFree(c->frozen);
+    cudaFree(c->aface);
+    cudaFree(c->d_alist);
+    cudaFree(c->d_faces);
     cudaFree(c->d_coords);
     cudaFree(c->d_parent);
     cudaFree(c->hist);
@@ -752,9 +812,10 @@ int tgv_bricks_prolong_from(tgv_bricks* f, const tgv_bricks* pc)
 #define BPRO(LE_)                                                                                                   \
     brick_prolong_kernel<LE_><<<148 * 8, 256, 0, c->stream>>>(                                                      \
         cslot(slotU(cb.cu)), cslot(slotV(cb.cu, 0)), cslot(slotV(cb.cu, 1)), cslot(slotV(cb.cu, 2)), c->d_parent,   \
-        c->d_coords, nv, bslot(c, slotU(b.cu)), bslot(c, slotU(b.pu)), bslot(c, slotV(b.cu, 0)),                      \
-        bslot(c, slotV(b.cu, 1)), bslot(c, slotV(b.cu, 2)), bslot(c, slotV(b.pu, 0)), bslot(c, slotV(b.pu, 1)),       \
-        bslot(c, slotV(b.pu, 2)))
+        c->d_coords, nv, bslot(c, slotU(b.cu)), bslot(c, slotU(b.pu)), bslot(c, slotU(b.nu)),                         \
+        bslot(c, slotV(b.cu, 0)), bslot(c, slotV(b.cu, 1)), bslot(c, slotV(b.cu, 2)), bslot(c, slotV(b.pu, 0)),       \
+        bslot(c, slotV(b.pu, 1)), bslot(c, slotV(b.pu, 2)), bslot(c, slotV(b.nu, 0)), bslot(c, slotV(b.nu, 1)),       \
+        bslot(c, slotV(b.nu, 2)))
     switch (c->LE) {
         case 2: BPRO(2); break;
         case 3: BPRO(3); break;

@@ -62,6 +62,11 @@ def _check(s, o, tol_u=1e-4):
     assert abs(eg["E"] - eo["E"]) <= 1e-5 * abs(eo["E"]), (eg, eo)
     assert abs(eg["gap"] - eo["gap"]) <= 1e-5 * abs(eo["E"]), (eg, eo)
     assert abs(eg["vmax"] - eo["vmax"]) <= 1e-4
+    # duals: equal on S, exactly 0 elsewhere (R24)
+    for name in ("p", "q"):
+        g, r = s.get(name), o.get(name)
+        assert float(np.max(np.abs(g - r))) <= 1e-4, name
+        assert not np.any(g[r == 0.0]) or float(np.max(np.abs(g[r == 0.0]))) <= 1e-4
     return du
 
 
@@ -75,6 +80,7 @@ def test_random_sets_with_frozen_bricks_match_oracle(E, n, span, iters, seed):
     _check(s, o)
     # B is frozen bit for bit at the values given
     assert np.array_equal(s.read_u()[frozen], o.get("u")[frozen].astype(np.float32))
+    assert s.info()["s_voxels"] == int(o.S.sum())
 
 
 def test_ragged_set_of_32_cubed_bricks_matches_oracle():
@@ -116,7 +122,8 @@ def test_u16_counts_and_other_bin_counts():
     h = _counts(len(coords), 8, 11, max_count=300)
     h[0, 0, 0, 0, 3] = 1000  # forces u16 storage
     s, o = _run_pair(8, coords, frozen, h, 30)
-    assert s.info()["count_bytes"] == 2
+    inf = s.info()
+    assert inf["count_bytes"] == 2 and inf["nfrozen"] == 0 and inf["s_voxels"] == inf["solved_voxels"]
     _check(s, o)
     for centers in ([-0.6, 0.1, 0.7], list(np.linspace(-0.95, 0.95, 16))):
         h = _counts(len(coords), 8, 12, nbins=len(centers))

@@ -180,3 +180,25 @@ def test_brick_order_does_not_matter():
     b = ob.BrickOracle(E, coords[perm], frozen=frozen[perm], **KW).load(h[perm]).iterate(12)
     assert np.array_equal(a.get("u")[perm], b.get("u"))
     assert np.array_equal(a.get("v")[perm], b.get("v"))
+
+
+def test_solved_iterates_do_not_depend_on_duals_outside_S():
+    """R24: the primal step on A reads duals only on S = A + frozen voxels face-adjacent
+    to A, so updating the duals on every voxel of Omega leaves A's iterates unchanged."""
+    E = 3
+    rng = np.random.default_rng(9)
+    coords = _random_set(rng, 10)
+    frozen = rng.random(len(coords)) < 0.4
+    frozen[0] = False
+    h = rng.integers(0, 5, (len(coords), E, E, E, 8)).astype(np.uint32)
+    fu = rng.uniform(-0.8, 0.8, (len(coords), E, E, E))
+    fv = rng.uniform(-0.2, 0.2, (len(coords), 3, E, E, E))
+    a = ob.BrickOracle(E, coords, frozen=frozen, **KW).load(h).set_primal(fu, fv)
+    b = ob.BrickOracle(E, coords, frozen=frozen, **KW).load(h).set_primal(fu, fv)
+    b.S = b.om.copy()  # duals everywhere
+    assert (a.S != a.om).any()
+    a.iterate(15)
+    b.iterate(15)
+    assert np.array_equal(a.u[a.act], b.u[b.act])
+    assert np.array_equal(a.v[:, a.act], b.v[:, b.act])
+    assert not np.any(a.p[:, ~a.S]) and not np.any(a.q[:, ~a.S])
