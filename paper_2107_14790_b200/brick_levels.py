@@ -5,8 +5,8 @@ Host logic only (which bricks exist, which are frozen); every arithmetic step --
 Alg. 1 votes, the refinement flags, the prolongation, the iterations, the energy --
 runs in libtgv.so through include/tgv_bricks.h.
 
-How a level's bricks are chosen (R24): the paper refines its octree where the depth
-samples are (PAPER.md:203-218, §4.1) and solves each level over the cubes that exist
+How a level's bricks are chosen (R25): the paper refines its octree where the depth
+samples are (PAPER.md:208-218, §4.1) and solves each level over the cubes that exist
 (PAPER.md:431-461).  Here:
   * the coarsest level is every brick of its grid, all solved;
   * a level's solved set A is every octant (a finer brick) of the coarser level's
