@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--out-of-core", type=int, default=0, metavar="LEAF_VOXELS",
                     help="NEXT-3: out-of-core coarse-to-fine over z-slab leaves of <= LEAF_VOXELS voxels "
                          "(host-resident counts and levels; a step = the whole solve, --levels levels)")
+    ap.add_argument("--parts", type=int, default=0,
+                    help="C5: solve the finest brick level in this many Morton parts with frozen shells (R26); "
+                         "streamed through one GPU, or shared round-robin by the ranks of a torchrun job")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
@@ -514,6 +517,89 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+def run_brick_parts(a):
+    """NEXT-3 parts (R26, BASELINE configs[4] "streamed out-of-core across 8 B200"): the
+    coarse brick levels are solved on every rank (redundantly, counted once), the finest
+    level in --parts Morton parts with frozen shells, parts r, r + N, ... on rank r.
+    Parts need no exchange, so there is no collective in the solve.  With more parts
+    than ranks each rank streams its parts through its GPU (one part resident at a time,
+    counts in pinned host memory, H2D + D2H of every part inside the timed region).
+    value = solved voxel-iterations of all levels / the slowest rank's step time."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2107_14790_b200.brick_levels import BrickLevels, PartSolver
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = synth.workload(a.workload)
+    iters = a.iters or wl.iters
+    levels = max(2, a.levels if a.levels > 1 else 3)
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
+    cams, depths = cams_of(wl), render_shared(wl, rank, world)
+    bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius,
+                     resident_finest=False, device=local, **kw)
+    mine = list(range(rank, a.parts, world))
+    ps = PartSolver(bl, a.parts, mine=mine, pinned=True)
+    stream = len(ps.mine) > 1  # several parts per GPU: one resident at a time
+    pool = None if stream else {}
+    coarse_solved = sum(int((~bl.frozen[lev]).sum()) for lev in range(1, levels)) * 32 ** 3
+    fine_solved_all = int((~bl.frozen[0]).sum()) * 32 ** 3
+    vox_its = (coarse_solved + fine_solved_all) * iters
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        ps.solve(iters, pool)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        ps.solve(iters, pool)
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / a.steps
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([el], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el_max = float(t[0])
+    pv = ps.part_voxels()
+    h2d = sum(int(ps.sets[p][2].nbytes) for p in ps.mine)
+    d2h = sum(int((~ps.sets[p][1]).sum()) * 32 ** 3 * 4 for p in ps.mine)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " (NEXT-3 brick parts, frozen shells)", "value": vox_its / el_max, "unit": UNIT,
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el_max * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{wl.name}: {wl.description}", "levels": levels, "iters_per_level": iters,
+                       "parts": a.parts, "parts_rank0": mine, "part_voxels_rank0": pv,
+                       "bricks_solved_frozen_finest_first": bl.bricks(),
+                       "step": "coarse levels (every rank), then per owned part: H2D counts (pinned u8), prolong "
+                               "from level 1 (frozen shell), iters, D2H of its solved u",
+                       "parallelism": f"{world} rank(s), parts round-robin, no collective in the solve",
+                       "resident": "one part at a time" if stream else "each rank's part resident"},
+            "e2e": {"value": vox_its / el_max, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "note": "the step itself is host to host (counts H2D, u D2H per part)"},
+            "clocks": clk,
+        }), flush=True)
+    if pool:
+        for s_ in pool.values():
+            s_.close()
+    bl.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_bricks(a):
     """NEXT-3 block-sparse brick sets (BASELINE configs[4], workload C5): the brick
     levels are built once from the GPU votes (brick_levels.BrickLevels); a step is the
@@ -658,6 +744,8 @@ def main():
         run_reference(a)
     elif a.out_of_core:
         run_out_of_core(a)
+    elif a.workload == "C5" and a.parts:
+        run_brick_parts(a)
     elif a.workload == "C5":
         run_bricks(a)
     else:

@@ -8,8 +8,9 @@ product: the two share no code (see oracle/tgv_oracle.c header).
 The arithmetic lives in ``tgv_oracle.c`` (plain fp64 loops, each function
 citing the passage it follows).  This module only compiles it and marshals
 numpy arrays.  Parity status of every function is listed in DESIGN.md §3;
-the 3-D minimum value of the functional is "parity unpinned" beyond the
-long-run / gap checks (no closed form exists).
+the 3-D minimum value of the functional has no closed form and is pinned by an
+independent cone-program optimiser on tiny grids (tests/test_oracle_socp_pin.py)
+and by the restricted gap elsewhere.
 """
 from __future__ import annotations
 

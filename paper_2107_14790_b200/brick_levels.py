@@ -70,8 +70,12 @@ class BrickLevels:
 
     def __init__(self, extent, cams, depths, levels=3, edge=32, grid_origin=(0.0, 0.0, 0.0), voxel_size=1.0,
                  voxel_radius=0.5, min_votes=2, centers=None, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25,
-                 device=0):
+                 device=0, resident_finest=True):
+        """resident_finest=False: the finest level's bricks are chosen (from level 1's
+        flags) but no context is created for it -- PartSolver solves it part by part."""
         kw = dict(centers=centers, lam=lam, alpha0=alpha0, alpha1=alpha1, tau=tau, sigma=sigma, device=device)
+        self.kw = kw
+        self.extent = tuple(int(n) for n in extent)
         self.edge, self.levels = edge, levels
         self.solvers = [None] * levels
         self.coords = [None] * levels
@@ -87,11 +91,15 @@ class BrickLevels:
             B = shell(A, g)
             c = np.concatenate([A, B]).astype(np.int32)
             fr = np.concatenate([np.zeros(len(A), bool), np.ones(len(B), bool)])
-            self._add(lev, c, fr, cams, depths, grid_origin, voxel_size, voxel_radius, kw)
+            self._add(lev, c, fr, cams, depths, grid_origin, voxel_size, voxel_radius, kw,
+                      create=resident_finest or lev > 0)
+        self.vote_args = (cams, depths, grid_origin, voxel_size, voxel_radius)
 
-    def _add(self, lev, coords, frozen, cams, depths, origin, h, r, kw):
-        s = BrickSolver(self.edge, coords, frozen, **kw)
-        s.vote(cams, depths, grid_origin=origin, voxel_size=h * (1 << lev), voxel_radius=r * (1 << lev))
+    def _add(self, lev, coords, frozen, cams, depths, origin, h, r, kw, create=True):
+        s = None
+        if create:
+            s = BrickSolver(self.edge, coords, frozen, **kw)
+            s.vote(cams, depths, grid_origin=origin, voxel_size=h * (1 << lev), voxel_radius=r * (1 << lev))
         self.solvers[lev], self.coords[lev], self.frozen[lev] = s, np.asarray(coords), np.asarray(frozen)
 
     def bricks(self):
@@ -119,3 +127,99 @@ class BrickLevels:
             if s is not None:
                 s.close()
         self.solvers = []
+
+
+# ---------------------------------------------------------------------------
+# Parts of the finest level: the treetop leaves of PAPER.md:370-388 / :446-461.
+# A part is a Morton-contiguous run of the finest level's solved bricks; its frozen
+# shell is the rest of its 26-neighbourhood (other parts' solved bricks included),
+# held at the parent level's values -- the borders of Fig. 9, so parts need no
+# exchange: they can be streamed through one GPU (memory bounded by the part) or
+# spread over several GPUs (R26).
+# ---------------------------------------------------------------------------
+def _spread(v):
+    v = np.asarray(v, np.uint64) & np.uint64(0x1FFFFF)
+    v = (v | v << np.uint64(32)) & np.uint64(0x1F00000000FFFF)
+    v = (v | v << np.uint64(16)) & np.uint64(0x1F0000FF0000FF)
+    v = (v | v << np.uint64(8)) & np.uint64(0x100F00F00F00F00F)
+    v = (v | v << np.uint64(4)) & np.uint64(0x10C30C30C30C30C3)
+    v = (v | v << np.uint64(2)) & np.uint64(0x1249249249249249)
+    return v
+
+
+def morton(coords):
+    c = np.asarray(coords, np.int64)
+    return _spread(c[:, 0]) | _spread(c[:, 1]) << np.uint64(1) | _spread(c[:, 2]) << np.uint64(2)
+
+
+def split_parts(solved, nparts):
+    """Morton-ordered solved bricks cut into nparts contiguous runs of near-equal size."""
+    s = np.asarray(solved, np.int64)
+    s = s[np.argsort(morton(s), kind="stable")]
+    return [_sorted(p) for p in np.array_split(s, nparts) if len(p)]
+
+
+class PartSolver:
+    """The finest level of a BrickLevels solved part by part: out of core (one part's
+    bricks on the GPU at a time, its counts in host memory, voted once per part at
+    set-up) or only the parts `mine` (a rank's share on several GPUs).  The coarser
+    levels stay resident in `levels`."""
+
+    def __init__(self, levels: BrickLevels, nparts, mine=None, pinned=False):
+        self.bl, self.E = levels, levels.edge
+        self.grid = brick_grid(levels.extent, levels.edge, 0)
+        A = levels.coords[0][~levels.frozen[0]]
+        self.parts = split_parts(A, nparts)
+        self.mine = list(range(len(self.parts))) if mine is None else [p for p in mine if p < len(self.parts)]
+        cams, depths, origin, h, r = levels.vote_args
+        self.kw = levels.kw
+        self.sets = {}
+        for p in self.mine:
+            Ap = self.parts[p]
+            Bp = shell(Ap, self.grid)
+            c = np.concatenate([Ap, Bp]).astype(np.int32)
+            fr = np.concatenate([np.zeros(len(Ap), bool), np.ones(len(Bp), bool)])
+            ps = BrickSolver(self.E, c, fr, **self.kw).vote(cams, depths, grid_origin=origin, voxel_size=h,
+                                                            voxel_radius=r)
+            cnt = ps.read_counts()
+            if cnt.max() <= 255:
+                cnt = cnt.astype(np.uint8)
+            ps.close()
+            if pinned:
+                import torch
+                cnt = torch.from_numpy(cnt).pin_memory().numpy()
+            self.sets[p] = (c, fr, cnt)
+
+    def solve(self, iters, pool=None):
+        """Coarse levels (resident), then every owned part: H2D of its counts,
+        prolongation from the next coarser level, iterations, D2H of its solved bricks'
+        u.  pool (dict): keep each part's context between solves (allocation outside
+        the solve).  Returns {part: (coords of its solved bricks, u [n, E, E, E])}."""
+        bl = self.bl
+        top = bl.levels - 1
+        s = bl.solvers[top].reset().iterate(iters)
+        for lev in range(top - 1, 0, -1):
+            f = bl.solvers[lev]
+            f.prolong_from(s)
+            f.iterate(iters)
+            s = f
+        out = {}
+        for p in self.mine:
+            c, fr, cnt = self.sets[p]
+            ps = pool.get(p) if pool is not None else None
+            if ps is None:
+                ps = BrickSolver(self.E, c, fr, **self.kw)
+                if pool is not None:
+                    pool[p] = ps
+            ps.load(cnt).prolong_from(s).iterate(iters)
+            nA = int((~fr).sum())
+            out[p] = (c[:nA], ps.read_u()[:nA])
+            if pool is None:
+                ps.close()
+        return out
+
+    def solved_voxels(self):
+        return sum(len(self.parts[p]) for p in self.mine) * self.E ** 3
+
+    def part_voxels(self):
+        return {p: len(self.sets[p][0]) * self.E ** 3 for p in self.mine}
