@@ -359,7 +359,7 @@ def run_ours(a):
         return run_vote(a, s, wl, rank, world, z0, z1, barrier_fn=(dist.barrier if world > 1 else None))
     if a.workload in GPU_VOTED:  # NEXT-2 on the GPU: the same counts as synth.make_histograms
         s.vote(cams_of(wl), render_shared(wl, rank, world), voxel_radius=wl.voxel_radius)
-        counts = s.read_counts() if (z1 - z0) * ny * nx * 32 <= (16 << 30) else None
+        counts = s.read_counts() if (z1 - z0) * ny * nx * 32 <= (40 << 30) else None
     else:
         counts = synth.make_histograms(a.workload, z0, z1)
         s.load(counts)
