@@ -97,3 +97,49 @@ def test_c3_slab_group_equals_single_context_bitwise():
     assert np.array_equal(grp.read_u(), one.read_u())
     eg, e1 = grp.energy(), one.energy()
     assert abs(eg["E"] - e1["E"]) <= 1e-12 * abs(e1["E"])
+
+
+def test_c5_finest_brick_level_samples_match_oracle_windows():
+    """C5 (BASELINE configs[4]) at full size: the finest brick level of the bench's
+    hierarchy (13 912 solved + 9383 frozen 32^3 bricks, counts from GPU Alg. 1 into the
+    bricks) iterated ITERS times from its vote initialisation; sampled solved bricks are
+    compared with the brick oracle on the window of the brick and its 26 neighbours in
+    the set (the same solved / frozen flags, counts from the oracle's own Alg. 1).  The
+    window's outer faces are 32 voxels from the sample, outside its light cone."""
+    import torch
+    from paper_2107_14790_b200.brick_levels import BrickLevels
+    from paper_2107_14790_b200.bricks import BrickSolver
+    from oracle import bricks as ob
+    if torch.cuda.get_device_properties(0).total_memory < 120e9:
+        pytest.skip("C5's finest level needs about 110 GB of device memory")
+    wl = synth.workload("C5")
+    kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
+    depths = synth.render_depths(wl)
+    cams = _cams(wl)
+    bl = BrickLevels(wl.shape, cams, depths, levels=3, edge=B, resident_finest=False, **kw)
+    coords, frozen = bl.coords[0], bl.frozen[0]
+    bl.close()
+    s = BrickSolver(B, coords, frozen, **kw).vote(cams, depths, voxel_radius=wl.voxel_radius).iterate(ITERS)
+    e = s.energy()
+    assert np.isfinite(e["E"]) and e["gap"] >= -1e-9 * e["E"]
+    index = {tuple(int(t) for t in c): i for i, c in enumerate(coords)}
+    solved = np.nonzero(~frozen)[0]
+    nfrozen_nb = np.array([sum(frozen[index[n]] for n in
+                               [(c[0] + dx, c[1] + dy, c[2] + dz) for dx in (-1, 0, 1) for dy in (-1, 0, 1)
+                                for dz in (-1, 0, 1)] if n in index) for c in coords[solved]])
+    rng = np.random.default_rng(5)
+    samples = [solved[0], solved[int(np.argmax(nfrozen_nb))], solved[len(solved) // 2], rng.choice(solved)]
+    u = s.read_u()
+    s.close()
+    worst = 0.0
+    for b in samples:
+        c = coords[b]
+        win = [index[n] for n in [(c[0] + dx, c[1] + dy, c[2] + dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1)
+                                  for dx in (-1, 0, 1)] if n in index]
+        wc, wf = coords[win], frozen[win]
+        o = ob.BrickOracle(B, wc, wf, **kw).load(ob.vote(wc, B, cams, depths, r=wl.voxel_radius)).iterate(ITERS)
+        k = win.index(b)
+        d = float(np.max(np.abs(u[b].astype(np.float64) - o.get("u")[k])))
+        worst = max(worst, d)
+        assert d <= 1e-4, (tuple(c), d)
+    print(f"C5 finest level: {len(samples)} sampled bricks, max|du| = {worst:.2e}")
