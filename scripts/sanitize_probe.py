@@ -36,4 +36,18 @@ cs = tuple((n + 1) // 2 for n in shape)
 leaf.prolong_slab(np.zeros((6, cs[1], cs[0]), np.float32), np.zeros((3, 6, cs[1], cs[0]), np.float32), 2)
 leaf.iterate(3).close()
 out_of_core.solve(shape, h, C8, levels=2, iters=2, leaf_voxels=70 * 33 * 6)
+# NEXT-3 brick sets: votes, refinement, dual (solved bricks + frozen faces), primal,
+# prolongation, energy, count read-back
+from paper_2107_14790_b200.bricks import BrickSolver  # noqa: E402
+bc = np.array([(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 1), (2, 1, 1)], np.int32)
+bf = np.array([0, 0, 1, 0, 1], bool)
+coarse = BrickSolver(8, np.unique(bc // 2, axis=0)).vote([cam], [np.full((64, 64), 50.0, np.float32)])
+coarse.refine_flags(1)
+coarse.iterate(2)
+fine = BrickSolver(8, bc, bf).vote([cam], [np.full((64, 64), 50.0, np.float32)]).prolong_from(coarse)
+fine.iterate(3)
+fine.energy()
+fine.read_counts()
+fine.close()
+coarse.close()
 print("sanitize probe done")
