@@ -621,6 +621,8 @@ def run_bricks(a):
     t_build = time.perf_counter()
     bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius, **kw)
     t_build = time.perf_counter() - t_build
+    for s_ in bl.solvers:
+        s_.set_schedule(a.schedule)  # FUSED by default (32^3 bricks), SPLIT on request
     vox = bl.voxels()
     infos = [s.info() for s in bl.solvers]
     solved = [i["solved_voxels"] for i in infos]
@@ -652,20 +654,31 @@ def run_bricks(a):
         s.set_timing(False)
     clk = clocks.stop()
     cb = bl.solvers[0].info()["count_bytes"]
-    # algorithmic bytes: dual on S, 17 reads + 9 writes; primal on the
-    # solved voxels, 13 reads + counts + 4 writes
-    dual_b = sum(svox) * 104 * iters
-    primal_b = sum(solved) * (68 + 8 * cb) * iters
+    fused = infos[0]["schedule"] == 0
+    # algorithmic bytes: SPLIT: dual on S, 17 reads + 9 writes; primal on
+    # the solved voxels, 13 reads + counts + 4 writes.  FUSED: the frozen-face dual on
+    # S minus the solved voxels (104 B) and the single sweep over the solved voxels
+    # (17 reads + counts + 13 writes)
+    if fused:
+        dual_b = sum(sv - so for sv, so in zip(svox, solved)) * 104 * iters
+        primal_b = sum(solved) * (120 + 8 * cb) * iters
+    else:
+        dual_b = sum(svox) * 104 * iters
+        primal_b = sum(solved) * (68 + 8 * cb) * iters
     dual_ms = sum(t["dual_ms"] for t in tms) / a.steps
-    primal_ms = sum(t["primal_ms"] for t in tms) / a.steps
+    primal_ms = sum(t["primal_ms"] + t["fused_ms"] for t in tms) / a.steps
     peak, peak_src = measured_peaks()
-    dom, dbytes, dms = ("dual", dual_b, dual_ms) if dual_ms >= primal_ms else ("primal", primal_b, primal_ms)
+    if fused:
+        dom, dbytes, dms = "fused", primal_b, primal_ms
+    else:
+        dom, dbytes, dms = ("dual", dual_b, dual_ms) if dual_ms >= primal_ms else ("primal", primal_b, primal_ms)
     achieved = dbytes / (dms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(a.workload, {}).get(f"brick_{dom}")
-    launches = sum(t["dual_launches"] + t["primal_launches"] + t["energy_launches"] for t in tms) / a.steps \
+    launches = sum(t["dual_launches"] + t["primal_launches"] + t["fused_launches"] + t["energy_launches"]
+                   for t in tms) / a.steps \
         + 2 * levels  # + per level the init / prolongation kernel; + the energy final kernel
 
     # e2e through the public API: H2D of the depth maps and Alg. 1 votes into every
@@ -706,11 +719,13 @@ def run_bricks(a):
                    "l2": "no flush: resident brick state >> 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": f"brick_{dom}", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "bytes_per_voxel": 104 if dom == "dual" else 68 + 8 * cb, "kernel_ms_per_step": dms,
+                     "bytes_per_voxel": {"dual": 104, "primal": 68 + 8 * cb, "fused": 120 + 8 * cb}[dom],
+                     "schedule": "fused" if fused else "split", "kernel_ms_per_step": dms,
                      "schedule_gbs": (dual_b + primal_b) / (ms * 1e-3) / 1e9, "count_bytes": cb,
                      "kernel_share_of_step": (dual_ms + primal_ms) / ms},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches * a.steps)),
-        "kernel_ms": {"dual": dual_ms, "primal": primal_ms,
+        "kernel_ms": {"dual" if not fused else "frozen_face_dual": dual_ms,
+                      "primal" if not fused else "fused": primal_ms,
                       "energy": sum(t["energy_ms"] for t in tms) / a.steps},
         "wall_ms_per_step": wall * 1e3,
     }

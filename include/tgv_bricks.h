@@ -28,9 +28,10 @@
  * Layout of every per-voxel host array: brick-major in the order the bricks were
  * given, inside a brick z, y, x (x fastest): element (b, z, y, x) is at
  * ((b * E + z) * E + y) * E + x.  Conventions (status codes, ownership,
- * poisoning) are those of tgv.h.  One iteration is a dual kernel over S (104 B
- * per voxel) and a primal kernel over A (76 B per voxel with u8 counts, 84 B with
- * u16).
+ * poisoning) are those of tgv.h.  One iteration is a single sweep over the solved
+ * bricks (128 B per voxel with u8 counts) after the duals of the frozen faces, or
+ * (SPLIT, tgv_bricks_set_schedule) a dual kernel over S (104 B per voxel) and a
+ * primal kernel over A (76 B per voxel with u8 counts, 84 B with u16).
  */
 #ifndef TGV_BRICKS_H
 #define TGV_BRICKS_H
@@ -121,7 +122,16 @@ int tgv_bricks_prolong_from(tgv_bricks* fine, const tgv_bricks* coarse);
  * Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
 int tgv_bricks_set_primal(tgv_bricks* ctx, const float* u, const float* v, int64_t n_voxels);
 
-/* Run n >= 0 iterations (a dual kernel then a primal kernel each) and wait.
+/* Iteration schedule (same results bit for bit):
+ *   TGV_SCHEDULE_FUSED (default for E = 32, the only edge it supports): per
+ *     iteration the frozen-face dual launch, then one single-sweep launch over the
+ *     solved bricks, two CTAs per brick (128 B per solved voxel with u8 counts);
+ *   TGV_SCHEDULE_SPLIT (default otherwise): a dual launch over S and a primal
+ *     launch over the solved bricks (180 B per solved voxel).
+ * Errors: TGV_EINVAL (bad value; FUSED with E != 32). */
+int tgv_bricks_set_schedule(tgv_bricks* ctx, int schedule);
+
+/* Run n >= 0 iterations of the context's schedule and wait.
  * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load), TGV_ECUDA. */
 int tgv_bricks_iterate(tgv_bricks* ctx, int32_t n);
 
@@ -141,9 +151,9 @@ int tgv_bricks_read(tgv_bricks* ctx, int field, float* out, int64_t n_voxels);
  * Errors: TGV_EINVAL (NULL), TGV_ESTATE, TGV_ECUDA. */
 int tgv_bricks_energy(tgv_bricks* ctx, double out[6]);
 
-/* Per-kernel device timing with CUDA events on the context's stream (dual_ms,
- * primal_ms, energy_ms and the launch counts of tgv_timing; the other members
- * are 0).  Enabling resets the sums.  Errors: TGV_EINVAL, TGV_ECUDA. */
+/* Per-kernel device timing with CUDA events on the context's stream (dual_ms --
+ * the frozen-face launch included --, primal_ms, fused_ms, energy_ms and the launch
+ * counts of tgv_timing; halo members are 0).  Enabling resets the sums.  Errors: TGV_EINVAL, TGV_ECUDA. */
 int tgv_bricks_set_timing(tgv_bricks* ctx, int enable);
 int tgv_bricks_get_timing(tgv_bricks* ctx, tgv_timing* out);
 
@@ -158,6 +168,8 @@ typedef struct {
     int64_t nbricks, nfrozen;
     int64_t solved_voxels;  /* (nbricks - nfrozen) * E^3                          */
     int64_t s_voxels;       /* |S|                                                */
+    int32_t schedule;       /* TGV_SCHEDULE_FUSED or TGV_SCHEDULE_SPLIT           */
+    int32_t pad;
 } tgv_bricks_info_t;
 int tgv_bricks_info(const tgv_bricks* ctx, tgv_bricks_info_t* out);
 

@@ -17,13 +17,13 @@ from .tgv import _check, lib, tgv_params, tgv_timing
 EXPORTS = ["tgv_bricks_create", "tgv_bricks_load", "tgv_bricks_set_primal", "tgv_bricks_iterate", "tgv_bricks_read",
            "tgv_bricks_energy", "tgv_bricks_set_timing", "tgv_bricks_get_timing", "tgv_bricks_info",
            "tgv_bricks_last_error", "tgv_bricks_destroy", "tgv_bricks_vote_depth_maps", "tgv_bricks_read_counts",
-           "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from"]
+           "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from", "tgv_bricks_set_schedule"]
 
 
 class tgv_bricks_info_t(ctypes.Structure):
     _fields_ = [("device_bytes", ctypes.c_int64), ("count_bytes", ctypes.c_int32), ("edge", ctypes.c_int32),
                 ("nbricks", ctypes.c_int64), ("nfrozen", ctypes.c_int64), ("solved_voxels", ctypes.c_int64),
-                ("s_voxels", ctypes.c_int64)]
+                ("s_voxels", ctypes.c_int64), ("schedule", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class tgv_brickset(ctypes.Structure):
@@ -49,6 +49,7 @@ def _setup():
     lib.tgv_bricks_reset.argtypes = [vp]
     lib.tgv_bricks_refine_flags.argtypes = [vp, i32, vp, i64]
     lib.tgv_bricks_prolong_from.argtypes = [vp, vp]
+    lib.tgv_bricks_set_schedule.argtypes = [vp, ctypes.c_int]
     lib.tgv_bricks_last_error.argtypes = [vp]
     lib.tgv_bricks_last_error.restype = ctypes.c_char_p
     lib.tgv_bricks_destroy.argtypes = [vp]
@@ -156,6 +157,12 @@ class BrickSolver:
         out = np.zeros(6, dtype=np.float64)
         _bcheck(lib.tgv_bricks_energy(self.ctx, out.ctypes.data), self.ctx)
         return {"E": out[0], "alpha1": out[1], "alpha0": out[2], "data": out[3], "gap": out[4], "vmax": out[5]}
+
+    def set_schedule(self, schedule):
+        """"fused" (default for 32^3 bricks) or "split" (or the tgv.SCHEDULE_* value)."""
+        v = {"fused": tgv.SCHEDULE_FUSED, "split": tgv.SCHEDULE_SPLIT}.get(schedule, schedule)
+        _bcheck(lib.tgv_bricks_set_schedule(self.ctx, int(v)), self.ctx)
+        return self
 
     def set_timing(self, enable=True):
         _bcheck(lib.tgv_bricks_set_timing(self.ctx, 1 if enable else 0), self.ctx)

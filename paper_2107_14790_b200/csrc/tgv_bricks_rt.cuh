@@ -9,6 +9,7 @@
 
 #include "../../include/tgv_bricks.h"
 #include "tgv_bricks.cuh"
+#include "tgv_bricks_fused.cuh"
 
 struct tgv_bricks {
     int device = 0;
@@ -24,8 +25,10 @@ struct tgv_bricks {
     uint8_t* aface = nullptr;   // [nbricks]: solved face neighbours (BrickGeo::aface)
     int64_t nfrozen = 0;
     int* d_alist = nullptr;     // solved brick indices
-    int* d_faces = nullptr;     // (frozen brick, face) pairs with a solved brick across the face
-    int n_alist = 0, n_faces = 0;
+    int* d_faces = nullptr;     // (frozen brick, face) pairs with a solved brick across the face: y, z faces first
+    int n_alist = 0, n_faces = 0, n_faces_yz = 0;  // the fused sweep computes the x faces itself
+    int* d_nb27 = nullptr;      // [n_alist][27] neighbourhood of each solved brick (fused schedule)
+    int schedule = TGV_SCHEDULE_SPLIT;
     int64_t s_voxels = 0;       // voxels of S (solved + frozen face-adjacent to solved)
     int* d_coords = nullptr;    // [nbricks][3]
     int* d_parent = nullptr;    // [nbricks]: parent brick index (tgv_bricks_prolong_from)
@@ -44,9 +47,9 @@ struct tgv_bricks {
 
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // pairs
-    std::vector<int> ev_kind;     // 0 dual, 1 primal, 2 energy
-    double t_ms[3]{};
-    int64_t t_n[3]{};
+    std::vector<int> ev_kind;     // 0 dual, 1 primal, 2 energy, 3 fused
+    double t_ms[4]{};
+    int64_t t_n[4]{};
 };
 
 namespace {
@@ -203,8 +206,52 @@ void launch_brick_dual_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp
     if (n1) brick_dual_kernel<LE, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_faces, n1);
 }
 
+template <int SLOTS, typename CT>
+void launch_brick_fused_t(tgv_bricks* c, const BrickFusedArgs& A)
+{
+    auto kern = brick_fused_kernel<5, SLOTS, CT>;
+    static thread_local int configured_dev = -1;  // the attribute is per device
+    if (configured_dev != c->device) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrickFusedSmem));
+        configured_dev = c->device;
+    }
+    kern<<<2 * c->n_alist, dim3(32, BF_WARPS), sizeof(BrickFusedSmem), c->stream>>>(A);
+}
+
+// FUSED schedule: the frozen-face duals, then one single sweep over the solved bricks
+int brick_iterate_fused(tgv_bricks* c, int32_t n)
+{
+    const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
+    int rc;
+    for (int32_t it = 0; it < n; ++it) {
+        const IterPtrs a = biter_ptrs(c, c->k);
+        const int fold_x = (int)env_int("TGV_BRICK_FOLD_X", 1);
+        const int nf = fold_x ? c->n_faces_yz : c->n_faces;
+        if (nf) {  // y and z faces (and x faces unless the fused sweep stores them)
+            const int n1 = nf << (2 * 5);
+            if ((rc = btimer(c, 0, false))) return rc;
+            brick_dual_kernel<5, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_faces, n1);
+            BCU(cudaGetLastError());
+            if ((rc = btimer(c, 0, true))) return rc;
+        }
+        if (c->n_alist) {
+            BrickFusedArgs A{a, sp, bcenters(c), c->d_nb27, c->frozen, c->n_alist, fold_x};
+            if ((rc = btimer(c, 3, false))) return rc;
+            if (c->slots == 8 && c->count_bytes == 1) launch_brick_fused_t<8, uint8_t>(c, A);
+            else if (c->slots == 8) launch_brick_fused_t<8, uint16_t>(c, A);
+            else if (c->count_bytes == 1) launch_brick_fused_t<16, uint8_t>(c, A);
+            else launch_brick_fused_t<16, uint16_t>(c, A);
+            BCU(cudaGetLastError());
+            if ((rc = btimer(c, 3, true))) return rc;
+        }
+        c->k += 1;
+    }
+    return TGV_OK;
+}
+
 int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
 {
+    if (c->schedule == TGV_SCHEDULE_FUSED) return brick_iterate_fused(c, n);
     const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
     int rc;
     for (int32_t it = 0; it < n; ++it) {
@@ -401,14 +448,38 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
         c->s_voxels += E2 * c->E - Em2[0] * Em2[1] * Em2[2];
     }
     std::vector<int> alist, faces;
-    for (int64_t b = 0; b < nb; ++b) {
-        if (!fr[(size_t)b]) alist.push_back((int)b);
-        else
-            for (int f = 0; f < 6; ++f)
+    for (int pass = 0; pass < 2; ++pass) {  // y / z faces, then x faces
+        for (int64_t b = 0; b < nb; ++b) {
+            if (!fr[(size_t)b]) {
+                if (pass == 0) alist.push_back((int)b);
+                continue;
+            }
+            for (int f = pass == 0 ? 2 : 0; f < (pass == 0 ? 6 : 2); ++f)
                 if (af[(size_t)b] >> f & 1) {
                     faces.push_back((int)b);
                     faces.push_back(f);
                 }
+        }
+        if (pass == 0) c->n_faces_yz = (int)faces.size() / 2;
+    }
+    // optional Morton order of the solved bricks (TGV_BRICK_MORTON=1); the result does
+    // not depend on the order (Jacobi sweeps)
+    {
+        auto spread = [](uint64_t v) {
+            v &= 0x1FFFFF;
+            v = (v | v << 32) & 0x1F00000000FFFFull;
+            v = (v | v << 16) & 0x1F0000FF0000FFull;
+            v = (v | v << 8) & 0x100F00F00F00F00Full;
+            v = (v | v << 4) & 0x10C30C30C30C30C3ull;
+            v = (v | v << 2) & 0x1249249249249249ull;
+            return v;
+        };
+        auto mort = [&](int b) {
+            const int32_t* q = S->coords + 3 * (int64_t)b;
+            return spread((uint64_t)q[0]) | spread((uint64_t)q[1]) << 1 | spread((uint64_t)q[2]) << 2;
+        };
+        if (env_int("TGV_BRICK_MORTON", 0))  // measured: brick order (z, y, x) is 3-4 % faster on C5
+            std::stable_sort(alist.begin(), alist.end(), [&](int a1, int a2) { return mort(a1) < mort(a2); });
     }
     c->n_alist = (int)alist.size();
     c->n_faces = (int)faces.size() / 2;
@@ -419,6 +490,33 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
         cudaGetLastError();
         bfail(c, TGV_ENOMEM, "brick list allocation failed");
         return bail(TGV_ENOMEM);
+    }
+    if (c->E == 32) {  // the fused schedule's neighbourhood table (and its default)
+        std::vector<int> nb27((size_t)alist.size() * 27, -1);
+        std::unordered_map<uint64_t, int> at2;
+        at2.reserve((size_t)nb * 2);
+        auto key2 = [](int64_t x, int64_t y, int64_t z) { return (uint64_t)x | (uint64_t)y << 21 | (uint64_t)z << 42; };
+        for (int64_t b = 0; b < nb; ++b) at2.emplace(key2(S->coords[3 * b], S->coords[3 * b + 1], S->coords[3 * b + 2]), (int)b);
+        for (size_t jj = 0; jj < alist.size(); ++jj) {
+            const int32_t* q = S->coords + 3 * (int64_t)alist[jj];
+            for (int dz = -1; dz <= 1; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int64_t X = q[0] + dx, Y = q[1] + dy, Z = q[2] + dz;
+                        if (X < 0 || Y < 0 || Z < 0) continue;
+                        auto it = at2.find(key2(X, Y, Z));
+                        if (it != at2.end()) nb27[jj * 27 + (size_t)((dz + 1) * 9 + (dy + 1) * 3 + dx + 1)] = it->second;
+                    }
+        }
+        if (cudaMalloc(&c->d_nb27, sizeof(int) * std::max<size_t>(1, nb27.size())) != cudaSuccess ||
+            (!nb27.empty() && cudaMemcpy(c->d_nb27, nb27.data(), sizeof(int) * nb27.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+            cudaGetLastError();
+            bfail(c, TGV_ENOMEM, "neighbourhood table allocation failed");
+            return bail(TGV_ENOMEM);
+        }
+        c->device_bytes += (int64_t)sizeof(int) * nb27.size();
+        c->schedule = env_int("TGV_BRICK_SCHEDULE", TGV_SCHEDULE_FUSED) == TGV_SCHEDULE_SPLIT ? TGV_SCHEDULE_SPLIT
+                                                                                              : TGV_SCHEDULE_FUSED;
     }
     c->coords_h.assign(S->coords, S->coords + 3 * nb);
     if (cudaMalloc(&c->d_coords, sizeof(int) * 3 * (size_t)nb) != cudaSuccess ||
@@ -571,6 +669,16 @@ int tgv_bricks_energy(tgv_bricks* c, double out[6])
     return TGV_OK;
 }
 
+int tgv_bricks_set_schedule(tgv_bricks* c, int schedule)
+{
+    int rc = bready(c);
+    if (rc) return rc;
+    if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT) return bfail(c, TGV_EINVAL, "bad schedule %d", schedule);
+    if (schedule == TGV_SCHEDULE_FUSED && c->E != 32) return bfail(c, TGV_EINVAL, "the fused schedule needs E = 32");
+    c->schedule = schedule;
+    return TGV_OK;
+}
+
 int tgv_bricks_set_timing(tgv_bricks* c, int enable)
 {
     int rc = bready(c);
@@ -579,7 +687,7 @@ int tgv_bricks_set_timing(tgv_bricks* c, int enable)
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     c->ev.clear();
     c->ev_kind.clear();
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j < 4; ++j) {
         c->t_ms[j] = 0.0;
         c->t_n[j] = 0;
     }
@@ -598,6 +706,8 @@ int tgv_bricks_get_timing(tgv_bricks* c, tgv_timing* o)
     o->dual_ms = c->t_ms[0];
     o->primal_ms = c->t_ms[1];
     o->energy_ms = c->t_ms[2];
+    o->fused_ms = c->t_ms[3];
+    o->fused_launches = c->t_n[3];
     o->dual_launches = c->t_n[0];
     o->primal_launches = c->t_n[1];
     o->energy_launches = c->t_n[2];
@@ -615,6 +725,7 @@ int tgv_bricks_info(const tgv_bricks* c, tgv_bricks_info_t* o)
     o->nfrozen = c->nfrozen;
     o->solved_voxels = (c->nbricks - c->nfrozen) * c->E * c->E * c->E;
     o->s_voxels = c->s_voxels;
+    o->schedule = c->schedule;
     return TGV_OK;
 }
 
@@ -629,6 +740,7 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->frozen);
     cudaFree(c->aface);
     cudaFree(c->d_alist);
+    cudaFree(c->d_nb27);
     cudaFree(c->d_faces);
     cudaFree(c->d_coords);
     cudaFree(c->d_parent);

@@ -29,6 +29,8 @@ def _rand_set(rng, n, span):
 def _counts(nb, E, seed, nbins=8, max_count=12):
     h = synth.random_histograms((E, E, nb * E), seed, max_count=max_count)  # [nb*E, E, E, 8]
     h = h.reshape(nb, E, E, E, 8)
+    if max_count > 255:
+        h[0, 0, 0, 0, 3] = 1000  # u16 storage
     if nbins != 8:
         rng = np.random.default_rng(seed)
         h = rng.integers(0, max_count, (nb, E, E, E, nbins)).astype(np.uint32)
@@ -172,3 +174,43 @@ def test_error_paths_and_timing():
     s.iterate(3)
     t = s.timing()
     assert t["dual_launches"] == 3 and t["primal_launches"] == 3 and t["dual_ms"] > 0
+
+
+@pytest.mark.parametrize("seed,nbins,big", [(0, 8, False), (1, 8, True), (2, 3, False)])
+def test_fused_schedule_equals_split_bitwise(seed, nbins, big):
+    """The single-sweep brick kernel (FUSED, default for 32^3 bricks) and the SPLIT
+    schedule agree bit for bit on u, v, p, q: random sparse sets with frozen bricks,
+    u8 / u16 counts, 3 bins; and the fused run matches the oracle."""
+    from paper_2107_14790_b200.bricks import BrickSolver
+    rng = np.random.default_rng(seed)
+    coords = _rand_set(rng, 16, 3)
+    frozen = rng.random(len(coords)) < 0.3
+    frozen[0] = False
+    centers = None if nbins == 8 else [-0.6, 0.1, 0.7]
+    h = _counts(len(coords), 32, 40 + seed, nbins=nbins, max_count=300 if big else 12)
+    u0, v0 = _frozen_state(rng, len(coords), 32)
+    runs = {}
+    for sched in ("fused", "split"):
+        s = BrickSolver(32, coords, frozen, centers=centers, **KW).set_schedule(sched).load(h)
+        assert s.info()["schedule"] == (0 if sched == "fused" else 1)
+        ua = np.where(frozen[:, None, None, None], u0, s.read_u()).astype(np.float32)
+        s.set_primal(ua, (v0 * frozen[:, None, None, None, None]).astype(np.float32))
+        s.iterate(7)
+        runs[sched] = {n: s.get(n) for n in ("u", "v", "p", "q")}
+        runs[sched]["E"] = s.energy()["E"]
+        if big:
+            assert s.info()["count_bytes"] == 2
+        s.close()
+    for n in ("u", "v", "p", "q"):
+        assert np.array_equal(runs["fused"][n], runs["split"][n]), n
+    assert runs["fused"]["E"] == runs["split"]["E"]
+
+
+def test_fused_schedule_only_for_32_cubed_bricks():
+    from paper_2107_14790_b200 import tgv
+    from paper_2107_14790_b200.bricks import BrickSolver
+    s = BrickSolver(16, [(0, 0, 0)], **KW)
+    assert s.info()["schedule"] == 1
+    with pytest.raises(tgv.TgvError) as ei:
+        s.set_schedule("fused")
+    assert ei.value.status == tgv.TGV_EINVAL
