@@ -165,7 +165,11 @@ class PartSolver:
     set-up) or only the parts `mine` (a rank's share on several GPUs).  The coarser
     levels stay resident in `levels`."""
 
-    def __init__(self, levels: BrickLevels, nparts, mine=None, pinned=False):
+    def __init__(self, levels: BrickLevels, nparts, mine=None, pinned=False, schedule="split"):
+        """schedule: the parts' iteration schedule.  SPLIT by default: a part's frozen
+        shell is large next to its solved bricks, and on C5's 8 parts the fused sweep
+        measured 7.1 s per solve against SPLIT's 6.3 s."""
+        self.schedule = schedule
         self.bl, self.E = levels, levels.edge
         self.grid = brick_grid(levels.extent, levels.edge, 0)
         A = levels.coords[0][~levels.frozen[0]]
@@ -209,6 +213,8 @@ class PartSolver:
             ps = pool.get(p) if pool is not None else None
             if ps is None:
                 ps = BrickSolver(self.E, c, fr, **self.kw)
+                if self.E == 32 or self.schedule == "split":
+                    ps.set_schedule(self.schedule)
                 if pool is not None:
                     pool[p] = ps
             ps.load(cnt).prolong_from(s).iterate(iters)
