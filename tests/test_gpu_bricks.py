@@ -176,7 +176,7 @@ def test_error_paths_and_timing():
     assert t["dual_launches"] == 3 and t["primal_launches"] == 3 and t["dual_ms"] > 0
 
 
-@pytest.mark.parametrize("seed,nbins,big", [(0, 8, False), (1, 8, True), (2, 3, False)])
+@pytest.mark.parametrize("seed,nbins,big", [(0, 8, False), (1, 8, True), (2, 3, False), (3, 16, False)])
 def test_fused_schedule_equals_split_bitwise(seed, nbins, big):
     """The single-sweep brick kernel (FUSED, default for 32^3 bricks) and the SPLIT
     schedule agree bit for bit on u, v, p, q: random sparse sets with frozen bricks,
@@ -186,7 +186,7 @@ def test_fused_schedule_equals_split_bitwise(seed, nbins, big):
     coords = _rand_set(rng, 16, 3)
     frozen = rng.random(len(coords)) < 0.3
     frozen[0] = False
-    centers = None if nbins == 8 else [-0.6, 0.1, 0.7]
+    centers = {8: None, 3: [-0.6, 0.1, 0.7], 16: list(np.linspace(-0.95, 0.95, 16))}[nbins]
     h = _counts(len(coords), 32, 40 + seed, nbins=nbins, max_count=300 if big else 12)
     u0, v0 = _frozen_state(rng, len(coords), 32)
     runs = {}
@@ -214,3 +214,27 @@ def test_fused_schedule_only_for_32_cubed_bricks():
     with pytest.raises(tgv.TgvError) as ei:
         s.set_schedule("fused")
     assert ei.value.status == tgv.TGV_EINVAL
+
+
+def test_fused_schedule_edge_sets():
+    """A single brick (every neighbour outside Omega), a line of bricks with frozen ends,
+    and a set with no solved brick: FUSED = SPLIT bitwise, frozen values untouched."""
+    from paper_2107_14790_b200.bricks import BrickSolver
+    rng = np.random.default_rng(7)
+    cases = [(np.array([(3, 2, 1)]), np.array([False])),
+             (np.array([(x, 0, 0) for x in range(5)]), np.array([True, False, False, False, True])),
+             (np.array([(0, 0, 0), (0, 1, 0)]), np.array([True, True]))]
+    for coords, frozen in cases:
+        h = _counts(len(coords), 32, 60 + len(coords))
+        u0, v0 = _frozen_state(rng, len(coords), 32)
+        out = {}
+        for sched in ("fused", "split"):
+            s = BrickSolver(32, coords, frozen, **KW).set_schedule(sched).load(h)
+            s.set_primal(np.where(frozen[:, None, None, None], u0, s.read_u()).astype(np.float32),
+                         (v0 * frozen[:, None, None, None, None]).astype(np.float32))
+            s.iterate(5)
+            out[sched] = (s.read_u(), s.get("q"))
+            s.close()
+        assert np.array_equal(out["fused"][0], out["split"][0])
+        assert np.array_equal(out["fused"][1], out["split"][1])
+        assert np.array_equal(out["fused"][0][frozen], u0[frozen].astype(np.float32))
