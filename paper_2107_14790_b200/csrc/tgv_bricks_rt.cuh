@@ -478,8 +478,20 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
             const int32_t* q = S->coords + 3 * (int64_t)b;
             return spread((uint64_t)q[0]) | spread((uint64_t)q[1]) << 1 | spread((uint64_t)q[2]) << 2;
         };
-        if (env_int("TGV_BRICK_MORTON", 0))  // measured: brick order (z, y, x) is 3-4 % faster on C5
+        // TGV_BRICK_ORDER: 0 storage order, 1 Morton (measured 3-4 % slower on C5), 2 (z, 8 x 8 tiles
+        // of (x, y), y, x): a CTA wave covers a compact x-y tile, so y-halo rows are read
+        // while the neighbour brick's own CTAs have them in L2
+        const int64_t order = env_int("TGV_BRICK_ORDER", 0);
+        if (order == 1)
             std::stable_sort(alist.begin(), alist.end(), [&](int a1, int a2) { return mort(a1) < mort(a2); });
+        if (order == 2) {
+            auto key = [&](int b) {
+                const int32_t* q = S->coords + 3 * (int64_t)b;
+                return (uint64_t)q[2] << 44 | (uint64_t)(q[1] >> 3) << 32 | (uint64_t)(q[0] >> 3) << 20 |
+                       (uint64_t)(q[1] & 7) << 10 | (uint64_t)(q[0] & 7);
+            };
+            std::stable_sort(alist.begin(), alist.end(), [&](int a1, int a2) { return key(a1) < key(a2); });
+        }
     }
     c->n_alist = (int)alist.size();
     c->n_faces = (int)faces.size() / 2;

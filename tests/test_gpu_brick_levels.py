@@ -145,3 +145,21 @@ def test_finest_level_in_parts_matches_oracle_parts():
         differs |= not np.array_equal(u, ref[rows])
     assert differs
     bl.close()
+
+
+def test_parts_shared_by_ranks_equal_one_rank():
+    """R26 on several GPUs: rank r solves parts r, r + N, ...; parts need no exchange, so
+    the union of two ranks' shares (emulated in one process on one GPU) is the one-rank
+    solve of all parts, bit for bit."""
+    from paper_2107_14790_b200.brick_levels import BrickLevels, PartSolver
+    wl = synth.workload("C1")
+    depths = synth.render_depths(wl)
+    E, iters = 4, 20
+    bl = BrickLevels((32, 32, 32), cams_of(wl), depths, levels=3, edge=E, **KW)
+    allp = PartSolver(bl, 4).solve(iters)
+    shares = [PartSolver(bl, 4, mine=list(range(r, 4, 2))).solve(iters) for r in range(2)]
+    merged = {**shares[0], **shares[1]}
+    assert sorted(merged) == sorted(allp) == [0, 1, 2, 3]
+    for p in allp:
+        assert np.array_equal(merged[p][0], allp[p][0]) and np.array_equal(merged[p][1], allp[p][1])
+    bl.close()
