@@ -28,14 +28,11 @@ constexpr int BF_TY = 16;            // owned rows per CTA
 constexpr int BF_R = BF_TY + 2;      // rows incl. the y-halo
 constexpr int BF_W = 34;             // exchange-plane width: x = -1 .. 32
 constexpr int BF_WARPS = BF_R + 2;   // + the two x-halo warps
-// compact frozen x-face fields: 0 ubar, 1-3 vbar, 4-6 vbar of the second column (face x = E-1),
-// 7 ubar of the second column (face x = 0), 8 + 9 slot + (0-2 p, 3-8 q) for the two p / q slots
-constexpr int BF_XF = 26;
 
 struct BrickFusedSmem {
     float suv[2][4][BF_R][BF_W];  // ubar, vbar(3) of plane s (parity)
     float sr[2][7][BF_R][BF_W];   // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
-    float xb[3][2][BF_R][8];      // x-face cells (plane mod 3, column): v_k, v_{k-1} at x = -2 / u_k, u_{k-1} at x = E + 1
+    float xb[2][2][BF_R][8];      // x-face cells (plane parity, column): v_k, v_{k-1} at x = -2 / u_k, u_{k-1} at x = E + 1
     int nb[27];
 };
 
@@ -58,11 +55,6 @@ struct BrickFusedArgs {
     const uint8_t* frozen;  // [nbricks]
     int n_alist;
     int fold_x;             // 1: this kernel stores the frozen x-faces' duals (else the face launch does)
-    // compact frozen x-faces (fold_x): per solved brick the face ids of its frozen -x / +x
-    // neighbour's face towards it (or -1), and the face arrays [face][BF_XF][z][y]
-    const int2* xf_ids;
-    float* xfa;
-    int cp, np;             // p / q slot of iteration k and k+1 in the face arrays
 };
 
 template <int LE, int SLOTS, typename CT>
@@ -103,9 +95,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     const bool xface = (role == 3 && xm_fz && halop_row) || (role == 4 && xp_fz && haloq_row);
     const bool needP = role == 0 || role == 1 || halop_row || xface;
     const bool needQ = role == 0 || role == 2 || haloq_row || xface;
-    // a column in a frozen x-neighbour reads (and its face cells write) the compact face
-    // arrays: coalesced over y instead of one 4-B value per 32-B sector
-    const int fid = role == 3 && xm_fz ? __ldg(&A.xf_ids[j].x) : (role == 4 && xp_fz ? __ldg(&A.xf_ids[j].y) : -1);
     auto dcoord = [](int c) { return c < 0 ? -1 : (c >= E ? 1 : 0); };
     auto brick_at = [&](int xx, int yy, int dz) { return nb[(dz + 1) * 9 + (dcoord(yy) + 1) * 3 + dcoord(xx) + 1]; };
     // existence of the neighbours this cell's stencils reach, per brick layer dz = -1, 0, 1
@@ -132,9 +121,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         return bb < 0 ? -1 : bb + (zin << (2 * LE));
     };
     auto bit = [](unsigned m, int s) { return ((m >> (s < 0 ? 0 : (s >= E ? 2 : 1))) & 1u) != 0; };
-    const bool ycomp = fid >= 0 && y >= 0 && y < E;
-    auto cf = [&](int s) { return ycomp && s >= 0 && s < E; };  // plane s of this column is a compact face cell
-    auto cidx = [&](int f, int s) { return ((fid * BF_XF + f) * E + s) * E + y; };
 
     struct U2 {
         float uk, um;
@@ -144,10 +130,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
     auto load_u = [&](int s) {
         U2 o{0.f, 0.f};
-        if (cf(s)) {  // frozen: u_k = u_{k-1} = ubar
-            o.uk = o.um = __ldg(A.xfa + cidx(0, s));
-            return o;
-        }
         const int i = at(s);
         if (i >= 0) {
             o.uk = __ldg(a.uk + i);
@@ -157,19 +139,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
     auto load_x = [&](int s) {
         X o{};
-        if (cf(s)) {
-#pragma unroll
-            for (int k = 0; k < 3; ++k) o.vk[k] = o.vm[k] = __ldg(A.xfa + cidx(1 + k, s));
-            if (needP) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) o.p[k] = __ldg(A.xfa + cidx(8 + 9 * A.cp + k, s));
-            }
-            if (needQ) {
-#pragma unroll
-                for (int m = 0; m < 6; ++m) o.q[m] = __ldg(A.xfa + cidx(11 + 9 * A.cp + m, s));
-            }
-            return o;
-        }
         const int i = (s <= E) ? at(s) : -1;
         if (i >= 0) {
 #pragma unroll
@@ -195,20 +164,9 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
 
     auto xissue = [&](int t) {  // x-face cells: plane t's second column into smem
-        float* d = S.xb[(t + 3) % 3][role - 3][r];
+        float* d = S.xb[t & 1][role - 3][r];
         const int i = at(t);
-        if (cf(t)) {  // frozen second column: k and k-1 equal
-            if (role == 3) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    bf_cp_async4(d + k, A.xfa + cidx(4 + k, t));
-                    bf_cp_async4(d + 3 + k, A.xfa + cidx(4 + k, t));
-                }
-            } else {
-                bf_cp_async4(d, A.xfa + cidx(7, t));
-                bf_cp_async4(d + 1, A.xfa + cidx(7, t));
-            }
-        } else if (i < 0) {
+        if (i < 0) {
 #pragma unroll
             for (int k = 0; k < 6; ++k) d[k] = 0.f;
         } else if (role == 3) {
@@ -223,10 +181,7 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (xface) {  // two planes in flight
-        xissue(-1);
-        xissue(0);
-    }
+    if (xface) xissue(-1);
 
     struct Carry {
         float vb[3];      // vbar(s-1)
@@ -252,16 +207,15 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         // copied one plane ahead with cp.async
         float ux2 = 0.f, vbx2[3] = {0.f, 0.f, 0.f};
         if (xface) {
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // plane s landed, s + 1 may be in flight
-            const float* xv = S.xb[(s + 3) % 3][role - 3][r];
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            const float* xv = S.xb[s & 1][role - 3][r];
             if (role == 3) {  // x = -2: vbar for D-_x
 #pragma unroll
                 for (int k = 0; k < 3; ++k) vbx2[k] = fmaf(2.f, xv[k], -xv[3 + k]);
             } else {  // x = E + 1: ubar for D+_x
                 ux2 = fmaf(2.f, xv[0], -xv[1]);
             }
-            if (s + 2 <= E) xissue(s + 2);
-            else asm volatile("cp.async.commit_group;" ::: "memory");  // keep one group per step
+            if (s + 1 <= E) xissue(s + 1);
         }
         // (a3) over-relaxed iterate at planes s and s+1
         const float ub = fmaf(2.f, u0.uk, -u0.um);
@@ -326,10 +280,11 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
             sr[par][6][r][cc] = qn[5];
         }
         if (xface && s >= 0 && s < E) {  // the frozen x-neighbour's face cell of plane s (in S)
+            const int o = at(s);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) A.xfa[cidx(8 + 9 * A.np + k, s)] = pn[k];
+            for (int k = 0; k < 3; ++k) a.pn[k][o] = pn[k];
 #pragma unroll
-            for (int m = 0; m < 6; ++m) A.xfa[cidx(11 + 9 * A.np + m, s)] = qn[m];
+            for (int m = 0; m < 6; ++m) a.qn[m][o] = qn[m];
         }
         if (role == 0) {
             if (s >= 0 && s < E) {  // p, q of the owned plane s
@@ -381,53 +336,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         u0 = u1;
         u1 = u2;
         x0 = x1;
-    }
-}
-
-// compact frozen x-faces <-> brick storage.  faces: (frozen brick, face f) with f = 0
-// the x = 0 face, f = 1 the x = E - 1 face; one thread per (face, z, y), y fastest.
-template <int LE>
-__global__ void brick_xface_gather_kernel(const IterPtrs a, const int* __restrict__ faces, int nf, float* __restrict__ xfa,
-                                          int cp)
-{
-    constexpr int E = 1 << LE;
-    const int64_t n = (int64_t)nf << (2 * LE);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int fidx = (int)(t >> (2 * LE)), z = (int)(t >> LE) & (E - 1), y = (int)t & (E - 1);
-        const int b = faces[2 * fidx], f = faces[2 * fidx + 1];
-        const int x = f ? E - 1 : 0, x2 = f ? E - 2 : 1;
-        const int i = (((b << LE | z) << LE | y) << LE) | x, i2 = i - x + x2;
-        auto c = [&](int fld) { return ((fidx * BF_XF + fld) * E + z) * E + y; };
-        xfa[c(0)] = fmaf(2.f, a.uk[i], -a.um[i]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) xfa[c(1 + k)] = fmaf(2.f, a.vk[k][i], -a.vm[k][i]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) xfa[c(4 + k)] = f ? fmaf(2.f, a.vk[k][i2], -a.vm[k][i2]) : 0.f;
-        xfa[c(7)] = f ? 0.f : fmaf(2.f, a.uk[i2], -a.um[i2]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) xfa[c(8 + 9 * cp + k)] = a.pk[k][i];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) xfa[c(11 + 9 * cp + m)] = a.qk[m][i];
-    }
-}
-
-template <int LE>
-__global__ void brick_xface_scatter_kernel(const IterPtrs a, const int* __restrict__ faces, int nf,
-                                           const float* __restrict__ xfa, int cp)
-{
-    constexpr int E = 1 << LE;
-    const int64_t n = (int64_t)nf << (2 * LE);
-    float* const* pk = const_cast<float* const*>(a.pk);
-    float* const* qk = const_cast<float* const*>(a.qk);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int fidx = (int)(t >> (2 * LE)), z = (int)(t >> LE) & (E - 1), y = (int)t & (E - 1);
-        const int b = faces[2 * fidx], f = faces[2 * fidx + 1];
-        const int i = (((b << LE | z) << LE | y) << LE) | (f ? E - 1 : 0);
-        auto c = [&](int fld) { return ((fidx * BF_XF + fld) * E + z) * E + y; };
-#pragma unroll
-        for (int k = 0; k < 3; ++k) pk[k][i] = xfa[c(8 + 9 * cp + k)];
-#pragma unroll
-        for (int m = 0; m < 6; ++m) qk[m][i] = xfa[c(11 + 9 * cp + m)];
     }
 }
 

@@ -28,10 +28,6 @@ struct tgv_bricks {
     int* d_faces = nullptr;     // (frozen brick, face) pairs with a solved brick across the face: y, z faces first
     int n_alist = 0, n_faces = 0, n_faces_yz = 0;  // the fused sweep computes the x faces itself
     int* d_nb27 = nullptr;      // [n_alist][27] neighbourhood of each solved brick (fused schedule)
-    int2* d_xf_ids = nullptr;   // [n_alist]: compact face id of the frozen -x / +x neighbour's face, or -1
-    float* xfa = nullptr;       // compact frozen x-faces [n_faces - n_faces_yz][BF_XF][E][E]
-    bool xf_dirty = true;       // brick storage changed: gather the compact faces before the next sweep
-    bool xf_live = false;       // the compact faces hold newer p, q than brick storage: scatter before use
     int schedule = TGV_SCHEDULE_SPLIT;
     int64_t s_voxels = 0;       // voxels of S (solved + frozen face-adjacent to solved)
     int* d_coords = nullptr;    // [nbricks][3]
@@ -227,17 +223,9 @@ int brick_iterate_fused(tgv_bricks* c, int32_t n)
 {
     const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
     int rc;
-    const int nxf = c->n_faces - c->n_faces_yz;
-    const int* d_xfaces = c->d_faces + 2 * c->n_faces_yz;
-    if (n > 0 && c->xfa && c->xf_dirty && env_int("TGV_BRICK_FOLD_X", 1)) {
-        brick_xface_gather_kernel<5><<<148 * 8, 256, 0, c->stream>>>(biter_ptrs(c, c->k), d_xfaces, nxf, c->xfa,
-                                                                      (int)(c->k % 2));
-        BCU(cudaGetLastError());
-        c->xf_dirty = false;
-    }
     for (int32_t it = 0; it < n; ++it) {
         const IterPtrs a = biter_ptrs(c, c->k);
-        const int fold_x = (int)env_int("TGV_BRICK_FOLD_X", 1) && c->xfa;
+        const int fold_x = (int)env_int("TGV_BRICK_FOLD_X", 1);
         const int nf = fold_x ? c->n_faces_yz : c->n_faces;
         if (nf) {  // y and z faces (and x faces unless the fused sweep stores them)
             const int n1 = nf << (2 * 5);
@@ -247,8 +235,7 @@ int brick_iterate_fused(tgv_bricks* c, int32_t n)
             if ((rc = btimer(c, 0, true))) return rc;
         }
         if (c->n_alist) {
-            BrickFusedArgs A{a, sp, bcenters(c), c->d_nb27, c->frozen, c->n_alist, fold_x,
-                             c->d_xf_ids, c->xfa, (int)(c->k % 2), (int)((c->k + 1) % 2)};
+            BrickFusedArgs A{a, sp, bcenters(c), c->d_nb27, c->frozen, c->n_alist, fold_x};
             if ((rc = btimer(c, 3, false))) return rc;
             if (c->slots == 8 && c->count_bytes == 1) launch_brick_fused_t<8, uint8_t>(c, A);
             else if (c->slots == 8) launch_brick_fused_t<8, uint16_t>(c, A);
@@ -258,20 +245,7 @@ int brick_iterate_fused(tgv_bricks* c, int32_t n)
             if ((rc = btimer(c, 3, true))) return rc;
         }
         c->k += 1;
-        if (fold_x && nxf) c->xf_live = true;
     }
-    return TGV_OK;
-}
-
-// the compact x-faces' p, q back into brick storage (before anything reads p, q there)
-int bricks_xface_sync(tgv_bricks* c)
-{
-    if (!c->xf_live) return TGV_OK;
-    const int nxf = c->n_faces - c->n_faces_yz;
-    brick_xface_scatter_kernel<5><<<148 * 8, 256, 0, c->stream>>>(biter_ptrs(c, c->k), c->d_faces + 2 * c->n_faces_yz,
-                                                                   nxf, c->xfa, (int)(c->k % 2));
-    BCU(cudaGetLastError());
-    c->xf_live = false;
     return TGV_OK;
 }
 
@@ -342,8 +316,6 @@ int bricks_finish_counts(tgv_bricks* c, const uint16_t* h16)
 // initial state (R9): zero every slot, then u_0 into the current and previous u
 int bricks_init_state(tgv_bricks* c)
 {
-    c->xf_dirty = true;
-    c->xf_live = false;
     BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
     BRICK_LE_DISPATCH(launch_brick_init_le, c);
     BCU(cudaGetLastError());
@@ -555,28 +527,6 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
             return bail(TGV_ENOMEM);
         }
         c->device_bytes += (int64_t)sizeof(int) * nb27.size();
-        // compact frozen x-faces: the x part of the face list, ids in list order
-        const int nxf = c->n_faces - c->n_faces_yz;
-        if (nxf > 0) {
-            std::unordered_map<int64_t, int> fid;
-            for (int f = 0; f < nxf; ++f) fid.emplace(2 * (int64_t)faces[2 * (c->n_faces_yz + f)] + faces[2 * (c->n_faces_yz + f) + 1], f);
-            std::vector<int2> ids(alist.size(), make_int2(-1, -1));
-            for (size_t jj = 0; jj < alist.size(); ++jj) {
-                const int am = nbr[(size_t)alist[jj] * 6 + 0], ap = nbr[(size_t)alist[jj] * 6 + 1];
-                if (am >= 0 && fr[(size_t)am]) ids[jj].x = fid.at(2 * (int64_t)am + 1);  // its x = E-1 face
-                if (ap >= 0 && fr[(size_t)ap]) ids[jj].y = fid.at(2 * (int64_t)ap + 0);  // its x = 0 face
-            }
-            const size_t nxfa = (size_t)nxf * BF_XF * 32 * 32;
-            if (cudaMalloc(&c->d_xf_ids, sizeof(int2) * ids.size()) != cudaSuccess ||
-                cudaMalloc(&c->xfa, sizeof(float) * nxfa) != cudaSuccess ||
-                cudaMemcpy(c->d_xf_ids, ids.data(), sizeof(int2) * ids.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-                cudaMemset(c->xfa, 0, sizeof(float) * nxfa) != cudaSuccess) {
-                cudaGetLastError();
-                bfail(c, TGV_ENOMEM, "compact x-face allocation failed");
-                return bail(TGV_ENOMEM);
-            }
-            c->device_bytes += (int64_t)(sizeof(int2) * ids.size() + sizeof(float) * nxfa);
-        }
         c->schedule = env_int("TGV_BRICK_SCHEDULE", TGV_SCHEDULE_FUSED) == TGV_SCHEDULE_SPLIT ? TGV_SCHEDULE_SPLIT
                                                                                               : TGV_SCHEDULE_FUSED;
     }
@@ -653,8 +603,6 @@ int tgv_bricks_set_primal(tgv_bricks* c, const float* u, const float* v, int64_t
     if (!c->loaded) return bfail(c, TGV_ESTATE, "set_primal before load");
     const size_t fb = sizeof(float) * (size_t)c->nvox;
     c->k = 0;
-    c->xf_dirty = true;
-    c->xf_live = false;
     const Bufs b = bufs(0);
     BCU(cudaMemsetAsync(c->state, 0, sizeof(float) * (size_t)NSLOT * c->nvox, c->stream));
     for (int s : {b.cu, b.pu, b.nu}) {  // all three: the frozen bricks are never written again
@@ -686,7 +634,6 @@ int tgv_bricks_read(tgv_bricks* c, int f, float* out, int64_t n)
     if (n != c->nvox) return bfail(c, TGV_EINVAL, "n_voxels %lld != %lld", (long long)n, (long long)c->nvox);
     if (f < 0 || f >= TGV_NUM_FIELDS) return bfail(c, TGV_EINVAL, "bad field id %d", f);
     if (!c->loaded) return bfail(c, TGV_ESTATE, "read before load");
-    if (f >= TGV_FIELD_P && (rc = bricks_xface_sync(c))) return rc;
     const Bufs b = bufs(c->k);
     const size_t fb = sizeof(float) * (size_t)c->nvox;
     if (f == TGV_FIELD_UBAR || (f >= TGV_FIELD_VBAR && f < TGV_FIELD_VBAR + 3))
@@ -707,7 +654,6 @@ int tgv_bricks_energy(tgv_bricks* c, double out[6])
     if (rc) return rc;
     if (!out) return bfail(c, TGV_EINVAL, "out is NULL");
     if (!c->loaded) return bfail(c, TGV_ESTATE, "energy before load");
-    if ((rc = bricks_xface_sync(c))) return rc;
     const Bufs b = bufs(c->k);
     EnergyArgs ea{};
     ea.u = bslot(c, slotU(b.cu));
@@ -741,10 +687,6 @@ int tgv_bricks_set_schedule(tgv_bricks* c, int schedule)
     if (rc) return rc;
     if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT) return bfail(c, TGV_EINVAL, "bad schedule %d", schedule);
     if (schedule == TGV_SCHEDULE_FUSED && c->E != 32) return bfail(c, TGV_EINVAL, "the fused schedule needs E = 32");
-    if (schedule != c->schedule) {
-        if ((rc = bricks_xface_sync(c))) return rc;  // brick storage current for SPLIT
-        c->xf_dirty = true;                          // and re-gathered when FUSED resumes
-    }
     c->schedule = schedule;
     return TGV_OK;
 }
@@ -811,8 +753,6 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->aface);
     cudaFree(c->d_alist);
     cudaFree(c->d_nb27);
-    cudaFree(c->d_xf_ids);
-    cudaFree(c->xfa);
     cudaFree(c->d_faces);
     cudaFree(c->d_coords);
     cudaFree(c->d_parent);
@@ -1010,8 +950,6 @@ int tgv_bricks_prolong_from(tgv_bricks* f, const tgv_bricks* pc)
     BCU(cudaGetLastError());
     BCU(cudaStreamSynchronize(c->stream));
     c->k = 0;
-    c->xf_dirty = true;
-    c->xf_live = false;
     return TGV_OK;
 }
 
