@@ -32,7 +32,8 @@ constexpr int BF_WARPS = BF_R + 2;   // + the two x-halo warps
 struct BrickFusedSmem {
     float suv[2][4][BF_R][BF_W];  // ubar, vbar(3) of plane s (parity)
     float sr[2][7][BF_R][BF_W];   // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
-    float xb[2][2][BF_R][8];      // x-face cells (plane parity, column): v_k, v_{k-1} at x = -2 / u_k, u_{k-1} at x = E + 1
+    float xb[3][2][BF_R][8];      // x-face cells (plane mod 3, column): v_k, v_{k-1} at x = -2 / u_k, u_{k-1} at x = E + 1
+    float hr[4][2][32][17];       // x-halo columns' inputs (plane mod 4, column, lane): u_k, u_{k-1}, v_k(3), v_{k-1}(3), p(3), q(6)
     int nb[27];
 };
 
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
     auto load_u = [&](int s) {
         U2 o{0.f, 0.f};
+        if (role >= 3) return o;  // x-halo columns: staged by cp.async (hissue)
         const int i = at(s);
         if (i >= 0) {
             o.uk = __ldg(a.uk + i);
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
     auto load_x = [&](int s) {
         X o{};
+        if (role >= 3) return o;
         const int i = (s <= E) ? at(s) : -1;
         if (i >= 0) {
 #pragma unroll
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
 
     auto xissue = [&](int t) {  // x-face cells: plane t's second column into smem
-        float* d = S.xb[t & 1][role - 3][r];
+        float* d = S.xb[(t + 3) % 3][role - 3][r];
         const int i = at(t);
         if (i < 0) {
 #pragma unroll
@@ -179,9 +182,47 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
             bf_cp_async4(d, a.uk + i + 1);
             bf_cp_async4(d + 1, a.um + i + 1);
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (xface) xissue(-1);
+    // x-halo columns: their inputs are one strided 4-B value per 32-B sector, so they come
+    // by cp.async two planes ahead of use (u one more: ubar at s+1) instead of one plane
+    // ahead in registers.  One commit group per plane; each lane owns its ring row.
+    auto hissue = [&](int t) {
+        float* d = S.hr[(t + 4) & 3][role - 3][lane];
+        const int i = (t <= E + 1) ? at(t) : -1;
+        if (i < 0) {
+#pragma unroll
+            for (int f = 0; f < 17; ++f) d[f] = 0.f;
+        } else {
+            bf_cp_async4(d + 0, a.uk + i);
+            bf_cp_async4(d + 1, a.um + i);
+            if (t <= E) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    bf_cp_async4(d + 2 + k, a.vk[k] + i);
+                    bf_cp_async4(d + 5 + k, a.vm[k] + i);
+                }
+                if (needP) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) bf_cp_async4(d + 8 + k, a.pk[k] + i);
+                }
+                if (needQ) {
+#pragma unroll
+                    for (int m = 0; m < 6; ++m) bf_cp_async4(d + 11 + m, a.qk[m] + i);
+                }
+            }
+        }
+    };
+    // commit groups of the x-halo columns: G(s) = {h(s+3), x(s+2)}, issued at step s; at
+    // step s all but the newest group have landed: h(s), h(s+1), x(s)
+    if (role >= 3) {
+        hissue(-1);
+        hissue(0);
+        if (xface) xissue(-1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        hissue(1);
+        if (xface) xissue(0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
 
     struct Carry {
         float vb[3];      // vbar(s-1)
@@ -203,19 +244,36 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         const HistRaw<SLOTS, CT> h1 = load_h(s + 1);
 
         const bool xl = bit(xl_m, s), yl = bit(yl_m, s), zl = bit(own_ex, s + 1);
+        if (role >= 3) {  // the x-halo columns' current planes from the ring
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            const float* d0 = S.hr[(s + 4) & 3][role - 3][lane];
+            const float* d1 = S.hr[(s + 5) & 3][role - 3][lane];
+            u0.uk = d0[0], u0.um = d0[1], u1.uk = d1[0], u1.um = d1[1];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                x0.vk[k] = d0[2 + k];
+                x0.vm[k] = d0[5 + k];
+                x0.p[k] = d0[8 + k];
+            }
+#pragma unroll
+            for (int m = 0; m < 6; ++m) x0.q[m] = d0[11 + m];
+        }
         // x-face cells: the second column into the frozen brick (same 32-B sectors),
         // copied one plane ahead with cp.async
         float ux2 = 0.f, vbx2[3] = {0.f, 0.f, 0.f};
-        if (xface) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            const float* xv = S.xb[s & 1][role - 3][r];
+        if (xface) {  // landed with G(s-2)
+            const float* xv = S.xb[(s + 3) % 3][role - 3][r];
             if (role == 3) {  // x = -2: vbar for D-_x
 #pragma unroll
                 for (int k = 0; k < 3; ++k) vbx2[k] = fmaf(2.f, xv[k], -xv[3 + k]);
             } else {  // x = E + 1: ubar for D+_x
                 ux2 = fmaf(2.f, xv[0], -xv[1]);
             }
-            if (s + 1 <= E) xissue(s + 1);
+        }
+        if (role >= 3) {  // G(s)
+            hissue(s + 3);
+            if (xface && s + 2 <= E) xissue(s + 2);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
         // (a3) over-relaxed iterate at planes s and s+1
         const float ub = fmaf(2.f, u0.uk, -u0.um);
