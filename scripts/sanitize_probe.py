@@ -50,4 +50,14 @@ fine.energy()
 fine.read_counts()
 fine.close()
 coarse.close()
+# the fused brick sweep (32^3 bricks): frozen x-neighbours on both sides (x-face cells, cp.async rings),
+# a frozen y-neighbour (face launch), a missing z-neighbour
+fc = np.array([(0, 0, 0), (1, 0, 0), (2, 0, 0), (1, 1, 0)], np.int32)
+ff = np.array([1, 0, 1, 1], bool)
+hb = synth.random_histograms((32, 32, 4 * 32), 3).reshape(4, 32, 32, 32, 8)
+fb = BrickSolver(32, fc, ff).load(hb)
+fb.set_primal(np.full((4, 32, 32, 32), 0.25, np.float32), np.full((4, 3, 32, 32, 32), 0.01, np.float32))
+fb.iterate(2)
+fb.energy()
+fb.close()
 print("sanitize probe done")
