@@ -40,8 +40,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None,
-                    help="default: C2 (BASELINE configs[1]) on 1 GPU, C4 (configs[3], 1024^3 z-slabs) on 2/4/8")
+    ap.add_argument("--workload", default="C4",
+                    help="default C4 (BASELINE configs[3]: 1024^3, z-slabs across the ranks) at every N, so the "
+                         "1/2/4/8-GPU lines are one workload; C2 / C3 (configs[1] / [2]) and C5 on request")
     ap.add_argument("--iters", type=int, default=None, help="iterations per step (default: the workload's)")
     ap.add_argument("--schedule", default="fused", choices=["fused", "split"])
     ap.add_argument("--model", default="tgv", choices=["tgv", "tvl1"], help="tvl1: NEXT-4 (Eq. 1)")
@@ -57,10 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--vote", action="store_true", help="NEXT-2: measure GPU Alg. 1 voting instead of the solve")
-    a = ap.parse_args()
-    if a.workload is None:
-        a.workload = "C2" if int(os.environ.get("WORLD_SIZE", a.gpus)) == 1 else "C4"
-    return a
+    ap.add_argument("--no-self-check", action="store_true", help="N > 1: skip the slab-vs-one-context check")
+    return ap.parse_args()
 
 
 # workloads whose inputs are voted on the GPU (bit-identical to the CPU generator,
@@ -331,6 +330,40 @@ def run_out_of_core(a):
     }), flush=True)
 
 
+def slab_self_check(rank, world, local):
+    """N > 1, before the timed region: a small grid (96 x 64 x 16N, C2-like random
+    counts) solved in z-slabs across the N ranks (the bench's own halo mode) and, on
+    every rank, in one context of its own; each rank compares its slab of u, v, p, q
+    bitwise (any decomposition is bitwise the one-GPU iterate).  Returns
+    (all ranks bitwise equal, halo mode, communicator size)."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2107_14790_b200 import Solver
+    from paper_2107_14790_b200.tgv import slab
+    shape = (96, 64, 16 * world)
+    h = synth.random_histograms(shape, 77)
+    c = [-0.875 + 0.25 * b for b in range(8)]
+    z0, z1 = slab(shape[2], rank, world)
+    d = Solver.distributed(shape, c, z0, z1, local).load(np.ascontiguousarray(h[z0:z1])).iterate(23)
+    one = Solver(shape, c, device=local).load(h).iterate(23)
+    ok = True
+    for f in ("u", "v", "p", "q"):
+        a_, b_ = d.get(f), one.get(f)
+        b_ = b_[z0:z1] if f == "u" else b_[:, z0:z1]
+        ok &= bool(np.array_equal(a_, b_))
+    info = d.info()
+    e1, e2 = d.energy(), one.energy()
+    ok &= abs(e1["E"] - e2["E"]) <= 1e-12 * abs(e2["E"])
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    dist.barrier()  # peer mode: no rank frees state a neighbour may still write
+    d.close()
+    one.close()
+    return bool(flag.item()), ("peer" if info.get("peer_halo") else "nccl"), int(info.get("nranks", world))
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -345,6 +378,11 @@ def run_ours(a):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    check = None
+    if world > 1 and not a.no_self_check:
+        ok, mode, nr = slab_self_check(rank, world, local)
+        check = {"slab_bitwise": ok, "halo_mode": mode, "comm_ranks": nr,
+                 "grid": [96, 64, 16 * world], "iters": 23}
     wl = synth.workload(a.workload)
     iters = a.iters or wl.iters
     nx, ny, nz = wl.shape
@@ -459,6 +497,7 @@ def run_ours(a):
         narrow = np.uint8 if cmax <= 255 else (np.uint16 if cmax <= 65535 else np.uint32)
         hc = torch.from_numpy(counts.astype(narrow)).pin_memory()
         hcn = hc.numpy()
+        del counts  # the u32 read-back (34 GB at C4) is not needed any more
         hu = torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory()
         from paper_2107_14790_b200 import tgv
         barrier()
@@ -476,6 +515,28 @@ def run_ours(a):
         e2e = {"value": vox_its / float(el[0]), "unit": UNIT, "h2d_bytes_per_step": int(hcn.nbytes),
                "d2h_bytes_per_step": int(hu.numel() * 4 + 6 * 8), "count_type": str(hcn.dtype),
                "calls": "tgv_load_histograms_coarsened (factor 1), tgv_iterate, tgv_energy, tgv_read_u"}
+        del hc
+        # the north-star loader: tgv_load_histograms with host uint32 counts (4x the bytes)
+        k32 = min(a.steps, 2)
+        h32 = torch.empty(tuple(hcn.shape), dtype=torch.int32).pin_memory()
+        h32n = h32.numpy().view(np.uint32)
+        h32n[...] = hcn
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k32):
+            tgv.tgv_load_histograms(s.ctx, h32n)
+            solve()
+            s.energy()
+            tgv.tgv_read_u(s.ctx, hu)
+        torch.cuda.synchronize()
+        el = torch.tensor([(time.perf_counter() - t0) / k32], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e["u32_loader"] = {"value": vox_its / float(el[0]), "unit": UNIT, "steps": k32,
+                             "h2d_bytes_per_step": int(h32n.nbytes), "d2h_bytes_per_step": int(hu.numel() * 4 + 6 * 8),
+                             "calls": "tgv_load_histograms (uint32), tgv_iterate, tgv_energy, tgv_read_u"}
+        del h32, h32n, hcn
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -506,6 +567,8 @@ def run_ours(a):
                          "schedule_gbs": bytes_per_it * vox_its / (ms_max * 1e-3) / 1e9 / world,
                          "kernel_share_of_step": step_kernel_ms / a.steps / ms},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches_per_step * a.steps)),
+            **({"slab_bitwise": check["slab_bitwise"], "halo_mode": check["halo_mode"],
+                "comm_ranks": check["comm_ranks"], "multi_gpu_check": check} if check else {}),
             "kernel_ms": {**{k: v[0] for k, v in kern.items()},
                           "energy": tm["energy_ms"] / max(1, tm["energy_launches"])},
             "wall_ms_per_step": float(ms_t[1]),
@@ -544,7 +607,7 @@ def run_brick_parts(a):
     bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius,
                      resident_finest=False, device=local, **kw)
     mine = list(range(rank, a.parts, world))
-    ps = PartSolver(bl, a.parts, mine=mine, pinned=True)
+    ps = PartSolver(bl, a.parts, mine=mine, pinned=True, schedule=a.schedule)
     stream = len(ps.mine) > 1  # several parts per GPU: one resident at a time
     pool = None if stream else {}
     coarse_solved = sum(int((~bl.frozen[lev]).sum()) for lev in range(1, levels)) * 32 ** 3
@@ -582,7 +645,7 @@ def run_brick_parts(a):
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el_max * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{wl.name}: {wl.description}", "levels": levels, "iters_per_level": iters,
-                       "parts": a.parts, "parts_rank0": mine, "part_voxels_rank0": pv,
+                       "parts": a.parts, "parts_rank0": mine, "part_voxels_rank0": pv, "schedule": ps.schedule,
                        "bricks_solved_frozen_finest_first": bl.bricks(),
                        "step": "coarse levels (every rank), then per owned part: H2D counts (pinned u8), prolong "
                                "from level 1 (frozen shell), iters, D2H of its solved u",

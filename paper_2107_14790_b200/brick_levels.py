@@ -171,7 +171,12 @@ class PartSolver:
         sweep measured 21.7-22.7 G solved vox-it/s against SPLIT's 13.6-17.5 G on the
         same box."""
         import os
-        self.schedule = schedule or os.environ.get("TGV_PARTS_SCHEDULE", "fused")
+        sched = (schedule or os.environ.get("TGV_PARTS_SCHEDULE") or "fused").strip().lower()
+        if sched not in ("fused", "split"):
+            raise ValueError(f"PartSolver schedule must be 'fused' or 'split', got {sched!r}")
+        if sched == "fused" and levels.edge != 32:
+            sched = "split"  # the fused brick sweep is built for 32^3 bricks only
+        self.schedule = sched
         self.bl, self.E = levels, levels.edge
         self.grid = brick_grid(levels.extent, levels.edge, 0)
         A = levels.coords[0][~levels.frozen[0]]
@@ -215,8 +220,7 @@ class PartSolver:
             ps = pool.get(p) if pool is not None else None
             if ps is None:
                 ps = BrickSolver(self.E, c, fr, **self.kw)
-                if self.E == 32 or self.schedule == "split":
-                    ps.set_schedule(self.schedule)
+                ps.set_schedule(self.schedule)
                 if pool is not None:
                     pool[p] = ps
             ps.load(cnt).prolong_from(s).iterate(iters)

@@ -238,7 +238,7 @@ __global__ void brick_init_kernel(float* __restrict__ u_cur, float* __restrict__
 // (duals are 0 outside S); vmax over A.  Partials in the layout of energy_partial_kernel.
 template <int LE, int SLOTS, typename CT>
 __global__ void __launch_bounds__(256)
-    brick_energy_kernel(const EnergyArgs ea, const BrickGeo bg, Centers C, double* __restrict__ partials)
+    brick_energy_kernel(const EnergyArgs ea, const BrickGeo bg, const EnergyConsts K, double* __restrict__ partials)
 {
     double t1 = 0, t0 = 0, td = 0, dv = 0, vm = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < bg.nvox; v += (int64_t)gridDim.x * blockDim.x) {
@@ -270,18 +270,9 @@ __global__ void __launch_bounds__(256)
             continue;
         }
         const auto h = load_hist<SLOTS, CT>(ea.hist, i);
-        double hb[SLOTS];
-        for (int b = 0; b < SLOTS; ++b) hb[b] = (double)hist_count<SLOTS, CT>(h, b);
-        double dterm = 0.0;
-        for (int b = 0; b < ea.nbins; ++b) dterm += hb[b] * fabs(u - (double)C.c[b]);
-        td += ea.lambda * dterm;
-        double best = INFINITY;
-        for (int j = -1; j <= ea.nbins; ++j) {
-            const double uu = j < 0 ? -1.0 : (j == ea.nbins ? 1.0 : (double)C.c[j]);
-            double s = 0.0;
-            for (int b = 0; b < ea.nbins; ++b) s += hb[b] * fabs(uu - (double)C.c[b]);
-            best = fmin(best, ea.lambda * s - uu * divp);
-        }
+        double data, best;
+        data_box_terms<SLOTS, CT>(h, K, ea.lambda, u, divp, data, best);
+        td += data;
         dv += best - ea.V * (fabs(w0) + fabs(w1) + fabs(w2));
         vm = fmax(vm, fmax(fabs(v0), fmax(fabs(v1), fabs(v2))));
     }

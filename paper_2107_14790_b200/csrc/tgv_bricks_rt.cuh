@@ -180,12 +180,12 @@ template <int LE>
 void launch_brick_energy_le(tgv_bricks* c, const EnergyArgs& ea)
 {
     const BrickGeo bg = bgeo(c);
-    const Centers C = bcenters(c);
+    const EnergyConsts K8 = energy_consts(c->centers, c->nbins, 8), K16 = energy_consts(c->centers, c->nbins, 16);
     const int nb = c->energy_blocks;
-    if (c->slots == 8 && c->count_bytes == 1) brick_energy_kernel<LE, 8, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
-    else if (c->slots == 8) brick_energy_kernel<LE, 8, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
-    else if (c->count_bytes == 1) brick_energy_kernel<LE, 16, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
-    else brick_energy_kernel<LE, 16, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, C, c->partials);
+    if (c->slots == 8 && c->count_bytes == 1) brick_energy_kernel<LE, 8, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, K8, c->partials);
+    else if (c->slots == 8) brick_energy_kernel<LE, 8, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, K8, c->partials);
+    else if (c->count_bytes == 1) brick_energy_kernel<LE, 16, uint8_t><<<nb, 256, 0, c->stream>>>(ea, bg, K16, c->partials);
+    else brick_energy_kernel<LE, 16, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, K16, c->partials);
 }
 
 #define BRICK_LE_DISPATCH(fn, ...)            \

@@ -836,75 +836,164 @@ __device__ __forceinline__ double warp_max(double v)
     return v;
 }
 
+// fp64 constants of the data term and of the box-restricted dual (R14), from the bin
+// centres: padded bins (b >= nbins, whose counts are 0) sit at +1, so every walk below
+// runs over SLOTS bins at compile time with no local arrays
+struct EnergyConsts {
+    double c[16];   // c_b (1.0 beyond nbins)
+    double c1[16];  // c_b + 1
+    double dc[17];  // c_b - c_{b-1} with c_{-1} = -1; dc[16]: 1 - c_15 (unused, the walk ends at the last slot)
+    double end;     // 1 - c_{SLOTS-1} for the template's SLOTS (set per launch)
+};
+
+// count b as an exact double: the count in the low mantissa word of 2^52, minus 2^52
 template <int SLOTS, typename CT>
-__global__ void __launch_bounds__(256)
-    energy_partial_kernel(const EnergyArgs ea, Geo g, Centers C, double* __restrict__ partials)
+__device__ __forceinline__ double hist_count_f64(const HistRaw<SLOTS, CT>& h, int b)
 {
-    const int64_t n = (int64_t)g.nzl * g.ny * g.nx;
-    double t1 = 0, t0 = 0, td = 0, dv = 0, vm = 0;
+    uint32_t lo;
+    if constexpr (sizeof(CT) == 1)
+        lo = __byte_perm(h.w[b >> 2], 0u, (b & 3) | 0x4 << 4 | 0x4 << 8 | 0x4 << 12);
+    else
+        lo = __byte_perm(h.w[b >> 1], 0u, (2 * (b & 1)) | (2 * (b & 1) + 1) << 4 | 0x4 << 8 | 0x4 << 12);
+    return __hiloint2double(0x43300000, (int)lo) - 4503599627370496.0;
+}
+
+template <int SLOTS, typename CT>
+__device__ __forceinline__ uint32_t hist_total(const HistRaw<SLOTS, CT>& h)
+{
+    uint32_t W = 0;
+    if constexpr (sizeof(CT) == 1) {
+#pragma unroll
+        for (int k = 0; k < SLOTS / 4; ++k) W = __dp4a(h.w[k], 0x01010101u, W);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SLOTS / 2; ++k) W += (h.w[k] & 0xffffu) + (h.w[k] >> 16);
+    }
+    return W;
+}
+
+// Per voxel, in fp64 (PAPER.md:153 data term with the R2 histogram form; R14 box dual):
+//   data = lam sum_b h_b |u - c_b|
+//   box  = min_{x in [-1,1]} g(x),  g(x) = lam sum_b h_b |x - c_b| - x divp
+// g is convex and piecewise linear with kinks at the centres, so its minimum over [-1, 1] is
+// at -1, a centre or +1.  One left-to-right walk evaluates g at all of them: g(-1) = lam sum h (c+1)
+// + divp, then g grows by (gap) x (slope) with slope = lam (2 C_b - W) - divp on (c_{b-1}, c_b).
+template <int SLOTS, typename CT>
+__device__ __forceinline__ void data_box_terms(const HistRaw<SLOTS, CT>& h, const EnergyConsts& K, double lam,
+                                               double u, double divp, double& data, double& box)
+{
+    const double W = (double)hist_total<SLOTS, CT>(h);
+    double d = 0.0, G = 0.0, f = 0.0, best = 0.0;
+    double slope = -fma(lam, W, divp);
+    const double l2 = 2.0 * lam;
+#pragma unroll
+    for (int b = 0; b < SLOTS; ++b) {
+        const double hb = hist_count_f64<SLOTS, CT>(h, b);
+        d = fma(hb, fabs(u - K.c[b]), d);
+        G = fma(hb, K.c1[b], G);
+        f = fma(K.dc[b], slope, f);  // g(c_b) - g(-1)
+        best = fmin(best, f);
+        slope = fma(l2, hb, slope);
+    }
+    f = fma(K.end, slope, f);  // g(1) - g(-1)
+    best = fmin(best, f);
+    data = lam * d;
+    box = fma(lam, G, divp) + best;
+}
+
+// Grid of the energy sweep: warp = a 32-voxel x segment of one row, block = 8 consecutive
+// rows of one x tile, item = (x tile, 8-row group, z chunk); each warp marches its chunk in z.
+struct EnergySched {
+    int ntx, nyg, zc, items;
+};
+
+// (a4) dense energy / restricted gap (R14).  HBM-bound: each of the
+// 13 fields and the counts is read once (60 B per voxel with u8 counts); the z-neighbours
+// ride in registers along the march, the x / y neighbours are L1 / L2 hits of the same or
+// the neighbouring warp's rows.  fp64 per-voxel terms, warp shuffles, fixed-order block
+// partials (energy_final_kernel sums them): deterministic.
+template <int SLOTS, typename CT>
+__global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
+    energy_partial_kernel(const EnergyArgs ea, Geo g, const EnergyConsts K, const EnergySched es,
+                          double* __restrict__ partials)
+{
+    double t1 = 0, t0 = 0, td = 0, dv = 0;
+    float vm = 0.f;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int sy = g.px, sz = g.plane;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(v % g.nx);
-        const int64_t r = v / g.nx;
-        const int y = (int)(r % g.ny);
-        const int z = (int)(r / g.ny);
-        const int zg = g.z0 + z;
-        const int i = eoff(g, x, y, z);
-        const bool xl = x < g.nx - 1, yl = y < g.ny - 1, zl = zg < g.nz - 1;
-        const bool xf = x > 0, yf = y > 0, zf = zg > 0;
-        auto F = [&](const float* f, int off) { return (double)f[i + off]; };
-        auto dp = [&](const float* f, bool l, int s) { return l ? F(f, s) - F(f, 0) : 0.0; };
-        auto dm = [&](const float* f, bool l, bool fst, int s) { return (l ? F(f, 0) : 0.0) - (fst ? F(f, -s) : 0.0); };
-        const double u = F(ea.u, 0);
-        const double v0 = F(ea.v[0], 0), v1 = F(ea.v[1], 0), v2 = F(ea.v[2], 0);
-        const double a0 = dp(ea.u, xl, 1) - v0, a1 = dp(ea.u, yl, sy) - v1, a2 = dp(ea.u, zl, sz) - v2;
-        t1 += ea.alpha1 * sqrt(a0 * a0 + a1 * a1 + a2 * a2);
-        const double exx = dm(ea.v[0], xl, xf, 1), eyy = dm(ea.v[1], yl, yf, sy), ezz = dm(ea.v[2], zl, zf, sz);
-        const double exy = 0.5 * (dm(ea.v[0], yl, yf, sy) + dm(ea.v[1], xl, xf, 1));
-        const double exz = 0.5 * (dm(ea.v[0], zl, zf, sz) + dm(ea.v[2], xl, xf, 1));
-        const double eyz = 0.5 * (dm(ea.v[1], zl, zf, sz) + dm(ea.v[2], yl, yf, sy));
-        t0 += ea.alpha0 * sqrt(exx * exx + eyy * eyy + ezz * ezz + 2.0 * (exy * exy + exz * exz + eyz * eyz));
-        const auto h = load_hist<SLOTS, CT>(ea.hist, (int64_t)z * g.plane + (int64_t)y * g.px + x);
-        double hb[SLOTS];
-        for (int b = 0; b < SLOTS; ++b) hb[b] = (double)hist_count<SLOTS, CT>(h, b);
-        double dterm = 0.0;
-        for (int b = 0; b < ea.nbins; ++b) dterm += hb[b] * fabs(u - (double)C.c[b]);
-        td += ea.lambda * dterm;
-        const double divp = dm(ea.p[0], xl, xf, 1) + dm(ea.p[1], yl, yf, sy) + dm(ea.p[2], zl, zf, sz);
-        double best = INFINITY;
-        for (int j = -1; j <= ea.nbins; ++j) {
-            const double uu = j < 0 ? -1.0 : (j == ea.nbins ? 1.0 : (double)C.c[j]);
-            double s = 0.0;
-            for (int b = 0; b < ea.nbins; ++b) s += hb[b] * fabs(uu - (double)C.c[b]);
-            best = fmin(best, ea.lambda * s - uu * divp);
+    for (int it = blockIdx.x; it < es.items; it += gridDim.x) {
+        const int xt = it % es.ntx, r = it / es.ntx;
+        const int x = xt * 32 + lane, y = (r % es.nyg) * 8 + wid;
+        const int za = (r / es.nyg) * es.zc, zb = min(g.nzl, za + es.zc);
+        if (x >= g.nx || y >= g.ny) continue;
+        const bool xl = x < g.nx - 1, yl = y < g.ny - 1, xf = x > 0, yf = y > 0;
+        int i = eoff(g, x, y, za);
+        int64_t hv = (int64_t)za * g.plane + (int64_t)y * g.px + x;
+        auto L = [&](const float* f, int o) { return __ldg(f + o); };
+        // carried along z: v (3) and p_z at z-1; u, q_zz, q_xz, q_yz at z (loaded as z+1)
+        float vm0 = L(ea.v[0], i - sz), vm1 = L(ea.v[1], i - sz), vm2 = L(ea.v[2], i - sz), pzm = L(ea.p[2], i - sz);
+        float uc = L(ea.u, i), qzz = L(ea.q[2], i), qxz = L(ea.q[4], i), qyz = L(ea.q[5], i);
+        for (int z = za; z < zb; ++z, i += sz, hv += g.plane) {
+            const int zg = g.z0 + z;
+            const bool zl = zg < g.nz - 1, zf = zg > 0;
+            // ---- loads: plane z+1 (carried fields), plane z centres and x / y neighbours
+            const float un = L(ea.u, i + sz), qzzn = L(ea.q[2], i + sz), qxzn = L(ea.q[4], i + sz),
+                        qyzn = L(ea.q[5], i + sz);
+            const float v0 = L(ea.v[0], i), v1 = L(ea.v[1], i), v2 = L(ea.v[2], i);
+            const float p0 = L(ea.p[0], i), p1 = L(ea.p[1], i), p2 = L(ea.p[2], i);
+            const float qxx = L(ea.q[0], i), qyy = L(ea.q[1], i), qxy = L(ea.q[3], i);
+            const float ux = L(ea.u, i + 1), uy = L(ea.u, i + sy);
+            const float qxxx = L(ea.q[0], i + 1), qxyx = L(ea.q[3], i + 1), qxzx = L(ea.q[4], i + 1);
+            const float qxyy = L(ea.q[3], i + sy), qyyy = L(ea.q[1], i + sy), qyzy = L(ea.q[5], i + sy);
+            const float v0x = L(ea.v[0], i - 1), v1x = L(ea.v[1], i - 1), v2x = L(ea.v[2], i - 1), p0x = L(ea.p[0], i - 1);
+            const float v0y = L(ea.v[0], i - sy), v1y = L(ea.v[1], i - sy), v2y = L(ea.v[2], i - sy),
+                        p1y = L(ea.p[1], i - sy);
+            const auto h = load_hist<SLOTS, CT>(ea.hist, hv);
+            // ---- fp64 terms (the masks are R6's Neumann D+ / D-)
+            auto dp = [](bool l, float a, float b) { return l ? (double)a - (double)b : 0.0; };
+            auto dm = [](bool l, bool f, float a, float b) { return (l ? (double)a : 0.0) - (f ? (double)b : 0.0); };
+            const double a0 = dp(xl, ux, uc) - v0, a1 = dp(yl, uy, uc) - v1, a2 = dp(zl, un, uc) - v2;
+            t1 = fma(ea.alpha1, sqrt(fma(a0, a0, fma(a1, a1, a2 * a2))), t1);
+            const double exx = dm(xl, xf, v0, v0x), eyy = dm(yl, yf, v1, v1y), ezz = dm(zl, zf, v2, vm2);
+            const double exy = 0.5 * (dm(yl, yf, v0, v0y) + dm(xl, xf, v1, v1x));
+            const double exz = 0.5 * (dm(zl, zf, v0, vm0) + dm(xl, xf, v2, v2x));
+            const double eyz = 0.5 * (dm(zl, zf, v1, vm1) + dm(yl, yf, v2, v2y));
+            const double off = fma(exy, exy, fma(exz, exz, eyz * eyz));
+            t0 = fma(ea.alpha0, sqrt(fma(exx, exx, fma(eyy, eyy, fma(ezz, ezz, 2.0 * off)))), t0);
+            const double divp = dm(xl, xf, p0, p0x) + dm(yl, yf, p1, p1y) + dm(zl, zf, p2, pzm);
+            const double w0 = dp(xl, qxxx, qxx) + dp(yl, qxyy, qxy) + dp(zl, qxzn, qxz);
+            const double w1 = dp(xl, qxyx, qxy) + dp(yl, qyyy, qyy) + dp(zl, qyzn, qyz);
+            const double w2 = dp(xl, qxzx, qxz) + dp(yl, qyzy, qyz) + dp(zl, qzzn, qzz);
+            const double l1 = fabs((double)p0 + w0) + fabs((double)p1 + w1) + fabs((double)p2 + w2);
+            double data, box;
+            data_box_terms<SLOTS, CT>(h, K, ea.lambda, (double)uc, divp, data, box);
+            td += data;
+            dv += box - ea.V * l1;
+            vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
+            // ---- carry
+            vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;
+            uc = un, qzz = qzzn, qxz = qxzn, qyz = qyzn;
         }
-        const double w0 = dp(ea.q[0], xl, 1) + dp(ea.q[3], yl, sy) + dp(ea.q[4], zl, sz);
-        const double w1 = dp(ea.q[3], xl, 1) + dp(ea.q[1], yl, sy) + dp(ea.q[5], zl, sz);
-        const double w2 = dp(ea.q[4], xl, 1) + dp(ea.q[5], yl, sy) + dp(ea.q[2], zl, sz);
-        const double l1 = fabs(F(ea.p[0], 0) + w0) + fabs(F(ea.p[1], 0) + w1) + fabs(F(ea.p[2], 0) + w2);
-        dv += best - ea.V * l1;
-        vm = fmax(vm, fmax(fabs(v0), fmax(fabs(v1), fabs(v2))));
     }
     __shared__ double red[EN_TERMS][8];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double vmd = (double)vm;
     t1 = warp_sum(t1);
     t0 = warp_sum(t0);
     td = warp_sum(td);
     dv = warp_sum(dv);
-    vm = warp_max(vm);
+    vmd = warp_max(vmd);
     if (lane == 0) {
         red[0][wid] = t1;
         red[1][wid] = t0;
         red[2][wid] = td;
         red[3][wid] = dv;
-        red[4][wid] = vm;
+        red[4][wid] = vmd;
     }
     __syncthreads();
     if (threadIdx.x < EN_TERMS) {
         const int k = threadIdx.x;
-        const int nw = blockDim.x >> 5;
         double s = red[k][0];
-        for (int w = 1; w < nw; ++w) s = (k == 4) ? fmax(s, red[k][w]) : s + red[k][w];
+        for (int w = 1; w < 8; ++w) s = (k == 4) ? fmax(s, red[k][w]) : s + red[k][w];
         partials[(int64_t)blockIdx.x * EN_TERMS + k] = s;
     }
 }

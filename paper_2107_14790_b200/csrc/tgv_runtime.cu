@@ -809,10 +809,41 @@ int init_from_hist(tgv_ctx* c)
     return TGV_OK;
 }
 
+// fp64 constants of the energy's data / box-dual walk (tgv_kernels.cuh data_box_terms)
+EnergyConsts energy_consts(const float* centers, int nbins, int slots)
+{
+    EnergyConsts K{};
+    double prev = -1.0;
+    for (int b = 0; b < 16; ++b) {
+        K.c[b] = b < nbins ? (double)centers[b] : 1.0;
+        K.c1[b] = K.c[b] + 1.0;
+        K.dc[b] = K.c[b] - prev;
+        prev = K.c[b];
+    }
+    K.dc[16] = 1.0 - prev;
+    K.end = 1.0 - K.c[slots - 1];
+    return K;
+}
+
+// z-marching items of the energy sweep: about 8 per block, so the last round is short
+EnergySched energy_sched(const Geo& g, int blocks)
+{
+    EnergySched es{};
+    es.ntx = (g.nx + 31) / 32;
+    es.nyg = (g.ny + 7) / 8;
+    const int64_t cols = (int64_t)es.ntx * es.nyg;
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(g.nzl, (8LL * blocks + cols - 1) / cols));
+    es.zc = (int)((g.nzl + nch - 1) / nch);
+    es.items = (int)(cols * ((g.nzl + es.zc - 1) / es.zc));
+    return es;
+}
+
 template <int SLOTS, typename CT>
 void launch_energy_t(tgv_ctx* c, const EnergyArgs& ea)
 {
-    energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, centers(c), c->partials);
+    const EnergySched es = energy_sched(c->g, c->energy_blocks);
+    energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(
+        ea, c->g, energy_consts(c->centers, c->nbins, SLOTS), es, c->partials);
 }
 
 int64_t env_int(const char* name, int64_t dflt)
@@ -1035,7 +1066,7 @@ static int create_impl(const tgv_layout* L, const tgv_params* P, int rank, int n
     }
     const size_t state_bytes = sizeof(float) * (size_t)NSLOT * (size_t)g.fs;
     const size_t hist_bytes = sizeof(uint16_t) * (size_t)c->slots * (size_t)g.nzl * (size_t)g.plane;
-    c->energy_blocks = 148 * 4;
+    c->energy_blocks = 148 * 3;  // energy_partial_kernel: 3 blocks of 256 per SM (<= 85 registers)
     if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->hist16, hist_bytes) != cudaSuccess ||
         cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * 8) != cudaSuccess ||

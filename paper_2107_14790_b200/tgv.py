@@ -134,13 +134,20 @@ def _host_ptr(a, dtype):
     """Pointer + element count of a C-contiguous host buffer (numpy or torch CPU tensor)."""
     try:
         import torch
-        if isinstance(a, torch.Tensor):
-            assert a.device.type == "cpu" and a.is_contiguous(), "host buffer must be a contiguous CPU tensor"
-            assert a.dtype == {np.uint32: torch.uint32, np.float32: torch.float32}[dtype]
-            return a.data_ptr(), a.numel()
     except ImportError:  # pragma: no cover
-        pass
-    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype == dtype, "need a C-contiguous array"
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if a.device.type != "cpu" or not a.is_contiguous():
+            raise ValueError("host buffer must be a contiguous CPU tensor")
+        if a.dtype != {np.uint32: torch.uint32, np.float32: torch.float32}[dtype]:
+            raise TypeError(f"host buffer dtype {a.dtype}, expected {np.dtype(dtype).name}")
+        return a.data_ptr(), a.numel()
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"host buffer must be a numpy array or CPU tensor, got {type(a).__name__}")
+    if a.dtype != dtype:
+        raise TypeError(f"host buffer dtype {a.dtype}, expected {np.dtype(dtype).name}")
+    if not a.flags.c_contiguous:
+        raise ValueError("host buffer must be C-contiguous (no negative or gapped strides)")
     return a.ctypes.data, a.size
 
 
@@ -291,7 +298,8 @@ def tgv_peer_export(ctx) -> bytes:
 
 
 def tgv_peer_import(ctx, side: int, rec: bytes):
-    assert len(rec) == 192
+    if len(rec) != 192:
+        raise ValueError(f"peer record must be 192 bytes, got {len(rec)}")
     _check(lib.tgv_peer_import(ctx, int(side), rec), ctx)
 
 
@@ -302,7 +310,10 @@ def tgv_leaf_rebind(ctx, z_begin: int, z_end: int):
 def tgv_load_histograms_coarsened(ctx, fine_counts, fine_shape, factor: int):
     """fine_counts: C-contiguous uint8 / uint16 / uint32 numpy array."""
     a = fine_counts
-    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype in (np.uint8, np.uint16, np.uint32)
+    if not isinstance(a, np.ndarray) or a.dtype not in (np.uint8, np.uint16, np.uint32):
+        raise TypeError("fine_counts must be a uint8 / uint16 / uint32 numpy array")
+    if not a.flags.c_contiguous:
+        raise ValueError("fine_counts must be C-contiguous")
     nxf, nyf, nzf = fine_shape
     _check(lib.tgv_load_histograms_coarsened(ctx, a.ctypes.data, a.dtype.itemsize, a.size, nxf, nyf, nzf,
                                              int(factor)), ctx)
@@ -313,7 +324,8 @@ def tgv_prolong_slab(ctx, u_c, v_c, cz0: int):
     pu, nu = _host_ptr(u_c, np.float32)
     pv, nv = _host_ptr(v_c, np.float32)
     cnz, cny, cnx = u_c.shape
-    assert nv == 3 * nu
+    if nv != 3 * nu:
+        raise ValueError(f"v_c must hold 3 x {nu} floats, got {nv}")
     _check(lib.tgv_prolong_slab(ctx, pu, pv, cnx, cny, int(cz0), cnz), ctx)
 
 

@@ -53,6 +53,8 @@ def _lib():
                                  ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_void_p]
     lib.synth_vote.argtypes = [ctypes.POINTER(_Cam), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int64,
                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p]
+    lib.synth_vote_box.argtypes = [ctypes.POINTER(_Cam), ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)] + \
+        [ctypes.c_int64] * 6 + [ctypes.c_double, ctypes.c_void_p]
     lib.synth_alg1_bin.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double]
     lib.synth_alg1_bin.restype = ctypes.c_int
     return lib
@@ -307,6 +309,24 @@ def vote(cams, depths, nx, ny, z0, z1, r):
     out = np.empty((z1 - z0, ny, nx, 8), dtype=np.uint32)
     lib.synth_vote(cs, len(cams), ptrs, nx, ny, z0, z1, r, out.ctypes.data)
     return out
+
+
+def vote_box(cams, depths, box, r):
+    """Alg. 1 over the voxel box (x0, x1, y0, y1, z0, z1) -> uint32 [z1-z0, y1-y0, x1-x0, 8]
+    (the full-plane vote cropped to the box)."""
+    x0, x1, y0, y1, z0, z1 = (int(b) for b in box)
+    lib = _lib()
+    cs = _cams_struct(cams)
+    ptrs = (ctypes.c_void_p * len(depths))(*[d.ctypes.data for d in depths])
+    out = np.empty((z1 - z0, y1 - y0, x1 - x0, 8), dtype=np.uint32)
+    lib.synth_vote_box(cs, len(cams), ptrs, x0, x1, y0, y1, z0, z1, r, out.ctypes.data)
+    return out
+
+
+def make_histograms_box(name: str, box) -> np.ndarray:
+    """uint32 counts of the voxel box (x0, x1, y0, y1, z0, z1) of workload `name`."""
+    wl = workload(name)
+    return vote_box(wl.cams, _depths_cached(name), box, wl.voxel_radius)
 
 
 def alg1_bin(depth: float, distance: float, r: float) -> int:

@@ -249,18 +249,21 @@ int synth_alg1_bin(double depth, double distance, double r)
 /* Vote every camera into the 8-bin histograms of the voxels of global planes
  * [z0, z1) of an nx x ny x nz grid.  Voxel (x,y,z) has its centre at the
  * point (x, y, z) and radius r.  counts: [z1-z0][ny][nx][8], zeroed here. */
-int synth_vote(const synth_camera* cams, int ncams, const float* const* depths, int64_t nx, int64_t ny,
-               int64_t z0, int64_t z1, double r, uint32_t* counts)
+/* The box [x0, x1) x [y0, y1) x [z0, z1) of the grid (a window: the same votes as the
+ * full planes, cropped).  counts: [z1-z0][y1-y0][x1-x0][8], zeroed here. */
+int synth_vote_box(const synth_camera* cams, int ncams, const float* const* depths, int64_t x0, int64_t x1,
+                   int64_t y0, int64_t y1, int64_t z0, int64_t z1, double r, uint32_t* counts)
 {
     const int NB = 8;
+    const int64_t nx = x1 - x0, ny = y1 - y0;
     memset(counts, 0, sizeof(uint32_t) * (size_t)((z1 - z0) * ny * nx * NB));
     pyramid* pyr = (pyramid*)calloc((size_t)ncams, sizeof(pyramid));
     for (int c = 0; c < ncams; ++c) pyr_build(&pyr[c], depths[c], cams[c].width, cams[c].height);
 #pragma omp parallel for schedule(dynamic, 1) collapse(2)
     for (int64_t z = z0; z < z1; ++z)
-        for (int64_t y = 0; y < ny; ++y)
-            for (int64_t x = 0; x < nx; ++x) {
-                uint32_t* hv = counts + (((z - z0) * ny + y) * nx + x) * NB;
+        for (int64_t y = y0; y < y1; ++y)
+            for (int64_t x = x0; x < x1; ++x) {
+                uint32_t* hv = counts + (((z - z0) * ny + (y - y0)) * nx + (x - x0)) * NB;
                 for (int c = 0; c < ncams; ++c) {
                     const synth_camera* C = &cams[c];
                     double dwp[3] = {x - C->origin[0], y - C->origin[1], z - C->origin[2]};
@@ -290,5 +293,11 @@ int synth_vote(const synth_camera* cams, int ncams, const float* const* depths, 
     for (int c = 0; c < ncams; ++c) pyr_free(&pyr[c]);
     free(pyr);
     return 0;
+}
+
+int synth_vote(const synth_camera* cams, int ncams, const float* const* depths, int64_t nx, int64_t ny,
+               int64_t z0, int64_t z1, double r, uint32_t* counts)
+{
+    return synth_vote_box(cams, ncams, depths, 0, nx, 0, ny, z0, z1, r, counts);
 }
 

@@ -163,3 +163,29 @@ def test_parts_shared_by_ranks_equal_one_rank():
     for p in allp:
         assert np.array_equal(merged[p][0], allp[p][0]) and np.array_equal(merged[p][1], allp[p][1])
     bl.close()
+
+
+def test_parts_edge32_fused_one_part_bitwise_and_fused_equals_split():
+    """R26 with the bench's 32^3 bricks (the fused brick sweep, large frozen shells, pooled
+    contexts, pinned u8 counts): one part is the in-core finest level bit for bit, and
+    three parts give the same u with the fused sweep and with SPLIT."""
+    from paper_2107_14790_b200.brick_levels import BrickLevels, PartSolver
+    wl = synth.workload("C2")
+    depths = synth.render_depths(wl)
+    iters = 20
+    bl = BrickLevels(wl.shape, cams_of(wl), depths, levels=2, edge=32, voxel_radius=wl.voxel_radius, **KW)
+    ref = bl.solve(iters).read_u()
+    solved = bl.coords[0][~bl.frozen[0]]
+    one = PartSolver(bl, 1, pinned=True, schedule="fused")
+    assert one.schedule == "fused"
+    c1, u1 = one.solve(iters, pool={})[0]
+    assert np.array_equal(c1, solved) and np.array_equal(u1, ref[: len(solved)])
+    fz = PartSolver(bl, 3, pinned=True, schedule="fused").solve(iters, pool={})
+    sp = PartSolver(bl, 3, pinned=True, schedule="split").solve(iters)
+    assert sorted(fz) == sorted(sp) == [0, 1, 2]
+    for p in fz:
+        assert np.array_equal(fz[p][0], sp[p][0])
+        assert np.array_equal(fz[p][1], sp[p][1]), (p, float(np.max(np.abs(fz[p][1] - sp[p][1]))))
+    with pytest.raises(ValueError):
+        PartSolver(bl, 2, schedule="FAST")
+    bl.close()

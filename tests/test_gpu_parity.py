@@ -19,6 +19,8 @@ pytestmark = pytest.mark.gpu
 
 U_TOL = 1e-4
 E_RTOL = 1e-5
+GAP_RTOL = 1e-5  # |gap_gpu - gap_cpu| / |E_cpu|
+VMAX_TOL = 1e-4
 NT = max(1, oracle.max_threads())
 
 
@@ -55,6 +57,11 @@ def assert_parity(o, s, u_tol=U_TOL, e_rtol=E_RTOL):
     assert rel <= e_rtol, f"energy rel diff {rel} (gpu {es['E']}, cpu {eo['E']})"
     for k in ("alpha1", "alpha0", "data"):
         assert abs(es[k] - eo[k]) <= 1e-4 * max(1.0, abs(eo["E"])), k
+    # (a4) the restricted gap E - D_V (R14) and max|v|: the fp32 iterates differ from the fp64
+    # ones by ~1e-7, and every term of D_V is O(1)-Lipschitz in them
+    dgap = abs(es["gap"] - eo["gap"])
+    assert dgap <= GAP_RTOL * max(1.0, abs(eo["E"])), f"gap {es['gap']} vs {eo['gap']}"
+    assert abs(es["vmax"] - eo["vmax"]) <= VMAX_TOL, f"max|v| {es['vmax']} vs {eo['vmax']}"
     return du, rel
 
 
@@ -90,6 +97,50 @@ def test_one_iteration_from_random_state(shape, schedule):
     s.iterate(1)
     for f in ("p", "q", "u", "ubar", "v", "vbar"):
         np.testing.assert_allclose(s.get(f), o.get(f), rtol=0, atol=3e-6, err_msg=f)
+
+
+def random_state(shape, seed, model="tgv"):
+    nx, ny, nz = shape
+    rng = np.random.default_rng(seed)
+    st = {"u": rng.uniform(-1, 1, (nz, ny, nx)), "p": rng.normal(0, 0.7, (3, nz, ny, nx))}
+    if model == "tgv":
+        st.update(v=rng.normal(0, 0.5, (3, nz, ny, nx)), q=rng.normal(0, 1.0, (6, nz, ny, nx)))
+    return {k: a.astype(np.float32) for k, a in st.items()}
+
+
+@pytest.mark.parametrize("model", ["tgv", "tvl1"])
+@pytest.mark.parametrize("shape,nb,scale", [((37, 23, 19), 8, 1), ((64, 16, 5), 8, 1), ((1, 1, 9), 8, 1),
+                                            ((33, 1, 4), 8, 1), ((70, 9, 21), 3, 1), ((29, 14, 12), 16, 1),
+                                            ((40, 33, 17), 8, 100)])
+def test_energy_terms_from_random_state(shape, nb, scale, model):
+    """(a4) tgv_energy on a state both sides hold bit-identically (random u, v, p, q with every
+    boundary face and large ||p + div2 q||_1): E, its three terms, the restricted gap E - D_V
+    (R14, V = 2; TV-L1 V = 0) and max|v| equal the oracle's up to fp64 rounding order.  Counts
+    up to 100x (u16), 3 / 8 / 16 bins with non-uniform centres."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nb * 1000 + nx)
+    if nb == 8:
+        c = oracle.default_centers(8)
+    else:
+        c = np.sort(rng.uniform(-0.97, 0.97, nb)).astype(np.float32).astype(np.float64)
+    h = (rng.integers(0, 6, size=(nz, ny, nx, nb)) * scale).astype(np.uint32)
+    o = oracle.Oracle(shape, centers=c, model=model, **params()).load(h)
+    s = solver_cls()(shape, [float(x) for x in c], **params()).set_model(model).load(h)
+    st = random_state(shape, 40 + nx, model)
+    for k in ("u", "v", "p", "q"):
+        if k in st:
+            s.set(k, st[k])
+            o.set(k, st[k].astype(np.float64))
+    for k in ("u", "v", "p", "q"):
+        if k in st:
+            assert np.array_equal(s.get(k), st[k]), k
+    eo, es = o.energy(), s.energy()
+    scale_e = max(1.0, abs(eo["E"]))
+    for k in ("E", "alpha1", "alpha0", "data", "gap"):
+        assert abs(es[k] - eo[k]) <= 1e-10 * scale_e, (k, es[k], eo[k])
+    assert es["vmax"] == eo["vmax"]
+    # the V term matters here: it moves the gap by far more than the tolerance
+    assert model == "tvl1" or abs(o.energy(V=0.0)["gap"] - eo["gap"]) > 1e3 * 1e-10 * scale_e
 
 
 @pytest.mark.parametrize("schedule", SCHEDULES)
@@ -198,6 +249,18 @@ def test_c2_full_grid_truncated_count():
     s.reset()
     s.iterate(6)
     assert_parity(o, s)
+
+
+def test_c2_full_grid_full_count():
+    """C2 (BASELINE configs[1]) as the bench runs it: the full 256^3 grid at its stated 500
+    iterations, every voxel of u, E, its terms, the restricted gap and max|v| against the
+    oracle solving the same full grid (north-star tolerances)."""
+    wl = synth.workload("C2")
+    h = synth.make_histograms("C2")
+    o, s = pair(wl.shape, h, wl.iters, schedule="fused", **params(wl))
+    du, rel = assert_parity(o, s)
+    eo, es = o.energy(), s.energy()
+    print(f"C2 256^3 x{wl.iters}: max|du| = {du:.3e}, rel dE = {rel:.3e}, gap {es['gap']:.6g} vs {eo['gap']:.6g}")
 
 
 def test_c2_full_count_properties():
