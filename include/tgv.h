@@ -94,9 +94,10 @@ typedef struct {
 
 /* Models.  TGV: Eq. 2, the default.  TVL1: Eq. 1
  * (PAPER.md:135-144), min_u sum alpha1 |grad u| + lambda sum_b h_b |u - c_b|,
- * the same scheme with v = q = 0 (R21); it
- * runs as a dual kernel and a primal kernel (60 B per voxel-iteration with u8
- * counts) and its restricted gap uses V = 0. */
+ * the same scheme with v = q = 0 (R21).  Under
+ * FUSED it runs as one TMA single-sweep kernel per iteration (44 B per
+ * voxel-iteration with u8 counts), under SPLIT as a dual kernel and a primal
+ * kernel (60 B); its restricted gap uses V = 0. */
 #define TGV_MODEL_TGV 0
 #define TGV_MODEL_TVL1 1
 
@@ -139,9 +140,10 @@ int tgv_get_unique_id(uint8_t uid[128]);
  * the neighbours' state and hand-over flags are mapped with CUDA IPC (handles
  * exchanged by an NCCL all-gather) and the fused TGV kernel writes its boundary
  * planes straight into the neighbours' halo planes; if any rank cannot map its
- * neighbours, every rank keeps the NCCL halo exchange.  tgv_destroy is then
- * collective (no rank may free its state while a neighbour's kernel can still
- * write it: synchronise the ranks, e.g. with a barrier, before destroying).
+ * neighbours, every rank keeps the NCCL halo exchange.  tgv_destroy itself makes
+ * no collective call, but in peer mode the ranks must be synchronised before it
+ * (e.g. a barrier after their last tgv_iterate): no rank may free its state while
+ * a neighbour's kernel can still write it.
  * Errors: TGV_EINVAL for any invalid argument (see tgv_params / tgv_layout;
  * also non-contiguous slabs across ranks), TGV_ENOMEM, TGV_ECUDA, TGV_ENCCL.
  * On error *out is NULL. */
@@ -276,8 +278,11 @@ int tgv_prolong_from(tgv_ctx* fine, const tgv_ctx* coarse);
  *   ubar = 2 u+ - u,  vbar = 2 v+ - v
  * where P_a is the Euclidean (Frobenius for q) projection onto the ball of
  * radius a and the prox is the exact weighted median of the histogram-L1
- * term.  Multi-GPU: one-plane halos exchanged by NCCL send/recv each
- * half-step.  Blocks until the device work is done.
+ * term.  Multi-GPU: FUSED exchanges the one-plane halos of its
+ * plan once per iteration by NCCL send/recv, SPLIT before each half-step; in
+ * peer halo mode the fused kernel itself stores its boundary planes into the
+ * neighbours' halo planes (no exchange between iterations).  Blocks until the
+ * device work is done.
  * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load / poisoned), TGV_ECUDA, TGV_ENCCL. */
 int tgv_iterate(tgv_ctx* ctx, int32_t n);
 
@@ -362,8 +367,9 @@ int tgv_get_timing(const tgv_ctx* ctx, tgv_timing* out);
 /* Static facts (pitch, device bytes, algorithmic bytes per voxel per launch). */
 int tgv_info(const tgv_ctx* ctx, tgv_info_t* out);
 
-/* Release everything; NULL-safe.  Not collective (NCCL comm is aborted if a
- * peer failed, destroyed otherwise). */
+/* Release everything; NULL-safe.  Makes no collective call (the NCCL comm is
+ * aborted if a peer failed, destroyed otherwise); in peer halo mode synchronise
+ * the ranks first (see tgv_create). */
 void tgv_destroy(tgv_ctx* ctx);
 
 /* Static string for a status code. */

@@ -617,6 +617,7 @@ int tgv_bricks_set_primal(tgv_bricks* c, const float* u, const float* v, int64_t
 
 int tgv_bricks_iterate(tgv_bricks* c, int32_t n)
 {
+    NvtxRange nv("tgv_bricks_iterate");
     int rc = bready(c);
     if (rc) return rc;
     if (n < 0) return bfail(c, TGV_EINVAL, "n must be >= 0");
@@ -650,6 +651,7 @@ int tgv_bricks_read(tgv_bricks* c, int f, float* out, int64_t n)
 
 int tgv_bricks_energy(tgv_bricks* c, double out[6])
 {
+    NvtxRange nv("tgv_bricks_energy");
     int rc = bready(c);
     if (rc) return rc;
     if (!out) return bfail(c, TGV_EINVAL, "out is NULL");

@@ -22,6 +22,8 @@
 #include <atomic>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a tool (nsys / ncu) attaches
+
 #include "../../include/tgv.h"
 #include "nccl_api.h"
 #include "tgv_fused_tma.cuh"
@@ -30,6 +32,12 @@
 #include "tgv_vote.cuh"
 
 using namespace tgvk;
+
+// NVTX range for one ABI call or phase (nsys timeline: iterate / halo / energy / load)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -654,6 +662,7 @@ struct HaloPlan {
 int halo_exchange(tgv_ctx* c, const HaloPlan& hp)
 {
     if (c->nranks == 1) return TGV_OK;
+    NvtxRange nv("tgv halo exchange (NCCL)");
     const NcclApi* nccl = c->nccl;
     size_t sl = 0;
     int rc = timer_begin(c, T_HALO, &sl);
@@ -1253,6 +1262,7 @@ int tgv_set_border(tgv_ctx* c, int side, const float* u, const float* v, const f
 int tgv_load_histograms_coarsened(tgv_ctx* c, const void* fine_v, int count_bytes, int64_t n_fine, int64_t nxf,
                                   int64_t nyf, int64_t nzf, int factor)
 {
+    NvtxRange nv("tgv_load_histograms_coarsened");
     int rc = check_ready(c);
     if (rc) return rc;
     const Geo& g = c->g;
@@ -1423,6 +1433,7 @@ extern "C" {
 
 int tgv_load_histograms(tgv_ctx* c, const uint32_t* counts, int64_t n_counts)
 {
+    NvtxRange nv("tgv_load_histograms");
     int rc = check_ready(c);
     if (rc) return rc;
     const Geo& g = c->g;
@@ -1651,6 +1662,7 @@ int tgv_read_counts(tgv_ctx* c, uint32_t* out, int64_t n)
 
 int tgv_reset(tgv_ctx* c)
 {
+    NvtxRange nv("tgv_reset");
     int rc = check_ready(c);
     if (rc) return rc;
     if (!c->loaded) return fail(c, TGV_ESTATE, "reset before load");
@@ -1670,6 +1682,7 @@ static bool peer_ready(const tgv_ctx* c)
 
 int tgv_iterate(tgv_ctx* c, int32_t n)
 {
+    NvtxRange nv("tgv_iterate");
     int rc = iterate_enqueue(c, n);
     if (rc) return rc;
     return sync_stream(c);
@@ -1785,7 +1798,11 @@ int tgv_read_field(tgv_ctx* c, int f, float* out, int64_t n)
     return TGV_OK;
 }
 
-int tgv_read_u(tgv_ctx* c, float* u, int64_t n) { return tgv_read_field(c, TGV_FIELD_U, u, n); }
+int tgv_read_u(tgv_ctx* c, float* u, int64_t n)
+{
+    NvtxRange nv("tgv_read_u");
+    return tgv_read_field(c, TGV_FIELD_U, u, n);
+}
 
 int tgv_write_field(tgv_ctx* c, int f, const float* in, int64_t n)
 {
@@ -1854,6 +1871,7 @@ static void energy_out(const double h[EN_TERMS], double out[6])
 
 int tgv_energy(tgv_ctx* c, double out[6])
 {
+    NvtxRange nv("tgv_energy");
     int rc = check_ready(c);
     if (rc) return rc;
     if (!out) return fail(c, TGV_EINVAL, "out is NULL");
@@ -2000,6 +2018,7 @@ int tgv_create_group(const tgv_layout* layouts, const tgv_params* P, int n, cons
 
 int tgv_group_iterate(tgv_ctx* const* m, int n, int32_t iters)
 {
+    NvtxRange nv("tgv_group_iterate");
     int rc = group_check(m, n);
     if (rc) return rc;
     if (iters < 0) return fail(m[0], TGV_EINVAL, "n < 0");

@@ -67,3 +67,13 @@ def test_random_histograms_structure():
     assert h.shape == (6, 7, 8, 8)
     W = h.sum(-1)
     assert (W == 0).any() and ((h[..., 7] == W) & (W > 0)).any()
+
+
+def test_vote_box_is_the_cropped_full_vote():
+    """synth.vote_box (the golden windows of scripts/make_goldens.py) votes exactly the
+    full-plane vote cropped to the box."""
+    full = synth.make_histograms("C1", 3, 29)
+    for box in [(2, 30, 5, 17, 3, 29), (0, 32, 0, 32, 10, 11), (31, 32, 0, 1, 3, 29)]:
+        x0, x1, y0, y1, z0, z1 = box
+        got = synth.make_histograms_box("C1", box)
+        assert np.array_equal(got, full[z0 - 3:z1 - 3, y0:y1, x0:x1])
