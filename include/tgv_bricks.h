@@ -68,6 +68,26 @@ typedef struct {
  * tgv_last_error(NULL) when *out could not be created. */
 int tgv_bricks_create(const tgv_brickset* set, const tgv_params* params, int cuda_device, tgv_bricks** out);
 
+/* NEXT-3 2:1 mixed-level set (reading R27; "each cube has
+ * only 4 or less neighbors over each face", PAPER.md:446-453 frozen parent cubes).
+ *   levels  uint8 [nbricks], 0 = finest, <= 7; brick b's voxels have edge h = 2^levels[b]
+ *           in finest-level units and coords[b] is in its own level's brick units, so its
+ *           voxel (x, y, z) is the cube h (E coords[b] + (x, y, z)) + [0, h)^3; copied.
+ * The bricks must be disjoint and 2:1 balanced (face-adjacent bricks at most one level
+ * apart; a coarser brick's face may be covered by up to four finer bricks, one per
+ * quadrant, or partly by none).  Operators (R27): D+_k u(i) = (mean of u over the
+ * voxels across i's +k face - u(i)) / ((h_i + h_n) / 2), 0 without a neighbour;
+ * D-_k = -(D+_k)^* in the cell-volume-weighted inner product; every term of the energy
+ * and of the restricted gap is weighted by h^3.  A one-level set (all levels equal 0) is
+ * tgv_bricks_create's set bit for bit.  Mixed sets run the SPLIT schedule (FUSED is
+ * EINVAL); tgv_bricks_vote_depth_maps votes brick b at voxel size voxel_size 2^l and
+ * radius voxel_radius 2^l; tgv_bricks_prolong_from accepts levels 0 and 1 (a level-1
+ * brick copies the coarse brick at its own coordinates: u, v / 2).  Everything else as
+ * tgv_bricks_create.  Errors: TGV_EINVAL (also NULL levels, a level > 7, overlapping or
+ * unbalanced bricks), TGV_ENOMEM, TGV_ECUDA. */
+int tgv_bricks_create_mixed(const tgv_brickset* set, const uint8_t* levels, const tgv_params* params, int cuda_device,
+                            tgv_bricks** out);
+
 /* Load the histograms and initialise (R9): counts [nbricks][E^3][nbins]
  * of unsigned integers of count_bytes bytes (1, 2 or 4), host memory; frozen
  * bricks' entries are ignored.  On A: u = ubar = vote-weighted mean of the bin

@@ -17,7 +17,8 @@ from .tgv import _check, lib, tgv_params, tgv_timing
 EXPORTS = ["tgv_bricks_create", "tgv_bricks_load", "tgv_bricks_set_primal", "tgv_bricks_iterate", "tgv_bricks_read",
            "tgv_bricks_energy", "tgv_bricks_set_timing", "tgv_bricks_get_timing", "tgv_bricks_info",
            "tgv_bricks_last_error", "tgv_bricks_destroy", "tgv_bricks_vote_depth_maps", "tgv_bricks_read_counts",
-           "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from", "tgv_bricks_set_schedule"]
+           "tgv_bricks_reset", "tgv_bricks_refine_flags", "tgv_bricks_prolong_from", "tgv_bricks_set_schedule",
+           "tgv_bricks_create_mixed"]
 
 
 class tgv_bricks_info_t(ctypes.Structure):
@@ -35,6 +36,8 @@ def _setup():
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
     lib.tgv_bricks_create.argtypes = [ctypes.POINTER(tgv_brickset), ctypes.POINTER(tgv_params), ctypes.c_int,
                                       ctypes.POINTER(vp)]
+    lib.tgv_bricks_create_mixed.argtypes = [ctypes.POINTER(tgv_brickset), vp, ctypes.POINTER(tgv_params), ctypes.c_int,
+                                            ctypes.POINTER(vp)]
     lib.tgv_bricks_load.argtypes = [vp, vp, ctypes.c_int, i64]
     lib.tgv_bricks_set_primal.argtypes = [vp, vp, vp, i64]
     lib.tgv_bricks_iterate.argtypes = [vp, i32]
@@ -71,7 +74,9 @@ class BrickSolver:
     """One block-sparse level on one GPU (include/tgv_bricks.h)."""
 
     def __init__(self, edge, coords, frozen=None, centers=None, lam=0.5, alpha0=2.0, alpha1=1.0, tau=0.25, sigma=0.25,
-                 device=0):
+                 device=0, levels=None):
+        """levels: per-brick level of a 2:1 mixed-level set (tgv_bricks_create_mixed, R27),
+        coordinates in each brick's own level units; None = a one-level set."""
         coords = np.ascontiguousarray(np.asarray(coords, dtype=np.int32).reshape(-1, 3))
         self.E, self.nbricks = int(edge), len(coords)
         self.nvox = self.nbricks * self.E ** 3
@@ -81,9 +86,16 @@ class BrickSolver:
         cc = (ctypes.c_float * len(centers))(*centers)
         P = tgv_params(len(centers), ctypes.cast(cc, ctypes.POINTER(ctypes.c_float)), lam, alpha0, alpha1, tau, sigma)
         S = tgv_brickset(self.E, self.nbricks, coords.ctypes.data, None if fr is None else fr.ctypes.data)
-        self._keep = (coords, fr)
+        lv = None if levels is None else np.ascontiguousarray(np.asarray(levels, dtype=np.uint8).reshape(-1))
+        self._keep = (coords, fr, lv)
         out = ctypes.c_void_p()
-        _bcheck(lib.tgv_bricks_create(ctypes.byref(S), ctypes.byref(P), int(device), ctypes.byref(out)))
+        if lv is None:
+            _bcheck(lib.tgv_bricks_create(ctypes.byref(S), ctypes.byref(P), int(device), ctypes.byref(out)))
+        else:
+            if lv.size != self.nbricks:
+                raise ValueError(f"levels has {lv.size} entries for {self.nbricks} bricks")
+            _bcheck(lib.tgv_bricks_create_mixed(ctypes.byref(S), lv.ctypes.data, ctypes.byref(P), int(device),
+                                                ctypes.byref(out)))
         self.ctx = out
 
     def close(self):

@@ -311,17 +311,22 @@ namespace tgvk {
 // Alg. 1 (NEXT-2) at every voxel of every brick: the voxel centre is
 // origin + h (E * brick coordinate + in-brick offset); same per-point arithmetic as
 // vote_kernel (vote_point), so a brick's counts equal a dense vote of its box
+// Mixed-level sets (R27; levels != NULL): brick b is voted at voxel size h 2^l and radius
+// r 2^l of its level l (exact power-of-two scalings), as its level's own dense vote.
 template <int LE, int SLOTS>
 __global__ void __launch_bounds__(256) brick_vote_kernel(const VoteCam* __restrict__ cams, int ncams,
                                                          const float* __restrict__ depth, const int* __restrict__ coords,
-                                                         int nvox, double ox, double oy, double oz, double h, double r,
-                                                         uint16_t* __restrict__ H, unsigned int* __restrict__ maxc)
+                                                         int nvox, double ox, double oy, double oz, double h0, double r0,
+                                                         uint16_t* __restrict__ H, unsigned int* __restrict__ maxc,
+                                                         const uint8_t* __restrict__ levels = nullptr)
 {
     constexpr int E = 1 << LE;
-    const double delta = __dmul_rn(6.0, r), eta = __dmul_rn(3.0, delta);
     unsigned int m = 0;
     for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < nvox; vi += (int64_t)gridDim.x * blockDim.x) {
         const BrickIdx<LE> I((int)vi);
+        const int lv = levels ? levels[I.b] : 0;
+        const double h = ldexp(h0, lv), r = ldexp(r0, lv);
+        const double delta = __dmul_rn(6.0, r), eta = __dmul_rn(3.0, delta);
         const int gx = coords[3 * I.b] * E + I.c[0], gy = coords[3 * I.b + 1] * E + I.c[1],
                   gz = coords[3 * I.b + 2] * E + I.c[2];
         const double pw0 = __dadd_rn(ox, __dmul_rn(h, (double)gx));
@@ -381,15 +386,21 @@ __global__ void brick_prolong_kernel(const float* __restrict__ uc, const float* 
                                      float* __restrict__ v_cur0, float* __restrict__ v_cur1, float* __restrict__ v_cur2,
                                      float* __restrict__ v_prev0, float* __restrict__ v_prev1,
                                      float* __restrict__ v_prev2, float* __restrict__ v_next0,
-                                     float* __restrict__ v_next1, float* __restrict__ v_next2)
+                                     float* __restrict__ v_next1, float* __restrict__ v_next2,
+                                     const uint8_t* __restrict__ levels = nullptr)
 {
     constexpr int E = 1 << LE;
     for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < nvox; vi += (int64_t)gridDim.x * blockDim.x) {
         const BrickIdx<LE> I((int)vi);
         const int pb = parent[I.b];
-        const int px = ((coords[3 * I.b] & 1) * E + I.c[0]) >> 1;
-        const int py = ((coords[3 * I.b + 1] & 1) * E + I.c[1]) >> 1;
-        const int pz = ((coords[3 * I.b + 2] & 1) * E + I.c[2]) >> 1;
+        int px = ((coords[3 * I.b] & 1) * E + I.c[0]) >> 1;
+        int py = ((coords[3 * I.b + 1] & 1) * E + I.c[1]) >> 1;
+        int pz = ((coords[3 * I.b + 2] & 1) * E + I.c[2]) >> 1;
+        if (levels && levels[I.b] == 1) {  // a mixed set's level-1 brick is its parent level's own brick
+            px = I.c[0];
+            py = I.c[1];
+            pz = I.c[2];
+        }
         const int j = (((pb << LE) + pz) << LE | py) << LE | px;
         const float u = uc[j];
         const float v0 = 0.5f * vc0[j], v1 = 0.5f * vc1[j], v2 = 0.5f * vc2[j];

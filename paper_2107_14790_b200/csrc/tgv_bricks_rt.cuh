@@ -10,6 +10,7 @@
 #include "../../include/tgv_bricks.h"
 #include "tgv_bricks.cuh"
 #include "tgv_bricks_fused.cuh"
+#include "tgv_mixed.cuh"
 
 struct tgv_bricks {
     int device = 0;
@@ -44,6 +45,17 @@ struct tgv_bricks {
     bool loaded = false, poisoned = false;
     cudaStream_t stream = nullptr;
     char err[512] = "";
+
+    // 2:1 mixed-level sets (tgv_bricks_create_mixed, R27)
+    bool mixed = false;
+    std::vector<uint8_t> levels_h;
+    uint8_t* d_level = nullptr;  // [nbricks]
+    uint8_t* d_kind = nullptr;   // [nbricks][6]
+    int* d_nbr4 = nullptr;       // [nbricks][6][4]
+    uint8_t* d_par = nullptr;    // [nbricks]
+    uint8_t* d_sface = nullptr;  // [nbricks][6]
+    int* d_mfaces = nullptr;     // (frozen brick, face | quadrant mask << 3) towards solved voxels
+    int n_mfaces = 0;
 
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // pairs
@@ -88,6 +100,10 @@ int bready(tgv_bricks* c)
 }
 
 BrickGeo bgeo(const tgv_bricks* c) { return BrickGeo{(int)c->nvox, c->nbr, c->frozen, c->aface}; }
+MixGeo mgeo(const tgv_bricks* c)
+{
+    return MixGeo{(int)c->nvox, c->d_level, c->d_kind, c->d_nbr4, c->d_par, c->frozen, c->d_sface};
+}
 
 IterPtrs biter_ptrs(tgv_bricks* c, int64_t k)
 {
@@ -188,6 +204,40 @@ void launch_brick_energy_le(tgv_bricks* c, const EnergyArgs& ea)
     else brick_energy_kernel<LE, 16, uint16_t><<<nb, 256, 0, c->stream>>>(ea, bg, K16, c->partials);
 }
 
+template <int LE>
+void launch_mixed_energy_le(tgv_bricks* c, const EnergyArgs& ea)
+{
+    const MixGeo g = mgeo(c);
+    const EnergyConsts K8 = energy_consts(c->centers, c->nbins, 8), K16 = energy_consts(c->centers, c->nbins, 16);
+    const int nb = c->energy_blocks;
+    if (c->slots == 8 && c->count_bytes == 1) mixed_energy_kernel<LE, 8, uint8_t><<<nb, 256, 0, c->stream>>>(ea, g, K8, c->partials);
+    else if (c->slots == 8) mixed_energy_kernel<LE, 8, uint16_t><<<nb, 256, 0, c->stream>>>(ea, g, K8, c->partials);
+    else if (c->count_bytes == 1) mixed_energy_kernel<LE, 16, uint8_t><<<nb, 256, 0, c->stream>>>(ea, g, K16, c->partials);
+    else mixed_energy_kernel<LE, 16, uint16_t><<<nb, 256, 0, c->stream>>>(ea, g, K16, c->partials);
+}
+
+template <int LE>
+void launch_mixed_dual_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
+{
+    const int n0 = c->n_alist << (3 * LE), n1 = c->n_mfaces << (2 * LE);
+    if (n0) mixed_dual_kernel<LE, 0><<<(n0 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_alist, n0);
+    if (n1) mixed_dual_kernel<LE, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_mfaces, n1);
+}
+
+template <int LE>
+void launch_mixed_primal_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
+{
+    const Centers C = bcenters(c);
+    const int n = c->n_alist << (3 * LE), blocks = (n + 255) / 256;
+    if (!n) return;
+    const int* L = c->d_alist;
+    const MixGeo g = mgeo(c);
+    if (c->slots == 8 && c->count_bytes == 1) mixed_primal_kernel<LE, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
+    else if (c->slots == 8) mixed_primal_kernel<LE, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
+    else if (c->count_bytes == 1) mixed_primal_kernel<LE, 16, uint8_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
+    else mixed_primal_kernel<LE, 16, uint16_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
+}
+
 #define BRICK_LE_DISPATCH(fn, ...)            \
     switch (c->LE) {                          \
         case 2: fn<2>(__VA_ARGS__); break;    \
@@ -257,7 +307,11 @@ int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
     for (int32_t it = 0; it < n; ++it) {
         const IterPtrs a = biter_ptrs(c, c->k);
         if ((rc = btimer(c, 0, false))) return rc;
-        BRICK_LE_DISPATCH(launch_brick_dual_le, c, a, sp);
+        if (c->mixed) {
+            BRICK_LE_DISPATCH(launch_mixed_dual_le, c, a, sp);
+        } else {
+            BRICK_LE_DISPATCH(launch_brick_dual_le, c, a, sp);
+        }
         BCU(cudaGetLastError());
         if ((rc = btimer(c, 0, true))) return rc;
         // the primal reads p_{k+1}, q_{k+1}: the dual's outputs
@@ -265,7 +319,11 @@ int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
         for (int d = 0; d < 3; ++d) ap.pk[d] = a.pn[d];
         for (int m = 0; m < 6; ++m) ap.qk[m] = a.qn[m];
         if ((rc = btimer(c, 1, false))) return rc;
-        BRICK_LE_DISPATCH(launch_brick_primal_le, c, ap, sp);
+        if (c->mixed) {
+            BRICK_LE_DISPATCH(launch_mixed_primal_le, c, ap, sp);
+        } else {
+            BRICK_LE_DISPATCH(launch_brick_primal_le, c, ap, sp);
+        }
         BCU(cudaGetLastError());
         if ((rc = btimer(c, 1, true))) return rc;
         c->k += 1;
@@ -331,7 +389,12 @@ extern "C" {
 
 const char* tgv_bricks_last_error(const tgv_bricks* c) { return c ? c->err : g_bricks_error; }
 
-int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_bricks** out)
+}  // extern "C"
+
+namespace {
+int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* levels, const std::vector<uint8_t>& fr);
+
+int bricks_create_impl(const tgv_brickset* S, const tgv_params* P, int dev, tgv_bricks** out, const uint8_t* levels)
 {
     tgv_bricks* c = nullptr;
     if (!S || !P || !out) return bfail(c, TGV_EINVAL, "NULL argument");
@@ -363,22 +426,27 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
     {
         std::unordered_map<uint64_t, int> at;
         at.reserve((size_t)nb * 2);
-        auto key = [](int64_t x, int64_t y, int64_t z) { return (uint64_t)x | (uint64_t)y << 21 | (uint64_t)z << 42; };
+        // (level, coordinates): a one-level set has level 0 everywhere
+        auto key = [](int64_t l, int64_t x, int64_t y, int64_t z) {
+            return (uint64_t)x | (uint64_t)y << 20 | (uint64_t)z << 40 | (uint64_t)l << 60;
+        };
         for (int64_t b = 0; b < nb; ++b) {
             const int32_t* q = S->coords + 3 * b;
             for (int a = 0; a < 3; ++a)
                 if (q[a] < 0 || q[a] >= (1 << 20)) return bfail(c, TGV_EINVAL, "brick %lld coordinate outside [0, 2^20)", (long long)b);
-            if (!at.emplace(key(q[0], q[1], q[2]), (int)b).second)
+            if (levels && levels[b] > 7) return bfail(c, TGV_EINVAL, "brick %lld level %d > 7", (long long)b, levels[b]);
+            if (!at.emplace(key(levels ? levels[b] : 0, q[0], q[1], q[2]), (int)b).second)
                 return bfail(c, TGV_EINVAL, "duplicate brick coordinates (%d, %d, %d)", q[0], q[1], q[2]);
         }
         for (int64_t b = 0; b < nb; ++b) {
             const int32_t* q = S->coords + 3 * b;
+            const int lv = levels ? levels[b] : 0;
             for (int a = 0; a < 3; ++a)
                 for (int d = 0; d < 2; ++d) {
                     int64_t r[3] = {q[0], q[1], q[2]};
                     r[a] += d ? 1 : -1;
                     if (r[a] < 0 || r[a] >= (1 << 20)) continue;
-                    auto it = at.find(key(r[0], r[1], r[2]));
+                    auto it = at.find(key(lv, r[0], r[1], r[2]));
                     if (it != at.end()) nbr[(size_t)b * 6 + 2 * a + d] = it->second;
                 }
         }
@@ -503,7 +571,7 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
         bfail(c, TGV_ENOMEM, "brick list allocation failed");
         return bail(TGV_ENOMEM);
     }
-    if (c->E == 32) {  // the fused schedule's neighbourhood table (and its default)
+    if (c->E == 32 && !levels) {  // the fused schedule's neighbourhood table (and its default)
         std::vector<int> nb27((size_t)alist.size() * 27, -1);
         std::unordered_map<uint64_t, int> at2;
         at2.reserve((size_t)nb * 2);
@@ -546,8 +614,167 @@ int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_b
         bfail(c, TGV_ECUDA, "table upload failed");
         return bail(TGV_ECUDA);
     }
+    if (levels) {
+        int rc = build_mixed_tables(c, S, levels, fr);
+        if (rc) return bail(rc);
+    }
     *out = c;
     return TGV_OK;
+}
+
+// R27 tables of a 2:1 mixed-level set: face kinds, neighbour bricks (four quadrants for
+// a finer face), coordinate parities, solved-quadrant masks, the frozen faces of S, |S|
+int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* levels, const std::vector<uint8_t>& fr)
+{
+    const int64_t nb = c->nbricks;
+    const int E = c->E;
+    std::unordered_map<uint64_t, int> at;
+    at.reserve((size_t)nb * 2);
+    auto key = [](int64_t l, int64_t x, int64_t y, int64_t z) {
+        return (uint64_t)x | (uint64_t)y << 20 | (uint64_t)z << 40 | (uint64_t)l << 60;
+    };
+    auto find = [&](int64_t l, int64_t x, int64_t y, int64_t z) -> int {
+        if (l < 0 || l > 7 || x < 0 || y < 0 || z < 0 || x >= (1 << 20) || y >= (1 << 20) || z >= (1 << 20)) return -1;
+        auto it = at.find(key(l, x, y, z));
+        return it == at.end() ? -1 : it->second;
+    };
+    for (int64_t b = 0; b < nb; ++b) at.emplace(key(levels[b], S->coords[3 * b], S->coords[3 * b + 1], S->coords[3 * b + 2]), (int)b);
+    // disjoint: no brick has an ancestor position occupied by another brick
+    for (int64_t b = 0; b < nb; ++b)
+        for (int j = 1; levels[b] + j <= 7; ++j)
+            if (find(levels[b] + j, S->coords[3 * b] >> j, S->coords[3 * b + 1] >> j, S->coords[3 * b + 2] >> j) >= 0)
+                return bfail(c, TGV_EINVAL, "brick %lld overlaps a coarser brick", (long long)b);
+    std::vector<uint8_t> kind((size_t)nb * 6, 0), par((size_t)nb, 0), sface((size_t)nb * 6, 0);
+    std::vector<int> nbr4((size_t)nb * 24, -1);
+    for (int64_t b = 0; b < nb; ++b) {
+        const int l = levels[b];
+        const int64_t P[3] = {S->coords[3 * b], S->coords[3 * b + 1], S->coords[3 * b + 2]};
+        par[(size_t)b] = (uint8_t)((P[0] & 1) | (P[1] & 1) << 1 | (P[2] & 1) << 2);
+        for (int k = 0; k < 3; ++k) {
+            const int l0 = k == 0 ? 1 : 0, l1 = k == 2 ? 1 : 2;
+            for (int d = 0; d < 2; ++d) {
+                const int f = 2 * k + d;
+                int64_t Q[3] = {P[0], P[1], P[2]};
+                Q[k] += d ? 1 : -1;
+                if (Q[k] < 0) continue;
+                int* nb4 = &nbr4[(size_t)(b * 6 + f) * 4];
+                int j = find(l, Q[0], Q[1], Q[2]);
+                if (j >= 0) {
+                    kind[(size_t)b * 6 + f] = 1;
+                    nb4[0] = j;
+                    sface[(size_t)b * 6 + f] = fr[(size_t)j] ? 0 : 0xF;
+                    continue;
+                }
+                j = find(l + 1, Q[0] >> 1, Q[1] >> 1, Q[2] >> 1);
+                if (j >= 0) {
+                    kind[(size_t)b * 6 + f] = 2;
+                    nb4[0] = j;
+                    sface[(size_t)b * 6 + f] = fr[(size_t)j] ? 0 : 0xF;
+                    continue;
+                }
+                for (int jj = 2; l + jj <= 7; ++jj)
+                    if (find(l + jj, Q[0] >> jj, Q[1] >> jj, Q[2] >> jj) >= 0)
+                        return bfail(c, TGV_EINVAL, "not 2:1 balanced: brick %lld face %d meets a brick %d levels coarser",
+                                     (long long)b, f, jj);
+                if (l == 0) continue;
+                bool any = false;
+                for (int q = 0; q < 4; ++q) {
+                    int64_t F[3];
+                    F[k] = d ? 2 * Q[k] : 2 * Q[k] + 1;
+                    F[l0] = 2 * P[l0] + (q & 1);
+                    F[l1] = 2 * P[l1] + (q >> 1);
+                    const int fb = find(l - 1, F[0], F[1], F[2]);
+                    nb4[q] = fb;
+                    if (fb >= 0) {
+                        any = true;
+                        if (!fr[(size_t)fb]) sface[(size_t)b * 6 + f] |= (uint8_t)(1u << q);
+                    }
+                    // nothing two levels finer may touch the face
+                    if (l >= 2)
+                        for (int a2 = 0; a2 < 2; ++a2)
+                            for (int b2 = 0; b2 < 2; ++b2) {
+                                int64_t G[3];
+                                G[k] = d ? 2 * F[k] : 2 * F[k] + 1;
+                                G[l0] = 2 * F[l0] + a2;
+                                G[l1] = 2 * F[l1] + b2;
+                                if (find(l - 2, G[0], G[1], G[2]) >= 0)
+                                    return bfail(c, TGV_EINVAL, "not 2:1 balanced at brick %lld face %d", (long long)b, f);
+                            }
+                }
+                if (any) kind[(size_t)b * 6 + f] = 3;
+            }
+        }
+    }
+    // the frozen faces of S (quadrant masks) and |S|
+    std::vector<int> mf;
+    int64_t sv = 0;
+    std::vector<uint8_t> mark((size_t)E * E * E);
+    for (int64_t b = 0; b < nb; ++b) {
+        if (!fr[(size_t)b]) {
+            sv += (int64_t)E * E * E;
+            continue;
+        }
+        std::fill(mark.begin(), mark.end(), 0);
+        for (int f = 0; f < 6; ++f) {
+            const int m = sface[(size_t)b * 6 + f];
+            if (!m) continue;
+            mf.push_back((int)b);
+            mf.push_back(f | m << 3);
+            const int k = f >> 1, l0 = k == 0 ? 1 : 0, l1 = k == 2 ? 1 : 2;
+            for (int a1 = 0; a1 < E; ++a1)
+                for (int a0 = 0; a0 < E; ++a0) {
+                    const int q = (a0 >= E / 2 ? 1 : 0) | (a1 >= E / 2 ? 2 : 0);
+                    if (!((m >> q) & 1)) continue;
+                    int cc[3];
+                    cc[k] = (f & 1) ? E - 1 : 0;
+                    cc[l0] = a0;
+                    cc[l1] = a1;
+                    mark[((size_t)cc[2] * E + cc[1]) * E + cc[0]] = 1;
+                }
+        }
+        for (uint8_t m : mark) sv += m;
+    }
+    c->s_voxels = sv;
+    c->n_mfaces = (int)mf.size() / 2;
+    c->mixed = true;
+    c->schedule = TGV_SCHEDULE_SPLIT;
+    c->levels_h.assign(levels, levels + nb);
+    if (cudaMalloc(&c->d_level, (size_t)nb) != cudaSuccess || cudaMalloc(&c->d_kind, (size_t)nb * 6) != cudaSuccess ||
+        cudaMalloc(&c->d_nbr4, sizeof(int) * (size_t)nb * 24) != cudaSuccess ||
+        cudaMalloc(&c->d_par, (size_t)nb) != cudaSuccess || cudaMalloc(&c->d_sface, (size_t)nb * 6) != cudaSuccess ||
+        cudaMalloc(&c->d_mfaces, sizeof(int) * std::max<size_t>(2, mf.size())) != cudaSuccess) {
+        cudaGetLastError();
+        return bfail(c, TGV_ENOMEM, "mixed-level table allocation failed");
+    }
+    c->device_bytes += 14 * nb + 96 * nb + (int64_t)sizeof(int) * mf.size();
+    if (cudaMemcpy(c->d_level, levels, (size_t)nb, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_kind, kind.data(), kind.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_nbr4, nbr4.data(), sizeof(int) * nbr4.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_par, par.data(), par.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->d_sface, sface.data(), sface.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        (!mf.empty() && cudaMemcpy(c->d_mfaces, mf.data(), sizeof(int) * mf.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+        cudaGetLastError();
+        return bfail(c, TGV_ECUDA, "mixed-level table upload failed");
+    }
+    return TGV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int tgv_bricks_create(const tgv_brickset* S, const tgv_params* P, int dev, tgv_bricks** out)
+{
+    return bricks_create_impl(S, P, dev, out, nullptr);
+}
+
+int tgv_bricks_create_mixed(const tgv_brickset* S, const uint8_t* levels, const tgv_params* P, int dev,
+                            tgv_bricks** out)
+{
+    if (!levels) {
+        if (out) *out = nullptr;
+        return bfail(nullptr, TGV_EINVAL, "levels is NULL");
+    }
+    return bricks_create_impl(S, P, dev, out, levels);
 }
 
 int tgv_bricks_load(tgv_bricks* c, const void* counts, int count_bytes, int64_t n_counts)
@@ -671,7 +898,11 @@ int tgv_bricks_energy(tgv_bricks* c, double out[6])
     ea.V = 2.0;
     ea.nbins = c->nbins;
     if ((rc = btimer(c, 2, false))) return rc;
-    BRICK_LE_DISPATCH(launch_brick_energy_le, c, ea);
+    if (c->mixed) {
+        BRICK_LE_DISPATCH(launch_mixed_energy_le, c, ea);
+    } else {
+        BRICK_LE_DISPATCH(launch_brick_energy_le, c, ea);
+    }
     BCU(cudaGetLastError());
     energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, c->energy_blocks, c->d_out);
     BCU(cudaGetLastError());
@@ -689,6 +920,7 @@ int tgv_bricks_set_schedule(tgv_bricks* c, int schedule)
     if (rc) return rc;
     if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT) return bfail(c, TGV_EINVAL, "bad schedule %d", schedule);
     if (schedule == TGV_SCHEDULE_FUSED && c->E != 32) return bfail(c, TGV_EINVAL, "the fused schedule needs E = 32");
+    if (schedule == TGV_SCHEDULE_FUSED && c->mixed) return bfail(c, TGV_EINVAL, "mixed-level sets run the SPLIT schedule");
     c->schedule = schedule;
     return TGV_OK;
 }
@@ -758,6 +990,12 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->d_faces);
     cudaFree(c->d_coords);
     cudaFree(c->d_parent);
+    cudaFree(c->d_level);
+    cudaFree(c->d_kind);
+    cudaFree(c->d_nbr4);
+    cudaFree(c->d_par);
+    cudaFree(c->d_sface);
+    cudaFree(c->d_mfaces);
     cudaFree(c->hist);
     cudaFree(c->partials);
     cudaFree(c->d_out);
@@ -801,11 +1039,12 @@ int tgv_bricks_vote_depth_maps(tgv_bricks* c, const tgv_camera* cams, int ncams,
 #define BVOTE(LE_)                                                                                                \
     (c->slots == 8 ? brick_vote_kernel<LE_, 8><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth, c->d_coords, \
                                                                              nv, ox, oy, oz, voxel_size,          \
-                                                                             voxel_radius, h16, c->d_maxc)         \
+                                                                             voxel_radius, h16, c->d_maxc,        \
+                                                                             c->d_level)                          \
                    : brick_vote_kernel<LE_, 16><<<148 * 8, 256, 0, c->stream>>>(d_cams, ncams, d_depth,            \
                                                                               c->d_coords, nv, ox, oy, oz,         \
                                                                               voxel_size, voxel_radius, h16,       \
-                                                                              c->d_maxc))
+                                                                              c->d_maxc, c->d_level))
     if (e == cudaSuccess) {
         switch (c->LE) {
             case 2: BVOTE(2); break;
@@ -915,10 +1154,13 @@ int tgv_bricks_prolong_from(tgv_bricks* f, const tgv_bricks* pc)
     auto key = [](int64_t x, int64_t y, int64_t z) { return (uint64_t)x | (uint64_t)y << 21 | (uint64_t)z << 42; };
     for (int64_t b = 0; b < pc->nbricks; ++b)
         at.emplace(key(pc->coords_h[3 * b], pc->coords_h[3 * b + 1], pc->coords_h[3 * b + 2]), (int)b);
+    if (pc->mixed) return bfail(c, TGV_EINVAL, "the coarse context must be a one-level set");
     std::vector<int> parent((size_t)c->nbricks);
     for (int64_t b = 0; b < c->nbricks; ++b) {
         const int32_t* q = &c->coords_h[3 * b];
-        auto it = at.find(key(q[0] >> 1, q[1] >> 1, q[2] >> 1));
+        const int lv = c->mixed ? c->levels_h[(size_t)b] : 0;
+        if (lv > 1) return bfail(c, TGV_EINVAL, "prolongation into a mixed set needs levels 0 and 1 only");
+        auto it = at.find(lv == 1 ? key(q[0], q[1], q[2]) : key(q[0] >> 1, q[1] >> 1, q[2] >> 1));
         if (it == at.end())
             return bfail(c, TGV_EINVAL, "brick (%d, %d, %d) has no parent brick in the coarse level", q[0], q[1], q[2]);
         parent[(size_t)b] = it->second;
@@ -941,7 +1183,7 @@ int tgv_bricks_prolong_from(tgv_bricks* f, const tgv_bricks* pc)
         c->d_coords, nv, bslot(c, slotU(b.cu)), bslot(c, slotU(b.pu)), bslot(c, slotU(b.nu)),                         \
         bslot(c, slotV(b.cu, 0)), bslot(c, slotV(b.cu, 1)), bslot(c, slotV(b.cu, 2)), bslot(c, slotV(b.pu, 0)),       \
         bslot(c, slotV(b.pu, 1)), bslot(c, slotV(b.pu, 2)), bslot(c, slotV(b.nu, 0)), bslot(c, slotV(b.nu, 1)),       \
-        bslot(c, slotV(b.nu, 2)))
+        bslot(c, slotV(b.nu, 2)), c->d_level)
     switch (c->LE) {
         case 2: BPRO(2); break;
         case 3: BPRO(3); break;
