@@ -64,6 +64,28 @@ def _sorted(c):
     return c[np.lexsort((c[:, 0], c[:, 1], c[:, 2]))]
 
 
+_FACES = np.array([(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)], np.int64)
+
+
+def mixed_border(A, grid):
+    """A 2:1 mixed-level set around the level-0 bricks A (R27): A solved; frozen, every
+    face neighbour of A inside `grid` as a level-0 brick when its parent cube holds a
+    brick of A, else as that parent cube (level 1, deduplicated).  Levels 0 and 1 only,
+    so the set is 2:1 balanced, and no level-1 brick contains a level-0 brick.
+    Returns (coords int32 [n, 3] in each brick's level units, levels uint8, frozen bool)."""
+    A = _sorted(A)
+    nb = (A[:, None, :] + _FACES[None]).reshape(-1, 3)
+    nb = _sorted(nb[np.all((nb >= 0) & (nb < np.asarray(grid)), axis=1)])
+    nb = nb[~np.isin(_key(nb), _key(A))]
+    fine = np.isin(_key(nb >> 1), _key(A >> 1))
+    B0 = nb[fine]
+    B1 = _sorted(nb[~fine] >> 1)
+    coords = np.concatenate([A, B0, B1]).astype(np.int32)
+    levels = np.concatenate([np.zeros(len(A) + len(B0), np.uint8), np.ones(len(B1), np.uint8)])
+    frozen = np.concatenate([np.zeros(len(A), bool), np.ones(len(B0) + len(B1), bool)])
+    return coords, levels, frozen
+
+
 class BrickLevels:
     """Brick sets of `levels` levels (index 0 = finest) built from the depth maps, with
     their counts resident on the GPU; `solve` runs the coarse-to-fine TGV solve."""
@@ -122,11 +144,45 @@ class BrickLevels:
             s = f
         return s
 
+    def mixed_finest(self):
+        """The finest level as a 2:1 mixed-level set (R27):
+        its solved bricks A (level 0) with a frozen border B of face neighbours -- a
+        level-0 brick where the parent cube also holds a brick of A, else the parent
+        cube itself (a level-1 brick).  Returns (coords, levels, frozen); the solve
+        prolongates every brick from level 1 (R19; a level-1 brick keeps its own u, v / 2)."""
+        return mixed_border(self.coords[0][~self.frozen[0]], brick_grid(self.extent, self.edge, 0))
+
+    def build_mixed(self):
+        """Create and vote the finest level's mixed-level context (see mixed_finest)."""
+        coords, levels, frozen = self.mixed_finest()
+        cams, depths, origin, h, r = self.vote_args
+        m = BrickSolver(self.edge, coords, frozen, levels=levels, **self.kw)
+        m.vote(cams, depths, grid_origin=origin, voxel_size=h, voxel_radius=r)
+        self.mixed = (m, coords, levels, frozen)
+        return m
+
+    def solve_mixed(self, iters):
+        """solve(), with the finest level replaced by its mixed-level set."""
+        top = self.levels - 1
+        s = self.solvers[top].reset().iterate(iters)
+        for lev in range(top - 1, 0, -1):
+            f = self.solvers[lev]
+            f.prolong_from(s)
+            f.iterate(iters)
+            s = f
+        m = self.mixed[0]
+        m.prolong_from(s)
+        m.iterate(iters)
+        return m
+
     def close(self):
         for s in self.solvers:
             if s is not None:
                 s.close()
         self.solvers = []
+        if getattr(self, "mixed", None):
+            self.mixed[0].close()
+            self.mixed = None
 
 
 # ---------------------------------------------------------------------------

@@ -76,3 +76,29 @@ def test_morton_code_interleaves_bits():
     x, y, z = 5, 3, 6
     ref = sum(((x >> i & 1) << (3 * i)) | ((y >> i & 1) << (3 * i + 1)) | ((z >> i & 1) << (3 * i + 2)) for i in range(8))
     assert int(m[5]) == ref
+
+
+def test_mixed_border_is_a_balanced_disjoint_set_around_A():
+    """R27 host logic: the mixed finest level (A plus its frozen face border, level-0 where
+    the parent cube holds A, else the parent cube) is disjoint and 2:1 balanced (the oracle's
+    own checks), covers every face neighbour of A, and has only face neighbours of A (or
+    their parents) in B."""
+    from oracle import mixed as om
+    from paper_2107_14790_b200.brick_levels import mixed_border
+    rng = np.random.default_rng(3)
+    grid = (8, 8, 6)
+    A = np.unique(rng.integers(0, [8, 8, 6], (40, 3)), axis=0)
+    coords, levels, frozen = mixed_border(A, grid)
+    om.check_balanced(2, levels, coords)  # E = 2: the smallest brick-aligned geometry
+    fine = {tuple(c) for c, l in zip(coords, levels) if l == 0}
+    coarse = {tuple(c) for c, l in zip(coords, levels) if l == 1}
+    assert {tuple(a) for a in A} <= fine and not frozen[:len(A)].any() and frozen[len(A):].all()
+    for a in A:
+        for d in ([1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]):
+            n = a + np.array(d)
+            if np.any(n < 0) or np.any(n >= grid):
+                continue
+            assert tuple(n) in fine or tuple(n >> 1) in coarse
+    for c, l in zip(coords[len(A):], levels[len(A):]):
+        kids = [np.array(c)] if l == 0 else [2 * np.array(c) + np.array(o) for o in np.ndindex(2, 2, 2)]
+        assert any(np.abs(k - a).sum() == 1 for k in kids for a in A)
