@@ -844,7 +844,33 @@ struct EnergyConsts {
     double c1[16];  // c_b + 1
     double dc[17];  // c_b - c_{b-1} with c_{-1} = -1; dc[16]: 1 - c_15 (unused, the walk ends at the last slot)
     double end;     // 1 - c_{SLOTS-1} for the template's SLOTS (set per launch)
+    float cf[16], c1f[16], dcf[16], endf;  // the same in fp32 (dense energy kernel)
 };
+
+// data_box_terms in fp32 (the dense energy kernel's per-voxel terms; fp64 accumulation)
+template <int SLOTS, typename CT>
+__device__ __forceinline__ void data_box_terms_f32(const HistRaw<SLOTS, CT>& h, const EnergyConsts& K, float lam,
+                                                   float u, float divp, float& data, float& box)
+{
+    float d = 0.f, G = 0.f, f = 0.f, best = 0.f, W = 0.f;
+#pragma unroll
+    for (int b = 0; b < SLOTS; ++b) W += hist_count<SLOTS, CT>(h, b);
+    float slope = -fmaf(lam, W, divp);
+    const float l2 = 2.f * lam;
+#pragma unroll
+    for (int b = 0; b < SLOTS; ++b) {
+        const float hb = hist_count<SLOTS, CT>(h, b);
+        d = fmaf(hb, fabsf(u - K.cf[b]), d);
+        G = fmaf(hb, K.c1f[b], G);
+        f = fmaf(K.dcf[b], slope, f);
+        best = fminf(best, f);
+        slope = fmaf(l2, hb, slope);
+    }
+    f = fmaf(K.endf, slope, f);
+    best = fminf(best, f);
+    data = lam * d;
+    box = fmaf(lam, G, divp) + best;
+}
 
 // count b as an exact double: the count in the low mantissa word of 2^52, minus 2^52
 template <int SLOTS, typename CT>
@@ -910,8 +936,11 @@ struct EnergySched {
 // (a4) dense energy / restricted gap (R14).  HBM-bound: each of the
 // 13 fields and the counts is read once (60 B per voxel with u8 counts); the z-neighbours
 // ride in registers along the march, the x / y neighbours are L1 / L2 hits of the same or
-// the neighbouring warp's rows.  fp64 per-voxel terms, warp shuffles, fixed-order block
-// partials (energy_final_kernel sums them): deterministic.
+// the neighbouring warp's rows.  The per-voxel terms are formed in fp32 from the fp32
+// state (relative error of each term ~1e-7) and REDUCED in fp64: per-thread fp64 sums,
+// warp shuffles, fixed-order block partials (energy_final_kernel): deterministic.  (An
+// all-fp64 version spent its time in 38 fp32->fp64 conversions per voxel on the XU pipe:
+// 0.43 of the copy roofline, profiles/r2b_energy_*.)
 template <int SLOTS, typename CT>
 __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     energy_partial_kernel(const EnergyArgs ea, Geo g, const EnergyConsts K, const EnergySched es,
@@ -921,6 +950,7 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     float vm = 0.f;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int sy = g.px, sz = g.plane;
+    const float al1 = (float)ea.alpha1, al0 = (float)ea.alpha0, lam = (float)ea.lambda, VV = (float)ea.V;
     for (int it = blockIdx.x; it < es.items; it += gridDim.x) {
         const int xt = it % es.ntx, r = it / es.ntx;
         const int x = xt * 32 + lane, y = (r % es.nyg) * 8 + wid;
@@ -949,26 +979,26 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
             const float v0y = L(ea.v[0], i - sy), v1y = L(ea.v[1], i - sy), v2y = L(ea.v[2], i - sy),
                         p1y = L(ea.p[1], i - sy);
             const auto h = load_hist<SLOTS, CT>(ea.hist, hv);
-            // ---- fp64 terms (the masks are R6's Neumann D+ / D-)
-            auto dp = [](bool l, float a, float b) { return l ? (double)a - (double)b : 0.0; };
-            auto dm = [](bool l, bool f, float a, float b) { return (l ? (double)a : 0.0) - (f ? (double)b : 0.0); };
-            const double a0 = dp(xl, ux, uc) - v0, a1 = dp(yl, uy, uc) - v1, a2 = dp(zl, un, uc) - v2;
-            t1 = fma(ea.alpha1, sqrt(fma(a0, a0, fma(a1, a1, a2 * a2))), t1);
-            const double exx = dm(xl, xf, v0, v0x), eyy = dm(yl, yf, v1, v1y), ezz = dm(zl, zf, v2, vm2);
-            const double exy = 0.5 * (dm(yl, yf, v0, v0y) + dm(xl, xf, v1, v1x));
-            const double exz = 0.5 * (dm(zl, zf, v0, vm0) + dm(xl, xf, v2, v2x));
-            const double eyz = 0.5 * (dm(zl, zf, v1, vm1) + dm(yl, yf, v2, v2y));
-            const double off = fma(exy, exy, fma(exz, exz, eyz * eyz));
-            t0 = fma(ea.alpha0, sqrt(fma(exx, exx, fma(eyy, eyy, fma(ezz, ezz, 2.0 * off)))), t0);
-            const double divp = dm(xl, xf, p0, p0x) + dm(yl, yf, p1, p1y) + dm(zl, zf, p2, pzm);
-            const double w0 = dp(xl, qxxx, qxx) + dp(yl, qxyy, qxy) + dp(zl, qxzn, qxz);
-            const double w1 = dp(xl, qxyx, qxy) + dp(yl, qyyy, qyy) + dp(zl, qyzn, qyz);
-            const double w2 = dp(xl, qxzx, qxz) + dp(yl, qyzy, qyz) + dp(zl, qzzn, qzz);
-            const double l1 = fabs((double)p0 + w0) + fabs((double)p1 + w1) + fabs((double)p2 + w2);
-            double data, box;
-            data_box_terms<SLOTS, CT>(h, K, ea.lambda, (double)uc, divp, data, box);
-            td += data;
-            dv += box - ea.V * l1;
+            // ---- per-voxel terms (the masks are R6's Neumann D+ / D-)
+            auto dp = [](bool l, float a, float b) { return l ? a - b : 0.f; };
+            auto dm = [](bool l, bool f, float a, float b) { return (l ? a : 0.f) - (f ? b : 0.f); };
+            const float a0 = dp(xl, ux, uc) - v0, a1 = dp(yl, uy, uc) - v1, a2 = dp(zl, un, uc) - v2;
+            t1 += (double)(al1 * sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2))));
+            const float exx = dm(xl, xf, v0, v0x), eyy = dm(yl, yf, v1, v1y), ezz = dm(zl, zf, v2, vm2);
+            const float exy = 0.5f * (dm(yl, yf, v0, v0y) + dm(xl, xf, v1, v1x));
+            const float exz = 0.5f * (dm(zl, zf, v0, vm0) + dm(xl, xf, v2, v2x));
+            const float eyz = 0.5f * (dm(zl, zf, v1, vm1) + dm(yl, yf, v2, v2y));
+            const float off = fmaf(exy, exy, fmaf(exz, exz, eyz * eyz));
+            t0 += (double)(al0 * sqrtf(fmaf(exx, exx, fmaf(eyy, eyy, fmaf(ezz, ezz, 2.f * off)))));
+            const float divp = dm(xl, xf, p0, p0x) + dm(yl, yf, p1, p1y) + dm(zl, zf, p2, pzm);
+            const float w0 = dp(xl, qxxx, qxx) + dp(yl, qxyy, qxy) + dp(zl, qxzn, qxz);
+            const float w1 = dp(xl, qxyx, qxy) + dp(yl, qyyy, qyy) + dp(zl, qyzn, qyz);
+            const float w2 = dp(xl, qxzx, qxz) + dp(yl, qyzy, qyz) + dp(zl, qzzn, qzz);
+            const float l1 = fabsf(p0 + w0) + fabsf(p1 + w1) + fabsf(p2 + w2);
+            float data, box;
+            data_box_terms_f32<SLOTS, CT>(h, K, lam, uc, divp, data, box);
+            td += (double)data;
+            dv += (double)box - (double)(VV * l1);
             vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
             // ---- carry
             vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;

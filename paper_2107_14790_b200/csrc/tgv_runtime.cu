@@ -831,6 +831,12 @@ EnergyConsts energy_consts(const float* centers, int nbins, int slots)
     }
     K.dc[16] = 1.0 - prev;
     K.end = 1.0 - K.c[slots - 1];
+    for (int b = 0; b < 16; ++b) {
+        K.cf[b] = (float)K.c[b];
+        K.c1f[b] = K.cf[b] + 1.f;
+        K.dcf[b] = K.cf[b] - (b ? K.cf[b - 1] : -1.f);
+    }
+    K.endf = 1.f - K.cf[slots - 1];
     return K;
 }
 

@@ -115,8 +115,8 @@ def random_state(shape, seed, model="tgv"):
 def test_energy_terms_from_random_state(shape, nb, scale, model):
     """(a4) tgv_energy on a state both sides hold bit-identically (random u, v, p, q with every
     boundary face and large ||p + div2 q||_1): E, its three terms, the restricted gap E - D_V
-    (R14, V = 2; TV-L1 V = 0) and max|v| equal the oracle's up to fp64 rounding order.  Counts
-    up to 100x (u16), 3 / 8 / 16 bins with non-uniform centres."""
+    (R14, V = 2; TV-L1 V = 0) and max|v| equal the oracle's up to the kernel's fp32 per-voxel
+    rounding (fp64 sums).  Counts up to 100x (u16), 3 / 8 / 16 bins with non-uniform centres."""
     nx, ny, nz = shape
     rng = np.random.default_rng(nb * 1000 + nx)
     if nb == 8:
@@ -135,12 +135,14 @@ def test_energy_terms_from_random_state(shape, nb, scale, model):
         if k in st:
             assert np.array_equal(s.get(k), st[k]), k
     eo, es = o.energy(), s.energy()
-    scale_e = max(1.0, abs(eo["E"]))
+    # the kernel forms each voxel's terms in fp32 from the (identical) fp32 state and sums
+    # them in fp64: relative error ~1e-7 of the summed magnitudes |E| + |D_V|
+    tol = 2e-6 * max(1.0, abs(eo["E"]), abs(eo["dual"]))
     for k in ("E", "alpha1", "alpha0", "data", "gap"):
-        assert abs(es[k] - eo[k]) <= 1e-10 * scale_e, (k, es[k], eo[k])
+        assert abs(es[k] - eo[k]) <= tol, (k, es[k], eo[k], tol)
     assert es["vmax"] == eo["vmax"]
     # the V term matters here: it moves the gap by far more than the tolerance
-    assert model == "tvl1" or abs(o.energy(V=0.0)["gap"] - eo["gap"]) > 1e3 * 1e-10 * scale_e
+    assert model == "tvl1" or abs(o.energy(V=0.0)["gap"] - eo["gap"]) > 100 * tol
 
 
 @pytest.mark.parametrize("schedule", SCHEDULES)
