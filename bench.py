@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--out-of-core", type=int, default=0, metavar="LEAF_VOXELS",
                     help="NEXT-3: out-of-core coarse-to-fine over z-slab leaves of <= LEAF_VOXELS voxels "
                          "(host-resident counts and levels; a step = the whole solve, --levels levels)")
+    ap.add_argument("--mixed", action="store_true",
+                    help="C5: solve the finest brick level as a 2:1 mixed-level set (R27: frozen border of level-0 "
+                         "bricks or level-1 parent cubes), SPLIT mixed kernels")
     ap.add_argument("--parts", type=int, default=0,
                     help="C5: solve the finest brick level in this many Morton parts with frozen shells (R26); "
                          "streamed through one GPU, or shared round-robin by the ranks of a torchrun job")
@@ -682,25 +685,32 @@ def run_bricks(a):
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
     cams, depths = cams_of(wl), render_shared(wl, 0, 1)
     t_build = time.perf_counter()
-    bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius, **kw)
+    bl = BrickLevels(wl.shape, cams, depths, levels=levels, edge=32, voxel_radius=wl.voxel_radius,
+                     resident_finest=not a.mixed, **kw)
     t_build = time.perf_counter() - t_build
     for s_ in bl.solvers:
-        s_.set_schedule(a.schedule)  # FUSED by default (32^3 bricks), SPLIT on request
-    vox = bl.voxels()
-    infos = [s.info() for s in bl.solvers]
+        if s_ is not None:
+            s_.set_schedule(a.schedule)  # FUSED by default (32^3 bricks), SPLIT on request
+    sols = bl.solvers
+    if a.mixed:  # R27: the finest level as a 2:1 mixed-level set (SPLIT mixed kernels)
+        sols = [bl.build_mixed()] + bl.solvers[1:]
+    vox = [int(s_.info()["nbricks"]) * 32 ** 3 for s_ in sols]
+    infos = [s.info() for s in sols]
     solved = [i["solved_voxels"] for i in infos]
     svox = [i["s_voxels"] for i in infos]
     vox_its, vox_its_s = sum(solved) * iters, sum(svox) * iters
 
+    solve = bl.solve_mixed if a.mixed else bl.solve
+
     def step():
-        bl.solve(iters).energy()
+        solve(iters).energy()
 
     for _ in range(a.warmup):
         step()
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.3)
-    for s in bl.solvers:
+    for s in sols:
         s.set_timing(True)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -712,24 +722,36 @@ def run_bricks(a):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / a.steps
     ms = ev0.elapsed_time(ev1) / a.steps
-    tms = [s.timing() for s in bl.solvers]
-    for s in bl.solvers:
+    tms = [s.timing() for s in sols]
+    for s in sols:
         s.set_timing(False)
     clk = clocks.stop()
-    cb = bl.solvers[0].info()["count_bytes"]
+    cb = sols[0].info()["count_bytes"]
     fused = infos[0]["schedule"] == 0
-    # algorithmic bytes: SPLIT: dual on S, 17 reads + 9 writes; primal on
-    # the solved voxels, 13 reads + counts + 4 writes.  FUSED: the frozen-face dual on
-    # S minus the solved voxels (104 B) and the single sweep over the solved voxels
-    # (17 reads + counts + 13 writes)
-    if fused:
-        dual_b = sum(sv - so for sv, so in zip(svox, solved)) * 104 * iters
-        primal_b = sum(solved) * (120 + 8 * cb) * iters
-    else:
-        dual_b = sum(svox) * 104 * iters
-        primal_b = sum(solved) * (68 + 8 * cb) * iters
+    # algorithmic bytes, per level by its own schedule: SPLIT: dual on S,
+    # 17 reads + 9 writes; primal on the solved voxels, 13 reads + counts + 4 writes.
+    # FUSED: the frozen-face dual on S minus the solved voxels (104 B) and the single
+    # sweep over the solved voxels (17 reads + counts + 13 writes)
+    dual_b = primal_b = 0
+    for inf, sv, so in zip(infos, svox, solved):
+        if inf["schedule"] == 0:
+            dual_b += (sv - so) * 104 * iters
+            primal_b += so * (120 + 8 * cb) * iters
+        else:
+            dual_b += sv * 104 * iters
+            primal_b += so * (68 + 8 * cb) * iters
     dual_ms = sum(t["dual_ms"] for t in tms) / a.steps
     primal_ms = sum(t["primal_ms"] + t["fused_ms"] for t in tms) / a.steps
+    mixed = None
+    if a.mixed:  # the finest level's mixed kernels alone
+        t0_ = tms[0]
+        dms0, pms0 = t0_["dual_ms"] / a.steps, t0_["primal_ms"] / a.steps
+        lv_ = bl.mixed[2]
+        mixed = {"bricks_level0": int((lv_ == 0).sum()), "bricks_level1": int((lv_ == 1).sum()),
+                 "solved_bricks": int((~bl.mixed[3]).sum()), "s_voxels": svox[0],
+                 "dual_ms_per_step": dms0, "primal_ms_per_step": pms0,
+                 "dual_gbs": svox[0] * 104 * iters / (dms0 * 1e-3) / 1e9,
+                 "primal_gbs": solved[0] * (68 + 8 * cb) * iters / (pms0 * 1e-3) / 1e9}
     peak, peak_src = measured_peaks()
     if fused:
         dom, dbytes, dms = "fused", primal_b, primal_ms
@@ -752,9 +774,10 @@ def run_bricks(a):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(a.steps):
-            for lev, s in enumerate(bl.solvers):
+            for lev, s in enumerate(sols):
+                # a mixed set votes each brick at its own level (level 0 here)
                 s.vote(cams, depths, voxel_size=float(1 << lev), voxel_radius=wl.voxel_radius * (1 << lev))
-            f = bl.solve(iters)
+            f = solve(iters)
             f.energy()
             hu = f.read_u()
         el = (time.perf_counter() - t0) / a.steps
@@ -764,7 +787,8 @@ def run_bricks(a):
                         "tgv_bricks_energy, tgv_bricks_read"}
     cpu = None
     if not a.no_cpu_baseline:
-        cpu = cpu_brick_oracle_rate(bl, a.cpu_seconds, kw)
+        cpu = cpu_brick_oracle_rate(bl, a.cpu_seconds, kw, solver=sols[0],
+                                    sets=(bl.mixed[1], bl.mixed[3]) if a.mixed else None)
     bricks = bl.bricks()
     line = {
         "metric": METRIC + " (NEXT-3 block-sparse brick sets)", "value": vox_its / (ms * 1e-3), "unit": UNIT,
@@ -787,6 +811,7 @@ def run_bricks(a):
                      "schedule_gbs": (dual_b + primal_b) / (ms * 1e-3) / 1e9, "count_bytes": cb,
                      "kernel_share_of_step": (dual_ms + primal_ms) / ms},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches * a.steps)),
+        "mixed_finest": mixed,
         "kernel_ms": {"dual" if not fused else "frozen_face_dual": dual_ms,
                       "primal" if not fused else "fused": primal_ms,
                       "energy": sum(t["energy_ms"] for t in tms) / a.steps},
@@ -796,14 +821,15 @@ def run_bricks(a):
     bl.close()
 
 
-def cpu_brick_oracle_rate(bl, target_s, kw):
+def cpu_brick_oracle_rate(bl, target_s, kw, solver=None, sets=None):
     """The brick-set oracle (oracle/bricks.py, numpy fp64) as it stands, on a bounded
     sample: the first 8 solved bricks of the finest level with their counts."""
     import oracle.bricks as ob
-    s = bl.solvers[0]
-    sel = np.nonzero(~bl.frozen[0])[0][:8]
+    s = solver if solver is not None else bl.solvers[0]
+    coords, frozen = sets if sets is not None else (bl.coords[0], bl.frozen[0])
+    sel = np.nonzero(~np.asarray(frozen))[0][:8]
     counts = s.read_counts()[sel]
-    o = ob.BrickOracle(bl.edge, bl.coords[0][sel], **kw).load(counts)
+    o = ob.BrickOracle(bl.edge, np.asarray(coords)[sel], **kw).load(counts)
     t0 = time.perf_counter()
     o.iterate(1)
     t1 = time.perf_counter() - t0

@@ -187,3 +187,51 @@ def test_mixed_error_paths():
     assert s.info()["schedule"] == tgv.SCHEDULE_SPLIT
     with pytest.raises(tgv.TgvError):
         s.set_schedule("fused")
+
+
+def test_mixed_finest_level_matches_oracle_hierarchy():
+    """The C1 hierarchy (E = 4, 3 levels) with its finest level solved as a 2:1 mixed set:
+    A at level 0, the frozen border made of level-0 bricks under A's parents and of the
+    level-1 parent cubes elsewhere (R27); against the oracle solving the
+    same coarse levels and the same mixed set (votes per level, prolongation from level 1:
+    R19 for level-0 bricks, the parent's own u, v / 2 for level-1 bricks)."""
+    from paper_2107_14790_b200.brick_levels import BrickLevels
+    wl = synth.workload("C1")
+    depths = synth.render_depths(wl)
+    cams = [{"origin": c.origin, "rot": c.rot, "fx": c.f, "fy": c.f, "cx": c.width / 2.0, "cy": c.height / 2.0,
+             "width": c.width, "height": c.height, "vote_weight": c.vote_weight} for c in wl.cams]
+    E, levels, iters = 4, 3, 40
+    bl = BrickLevels((32, 32, 32), cams, depths, levels=levels, edge=E, min_votes=2, **KW)
+    m = bl.build_mixed()
+    _, coords, lv, fr = bl.mixed
+    assert (lv == 1).any() and (lv == 0).sum() > (~fr).sum()  # both kinds of border brick
+    s = bl.solve_mixed(iters)
+    assert s is m
+    # oracle: levels 2 and 1 (same sets as the GPU's), then the mixed set
+    o = ob.BrickOracle(E, bl.coords[2], bl.frozen[2], **KW)
+    o.load(ob.vote(bl.coords[2], E, cams, depths, voxel_size=4.0, r=2.0)).iterate(iters)
+    o1 = ob.BrickOracle(E, bl.coords[1], bl.frozen[1], **KW)
+    o1.load(ob.vote(bl.coords[1], E, cams, depths, voxel_size=2.0, r=1.0))
+    o1.set_primal(*ob.prolong(o, bl.coords[1]))
+    o1.iterate(iters)
+    counts = np.concatenate([ob.vote(coords[b:b + 1], E, cams, depths, voxel_size=float(1 << int(lv[b])),
+                                     r=0.5 * (1 << int(lv[b]))) for b in range(len(coords))])
+    mo = om.MixedOracle(E, lv, coords, fr, **KW).load(counts)
+    u0 = np.zeros((len(coords), E, E, E))
+    v0 = np.zeros((len(coords), 3, E, E, E))
+    fine = lv == 0
+    pu, pv = ob.prolong(o1, coords[fine])
+    u0[fine], v0[fine] = pu, pv
+    idx = {tuple(int(t) for t in c): i for i, c in enumerate(bl.coords[1])}
+    o1u, o1v = o1.get("u"), o1.get("v")
+    for b in np.nonzero(~fine)[0]:
+        j = idx[tuple(int(t) for t in coords[b])]
+        u0[b], v0[b] = o1u[j], 0.5 * o1v[j]
+    mo.set_primal(u0, v0).iterate(iters)
+    du = float(np.max(np.abs(s.read_u().astype(np.float64) - mo.get("u"))))
+    eg, eo = s.energy(), mo.energy()
+    assert du <= 1e-4, du
+    assert abs(eg["E"] - eo["E"]) <= 1e-5 * abs(eo["E"])
+    assert abs(eg["gap"] - eo["gap"]) <= 1e-5 * abs(eo["E"])
+    print(f"mixed finest level of C1: {len(coords)} bricks ({int((lv == 1).sum())} coarse), max|du| = {du:.2e}")
+    bl.close()
