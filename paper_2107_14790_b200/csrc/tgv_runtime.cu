@@ -392,11 +392,17 @@ int launch_tvl1_fused(tgv_ctx* c)
 int fused_zc(const tgv_ctx* c)
 {
     if (c->fused_zc > 0) return c->fused_zc;
-    if (c->fused_tma) {  // lock-step chunk of the persistent schedule: <= 256 planes, a divisor if possible
+    if (c->fused_tma) {  // lock-step chunk of the persistent schedule
+        // <= 256 planes: one chunk.  Deeper slabs: 128-plane chunks (a divisor near 128 if
+        // there is one).  The CTAs of a round march the chunk side by side and drift apart
+        // as they go; a neighbour's halo rows only hit L2 while the drift stays within the
+        // ~10 planes L2 holds, so shorter chunks keep more halo re-reads in L2.  Measured on
+        // C4 (1024^3, one B200, profiles/r2b_C4_probes.txt, r2c): zc 256 27.2-29.9 ms per
+        // launch, 128 25.8-26.4 ms, 96 27.8, 64 26.1-26.5 (chunk starts cost a plane each).
         if (c->g.nzl <= 256) return c->g.nzl;
-        for (int d = 256; d >= 128; --d)
+        for (int d = 128; d >= 112; --d)
             if (c->g.nzl % d == 0) return d;
-        return 256;
+        return 128;
     }
     const int tiles = c->fused_tma ? ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY)
                                    : ((c->g.nx + 29) / 30) * ((c->g.ny + FUSED_TY - 1) / FUSED_TY);
