@@ -62,7 +62,30 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     ap.add_argument("--vote", action="store_true", help="NEXT-2: measure GPU Alg. 1 voting instead of the solve")
     ap.add_argument("--no-self-check", action="store_true", help="N > 1: skip the slab-vs-one-context check")
-    return ap.parse_args()
+    # solver parameters (SPEC.md:387-388 names lambda, alpha0, alpha1; R1, R7): the workload's by default
+    ap.add_argument("--lambda", dest="lam", type=float, default=None, help="data weight lambda (R1)")
+    ap.add_argument("--alpha0", type=float, default=None)
+    ap.add_argument("--alpha1", type=float, default=None)
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--sigma", type=float, default=None)
+    a = ap.parse_args()
+    global ARGS
+    ARGS = a
+    return a
+
+
+ARGS = None
+
+
+def load_workload(name):
+    """synth.workload(name) with the command line's solver parameters applied."""
+    import dataclasses
+
+    import synth
+    wl = synth.workload(name)
+    over = {k: getattr(ARGS, k) for k in ("lam", "alpha0", "alpha1", "tau", "sigma")
+            if ARGS is not None and getattr(ARGS, k) is not None}
+    return dataclasses.replace(wl, **over) if over else wl
 
 
 # workloads whose inputs are voted on the GPU (bit-identical to the CPU generator,
@@ -164,7 +187,7 @@ def cpu_oracle_rate(workload: str, target_s: float, steps: int = 0, warmup: int 
     its own grid) for k iterations, all host threads."""
     import oracle
     import synth
-    wl = synth.workload(workload)
+    wl = load_workload(workload)
     nx, ny, nz = wl.shape
     zs = nz if wl.nvox <= 256 ** 3 else 16
     h = synth.make_histograms(workload, 0, zs)
@@ -197,7 +220,7 @@ def cpu_oracle_rate_1core(workload: str, target_s: float):
     over a bounded slab of the workload (at most 32 planes) as its own grid."""
     import oracle
     import synth
-    wl = synth.workload(workload)
+    wl = load_workload(workload)
     nx, ny, nz = wl.shape
     zs = min(nz, 32)
     h = synth.make_histograms(workload, 0, zs)
@@ -218,7 +241,7 @@ def run_reference(a):
     if rank != 0:
         return
     import synth
-    wl = synth.workload(a.workload)
+    wl = load_workload(a.workload)
     v, threads, sample, el = cpu_oracle_rate(a.workload, 0, steps=a.steps, warmup=a.warmup)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
@@ -275,7 +298,7 @@ def run_out_of_core(a):
     import synth
     from paper_2107_14790_b200 import out_of_core
     from paper_2107_14790_b200.multilevel import level_shapes
-    wl = synth.workload(a.workload)
+    wl = load_workload(a.workload)
     iters = a.iters or 200
     levels = max(1, a.levels)
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma)
@@ -386,7 +409,7 @@ def run_ours(a):
         ok, mode, nr = slab_self_check(rank, world, local)
         check = {"slab_bitwise": ok, "halo_mode": mode, "comm_ranks": nr,
                  "grid": [96, 64, 16 * world], "iters": 23}
-    wl = synth.workload(a.workload)
+    wl = load_workload(a.workload)
     iters = a.iters or wl.iters
     nx, ny, nz = wl.shape
     z0, z1 = slab(nz, rank, world)
@@ -557,6 +580,8 @@ def run_ours(a):
                        "step": ("reset + iters x (dual, primal+over-relax) + energy/gap" if a.levels == 1 else
                                 f"coarse-to-fine: restrict to {a.levels} levels, iters per level, prolong, energy"),
                        "model": a.model, "schedule": a.schedule, "levels": a.levels,
+                       "params": {"lambda": wl.lam, "alpha0": wl.alpha0, "alpha1": wl.alpha1, "tau": wl.tau,
+                                  "sigma": wl.sigma},
                        "parallelism": (f"z-slab x{world}, halos " + ("written by the kernel into the neighbours "
                                        "(peer mode)" if info.get("peer_halo") else "by NCCL send/recv"))
                        if world > 1 else "single GPU",
@@ -602,7 +627,7 @@ def run_brick_parts(a):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = synth.workload(a.workload)
+    wl = load_workload(a.workload)
     iters = a.iters or wl.iters
     levels = max(2, a.levels if a.levels > 1 else 3)
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
@@ -679,7 +704,7 @@ def run_bricks(a):
     from paper_2107_14790_b200.brick_levels import BrickLevels
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and int(os.environ.get("RANK", "0")) != 0:
         return  # single-GPU measurement: the other ranks have no work
-    wl = synth.workload(a.workload)
+    wl = load_workload(a.workload)
     iters = a.iters or wl.iters
     levels = max(2, a.levels if a.levels > 1 else 3)
     kw = dict(lam=wl.lam, alpha0=wl.alpha0, alpha1=wl.alpha1, tau=wl.tau, sigma=wl.sigma, centers=list(wl.centers))
