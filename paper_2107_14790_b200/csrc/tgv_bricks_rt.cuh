@@ -56,6 +56,12 @@ struct tgv_bricks {
     uint8_t* d_sface = nullptr;  // [nbricks][6]
     int* d_mfaces = nullptr;     // (frozen brick, face | quadrant mask << 3) towards solved voxels
     int n_mfaces = 0;
+    // solved bricks split by stencil: level 0 with only same-level (or no) face neighbours
+    // run the uniform brick kernels (R27's operators are R24's there, bit for bit), the
+    // rest the mixed kernels
+    int* d_alist_reg = nullptr;
+    int* d_alist_gen = nullptr;
+    int n_alist_reg = 0, n_alist_gen = 0;
 
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // pairs
@@ -219,8 +225,9 @@ void launch_mixed_energy_le(tgv_bricks* c, const EnergyArgs& ea)
 template <int LE>
 void launch_mixed_dual_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
 {
-    const int n0 = c->n_alist << (3 * LE), n1 = c->n_mfaces << (2 * LE);
-    if (n0) mixed_dual_kernel<LE, 0><<<(n0 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_alist, n0);
+    const int nr = c->n_alist_reg << (3 * LE), n0 = c->n_alist_gen << (3 * LE), n1 = c->n_mfaces << (2 * LE);
+    if (nr) brick_dual_kernel<LE, 0><<<(nr + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_alist_reg, nr);
+    if (n0) mixed_dual_kernel<LE, 0><<<(n0 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_alist_gen, n0);
     if (n1) mixed_dual_kernel<LE, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_mfaces, n1);
 }
 
@@ -228,9 +235,18 @@ template <int LE>
 void launch_mixed_primal_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp)
 {
     const Centers C = bcenters(c);
-    const int n = c->n_alist << (3 * LE), blocks = (n + 255) / 256;
+    const int nr = c->n_alist_reg << (3 * LE), br = (nr + 255) / 256;
+    if (nr) {
+        const BrickGeo bg = bgeo(c);
+        const int* R = c->d_alist_reg;
+        if (c->slots == 8 && c->count_bytes == 1) brick_primal_kernel<LE, 8, uint8_t><<<br, 256, 0, c->stream>>>(a, bg, sp, C, R, nr);
+        else if (c->slots == 8) brick_primal_kernel<LE, 8, uint16_t><<<br, 256, 0, c->stream>>>(a, bg, sp, C, R, nr);
+        else if (c->count_bytes == 1) brick_primal_kernel<LE, 16, uint8_t><<<br, 256, 0, c->stream>>>(a, bg, sp, C, R, nr);
+        else brick_primal_kernel<LE, 16, uint16_t><<<br, 256, 0, c->stream>>>(a, bg, sp, C, R, nr);
+    }
+    const int n = c->n_alist_gen << (3 * LE), blocks = (n + 255) / 256;
     if (!n) return;
-    const int* L = c->d_alist;
+    const int* L = c->d_alist_gen;
     const MixGeo g = mgeo(c);
     if (c->slots == 8 && c->count_bytes == 1) mixed_primal_kernel<LE, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
     else if (c->slots == 8) mixed_primal_kernel<LE, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(a, g, sp, C, L, n);
@@ -736,6 +752,22 @@ int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* leve
     }
     c->s_voxels = sv;
     c->n_mfaces = (int)mf.size() / 2;
+    std::vector<int> reg, gen;
+    for (int64_t b = 0; b < nb; ++b) {
+        if (fr[(size_t)b]) continue;
+        bool regular = levels[b] == 0;
+        for (int f = 0; f < 6; ++f) regular &= kind[(size_t)b * 6 + f] <= 1;
+        (regular ? reg : gen).push_back((int)b);
+    }
+    c->n_alist_reg = (int)reg.size();
+    c->n_alist_gen = (int)gen.size();
+    if (cudaMalloc(&c->d_alist_reg, sizeof(int) * std::max<size_t>(1, reg.size())) != cudaSuccess ||
+        cudaMalloc(&c->d_alist_gen, sizeof(int) * std::max<size_t>(1, gen.size())) != cudaSuccess ||
+        (!reg.empty() && cudaMemcpy(c->d_alist_reg, reg.data(), sizeof(int) * reg.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
+        (!gen.empty() && cudaMemcpy(c->d_alist_gen, gen.data(), sizeof(int) * gen.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+        cudaGetLastError();
+        return bfail(c, TGV_ENOMEM, "mixed-level brick lists allocation failed");
+    }
     c->mixed = true;
     c->schedule = TGV_SCHEDULE_SPLIT;
     c->levels_h.assign(levels, levels + nb);
@@ -996,6 +1028,8 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->d_par);
     cudaFree(c->d_sface);
     cudaFree(c->d_mfaces);
+    cudaFree(c->d_alist_reg);
+    cudaFree(c->d_alist_gen);
     cudaFree(c->hist);
     cudaFree(c->partials);
     cudaFree(c->d_out);

@@ -846,14 +846,18 @@ EnergyConsts energy_consts(const float* centers, int nbins, int slots)
     return K;
 }
 
-// z-marching items of the energy sweep: about 8 per block, so the last round is short
+// z-marching items of the energy sweep: at least 8 per block (a short last round) and
+// chunks of <= 64 planes: the blocks of a round march side by side, and a neighbouring
+// row group's halo rows only hit L2 while their drift stays small (C4 with whole
+// 1024-plane columns read 24 % more DRAM than the algorithmic bytes, profiles/r2d_*)
 EnergySched energy_sched(const Geo& g, int blocks)
 {
     EnergySched es{};
     es.ntx = (g.nx + 31) / 32;
     es.nyg = (g.ny + 7) / 8;
     const int64_t cols = (int64_t)es.ntx * es.nyg;
-    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(g.nzl, (8LL * blocks + cols - 1) / cols));
+    const int64_t want = std::max<int64_t>((g.nzl + 63) / 64, (8LL * blocks + cols - 1) / cols);
+    const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(g.nzl, want));
     es.zc = (int)((g.nzl + nch - 1) / nch);
     es.items = (int)(cols * ((g.nzl + es.zc - 1) / es.zc));
     return es;

@@ -113,7 +113,8 @@ def test_box_of_solved_bricks_is_the_dense_split_schedule_bitwise():
         for i, (bx, by, bz) in enumerate(coords):
             blk = a[lead + (slice(bz * E, (bz + 1) * E), slice(by * E, (by + 1) * E), slice(bx * E, (bx + 1) * E))]
             assert np.array_equal(b[i], blk), (name, i)
-    assert s.energy()["E"] == pytest.approx(d.energy()["E"], rel=1e-12)
+    # the dense energy kernel forms fp32 per-voxel terms (fp64 sums), the brick kernel fp64 ones
+    assert s.energy()["E"] == pytest.approx(d.energy()["E"], rel=1e-6)
     d.close()
 
 
