@@ -60,4 +60,18 @@ fb.set_primal(np.full((4, 32, 32, 32), 0.25, np.float32), np.full((4, 3, 32, 32,
 fb.iterate(2)
 fb.energy()
 fb.close()
+# 2:1 mixed-level set (R27): a level-1 brick with level-0 bricks on its +x face (one quadrant
+# missing) and a same-level chain; frozen bricks of both levels; the uniform kernels on its
+# regular bricks, the mixed kernels (dual on solved bricks and frozen faces, primal, energy),
+# votes per level and prolongation into levels 0 / 1
+ml = np.array([1, 0, 0, 0, 0, 1], np.uint8)
+mc = np.array([(0, 0, 0), (2, 0, 0), (2, 1, 0), (2, 0, 1), (3, 0, 0), (0, 1, 0)], np.int32)
+mf = np.array([0, 0, 1, 0, 0, 1], bool)
+mco = BrickSolver(8, np.array([(0, 0, 0), (1, 0, 0), (0, 1, 0)], np.int32)).vote([cam], [np.full((64, 64), 50.0, np.float32)])
+mco.iterate(2)
+mx = BrickSolver(8, mc, mf, levels=ml).vote([cam], [np.full((64, 64), 50.0, np.float32)]).prolong_from(mco)
+mx.iterate(3)
+mx.energy()
+mx.close()
+mco.close()
 print("sanitize probe done")
