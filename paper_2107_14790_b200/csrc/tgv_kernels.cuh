@@ -20,6 +20,7 @@
 // Histograms: 8 (or 16) counts per voxel, u8 when every count <= 255 else u16,
 // one vector load per voxel, no halo planes.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -847,31 +848,6 @@ struct EnergyConsts {
     float cf[16], c1f[16], dcf[16], endf;  // the same in fp32 (dense energy kernel)
 };
 
-// data_box_terms in fp32 (the dense energy kernel's per-voxel terms; fp64 accumulation)
-template <int SLOTS, typename CT>
-__device__ __forceinline__ void data_box_terms_f32(const HistRaw<SLOTS, CT>& h, const EnergyConsts& K, float lam,
-                                                   float u, float divp, float& data, float& box)
-{
-    float d = 0.f, G = 0.f, f = 0.f, best = 0.f, W = 0.f;
-#pragma unroll
-    for (int b = 0; b < SLOTS; ++b) W += hist_count<SLOTS, CT>(h, b);
-    float slope = -fmaf(lam, W, divp);
-    const float l2 = 2.f * lam;
-#pragma unroll
-    for (int b = 0; b < SLOTS; ++b) {
-        const float hb = hist_count<SLOTS, CT>(h, b);
-        d = fmaf(hb, fabsf(u - K.cf[b]), d);
-        G = fmaf(hb, K.c1f[b], G);
-        f = fmaf(K.dcf[b], slope, f);
-        best = fminf(best, f);
-        slope = fmaf(l2, hb, slope);
-    }
-    f = fmaf(K.endf, slope, f);
-    best = fminf(best, f);
-    data = lam * d;
-    box = fmaf(lam, G, divp) + best;
-}
-
 // count b as an exact double: the count in the low mantissa word of 2^52, minus 2^52
 template <int SLOTS, typename CT>
 __device__ __forceinline__ double hist_count_f64(const HistRaw<SLOTS, CT>& h, int b)
@@ -896,6 +872,36 @@ __device__ __forceinline__ uint32_t hist_total(const HistRaw<SLOTS, CT>& h)
         for (int k = 0; k < SLOTS / 2; ++k) W += (h.w[k] & 0xffffu) + (h.w[k] >> 16);
     }
     return W;
+}
+
+// data_box_terms in fp32 (the dense energy kernel's per-voxel terms; fp64 accumulation)
+template <int SLOTS, typename CT>
+__device__ __forceinline__ void data_box_terms_f32(const HistRaw<SLOTS, CT>& h, const EnergyConsts& K, float lam,
+                                                   float u, float divp, float& data, float& box)
+{
+    const uint32_t Wi = hist_total<SLOTS, CT>(h);
+    if (Wi == 0) {  // no votes: G = 0, so min over [-1, 1] of -x divp is -|divp| (unobserved space)
+        data = 0.f;
+        box = -fabsf(divp);
+        return;
+    }
+    float d = 0.f, G = 0.f, f = 0.f, best = 0.f;
+    const float W = (float)Wi;
+    float slope = -fmaf(lam, W, divp);
+    const float l2 = 2.f * lam;
+#pragma unroll
+    for (int b = 0; b < SLOTS; ++b) {
+        const float hb = hist_count<SLOTS, CT>(h, b);
+        d = fmaf(hb, fabsf(u - K.cf[b]), d);
+        G = fmaf(hb, K.c1f[b], G);
+        f = fmaf(K.dcf[b], slope, f);
+        best = fminf(best, f);
+        slope = fmaf(l2, hb, slope);
+    }
+    f = fmaf(K.endf, slope, f);
+    best = fminf(best, f);
+    data = lam * d;
+    box = fmaf(lam, G, divp) + best;
 }
 
 // Per voxel, in fp64 (PAPER.md:153 data term with the R2 histogram form; R14 box dual):
@@ -979,26 +985,36 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
             const float v0y = L(ea.v[0], i - sy), v1y = L(ea.v[1], i - sy), v2y = L(ea.v[2], i - sy),
                         p1y = L(ea.p[1], i - sy);
             const auto h = load_hist<SLOTS, CT>(ea.hist, hv);
-            // ---- per-voxel terms (the masks are R6's Neumann D+ / D-)
-            auto dp = [](bool l, float a, float b) { return l ? a - b : 0.f; };
-            auto dm = [](bool l, bool f, float a, float b) { return (l ? a : 0.f) - (f ? b : 0.f); };
-            const float a0 = dp(xl, ux, uc) - v0, a1 = dp(yl, uy, uc) - v1, a2 = dp(zl, un, uc) - v2;
-            t1 += (double)(al1 * sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2))));
-            const float exx = dm(xl, xf, v0, v0x), eyy = dm(yl, yf, v1, v1y), ezz = dm(zl, zf, v2, vm2);
-            const float exy = 0.5f * (dm(yl, yf, v0, v0y) + dm(xl, xf, v1, v1x));
-            const float exz = 0.5f * (dm(zl, zf, v0, vm0) + dm(xl, xf, v2, v2x));
-            const float eyz = 0.5f * (dm(zl, zf, v1, vm1) + dm(yl, yf, v2, v2y));
-            const float off = fmaf(exy, exy, fmaf(exz, exz, eyz * eyz));
-            t0 += (double)(al0 * sqrtf(fmaf(exx, exx, fmaf(eyy, eyy, fmaf(ezz, ezz, 2.f * off)))));
-            const float divp = dm(xl, xf, p0, p0x) + dm(yl, yf, p1, p1y) + dm(zl, zf, p2, pzm);
-            const float w0 = dp(xl, qxxx, qxx) + dp(yl, qxyy, qxy) + dp(zl, qxzn, qxz);
-            const float w1 = dp(xl, qxyx, qxy) + dp(yl, qyyy, qyy) + dp(zl, qyzn, qyz);
-            const float w2 = dp(xl, qxzx, qxz) + dp(yl, qyzy, qyz) + dp(zl, qzzn, qzz);
-            const float l1 = fabsf(p0 + w0) + fabsf(p1 + w1) + fabsf(p2 + w2);
-            float data, box;
-            data_box_terms_f32<SLOTS, CT>(h, K, lam, uc, divp, data, box);
-            td += (double)data;
-            dv += (double)box - (double)(VV * l1);
+            // ---- per-voxel terms (the masks are R6's Neumann D+ / D-; compile-time true away
+            // from the grid's faces, where nearly every voxel is)
+            auto terms = [&](auto INTc) {
+                constexpr bool INT = decltype(INTc)::value;
+                const bool xl_ = INT || xl, yl_ = INT || yl, zl_ = INT || zl, xf_ = INT || xf, yf_ = INT || yf,
+                           zf_ = INT || zf;
+                auto dp = [](bool l, float a, float b) { return l ? a - b : 0.f; };
+                auto dm = [](bool l, bool f, float a, float b) { return (l ? a : 0.f) - (f ? b : 0.f); };
+                const float a0 = dp(xl_, ux, uc) - v0, a1 = dp(yl_, uy, uc) - v1, a2 = dp(zl_, un, uc) - v2;
+                t1 += (double)(al1 * sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2))));
+                const float exx = dm(xl_, xf_, v0, v0x), eyy = dm(yl_, yf_, v1, v1y), ezz = dm(zl_, zf_, v2, vm2);
+                const float exy = 0.5f * (dm(yl_, yf_, v0, v0y) + dm(xl_, xf_, v1, v1x));
+                const float exz = 0.5f * (dm(zl_, zf_, v0, vm0) + dm(xl_, xf_, v2, v2x));
+                const float eyz = 0.5f * (dm(zl_, zf_, v1, vm1) + dm(yl_, yf_, v2, v2y));
+                const float off = fmaf(exy, exy, fmaf(exz, exz, eyz * eyz));
+                t0 += (double)(al0 * sqrtf(fmaf(exx, exx, fmaf(eyy, eyy, fmaf(ezz, ezz, 2.f * off)))));
+                const float divp = dm(xl_, xf_, p0, p0x) + dm(yl_, yf_, p1, p1y) + dm(zl_, zf_, p2, pzm);
+                const float w0 = dp(xl_, qxxx, qxx) + dp(yl_, qxyy, qxy) + dp(zl_, qxzn, qxz);
+                const float w1 = dp(xl_, qxyx, qxy) + dp(yl_, qyyy, qyy) + dp(zl_, qyzn, qyz);
+                const float w2 = dp(xl_, qxzx, qxz) + dp(yl_, qyzy, qyz) + dp(zl_, qzzn, qzz);
+                const float l1 = fabsf(p0 + w0) + fabsf(p1 + w1) + fabsf(p2 + w2);
+                float data, box;
+                data_box_terms_f32<SLOTS, CT>(h, K, lam, uc, divp, data, box);
+                td += (double)data;
+                dv += (double)box - (double)(VV * l1);
+            };
+            if (xl && xf && yl && yf && zl && zf)
+                terms(std::true_type{});
+            else
+                terms(std::false_type{});
             vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
             // ---- carry
             vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;
