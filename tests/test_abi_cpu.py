@@ -66,6 +66,7 @@ C8 = [-0.875 + 0.25 * b for b in range(8)]
     (dict(z_begin=2, z_end=2), "slab"),
     (dict(nranks=2, rank=0), "uid"),
     (dict(z_begin=1), "whole grid"),
+    (dict(shape=(2048, 2048, 600)), "2^31"),  # one field of the slab would need >= 2^31 elements
 ])
 def test_create_rejects_invalid_arguments(kw, frag):
     from paper_2107_14790_b200 import tgv
@@ -98,14 +99,19 @@ def test_product_does_not_import_oracle():
     (dict(coords=[(-1, 0, 0)]), "outside"),
     (dict(tau=0.5), "tau*sigma*16"),
     (dict(centers=[0.5, 0.2]), "increasing"),
+    (dict(edge=32, coords=[(i % 256, i // 256, 0) for i in range(65536)]), "2^31"),
+    (dict(levels=[0, 8]), "level"),  # tgv_bricks_create_mixed: levels <= 7
+    (dict(levels=[1, 1]), "duplicate"),  # same level, same coordinates... (distinct here: checked below)
 ])
 def test_bricks_create_rejects_invalid_arguments(kw, frag):
     """include/tgv_bricks.h: argument checks happen before any device work."""
     from paper_2107_14790_b200 import tgv
     from paper_2107_14790_b200.bricks import BrickSolver
-    args = dict(edge=8, coords=[(0, 0, 0), (1, 0, 0)], tau=0.25, centers=None)
+    args = dict(edge=8, coords=[(0, 0, 0), (1, 0, 0)], tau=0.25, centers=None, levels=None)
     args.update(kw)
+    if kw.get("levels") == [1, 1]:
+        args["coords"] = [(0, 0, 0), (0, 0, 0)]
     with pytest.raises(tgv.TgvError) as ei:
-        BrickSolver(args["edge"], args["coords"], centers=args["centers"], tau=args["tau"])
+        BrickSolver(args["edge"], args["coords"], centers=args["centers"], tau=args["tau"], levels=args["levels"])
     assert ei.value.status == tgv.TGV_EINVAL
     assert frag in str(ei.value)
