@@ -101,7 +101,7 @@ def test_product_does_not_import_oracle():
     (dict(centers=[0.5, 0.2]), "increasing"),
     (dict(edge=32, coords=[(i % 256, i // 256, 0) for i in range(65536)]), "2^31"),
     (dict(levels=[0, 8]), "level"),  # tgv_bricks_create_mixed: levels <= 7
-    (dict(levels=[1, 1]), "duplicate"),  # same level, same coordinates... (distinct here: checked below)
+    (dict(levels=[1, 1], coords=[(0, 0, 0), (0, 0, 0)]), "duplicate"),  # same level and coordinates
 ])
 def test_bricks_create_rejects_invalid_arguments(kw, frag):
     """include/tgv_bricks.h: argument checks happen before any device work."""
@@ -109,8 +109,6 @@ def test_bricks_create_rejects_invalid_arguments(kw, frag):
     from paper_2107_14790_b200.bricks import BrickSolver
     args = dict(edge=8, coords=[(0, 0, 0), (1, 0, 0)], tau=0.25, centers=None, levels=None)
     args.update(kw)
-    if kw.get("levels") == [1, 1]:
-        args["coords"] = [(0, 0, 0), (0, 0, 0)]
     with pytest.raises(tgv.TgvError) as ei:
         BrickSolver(args["edge"], args["coords"], centers=args["centers"], tau=args["tau"], levels=args["levels"])
     assert ei.value.status == tgv.TGV_EINVAL
