@@ -946,7 +946,9 @@ struct EnergySched {
 // state (relative error of each term ~1e-7) and REDUCED in fp64: per-thread fp64 sums,
 // warp shuffles, fixed-order block partials (energy_final_kernel): deterministic.  (An
 // all-fp64 version spent its time in 38 fp32->fp64 conversions per voxel on the XU pipe:
-// 0.43 of the copy roofline, profiles/r2b_energy_*.)
+// 0.43 of the copy roofline, profiles/r2b_energy_*.)  One barrier per plane keeps a block's
+// warps in step: free-running warps drifted apart and read 24 % more DRAM than the
+// algorithmic bytes on C4 (profiles/r2e_C4_launches_summary.txt).
 template <int SLOTS, typename CT>
 __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     energy_partial_kernel(const EnergyArgs ea, Geo g, const EnergyConsts K, const EnergySched es,
@@ -959,9 +961,12 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     const float al1 = (float)ea.alpha1, al0 = (float)ea.alpha0, lam = (float)ea.lambda, VV = (float)ea.V;
     for (int it = blockIdx.x; it < es.items; it += gridDim.x) {
         const int xt = it % es.ntx, r = it / es.ntx;
-        const int x = xt * 32 + lane, y = (r % es.nyg) * 8 + wid;
+        // cells past the grid's x / y ends (ragged last tile / row group) march along on a
+        // clamped in-grid cell without accumulating: every thread reaches the per-plane barrier
+        const int xr = xt * 32 + lane, yr = (r % es.nyg) * 8 + wid;
+        const bool act = xr < g.nx && yr < g.ny;
+        const int x = min(xr, g.nx - 1), y = min(yr, g.ny - 1);
         const int za = (r / es.nyg) * es.zc, zb = min(g.nzl, za + es.zc);
-        if (x >= g.nx || y >= g.ny) continue;
         const bool xl = x < g.nx - 1, yl = y < g.ny - 1, xf = x > 0, yf = y > 0;
         int i = eoff(g, x, y, za);
         int64_t hv = (int64_t)za * g.plane + (int64_t)y * g.px + x;
@@ -1011,14 +1016,19 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
                 td += (double)data;
                 dv += (double)box - (double)(VV * l1);
             };
-            if (xl && xf && yl && yf && zl && zf)
-                terms(std::true_type{});
-            else
-                terms(std::false_type{});
-            vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
+            if (act) {
+                if (xl && xf && yl && yf && zl && zf)
+                    terms(std::true_type{});
+                else
+                    terms(std::false_type{});
+                vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
+            }
             // ---- carry
             vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;
             uc = un, qzz = qzzn, qxz = qxzn, qyz = qyzn;
+            // the block's 8 rows advance plane by plane together, so the rows a warp reads from
+            // its neighbours are the ones they just loaded (L2 / L1 hits, not a second DRAM read)
+            __syncthreads();
         }
     }
     __shared__ double red[EN_TERMS][8];
