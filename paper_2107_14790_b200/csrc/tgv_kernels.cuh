@@ -946,9 +946,10 @@ struct EnergySched {
 // state (relative error of each term ~1e-7) and REDUCED in fp64: per-thread fp64 sums,
 // warp shuffles, fixed-order block partials (energy_final_kernel): deterministic.  (An
 // all-fp64 version spent its time in 38 fp32->fp64 conversions per voxel on the XU pipe:
-// 0.43 of the copy roofline, profiles/r2b_energy_*.)  One barrier per plane keeps a block's
-// warps in step: free-running warps drifted apart and read 24 % more DRAM than the
-// algorithmic bytes on C4 (profiles/r2e_C4_launches_summary.txt).
+// 0.43 of the copy roofline, profiles/r2b_energy_*.)  On C4 the halo rows / sectors of
+// neighbouring items mostly miss L2 (DRAM reads 1.24x the algorithmic bytes,
+// profiles/r2e_C4_launches_summary.txt); a barrier per plane to keep a block's rows in step
+// made it worse (1.34x, profiles/r2f_*) and is not used.
 template <int SLOTS, typename CT>
 __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     energy_partial_kernel(const EnergyArgs ea, Geo g, const EnergyConsts K, const EnergySched es,
@@ -1026,9 +1027,6 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
             // ---- carry
             vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;
             uc = un, qzz = qzzn, qxz = qxzn, qyz = qyzn;
-            // the block's 8 rows advance plane by plane together, so the rows a warp reads from
-            // its neighbours are the ones they just loaded (L2 / L1 hits, not a second DRAM read)
-            __syncthreads();
         }
     }
     __shared__ double red[EN_TERMS][8];
