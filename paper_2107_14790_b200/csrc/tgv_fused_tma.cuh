@@ -77,20 +77,6 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, uin
         "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
-// L2 prefetch of a box (no shared memory, no completion): the planes beyond the rings'
-// lookahead reach L2 early, so the ring loads that follow see L2 latency
-__device__ __forceinline__ void tma_prefetch4(const CUtensorMap* map, int c0, int c1, int c2, int c3)
-{
-    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0),
-                 "r"(c1), "r"(c2), "r"(c3)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int c0, int c1, int c2)
-{
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
-                 "r"(c2)
-                 : "memory");
-}
 __device__ __forceinline__ void tma_store4(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3)
 {
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
@@ -153,7 +139,6 @@ struct TmaArgs {
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
     int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
-    int l2pf;            // > 0: also prefetch into L2 the plane this many planes beyond each ring fill
     // Peer halo mode: the kernel itself writes the next iterate of its
     // boundary planes into the neighbours' halo planes (NVLink / same-device stores,
     // tile by tile as they are computed) -- down: u, v, q of plane 0 into the lower
@@ -271,10 +256,6 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             mbar_expect_tx(&S.bar_u[st], 2 * R * TMA_BW * 4);
             tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
             tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
-            if (A.l2pf > 0 && s + A.l2pf <= ze + 1) {
-                tma_prefetch4(&m_ld1, x0 - 4, y0 - 1, zclamp(s + A.l2pf), A.s_uk);
-                tma_prefetch4(&m_ld1, x0 - 4, y0 - 1, zclamp(s + A.l2pf), A.s_um);
-            }
         };
         auto issue_x = [&](int s) {  // v_k, v_{k-1}, p_k, q_k and the counts of plane s
             const int st = ix.st;
@@ -285,14 +266,6 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
             tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
             tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
-            if (A.l2pf > 0 && s + A.l2pf <= ze) {
-                const int sp_ = s + A.l2pf;
-                tma_prefetch4(&m_ld3, x0 - 4, y0 - 1, zclamp(sp_), A.s_vk);
-                tma_prefetch4(&m_ld3, x0 - 4, y0 - 1, zclamp(sp_), A.s_vm);
-                tma_prefetch4(&m_ld3, x0 - 4, y0 - 1, zclamp(sp_), A.s_pk);
-                tma_prefetch4(&m_ld6, x0 - 4, y0 - 1, zclamp(sp_), A.s_qk);
-                tma_prefetch3(&m_h, 8 * x0, y0, min(max(sp_, 0), g.nzl - 1));
-            }
         };
 
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
