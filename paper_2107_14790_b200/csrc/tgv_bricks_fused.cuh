@@ -48,12 +48,6 @@ __device__ __forceinline__ void bf_cp_async4(void* dst, const float* src)
         : "memory");
 }
 
-// L2 prefetch of one global line (no register, no completion)
-__device__ __forceinline__ void bf_prefetch_l2(const void* src)
-{
-    asm volatile("{\n .reg .u64 g;\n cvta.to.global.u64 g, %0;\n prefetch.global.L2 [g];\n}\n" ::"l"(src) : "memory");
-}
-
 struct BrickFusedArgs {
     IterPtrs a;
     StepParams sp;
@@ -62,7 +56,6 @@ struct BrickFusedArgs {
     const uint8_t* frozen;  // [nbricks]
     int n_alist;
     int fold_x;             // 1: this kernel stores the frozen x-faces' duals (else the face launch does)
-    int l2pf;               // > 0: the row warps prefetch their cells of plane s + l2pf into L2 at step s
 };
 
 template <int LE, int SLOTS, typename CT>
@@ -245,24 +238,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
 
     for (int s = -1; s <= E; ++s) {
         const int par = s & 1, pr = par ^ 1;
-        if (A.l2pf > 0 && role < 3) {  // deeper lookahead through L2 (the register prefetch is one plane)
-            const int ip = (s + A.l2pf <= E + 1) ? at(s + A.l2pf) : -1;
-            if (ip >= 0) {
-                bf_prefetch_l2(a.uk + ip);
-                bf_prefetch_l2(a.um + ip);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    bf_prefetch_l2(a.vk[k] + ip);
-                    bf_prefetch_l2(a.vm[k] + ip);
-                    bf_prefetch_l2(a.pk[k] + ip);
-                }
-#pragma unroll
-                for (int m = 0; m < 6; ++m) bf_prefetch_l2(a.qk[m] + ip);
-                if (role == 0 && s + A.l2pf < E)
-                    bf_prefetch_l2(static_cast<const uint8_t*>(a.hist) +
-                                   (size_t)(base_0 + ((s + A.l2pf) << (2 * LE))) * SLOTS * sizeof(CT));
-            }
-        }
         // prefetch: u at s+2, the other fields and the counts at s+1
         const U2 u2 = load_u(s + 2);
         const X x1 = load_x(s + 1);

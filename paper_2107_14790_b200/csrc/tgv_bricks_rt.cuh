@@ -301,8 +301,7 @@ int brick_iterate_fused(tgv_bricks* c, int32_t n)
             if ((rc = btimer(c, 0, true))) return rc;
         }
         if (c->n_alist) {
-            BrickFusedArgs A{a, sp, bcenters(c), c->d_nb27, c->frozen, c->n_alist, fold_x,
-                             (int)env_int("TGV_BRICK_L2_PREFETCH", 0)};  // dev knob until measured
+            BrickFusedArgs A{a, sp, bcenters(c), c->d_nb27, c->frozen, c->n_alist, fold_x};
             if ((rc = btimer(c, 3, false))) return rc;
             if (c->slots == 8 && c->count_bytes == 1) launch_brick_fused_t<8, uint8_t>(c, A);
             else if (c->slots == 8) launch_brick_fused_t<8, uint16_t>(c, A);
