@@ -302,6 +302,31 @@ int tgv_sync(tgv_ctx* ctx);
  * n_voxels must equal (z_end-z_begin)*ny*nx.  Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
 int tgv_read_u(tgv_ctx* ctx, float* u_out, int64_t n_voxels);
 
+/* Pipelined host I/O (a solve loop that overlaps the next step's input upload and this
+ * step's result download with the iterations; DESIGN.md §7 "e2e"):
+ *   tgv_stage_histograms  enqueue the H2D copy of this rank's counts (layout of
+ *                         tgv_load_histograms, unsigned integers of count_bytes = 1, 2 or 4
+ *                         bytes) into a device staging area on the context's upload stream
+ *                         and return; it first waits (on the device) until the previously
+ *                         staged counts were consumed.  The host buffer must stay valid and
+ *                         unchanged until the next tgv_load_staged returns; pinned memory
+ *                         lets the copy run beside the iterations.
+ *   tgv_load_staged       tgv_load_histograms from the staged counts (waits for the copy on
+ *                         the device; state reset as in tgv_load_histograms).  Blocks.
+ *   tgv_read_u_async      snapshot u on the device (ordered after the iterations enqueued
+ *                         so far), then copy it to u_out on the download stream and return;
+ *                         u_out must stay valid until tgv_wait_io.  A second call first waits
+ *                         (on the device) until the previous download has left the snapshot.
+ *   tgv_wait_io           wait for both copy streams.
+ * The staging area holds one whole slab of counts (count_bytes per count) and the snapshot one
+ * slab of u; both are allocated at first use.
+ * Errors: TGV_EINVAL (NULL, size, count_bytes), TGV_ESTATE (load_staged with nothing staged,
+ * read before load), TGV_ERANGE (a count > 65535), TGV_ENOMEM, TGV_ECUDA. */
+int tgv_stage_histograms(tgv_ctx* ctx, const void* counts, int count_bytes, int64_t n_counts);
+int tgv_load_staged(tgv_ctx* ctx);
+int tgv_read_u_async(tgv_ctx* ctx, float* u_out, int64_t n_voxels);
+int tgv_wait_io(tgv_ctx* ctx);
+
 /* Copy one state field (TGV_FIELD_*) of this rank to the host, same layout
  * and size rule as tgv_read_u.  Errors as tgv_read_u; TGV_EINVAL for a bad id. */
 int tgv_read_field(tgv_ctx* ctx, int field, float* out, int64_t n_voxels);

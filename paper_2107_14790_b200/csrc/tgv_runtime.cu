@@ -88,7 +88,7 @@ struct tgv_ctx {
     int* d_sched_off = nullptr;
     int sched_ctas = 0, sched_zc = -1, sched_per_sm = 1;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
-    CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
+    CUtensorMap m_ld1{}, m_ld3{}, m_ld3n{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
     Geo g{};
     int slots = 8;            // histogram slots per voxel
@@ -103,6 +103,13 @@ struct tgv_ctx {
     float* upload = nullptr;  // grow-only device buffer for tgv_prolong_slab's coarse fields
     size_t upload_bytes = 0;
     int64_t staging_elems = 0;
+    // pipelined host I/O (tgv_stage_histograms / tgv_load_staged / tgv_read_u_async)
+    void* stage = nullptr;          // whole-slab count staging (count_bytes per count)
+    size_t stage_bytes = 0;
+    int stage_cb = 0;               // count_bytes of the staged counts, 0: nothing staged
+    float* usnap = nullptr;         // u snapshot read by the asynchronous D2H
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr, ev_snap = nullptr, ev_read = nullptr;
     int energy_blocks = 0;
     int64_t device_bytes = 0;
     int64_t k = 0;  // iteration counter
@@ -473,7 +480,8 @@ int make_state_maps(tgv_ctx* c)
     int rc;
     if ((rc = make_state_map(c, &c->m_ld1, TMA_BW, TMA_TY + 2, 1))) return rc;
     if ((rc = make_state_map(c, &c->m_ld3, TMA_BW, TMA_TY + 2, 3))) return rc;
-    if ((rc = make_state_map(c, &c->m_ld6, TMA_BW, TMA_TY + 2, 6))) return rc;
+    if ((rc = make_state_map(c, &c->m_ld3n, TMA_PW, TMA_TY + 2, 3))) return rc;  // p: x0-4 .. x0+31
+    if ((rc = make_state_map(c, &c->m_ld6, TMA_PW, TMA_TY + 2, 6))) return rc;   // q: x0 .. x0+35
     if ((rc = make_state_map(c, &c->m_st1, 32, TMA_TY, 1))) return rc;
     if ((rc = make_state_map(c, &c->m_st3, 32, TMA_TY, 3))) return rc;
     return make_state_map(c, &c->m_st6, 32, TMA_TY, 6);
@@ -569,7 +577,7 @@ int launch_fused_tma_tp(tgv_ctx* c, const TmaArgs& A, dim3 grd)
         attr_set.fetch_or(bit);
     }
     fused_tma_kernel<TMA_TY, SLOTS, CT, PEER><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
-        c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
+        c->m_ld1, c->m_ld3, c->m_ld3n, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, A);
     return TGV_OK;
 }
 template <int SLOTS, typename CT>
@@ -588,6 +596,7 @@ int launch_fused_tma(tgv_ctx* c)
     A.z_lo = 0;
     A.z_hi = c->g.nzl;
     A.keep_halo_dual = c->leaf ? 1 : 0;
+    A.hist = hist_ptr(c);
     A.zc = fused_zc(c);
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
@@ -1814,6 +1823,113 @@ int tgv_read_field(tgv_ctx* c, int f, float* out, int64_t n)
     return TGV_OK;
 }
 
+// ---- pipelined host I/O: the next step's counts H2D and this step's u D2H on copy streams,
+// overlapped with the iterations (bench.py e2e; include/tgv.h)
+static int io_streams(tgv_ctx* c)
+{
+    if (c->s_in) return TGV_OK;
+    CU(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_staged, &c->ev_stage_free, &c->ev_snap, &c->ev_read})
+        CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CU(cudaEventRecord(c->ev_stage_free, c->stream));
+    CU(cudaEventRecord(c->ev_read, c->s_out));
+    return TGV_OK;
+}
+
+int tgv_stage_histograms(tgv_ctx* c, const void* counts, int count_bytes, int64_t n_counts)
+{
+    NvtxRange nv("tgv_stage_histograms");
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!counts) return fail(c, TGV_EINVAL, "counts is NULL");
+    if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4)
+        return fail(c, TGV_EINVAL, "count_bytes must be 1, 2 or 4");
+    const Geo& g = c->g;
+    const int64_t want = (int64_t)g.nzl * g.ny * g.nx * c->nbins;
+    if (n_counts != want) return fail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n_counts, (long long)want);
+    if ((rc = io_streams(c))) return rc;
+    const size_t bytes = (size_t)n_counts * count_bytes;
+    if (c->stage_bytes < bytes) {
+        CU(cudaStreamWaitEvent(c->s_in, c->ev_stage_free, 0));
+        CU(cudaStreamSynchronize(c->s_in));
+        cudaFree(c->stage);
+        c->stage = nullptr;
+        c->stage_bytes = 0;
+        if (cudaMalloc(&c->stage, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, TGV_ENOMEM, "count staging allocation of %.2f GB failed", bytes / 1e9);
+        }
+        c->stage_bytes = bytes;
+    }
+    // the previous staged counts must have been consumed before they are overwritten
+    CU(cudaStreamWaitEvent(c->s_in, c->ev_stage_free, 0));
+    CU(cudaMemcpyAsync(c->stage, counts, bytes, cudaMemcpyHostToDevice, c->s_in));
+    CU(cudaEventRecord(c->ev_staged, c->s_in));
+    c->stage_cb = count_bytes;
+    return TGV_OK;
+}
+
+int tgv_load_staged(tgv_ctx* c)
+{
+    NvtxRange nv("tgv_load_staged");
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!c->stage_cb) return fail(c, TGV_ESTATE, "nothing staged");
+    const Geo& g = c->g;
+    c->loaded = false;
+    CU(cudaStreamWaitEvent(c->stream, c->ev_staged, 0));
+    CU(cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream));
+    const int64_t per_plane = (int64_t)g.nx * g.ny * c->nbins * c->stage_cb;
+    const int cpc = (int)std::max<int64_t>(1, std::min<int64_t>(g.nzl, (256ll << 20) / per_plane));
+    for (int z0 = 0; z0 < g.nzl; z0 += cpc) {  // the coarsening kernels with factor 1, straight from the staging
+        const int nzc = std::min(cpc, g.nzl - z0);
+        const void* src = static_cast<const char*>(c->stage) + (size_t)z0 * per_plane;
+        if (c->stage_cb == 1) launch_coarsen_t<uint8_t>(c, src, g.nx, g.ny, nzc, 1, nzc, z0);
+        else if (c->stage_cb == 2) launch_coarsen_t<uint16_t>(c, src, g.nx, g.ny, nzc, 1, nzc, z0);
+        else launch_coarsen_t<uint32_t>(c, src, g.nx, g.ny, nzc, 1, nzc, z0);
+        CU(cudaGetLastError());
+    }
+    CU(cudaEventRecord(c->ev_stage_free, c->stream));
+    c->stage_cb = 0;
+    return finish_counts(c);
+}
+
+int tgv_read_u_async(tgv_ctx* c, float* u, int64_t n)
+{
+    NvtxRange nv("tgv_read_u_async");
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (!u) return fail(c, TGV_EINVAL, "u is NULL");
+    const Geo& g = c->g;
+    if (n != (int64_t)g.nzl * g.ny * g.nx) return fail(c, TGV_EINVAL, "n_voxels mismatch");
+    if (!c->loaded) return fail(c, TGV_ESTATE, "read before load");
+    if ((rc = io_streams(c))) return rc;
+    if (!c->usnap && cudaMalloc(&c->usnap, sizeof(float) * (size_t)g.nzl * g.plane) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, TGV_ENOMEM, "u snapshot allocation failed");
+    }
+    // the previous read must have left the snapshot before it is overwritten
+    CU(cudaStreamWaitEvent(c->stream, c->ev_read, 0));
+    CU(cudaMemcpyAsync(c->usnap, plane_ptr(c, slotU(bufs(c->k).cu), 0), sizeof(float) * (size_t)g.nzl * g.plane,
+                       cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaEventRecord(c->ev_snap, c->stream));
+    CU(cudaStreamWaitEvent(c->s_out, c->ev_snap, 0));
+    CU(cudaMemcpy2DAsync(u, sizeof(float) * g.nx, c->usnap, sizeof(float) * g.px, sizeof(float) * g.nx,
+                         (size_t)g.ny * g.nzl, cudaMemcpyDeviceToHost, c->s_out));
+    CU(cudaEventRecord(c->ev_read, c->s_out));
+    return TGV_OK;
+}
+
+int tgv_wait_io(tgv_ctx* c)
+{
+    int rc = check_ready(c);
+    if (rc) return rc;
+    if (c->s_in) CU(cudaStreamSynchronize(c->s_in));
+    if (c->s_out) CU(cudaStreamSynchronize(c->s_out));
+    return TGV_OK;
+}
+
 int tgv_read_u(tgv_ctx* c, float* u, int64_t n)
 {
     NvtxRange nv("tgv_read_u");
@@ -2232,6 +2348,14 @@ void tgv_destroy(tgv_ctx* c)
     cudaFree(c->d_maxc);
     cudaFree(c->staging);
     cudaFree(c->upload);
+    if (c->s_in) cudaStreamSynchronize(c->s_in);
+    if (c->s_out) cudaStreamSynchronize(c->s_out);
+    cudaFree(c->stage);
+    cudaFree(c->usnap);
+    for (cudaEvent_t e : {c->ev_staged, c->ev_stage_free, c->ev_snap, c->ev_read})
+        if (e) cudaEventDestroy(e);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
     cudaFree(c->d_sched);
     cudaFree(c->d_sched_off);
     if (c->stream) cudaStreamDestroy(c->stream);

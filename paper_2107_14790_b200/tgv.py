@@ -28,7 +28,8 @@ EXPORTS = ["tgv_get_unique_id", "tgv_create", "tgv_load_histograms", "tgv_reset"
            "tgv_destroy", "tgv_status_string", "tgv_last_error", "tgv_create_group", "tgv_group_iterate",
            "tgv_group_energy", "tgv_restrict_from", "tgv_prolong_from", "tgv_vote_depth_maps", "tgv_read_counts",
            "tgv_create_leaf", "tgv_set_border", "tgv_load_histograms_coarsened", "tgv_prolong_slab",
-           "tgv_leaf_rebind", "tgv_iterate_async", "tgv_sync", "tgv_peer_export", "tgv_peer_import"]
+           "tgv_leaf_rebind", "tgv_iterate_async", "tgv_sync", "tgv_peer_export", "tgv_peer_import",
+           "tgv_stage_histograms", "tgv_load_staged", "tgv_read_u_async", "tgv_wait_io"]
 
 
 class tgv_layout(ctypes.Structure):
@@ -79,6 +80,10 @@ def _load():
     lib.tgv_iterate_async.argtypes = [vp, i32]
     lib.tgv_sync.argtypes = [vp]
     lib.tgv_read_u.argtypes = [vp, vp, i64]
+    lib.tgv_stage_histograms.argtypes = [vp, vp, ctypes.c_int, i64]
+    lib.tgv_load_staged.argtypes = [vp]
+    lib.tgv_read_u_async.argtypes = [vp, vp, i64]
+    lib.tgv_wait_io.argtypes = [vp]
     lib.tgv_read_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_write_field.argtypes = [vp, ctypes.c_int, vp, i64]
     lib.tgv_energy.argtypes = [vp, vp]
@@ -194,6 +199,32 @@ def tgv_read_u(ctx, out):
     p, n = _host_ptr(out, np.float32)
     _check(lib.tgv_read_u(ctx, p, n), ctx)
     return out
+
+
+def tgv_stage_histograms(ctx, counts):
+    """counts: C-contiguous uint8 / uint16 / uint32 array (pinned for overlap); must stay alive
+    and unchanged until the next tgv_load_staged."""
+    a = counts
+    if not isinstance(a, np.ndarray) or a.dtype not in (np.uint8, np.uint16, np.uint32):
+        raise TypeError("counts must be a uint8 / uint16 / uint32 numpy array")
+    if not a.flags.c_contiguous:
+        raise ValueError("counts must be C-contiguous")
+    _check(lib.tgv_stage_histograms(ctx, a.ctypes.data, a.dtype.itemsize, a.size), ctx)
+
+
+def tgv_load_staged(ctx):
+    _check(lib.tgv_load_staged(ctx), ctx)
+
+
+def tgv_read_u_async(ctx, out):
+    """out must stay alive until tgv_wait_io."""
+    p, n = _host_ptr(out, np.float32)
+    _check(lib.tgv_read_u_async(ctx, p, n), ctx)
+    return out
+
+
+def tgv_wait_io(ctx):
+    _check(lib.tgv_wait_io(ctx), ctx)
 
 
 def tgv_read_field(ctx, field: int, out):

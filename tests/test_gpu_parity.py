@@ -355,3 +355,45 @@ def test_tvl1_fused_equals_split_bitwise(zc, impl, monkeypatch):
         b = solver_cls()(shape, c).set_schedule("split").set_model("tvl1").load(h).iterate(17)
         assert np.array_equal(a.read_u(), b.read_u())
         assert np.array_equal(a.get("p"), b.get("p"))
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.uint32])
+def test_staged_load_and_async_read_equal_the_synchronous_path(dtype):
+    """Pipelined host I/O (include/tgv.h tgv_stage_histograms / tgv_load_staged /
+    tgv_read_u_async): staged counts of any width give the state tgv_load_histograms gives,
+    bit for bit; a second staging while the first solve runs replaces it; the asynchronous u
+    read returns the iterate it was ordered after."""
+    import torch
+    from paper_2107_14790_b200 import tgv
+    shape = (45, 31, 22)
+    c = list(oracle.default_centers(8))
+    h1 = synth.random_histograms(shape, 51)
+    h2 = synth.random_histograms(shape, 52)
+    ref = []
+    for h in (h1, h2):
+        s = solver_cls()(shape, c).load(h).iterate(13)
+        ref.append(s.read_u().copy())
+        s.close()
+    s = solver_cls()(shape, c)
+    def pinned(a):  # page-locked host copy of any dtype (a uint8 torch buffer viewed as the array)
+        buf = torch.empty(a.nbytes, dtype=torch.uint8).pin_memory().numpy()
+        out_ = buf.view(a.dtype).reshape(a.shape)
+        out_[...] = a
+        return out_
+    pin = [pinned(np.ascontiguousarray(h.astype(dtype))) for h in (h1, h2)]
+    out = [torch.empty((shape[2], shape[1], shape[0]), dtype=torch.float32).pin_memory() for _ in range(2)]
+    tgv.tgv_stage_histograms(s.ctx, pin[0])
+    tgv.tgv_load_staged(s.ctx)
+    tgv.tgv_stage_histograms(s.ctx, pin[1])  # overlaps the next solve
+    s.iterate(13)
+    tgv.tgv_read_u_async(s.ctx, out[0])
+    tgv.tgv_load_staged(s.ctx)
+    s.iterate(13)
+    tgv.tgv_read_u_async(s.ctx, out[1])
+    tgv.tgv_wait_io(s.ctx)
+    assert np.array_equal(out[0].numpy(), ref[0])
+    assert np.array_equal(out[1].numpy(), ref[1])
+    with pytest.raises(tgv.TgvError) as ei:
+        tgv.tgv_load_staged(s.ctx)  # nothing staged any more
+    assert ei.value.status == tgv.TGV_ESTATE
+    s.close()
