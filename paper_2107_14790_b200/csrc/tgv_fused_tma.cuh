@@ -105,17 +105,14 @@ __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.pr
 
 // ---- shared memory ---------------------------------------------------------------
 constexpr int TMA_BW = 40;  // input box width: x0-4 .. x0+35 (the inner start must be 16-B aligned)
-constexpr int TMA_PW = 36;  // p boxes x0-4 .. x0+31 (left halo only), q boxes x0 .. x0+35 (right halo only)
 constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
 
-// Ring depths: u is read at planes s and s+1 (two planes beyond s+1 in flight), v / p / q
-// at plane s only (three planes beyond s in flight); v, p and q of a plane travel together
-// on one ring ("x").  The histograms are not staged: each owned thread loads its own 8-16 B
-// with a plain load one step ahead (no neighbour reads them), which leaves the shared memory
-// for the x ring's third plane in flight.
+// Ring depths: u is read at planes s and s+1, v / p / q / histogram at plane s only;
+// each ring prefetches two planes beyond what step s reads.
+// v, p, q and the histogram of a plane travel together on one ring ("x").
 template <int HB>
 struct TmaRings {
-    static constexpr int NU = 4, NX = 4;
+    static constexpr int NU = 4, NX = HB <= 16 ? 3 : 2;
 };
 
 template <int TY, int HB>
@@ -124,9 +121,10 @@ struct alignas(128) TmaSmem {
     using Rg = TmaRings<HB>;
     float u[Rg::NU][2][R][TMA_BW];   // ring: u_k, u_{k-1}
     float v[Rg::NX][6][R][TMA_BW];   // ring: v_k(3), v_{k-1}(3)
-    float pq[Rg::NX][9][R][TMA_PW];  // ring: p_k(3) (x0-4 ..), q_k(6) (x0 ..)
+    float pq[Rg::NX][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
     float out[13][TY][32];            // staged outputs: u, v(3), p(3), q(6) of iteration k+1
-    float suv[4][R][TMA_CW];          // ubar, vbar(3) of plane s (rewritten only after the step's last read)
+    uint8_t h[Rg::NX][TY][32 * HB];  // ring: histograms of the owned rows
+    float suv[2][4][R][TMA_CW];       // ubar, vbar(3) of plane s (parity)
     float sr[2][7][R][TMA_CW];        // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
     uint64_t bar_u[Rg::NU], bar_x[Rg::NX];
 };
@@ -141,7 +139,6 @@ struct TmaArgs {
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
     int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
-    const void* hist;    // counts [nzl][ny][px][SLOTS] (plain loads of the owned cells)
     // Peer halo mode: the kernel itself writes the next iterate of its
     // boundary planes into the neighbours' halo planes (NVLink / same-device stores,
     // tile by tile as they are computed) -- down: u, v, q of plane 0 into the lower
@@ -165,10 +162,9 @@ struct TmaArgs {
 template <int TY, int SLOTS, typename CT, bool PEER = false>
 __global__ void __launch_bounds__(32 * (TY + 3), 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
-                     const __grid_constant__ CUtensorMap m_ld3n, const __grid_constant__ CUtensorMap m_ld6,
-                     const __grid_constant__ CUtensorMap m_st1,
+                     const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_st1,
                      const __grid_constant__ CUtensorMap m_st3, const __grid_constant__ CUtensorMap m_st6,
-                     const TmaArgs A)
+                     const __grid_constant__ CUtensorMap m_h, const TmaArgs A)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
     constexpr int R = TY + 2;
@@ -203,8 +199,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         if (smem_addr(smem_raw) & 127) __trap();
         prefetch_map(&m_ld1);
         prefetch_map(&m_ld3);
-        prefetch_map(&m_ld3n);
         prefetch_map(&m_ld6);
+        prefetch_map(&m_h);
         for (int k = 0; k < Rg::NU; ++k) mbar_init(&S.bar_u[k], 1);
         for (int k = 0; k < Rg::NX; ++k) mbar_init(&S.bar_x[k], 1);
         fence_mbar_init();
@@ -229,15 +225,13 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         const int x0 = (t % tiles_x) * 32, y0 = (t / tiles_x) * TY;
 
         // ---- this thread's cell
-        // bc: column in the 40-wide u / v boxes (x0-4 ..); bp / bq: in the 36-wide p (x0-4 ..)
-        // and q (x0 ..) boxes (a halo lane reads only the one of p / q it needs)
-        int r, bc, bp, bq, cc, x;
+        int r, bc, cc, x;
         if (!halo) {
-            r = w, bc = lane + 4, bp = lane + 4, bq = lane, cc = lane + 1, x = x0 + lane;
+            r = w, bc = lane + 4, cc = lane + 1, x = x0 + lane;
         } else if (lane < 16) {  // rows beyond R (TY < 14) duplicate row R-1 exactly: identical writes
-            r = min(lane, R - 1), bc = 3, bp = 3, bq = 0, cc = 0, x = x0 - 1;
+            r = min(lane, R - 1), bc = 3, cc = 0, x = x0 - 1;
         } else {
-            r = min(lane - 16, R - 1), bc = 36, bp = 35, bq = 32, cc = TMA_CW - 1, x = x0 + 32;
+            r = min(lane - 16, R - 1), bc = 36, cc = TMA_CW - 1, x = x0 + 32;
         }
         const int y = y0 - 1 + r;
         // p is needed on rows 0..TY (row 0 feeds D-_y of row 1) and at column x0-1;
@@ -263,21 +257,15 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             tma_load4(&S.u[st][0][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_uk);
             tma_load4(&S.u[st][1][0][0], &m_ld1, &S.bar_u[st], x0 - 4, y0 - 1, zclamp(s), A.s_um);
         };
-        auto issue_x = [&](int s) {  // v_k, v_{k-1}, p_k, q_k of plane s
+        auto issue_x = [&](int s) {  // v_k, v_{k-1}, p_k, q_k and the counts of plane s
             const int st = ix.st;
             adv(ix, Rg::NX);
-            mbar_expect_tx(&S.bar_x[st], 6 * R * TMA_BW * 4 + 9 * R * TMA_PW * 4);
+            mbar_expect_tx(&S.bar_x[st], 15 * R * TMA_BW * 4 + TY * 32 * HB);
             tma_load4(&S.v[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_vk);
             tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
-            tma_load4(&S.pq[st][0][0][0], &m_ld3n, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
-            tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_x[st], x0, y0 - 1, zclamp(s), A.s_qk);
-        };
-        // this owned cell's counts of plane s (zeros elsewhere), loaded a step before use
-        const bool hval = own && x < g.nx && y < g.ny;
-        auto load_counts = [&](int s) {
-            Hist h{};
-            if (hval && s >= 0 && s < g.nzl) h = load_hist<SLOTS, CT>(A.hist, (int64_t)s * g.plane + (int64_t)y * g.px + x);
-            return h;
+            tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
+            tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
+            tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
         };
 
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
@@ -293,17 +281,14 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             float vb[3];      // vbar(s-1)
             float uk, vk[3];  // u_k, v_k at s-1 (the primal of plane s-1)
             Hist h;           // histogram of s-1
-            Hist hn;          // histogram of s (in flight one step)
             float pn[3], pz;  // p_{k+1}(s-1), p_z{k+1}(s-2)
             float qn[6];      // q_{k+1}(s-1)
         };
         Carry ca{}, cb{};
-        ca.hn = load_counts(zs - 1);
 
         auto step = [&](auto PAR, int s, const Carry& in, Carry& o) {
             constexpr int par = decltype(PAR)::value, pr = par ^ 1;
             const int zg = g.z0 + s;
-            const Hist hnew = load_counts(s + 1);  // used by the primal of plane s+1 (step s+2)
 
             mbar_wait(&S.bar_u[cu.st], cu.ph);
             mbar_wait(&S.bar_x[cx.st], cx.ph);
@@ -312,10 +297,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             const float* U0 = &S.u[su][0][r][bc];
             const float* U1 = &S.u[cu.st][0][r][bc];
             const float* V0 = &S.v[cx.st][0][r][bc];
-            const float* P0 = &S.pq[cx.st][0][r][bp];
-            const float* Q0 = &S.pq[cx.st][3][r][bq];
-            constexpr int F = R * TMA_BW;   // field stride in a u / v ring slot
-            constexpr int FP = R * TMA_PW;  // field stride in a p / q ring slot
+            const float* PQ = &S.pq[cx.st][0][r][bc];
+            constexpr int F = R * TMA_BW;  // field stride in a ring slot
             const float uk = U0[0], um = U0[F];
             float vk[3], vb[3];
     #pragma unroll
@@ -327,15 +310,31 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             const float ub1 = fmaf(2.f, U1[0], -U1[F]);    // ubar(s+1)
             float pk[3], qk[6];
     #pragma unroll
-            for (int k = 0; k < 3; ++k) pk[k] = P0[k * FP];
+            for (int k = 0; k < 3; ++k) pk[k] = PQ[k * F];
     #pragma unroll
-            for (int m = 0; m < 6; ++m) qk[m] = Q0[m * FP];
-            // suv is rewritten only here, after S2 of the previous step: every read of it (phase E)
-            // lies between S1 and S2, so one buffer suffices
-            S.suv[0][r][cc] = ub;
-            S.suv[1][r][cc] = vb[0];
-            S.suv[2][r][cc] = vb[1];
-            S.suv[3][r][cc] = vb[2];
+            for (int m = 0; m < 6; ++m) qk[m] = PQ[(3 + m) * F];
+            Hist hc{};
+            if (own) {
+                const uint8_t* hp = &S.h[cx.st][r - 1][lane * HB];
+                if constexpr (HB == 8) {
+                    const uint2 v2 = *reinterpret_cast<const uint2*>(hp);
+                    hc.w[0] = v2.x;
+                    hc.w[1] = v2.y;
+                } else {
+    #pragma unroll
+                    for (int q4 = 0; q4 < HB / 16; ++q4) {
+                        const uint4 v4 = reinterpret_cast<const uint4*>(hp)[q4];
+                        hc.w[4 * q4] = v4.x;
+                        hc.w[4 * q4 + 1] = v4.y;
+                        hc.w[4 * q4 + 2] = v4.z;
+                        hc.w[4 * q4 + 3] = v4.w;
+                    }
+                }
+            }
+            S.suv[par][0][r][cc] = ub;
+            S.suv[par][1][r][cc] = vb[0];
+            S.suv[par][2][r][cc] = vb[1];
+            S.suv[par][3][r][cc] = vb[2];
             if (tid0) tma_wait_read0();  // the previous step's output staging has been read
             __syncthreads();             // S1
             if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
@@ -358,8 +357,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 const bool needQ = ROLE == 0 || ROLE == 2 || (ROLE == 3 && lane >= 16 && r >= 1 && r <= TY);
                 const bool xl_ = INT || xl, yl_ = INT || yl, xf_ = INT || xf, yf_ = INT || yf;
                 if (needP) {
-                    const float ux = S.suv[0][r][cc + 1];
-                    const float uy = S.suv[0][r + 1][cc];
+                    const float ux = S.suv[par][0][r][cc + 1];
+                    const float uy = S.suv[par][0][r + 1][cc];
                     const float g0 = xl_ ? ux - ub : 0.f, g1 = yl_ ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
                     pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
                     pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
@@ -375,8 +374,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     float dx[3], dy[3], dz[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        const float vx = S.suv[1 + k][r][cc - 1];
-                        const float vy = S.suv[1 + k][r - 1][cc];
+                        const float vx = S.suv[par][1 + k][r][cc - 1];
+                        const float vy = S.suv[par][1 + k][r - 1][cc];
                         dx[k] = fmaf(INT ? 1.f : mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
                         dy[k] = fmaf(INT ? 1.f : myl, vb[k], -vy);
                         dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
@@ -509,8 +508,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
     #pragma unroll
             for (int m = 0; m < 6; ++m) o.qn[m] = qn[m];
             o.uk = uk;
-            o.h = in.hn;  // counts of plane s (loaded at step s-1)
-            o.hn = hnew;
+            o.h = hc;
         };
 
 

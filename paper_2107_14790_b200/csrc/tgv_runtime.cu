@@ -88,7 +88,7 @@ struct tgv_ctx {
     int* d_sched_off = nullptr;
     int sched_ctas = 0, sched_zc = -1, sched_per_sm = 1;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
-    CUtensorMap m_ld1{}, m_ld3{}, m_ld3n{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
+    CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
     Geo g{};
     int slots = 8;            // histogram slots per voxel
@@ -480,8 +480,7 @@ int make_state_maps(tgv_ctx* c)
     int rc;
     if ((rc = make_state_map(c, &c->m_ld1, TMA_BW, TMA_TY + 2, 1))) return rc;
     if ((rc = make_state_map(c, &c->m_ld3, TMA_BW, TMA_TY + 2, 3))) return rc;
-    if ((rc = make_state_map(c, &c->m_ld3n, TMA_PW, TMA_TY + 2, 3))) return rc;  // p: x0-4 .. x0+31
-    if ((rc = make_state_map(c, &c->m_ld6, TMA_PW, TMA_TY + 2, 6))) return rc;   // q: x0 .. x0+35
+    if ((rc = make_state_map(c, &c->m_ld6, TMA_BW, TMA_TY + 2, 6))) return rc;
     if ((rc = make_state_map(c, &c->m_st1, 32, TMA_TY, 1))) return rc;
     if ((rc = make_state_map(c, &c->m_st3, 32, TMA_TY, 3))) return rc;
     return make_state_map(c, &c->m_st6, 32, TMA_TY, 6);
@@ -577,7 +576,7 @@ int launch_fused_tma_tp(tgv_ctx* c, const TmaArgs& A, dim3 grd)
         attr_set.fetch_or(bit);
     }
     fused_tma_kernel<TMA_TY, SLOTS, CT, PEER><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
-        c->m_ld1, c->m_ld3, c->m_ld3n, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, A);
+        c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
     return TGV_OK;
 }
 template <int SLOTS, typename CT>
@@ -596,7 +595,6 @@ int launch_fused_tma(tgv_ctx* c)
     A.z_lo = 0;
     A.z_hi = c->g.nzl;
     A.keep_halo_dual = c->leaf ? 1 : 0;
-    A.hist = hist_ptr(c);
     A.zc = fused_zc(c);
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
