@@ -43,13 +43,16 @@ def two_level_set(E):
     return np.array(levels), np.array(coords), frozen
 
 
-def pair(E, seed, frozen_values=True):
+def pair(E, seed, frozen_values=True, nbins=8, scale=1):
     levels, coords, frozen = two_level_set(E)
     rng = np.random.default_rng(seed)
     nb = len(levels)
-    h = rng.integers(0, 6, (nb, E, E, E, 8)).astype(np.uint32)
-    o = om.MixedOracle(E, levels, coords, frozen, **KW).load(h)
-    s = BS()(E, coords, frozen.astype(np.uint8), levels=levels, **KW).load(h)
+    c = None
+    if nbins != 8:
+        c = np.sort(rng.uniform(-0.95, 0.95, nbins)).astype(np.float32).astype(np.float64)
+    h = (rng.integers(0, 6, (nb, E, E, E, nbins)) * scale).astype(np.uint32)
+    o = om.MixedOracle(E, levels, coords, frozen, centers=c, **KW).load(h)
+    s = BS()(E, coords, frozen.astype(np.uint8), levels=levels, centers=None if c is None else list(c), **KW).load(h)
     if frozen_values:
         u0 = np.where(frozen[:, None, None, None], rng.uniform(-1, 1, (nb, E, E, E)), o.get("u"))
         v0 = rng.normal(0, 0.2, (nb, 3, E, E, E)) * frozen[:, None, None, None, None]
@@ -79,9 +82,12 @@ def test_one_iteration_from_a_random_primal(E):
     assert s.info()["s_voxels"] == int(o.S.sum())
 
 
-@pytest.mark.parametrize("E", [4, 8])
-def test_mixed_set_matches_oracle(E):
-    o, s, _ = pair(E, 5)
+@pytest.mark.parametrize("E,nbins,scale", [(4, 8, 1), (8, 8, 1), (16, 16, 100), (8, 3, 1)])
+def test_mixed_set_matches_oracle(E, nbins, scale):
+    """Also 16 bins with u16 counts (x100) and 3 non-uniform bins."""
+    o, s, _ = pair(E, 5, nbins=nbins, scale=scale)
+    if scale > 1:
+        assert s.info()["count_bytes"] == 2
     o.iterate(60)
     s.iterate(60)
     du = float(np.max(np.abs(s.read_u().astype(np.float64) - o.get("u"))))
