@@ -77,6 +77,31 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, uin
         "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// L2 eviction-priority policies (createpolicy) and the hinted TMA forms: data no CTA
+// will read again (the outputs, the counts) can leave L2 first, keeping it for the halo
+// rows / columns that neighbouring tiles re-read
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load3_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                               uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+        "%4, %5}], [%2], %6;" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store4_hint(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                                uint64_t pol)
+{
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(map),
+                 "r"(smem_addr(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_store4(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3)
 {
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
@@ -139,6 +164,7 @@ struct TmaArgs {
     int s_uk, s_um, s_vk, s_vm, s_pk, s_qk;  // input slots (v/p/q: first of 3/3/6 consecutive)
     int s_un, s_vn, s_pn, s_qn;              // output slots
     int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
+    int hints;           // L2 policy: bit 0 the output stores evict first, bit 1 the count loads evict first
     // Peer halo mode: the kernel itself writes the next iterate of its
     // boundary planes into the neighbours' halo planes (NVLink / same-device stores,
     // tile by tile as they are computed) -- down: u, v, q of plane 0 into the lower
@@ -179,6 +205,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
     const int lane = threadIdx.x, w = threadIdx.y;
     const bool tid0 = lane == 0 && w == 0;
     const bool halo = w == TY + 2;
+    const uint64_t pol_ef = A.hints ? policy_evict_first() : 0ull;
 
     // ring cursors: next slot to fill (issue side) and next slot / phase to wait for.
     // Fills and waits happen in the same order on every ring, across all segments.
@@ -265,7 +292,10 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             tma_load4(&S.v[st][3][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_vm);
             tma_load4(&S.pq[st][0][0][0], &m_ld3, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_pk);
             tma_load4(&S.pq[st][3][0][0], &m_ld6, &S.bar_x[st], x0 - 4, y0 - 1, zclamp(s), A.s_qk);
-            tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
+            if (A.hints & 2)
+                tma_load3_hint(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1), pol_ef);
+            else
+                tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
         };
 
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
@@ -487,12 +517,22 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             __syncthreads();  // S2
             if (tid0) {
                 if ((s >= zs && s < ze) || (A.keep_halo_dual && (s == -1 || s == g.nzl))) {
-                    tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
-                    tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
+                    if (A.hints & 1) {
+                        tma_store4_hint(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn, pol_ef);
+                        tma_store4_hint(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn, pol_ef);
+                    } else {
+                        tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
+                        tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
+                    }
                 }
                 if (s - 1 >= zs) {
-                    tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
-                    tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
+                    if (A.hints & 1) {
+                        tma_store4_hint(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un, pol_ef);
+                        tma_store4_hint(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn, pol_ef);
+                    } else {
+                        tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
+                        tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
+                    }
                 }
                 tma_commit();
             }

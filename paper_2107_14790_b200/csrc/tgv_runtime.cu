@@ -596,6 +596,7 @@ int launch_fused_tma(tgv_ctx* c)
     A.z_hi = c->g.nzl;
     A.keep_halo_dual = c->leaf ? 1 : 0;
     A.zc = fused_zc(c);
+    A.hints = (int)env_int("TGV_L2_HINTS", 0);  // dev knob until measured
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
     A.s_vk = slotV(b.cu, 0);
