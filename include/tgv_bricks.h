@@ -79,8 +79,11 @@ int tgv_bricks_create(const tgv_brickset* set, const tgv_params* params, int cud
  * voxels across i's +k face - u(i)) / ((h_i + h_n) / 2), 0 without a neighbour;
  * D-_k = -(D+_k)^* in the cell-volume-weighted inner product; every term of the energy
  * and of the restricted gap is weighted by h^3.  A one-level set (all levels equal 0) is
- * tgv_bricks_create's set bit for bit.  Mixed sets run the SPLIT schedule (FUSED is
- * EINVAL); tgv_bricks_vote_depth_maps votes brick b at voxel size voxel_size 2^l and
+ * tgv_bricks_create's set bit for bit.  Schedules: SPLIT (any E), and for E = 32 FUSED
+ * (the default there): the fused sweep over the solved level-0 bricks whose whole
+ * 26-neighbourhood is level 0 or empty, the mixed SPLIT kernels over the other solved bricks,
+ * bit for bit the SPLIT schedule's iterates.  tgv_bricks_vote_depth_maps votes brick b at
+ * voxel size voxel_size 2^l and
  * radius voxel_radius 2^l; tgv_bricks_prolong_from accepts levels 0 and 1 (a level-1
  * brick copies the coarse brick at its own coordinates: u, v / 2).  Everything else as
  * tgv_bricks_create.  Errors: TGV_EINVAL (also NULL levels, a level > 7, overlapping or

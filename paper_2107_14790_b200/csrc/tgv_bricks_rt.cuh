@@ -62,6 +62,12 @@ struct tgv_bricks {
     int* d_alist_reg = nullptr;
     int* d_alist_gen = nullptr;
     int n_alist_reg = 0, n_alist_gen = 0;
+    // FUSED schedule of a mixed set (E = 32): solved level-0 bricks whose whole 26-neighbourhood
+    // is level 0 or empty run the fused brick sweep (their 27-entry tables); every other
+    // solved brick the mixed SPLIT kernels
+    int* d_fnb27 = nullptr;
+    int* d_alist_fgen = nullptr;  // the solved bricks the fused sweep does not cover
+    int n_fused = 0, n_fgen = 0;
 
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // pairs
@@ -315,8 +321,60 @@ int brick_iterate_fused(tgv_bricks* c, int32_t n)
     return TGV_OK;
 }
 
+// FUSED schedule of a mixed set (R27): per iteration (1) the duals of S on the frozen
+// bricks (mixed face launch, every face kind) and of the solved bricks the fused sweep does
+// not cover (mixed dual), (2) the fused sweep over the solved level-0 bricks whose whole
+// 26-neighbourhood is level 0 or empty (there R27's operators are R24's, and the sweep
+// recomputes every halo dual it needs), (3) the mixed primal of the remaining solved
+// bricks, which reads the duals (1) and (2) stored.
+int mixed_iterate_fused(tgv_bricks* c, int32_t n)
+{
+    const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
+    int rc;
+    for (int32_t it = 0; it < n; ++it) {
+        const IterPtrs a = biter_ptrs(c, c->k);
+        if ((rc = btimer(c, 0, false))) return rc;
+        {
+            const int n0 = c->n_fgen << 15, n1 = c->n_mfaces << 10;
+            if (n0) mixed_dual_kernel<5, 0><<<(n0 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_alist_fgen, n0);
+            if (n1) mixed_dual_kernel<5, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, mgeo(c), sp, c->d_mfaces, n1);
+        }
+        BCU(cudaGetLastError());
+        if ((rc = btimer(c, 0, true))) return rc;
+        if (c->n_fused) {
+            BrickFusedArgs A{a, sp, bcenters(c), c->d_fnb27, c->frozen, c->n_fused, 0};
+            if ((rc = btimer(c, 3, false))) return rc;
+            if (c->slots == 8 && c->count_bytes == 1) launch_brick_fused_t<8, uint8_t>(c, A);
+            else if (c->slots == 8) launch_brick_fused_t<8, uint16_t>(c, A);
+            else if (c->count_bytes == 1) launch_brick_fused_t<16, uint8_t>(c, A);
+            else launch_brick_fused_t<16, uint16_t>(c, A);
+            BCU(cudaGetLastError());
+            if ((rc = btimer(c, 3, true))) return rc;
+        }
+        if (c->n_fgen) {
+            IterPtrs ap = a;
+            for (int d = 0; d < 3; ++d) ap.pk[d] = a.pn[d];
+            for (int m = 0; m < 6; ++m) ap.qk[m] = a.qn[m];
+            const Centers C = bcenters(c);
+            const int n0 = c->n_fgen << 15, blocks = (n0 + 255) / 256;
+            const MixGeo g = mgeo(c);
+            const int* L = c->d_alist_fgen;
+            if ((rc = btimer(c, 1, false))) return rc;
+            if (c->slots == 8 && c->count_bytes == 1) mixed_primal_kernel<5, 8, uint8_t><<<blocks, 256, 0, c->stream>>>(ap, g, sp, C, L, n0);
+            else if (c->slots == 8) mixed_primal_kernel<5, 8, uint16_t><<<blocks, 256, 0, c->stream>>>(ap, g, sp, C, L, n0);
+            else if (c->count_bytes == 1) mixed_primal_kernel<5, 16, uint8_t><<<blocks, 256, 0, c->stream>>>(ap, g, sp, C, L, n0);
+            else mixed_primal_kernel<5, 16, uint16_t><<<blocks, 256, 0, c->stream>>>(ap, g, sp, C, L, n0);
+            BCU(cudaGetLastError());
+            if ((rc = btimer(c, 1, true))) return rc;
+        }
+        c->k += 1;
+    }
+    return TGV_OK;
+}
+
 int brick_iterate_enqueue(tgv_bricks* c, int32_t n)
 {
+    if (c->schedule == TGV_SCHEDULE_FUSED && c->mixed) return mixed_iterate_fused(c, n);
     if (c->schedule == TGV_SCHEDULE_FUSED) return brick_iterate_fused(c, n);
     const StepParams sp{c->sigma, c->tau, c->alpha1, c->alpha0, c->tau * c->lambda};
     int rc;
@@ -761,6 +819,37 @@ int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* leve
     }
     c->n_alist_reg = (int)reg.size();
     c->n_alist_gen = (int)gen.size();
+    if (E == 32) {  // the FUSED schedule's split of the solved bricks (see struct tgv_bricks)
+        std::vector<int> fnb, fgen;
+        for (int64_t b = 0; b < nb; ++b) {
+            if (fr[(size_t)b]) continue;
+            bool ok = levels[b] == 0;
+            int row[27];
+            const int64_t P[3] = {S->coords[3 * b], S->coords[3 * b + 1], S->coords[3 * b + 2]};
+            for (int dz = -1; dz <= 1 && ok; ++dz)
+                for (int dy = -1; dy <= 1 && ok; ++dy)
+                    for (int dx = -1; dx <= 1 && ok; ++dx) {
+                        const int64_t X = P[0] + dx, Y = P[1] + dy, Z = P[2] + dz;
+                        const int j = find(0, X, Y, Z);
+                        row[(dz + 1) * 9 + (dy + 1) * 3 + dx + 1] = j;
+                        if (j < 0 && X >= 0 && Y >= 0 && Z >= 0)
+                            for (int l = 1; l <= 7 && ok; ++l)
+                                if (find(l, X >> l, Y >> l, Z >> l) >= 0) ok = false;  // a coarser brick is there
+                    }
+            if (ok) fnb.insert(fnb.end(), row, row + 27);
+            else fgen.push_back((int)b);
+        }
+        c->n_fused = (int)fnb.size() / 27;
+        c->n_fgen = (int)fgen.size();
+        if (cudaMalloc(&c->d_fnb27, sizeof(int) * std::max<size_t>(1, fnb.size())) != cudaSuccess ||
+            cudaMalloc(&c->d_alist_fgen, sizeof(int) * std::max<size_t>(1, fgen.size())) != cudaSuccess ||
+            (!fnb.empty() && cudaMemcpy(c->d_fnb27, fnb.data(), sizeof(int) * fnb.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
+            (!fgen.empty() && cudaMemcpy(c->d_alist_fgen, fgen.data(), sizeof(int) * fgen.size(), cudaMemcpyHostToDevice) != cudaSuccess)) {
+            cudaGetLastError();
+            return bfail(c, TGV_ENOMEM, "mixed-level fused tables allocation failed");
+        }
+        c->device_bytes += (int64_t)sizeof(int) * (fnb.size() + fgen.size());
+    }
     if (cudaMalloc(&c->d_alist_reg, sizeof(int) * std::max<size_t>(1, reg.size())) != cudaSuccess ||
         cudaMalloc(&c->d_alist_gen, sizeof(int) * std::max<size_t>(1, gen.size())) != cudaSuccess ||
         (!reg.empty() && cudaMemcpy(c->d_alist_reg, reg.data(), sizeof(int) * reg.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
@@ -769,7 +858,7 @@ int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* leve
         return bfail(c, TGV_ENOMEM, "mixed-level brick lists allocation failed");
     }
     c->mixed = true;
-    c->schedule = TGV_SCHEDULE_SPLIT;
+    c->schedule = E == 32 ? TGV_SCHEDULE_FUSED : TGV_SCHEDULE_SPLIT;
     c->levels_h.assign(levels, levels + nb);
     if (cudaMalloc(&c->d_level, (size_t)nb) != cudaSuccess || cudaMalloc(&c->d_kind, (size_t)nb * 6) != cudaSuccess ||
         cudaMalloc(&c->d_nbr4, sizeof(int) * (size_t)nb * 24) != cudaSuccess ||
@@ -952,7 +1041,7 @@ int tgv_bricks_set_schedule(tgv_bricks* c, int schedule)
     if (rc) return rc;
     if (schedule != TGV_SCHEDULE_FUSED && schedule != TGV_SCHEDULE_SPLIT) return bfail(c, TGV_EINVAL, "bad schedule %d", schedule);
     if (schedule == TGV_SCHEDULE_FUSED && c->E != 32) return bfail(c, TGV_EINVAL, "the fused schedule needs E = 32");
-    if (schedule == TGV_SCHEDULE_FUSED && c->mixed) return bfail(c, TGV_EINVAL, "mixed-level sets run the SPLIT schedule");
+
     c->schedule = schedule;
     return TGV_OK;
 }
@@ -1030,6 +1119,8 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->d_mfaces);
     cudaFree(c->d_alist_reg);
     cudaFree(c->d_alist_gen);
+    cudaFree(c->d_fnb27);
+    cudaFree(c->d_alist_fgen);
     cudaFree(c->hist);
     cudaFree(c->partials);
     cudaFree(c->d_out);

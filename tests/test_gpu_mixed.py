@@ -241,3 +241,38 @@ def test_mixed_finest_level_matches_oracle_hierarchy():
     assert abs(eg["gap"] - eo["gap"]) <= 1e-5 * abs(eo["E"])
     print(f"mixed finest level of C1: {len(coords)} bricks ({int((lv == 1).sum())} coarse), max|du| = {du:.2e}")
     bl.close()
+
+
+def test_fused_schedule_of_a_mixed_set_equals_split_bitwise():
+    """E = 32: the FUSED schedule of a mixed set (the fused brick sweep over the solved
+    level-0 bricks whose 26-neighbourhood is level 0 or empty, the mixed kernels elsewhere)
+    gives the SPLIT schedule's iterates bit for bit, with both kinds of brick present."""
+    from paper_2107_14790_b200 import tgv
+    E = 32
+    # a 2 x 2 x 2 block of level-0 bricks (some far from any coarse brick), a level-1 brick on
+    # the -x side of it, frozen bricks of both levels
+    levels, coords = [], []
+    for x in range(2, 6):
+        for y in range(0, 2):
+            for z in range(0, 2):
+                levels.append(0)
+                coords.append((x, y, z))
+    levels += [1, 1]
+    coords += [(0, 0, 0), (3, 0, 0)]  # level 1: fine x in [0, 64) and [192, 256)
+    frozen = np.zeros(len(levels), np.uint8)
+    frozen[[1, len(levels) - 1]] = 1
+    rng = np.random.default_rng(12)
+    h = rng.integers(0, 6, (len(levels), E, E, E, 8)).astype(np.uint32)
+    u0 = rng.uniform(-1, 1, (len(levels), E, E, E)).astype(np.float32)
+    v0 = rng.normal(0, 0.3, (len(levels), 3, E, E, E)).astype(np.float32)
+    a = BS()(E, coords, frozen, levels=levels, **KW).load(h).set_primal(u0, v0)
+    assert a.info()["schedule"] == tgv.SCHEDULE_FUSED
+    b = BS()(E, coords, frozen, levels=levels, **KW).set_schedule("split").load(h).set_primal(u0, v0)
+    a.iterate(9)
+    b.iterate(9)
+    for f in ("u", "v", "p", "q"):
+        assert np.array_equal(a.get(f), b.get(f)), (f, float(np.max(np.abs(a.get(f) - b.get(f)))))
+    ea, eb = a.energy(), b.energy()
+    assert ea["E"] == eb["E"] and ea["gap"] == eb["gap"]
+    a.close()
+    b.close()
