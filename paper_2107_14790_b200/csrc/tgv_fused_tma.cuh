@@ -135,24 +135,29 @@ constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
 // Ring depths: u is read at planes s and s+1, v / p / q / histogram at plane s only;
 // each ring prefetches two planes beyond what step s reads.
 // v, p, q and the histogram of a plane travel together on one ring ("x").
-template <int HB>
+// DEEP (u8 counts, 8 bins): a fourth x slot -- three planes in flight -- paid for by staging
+// the outputs in the x slot of the plane being computed (its inputs are in registers after
+// phase B; its refill waits for the bulk stores' reads) and by one suv buffer (written in
+// phase B, read in phase E: S2 orders a step's reads before the next step's writes).
+template <int HB, bool DEEP = false>
 struct TmaRings {
-    static constexpr int NU = 4, NX = HB <= 16 ? 3 : 2;
+    static constexpr int NU = 4, NX = DEEP ? 4 : (HB <= 16 ? 3 : 2);
 };
 
-template <int TY, int HB>
+template <int TY, int HB, bool DEEP = false>
 struct alignas(128) TmaSmem {
     static constexpr int R = TY + 2;
-    using Rg = TmaRings<HB>;
+    using Rg = TmaRings<HB, DEEP>;
     float u[Rg::NU][2][R][TMA_BW];   // ring: u_k, u_{k-1}
     float v[Rg::NX][6][R][TMA_BW];   // ring: v_k(3), v_{k-1}(3)
     float pq[Rg::NX][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
-    float out[13][TY][32];            // staged outputs: u, v(3), p(3), q(6) of iteration k+1
+    float out[DEEP ? 1 : 13][TY][32];  // staged outputs: u, v(3), p(3), q(6) of iteration k+1 (DEEP: in the x slot)
     uint8_t h[Rg::NX][TY][32 * HB];  // ring: histograms of the owned rows
-    float suv[2][4][R][TMA_CW];       // ubar, vbar(3) of plane s (parity)
+    float suv[DEEP ? 1 : 2][4][R][TMA_CW];  // ubar, vbar(3) of plane s (parity; DEEP: one buffer)
     float sr[2][7][R][TMA_CW];        // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
     uint64_t bar_u[Rg::NU], bar_x[Rg::NX];
 };
+static_assert(sizeof(TmaSmem<14, 8, true>) + 128 <= 227 * 1024, "DEEP ring exceeds the 227 KB opt-in shared memory");
 
 struct TmaArgs {
     Geo g;
@@ -185,7 +190,7 @@ struct TmaArgs {
 };
 
 // PEER: the peer halo mode instantiation (the single-GPU kernel carries none of its code)
-template <int TY, int SLOTS, typename CT, bool PEER = false>
+template <int TY, int SLOTS, typename CT, bool PEER = false, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (TY + 3), 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
                      const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_st1,
@@ -194,9 +199,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
     constexpr int R = TY + 2;
-    using Smem = TmaSmem<TY, HB>;
+    using Smem = TmaSmem<TY, HB, DEEP>;
     using Hist = HistRaw<SLOTS, CT>;
-    using Rg = TmaRings<HB>;
+    using Rg = TmaRings<HB, DEEP>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);  // dynamic smem starts 128-B aligned (checked below)
     const Geo& g = A.g;
@@ -326,6 +331,12 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
             const float* U0 = &S.u[su][0][r][bc];
             const float* U1 = &S.u[cu.st][0][r][bc];
+            const int xs = cx.st;  // x slot of plane s (DEEP: the output staging after S1)
+            float* const Ouvp = DEEP ? &S.v[xs][0][0][0] : &S.out[0][0][0];  // u, v(3), p(3): [7][TY][32]
+            float* const Oq = DEEP ? &S.pq[xs][0][0][0] : Ouvp + 7 * TY * 32;          // q(6): [6][TY][32]
+            auto OUT = [&](int f, int row) -> float* {
+                return f < 7 ? Ouvp + (f * TY + row) * 32 : Oq + ((f - 7) * TY + row) * 32;
+            };
             const float* V0 = &S.v[cx.st][0][r][bc];
             const float* PQ = &S.pq[cx.st][0][r][bc];
             constexpr int F = R * TMA_BW;  // field stride in a ring slot
@@ -361,10 +372,10 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     }
                 }
             }
-            S.suv[par][0][r][cc] = ub;
-            S.suv[par][1][r][cc] = vb[0];
-            S.suv[par][2][r][cc] = vb[1];
-            S.suv[par][3][r][cc] = vb[2];
+            S.suv[DEEP ? 0 : par][0][r][cc] = ub;
+            S.suv[DEEP ? 0 : par][1][r][cc] = vb[0];
+            S.suv[DEEP ? 0 : par][2][r][cc] = vb[1];
+            S.suv[DEEP ? 0 : par][3][r][cc] = vb[2];
             if (tid0) tma_wait_read0();  // the previous step's output staging has been read
             __syncthreads();             // S1
             if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
@@ -387,8 +398,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 const bool needQ = ROLE == 0 || ROLE == 2 || (ROLE == 3 && lane >= 16 && r >= 1 && r <= TY);
                 const bool xl_ = INT || xl, yl_ = INT || yl, xf_ = INT || xf, yf_ = INT || yf;
                 if (needP) {
-                    const float ux = S.suv[par][0][r][cc + 1];
-                    const float uy = S.suv[par][0][r + 1][cc];
+                    const float ux = S.suv[DEEP ? 0 : par][0][r][cc + 1];
+                    const float uy = S.suv[DEEP ? 0 : par][0][r + 1][cc];
                     const float g0 = xl_ ? ux - ub : 0.f, g1 = yl_ ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
                     pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
                     pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
@@ -404,8 +415,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     float dx[3], dy[3], dz[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        const float vx = S.suv[par][1 + k][r][cc - 1];
-                        const float vy = S.suv[par][1 + k][r - 1][cc];
+                        const float vx = S.suv[DEEP ? 0 : par][1 + k][r][cc - 1];
+                        const float vy = S.suv[DEEP ? 0 : par][1 + k][r - 1][cc];
                         dx[k] = fmaf(INT ? 1.f : mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
                         dy[k] = fmaf(INT ? 1.f : myl, vb[k], -vy);
                         dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
@@ -433,9 +444,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 }
                 if constexpr (ROLE == 0) {
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) S.out[4 + k][r - 1][lane] = pn[k];
+                    for (int k = 0; k < 3; ++k) OUT(4 + k, r - 1)[lane] = pn[k];
 #pragma unroll
-                    for (int m = 0; m < 6; ++m) S.out[7 + m][r - 1][lane] = qn[m];
+                    for (int m = 0; m < 6; ++m) OUT(7 + m, r - 1)[lane] = qn[m];
                     [[maybe_unused]] const bool inb = x < g.nx && y < g.ny;
                     [[maybe_unused]] const int64_t cell = (int64_t)y * g.px + x;
                     if (PEER && A.pdn && s == 0 && s >= zs && s < ze && inb) {  // q of plane 0 -> lower neighbour's top halo
@@ -469,10 +480,10 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                         const float v0 = fmaf(sp.tau, in.pn[0] + w0, in.vk[0]);
                         const float v1 = fmaf(sp.tau, in.pn[1] + w1, in.vk[1]);
                         const float v2 = fmaf(sp.tau, in.pn[2] + w2, in.vk[2]);
-                        S.out[0][r - 1][lane] = un;
-                        S.out[1][r - 1][lane] = v0;
-                        S.out[2][r - 1][lane] = v1;
-                        S.out[3][r - 1][lane] = v2;
+                        OUT(0, r - 1)[lane] = un;
+                        OUT(1, r - 1)[lane] = v0;
+                        OUT(2, r - 1)[lane] = v1;
+                        OUT(3, r - 1)[lane] = v2;
                         // u, v of a boundary plane -> the neighbour's halo (peer mode)
                         if constexpr (PEER) {
                         float* po = nullptr;
@@ -518,20 +529,20 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             if (tid0) {
                 if ((s >= zs && s < ze) || (A.keep_halo_dual && (s == -1 || s == g.nzl))) {
                     if (A.hints & 1) {
-                        tma_store4_hint(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn, pol_ef);
-                        tma_store4_hint(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn, pol_ef);
+                        tma_store4_hint(&m_st3, OUT(4, 0), x0, y0, s + 1, A.s_pn, pol_ef);
+                        tma_store4_hint(&m_st6, OUT(7, 0), x0, y0, s + 1, A.s_qn, pol_ef);
                     } else {
-                        tma_store4(&m_st3, &S.out[4][0][0], x0, y0, s + 1, A.s_pn);
-                        tma_store4(&m_st6, &S.out[7][0][0], x0, y0, s + 1, A.s_qn);
+                        tma_store4(&m_st3, OUT(4, 0), x0, y0, s + 1, A.s_pn);
+                        tma_store4(&m_st6, OUT(7, 0), x0, y0, s + 1, A.s_qn);
                     }
                 }
                 if (s - 1 >= zs) {
                     if (A.hints & 1) {
-                        tma_store4_hint(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un, pol_ef);
-                        tma_store4_hint(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn, pol_ef);
+                        tma_store4_hint(&m_st1, OUT(0, 0), x0, y0, s, A.s_un, pol_ef);
+                        tma_store4_hint(&m_st3, OUT(1, 0), x0, y0, s, A.s_vn, pol_ef);
                     } else {
-                        tma_store4(&m_st1, &S.out[0][0][0], x0, y0, s, A.s_un);
-                        tma_store4(&m_st3, &S.out[1][0][0], x0, y0, s, A.s_vn);
+                        tma_store4(&m_st1, OUT(0, 0), x0, y0, s, A.s_un);
+                        tma_store4(&m_st3, OUT(1, 0), x0, y0, s, A.s_vn);
                     }
                 }
                 tma_commit();

@@ -933,6 +933,50 @@ __device__ __forceinline__ void data_box_terms(const HistRaw<SLOTS, CT>& h, cons
     box = fma(lam, G, divp) + best;
 }
 
+// One voxel's inputs to the energy / restricted-gap terms: the centre values and the
+// neighbours each difference reads (x / y / z suffixes: +1 for u and q, -1 for v and p).
+struct EnVoxel {
+    float uc, ux, uy, un;                            // u at (x,y,z), x+1, y+1, z+1
+    float v0, v1, v2, v0x, v1x, v2x, v0y, v1y, v2y;  // v at (x,y,z), x-1, y-1
+    float vm0, vm1, vm2;                             // v at z-1
+    float p0, p1, p2, p0x, p1y, pzm;                 // p; p_x at x-1, p_y at y-1, p_z at z-1
+    float qxx, qyy, qzz, qxy, qxz, qyz;              // q at (x,y,z)
+    float qxxx, qxyx, qxzx, qxyy, qyyy, qyzy;        // q_xx, q_xy, q_xz at x+1; q_xy, q_yy, q_yz at y+1
+    float qzzn, qxzn, qyzn;                          // q_zz, q_xz, q_yz at z+1
+};
+
+// Per-voxel energy terms (PAPER.md:133 E, R14 box-restricted dual), accumulated in fp64:
+//   t1 += alpha1 |D+u - v|, t0 += alpha0 |E(v)| (Frobenius, R5), td += lam sum_b h_b |u - c_b|,
+//   dv += min_{|x|<=1} (lam sum_b h_b |x - c_b| - x divp) - V ||p + div2 q||_1.
+// The masks are R6's Neumann D+ / D-; INT: all of them true (voxels away from the faces).
+template <int SLOTS, typename CT, bool INT>
+__device__ __forceinline__ void energy_voxel_terms(const EnVoxel& e, const HistRaw<SLOTS, CT>& h,
+                                                   const EnergyConsts& K, float al1, float al0, float lam, float VV,
+                                                   bool xl, bool yl, bool zl, bool xf, bool yf, bool zf, double& t1,
+                                                   double& t0, double& td, double& dv)
+{
+    const bool xl_ = INT || xl, yl_ = INT || yl, zl_ = INT || zl, xf_ = INT || xf, yf_ = INT || yf, zf_ = INT || zf;
+    auto dp = [](bool l, float a, float b) { return l ? a - b : 0.f; };
+    auto dm = [](bool l, bool f, float a, float b) { return (l ? a : 0.f) - (f ? b : 0.f); };
+    const float a0 = dp(xl_, e.ux, e.uc) - e.v0, a1 = dp(yl_, e.uy, e.uc) - e.v1, a2 = dp(zl_, e.un, e.uc) - e.v2;
+    t1 += (double)(al1 * sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2))));
+    const float exx = dm(xl_, xf_, e.v0, e.v0x), eyy = dm(yl_, yf_, e.v1, e.v1y), ezz = dm(zl_, zf_, e.v2, e.vm2);
+    const float exy = 0.5f * (dm(yl_, yf_, e.v0, e.v0y) + dm(xl_, xf_, e.v1, e.v1x));
+    const float exz = 0.5f * (dm(zl_, zf_, e.v0, e.vm0) + dm(xl_, xf_, e.v2, e.v2x));
+    const float eyz = 0.5f * (dm(zl_, zf_, e.v1, e.vm1) + dm(yl_, yf_, e.v2, e.v2y));
+    const float off = fmaf(exy, exy, fmaf(exz, exz, eyz * eyz));
+    t0 += (double)(al0 * sqrtf(fmaf(exx, exx, fmaf(eyy, eyy, fmaf(ezz, ezz, 2.f * off)))));
+    const float divp = dm(xl_, xf_, e.p0, e.p0x) + dm(yl_, yf_, e.p1, e.p1y) + dm(zl_, zf_, e.p2, e.pzm);
+    const float w0 = dp(xl_, e.qxxx, e.qxx) + dp(yl_, e.qxyy, e.qxy) + dp(zl_, e.qxzn, e.qxz);
+    const float w1 = dp(xl_, e.qxyx, e.qxy) + dp(yl_, e.qyyy, e.qyy) + dp(zl_, e.qyzn, e.qyz);
+    const float w2 = dp(xl_, e.qxzx, e.qxz) + dp(yl_, e.qyzy, e.qyz) + dp(zl_, e.qzzn, e.qzz);
+    const float l1 = fabsf(e.p0 + w0) + fabsf(e.p1 + w1) + fabsf(e.p2 + w2);
+    float data, box;
+    data_box_terms_f32<SLOTS, CT>(h, K, lam, e.uc, divp, data, box);
+    td += (double)data;
+    dv += (double)box - (double)(VV * l1);
+}
+
 // Grid of the energy sweep: warp = a 32-voxel x segment of one row, block = 8 consecutive
 // rows of one x tile, item = (x tile, 8-row group, z chunk); each warp marches its chunk in z.
 struct EnergySched {
@@ -991,37 +1035,21 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
             const float v0y = L(ea.v[0], i - sy), v1y = L(ea.v[1], i - sy), v2y = L(ea.v[2], i - sy),
                         p1y = L(ea.p[1], i - sy);
             const auto h = load_hist<SLOTS, CT>(ea.hist, hv);
-            // ---- per-voxel terms (the masks are R6's Neumann D+ / D-; compile-time true away
-            // from the grid's faces, where nearly every voxel is)
-            auto terms = [&](auto INTc) {
-                constexpr bool INT = decltype(INTc)::value;
-                const bool xl_ = INT || xl, yl_ = INT || yl, zl_ = INT || zl, xf_ = INT || xf, yf_ = INT || yf,
-                           zf_ = INT || zf;
-                auto dp = [](bool l, float a, float b) { return l ? a - b : 0.f; };
-                auto dm = [](bool l, bool f, float a, float b) { return (l ? a : 0.f) - (f ? b : 0.f); };
-                const float a0 = dp(xl_, ux, uc) - v0, a1 = dp(yl_, uy, uc) - v1, a2 = dp(zl_, un, uc) - v2;
-                t1 += (double)(al1 * sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2))));
-                const float exx = dm(xl_, xf_, v0, v0x), eyy = dm(yl_, yf_, v1, v1y), ezz = dm(zl_, zf_, v2, vm2);
-                const float exy = 0.5f * (dm(yl_, yf_, v0, v0y) + dm(xl_, xf_, v1, v1x));
-                const float exz = 0.5f * (dm(zl_, zf_, v0, vm0) + dm(xl_, xf_, v2, v2x));
-                const float eyz = 0.5f * (dm(zl_, zf_, v1, vm1) + dm(yl_, yf_, v2, v2y));
-                const float off = fmaf(exy, exy, fmaf(exz, exz, eyz * eyz));
-                t0 += (double)(al0 * sqrtf(fmaf(exx, exx, fmaf(eyy, eyy, fmaf(ezz, ezz, 2.f * off)))));
-                const float divp = dm(xl_, xf_, p0, p0x) + dm(yl_, yf_, p1, p1y) + dm(zl_, zf_, p2, pzm);
-                const float w0 = dp(xl_, qxxx, qxx) + dp(yl_, qxyy, qxy) + dp(zl_, qxzn, qxz);
-                const float w1 = dp(xl_, qxyx, qxy) + dp(yl_, qyyy, qyy) + dp(zl_, qyzn, qyz);
-                const float w2 = dp(xl_, qxzx, qxz) + dp(yl_, qyzy, qyz) + dp(zl_, qzzn, qzz);
-                const float l1 = fabsf(p0 + w0) + fabsf(p1 + w1) + fabsf(p2 + w2);
-                float data, box;
-                data_box_terms_f32<SLOTS, CT>(h, K, lam, uc, divp, data, box);
-                td += (double)data;
-                dv += (double)box - (double)(VV * l1);
-            };
             if (act) {
+                EnVoxel e;
+                e.uc = uc, e.ux = ux, e.uy = uy, e.un = un;
+                e.v0 = v0, e.v1 = v1, e.v2 = v2, e.v0x = v0x, e.v1x = v1x, e.v2x = v2x;
+                e.v0y = v0y, e.v1y = v1y, e.v2y = v2y, e.vm0 = vm0, e.vm1 = vm1, e.vm2 = vm2;
+                e.p0 = p0, e.p1 = p1, e.p2 = p2, e.p0x = p0x, e.p1y = p1y, e.pzm = pzm;
+                e.qxx = qxx, e.qyy = qyy, e.qzz = qzz, e.qxy = qxy, e.qxz = qxz, e.qyz = qyz;
+                e.qxxx = qxxx, e.qxyx = qxyx, e.qxzx = qxzx, e.qxyy = qxyy, e.qyyy = qyyy, e.qyzy = qyzy;
+                e.qzzn = qzzn, e.qxzn = qxzn, e.qyzn = qyzn;
                 if (xl && xf && yl && yf && zl && zf)
-                    terms(std::true_type{});
+                    energy_voxel_terms<SLOTS, CT, true>(e, h, K, al1, al0, lam, VV, xl, yl, zl, xf, yf, zf, t1, t0, td,
+                                                        dv);
                 else
-                    terms(std::false_type{});
+                    energy_voxel_terms<SLOTS, CT, false>(e, h, K, al1, al0, lam, VV, xl, yl, zl, xf, yf, zf, t1, t0,
+                                                         td, dv);
                 vm = fmaxf(vm, fmaxf(fabsf(v0), fmaxf(fabsf(v1), fabsf(v2))));
             }
             // ---- carry

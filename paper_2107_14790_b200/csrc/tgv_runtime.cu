@@ -27,6 +27,7 @@
 #include "../../include/tgv.h"
 #include "nccl_api.h"
 #include "tgv_fused_tma.cuh"
+#include "tgv_energy_tma.cuh"
 #include "tgv_tvl1_tma.cuh"
 #include "tgv_kernels.cuh"
 #include "tgv_vote.cuh"
@@ -87,6 +88,9 @@ struct tgv_ctx {
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
     int* d_sched_off = nullptr;
     int sched_ctas = 0, sched_zc = -1, sched_per_sm = 1;
+    int4* d_esched = nullptr;  // the energy sweep's own copy (its chunk and CTA count never change)
+    int* d_esched_off = nullptr;
+    int esched_ctas = 0, esched_zc = -1;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
     CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
@@ -315,7 +319,7 @@ void launch_tvl1_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
     tvl1_fused_kernel<FUSED_TY, SLOTS, CT><<<grd, dim3(32, FUSED_TY + 2), 0, c->stream>>>(A);
 }
 
-int build_schedule(tgv_ctx* c, int zc, int per_sm = 1);
+int build_schedule(tgv_ctx* c, int zc, int per_sm = 1, bool energy = false);
 int fused_zc(const tgv_ctx* c);
 
 template <int SLOTS, typename CT>
@@ -492,7 +496,7 @@ int make_state_maps(tgv_ctx* c)
 // remaining items are split evenly over all G CTAs as contiguous segments.
 int64_t env_int(const char* name, int64_t dflt);
 
-int build_schedule(tgv_ctx* c, int zc, int per_sm)
+int build_schedule(tgv_ctx* c, int zc, int per_sm, bool energy)
 {
     const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
     const int nzl = c->g.nzl;
@@ -548,41 +552,52 @@ int build_schedule(tgv_ctx* c, int zc, int per_sm)
         flat.insert(flat.end(), v.begin(), v.end());
         off.push_back((int)flat.size());
     }
-    cudaFree(c->d_sched);
-    cudaFree(c->d_sched_off);
-    c->d_sched = nullptr;
-    c->d_sched_off = nullptr;
-    CU(cudaMalloc(&c->d_sched, sizeof(int4) * std::max<size_t>(1, flat.size())));
-    CU(cudaMalloc(&c->d_sched_off, sizeof(int) * off.size()));
-    CU(cudaMemcpy(c->d_sched, flat.data(), sizeof(int4) * flat.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_sched_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
-    c->sched_ctas = G;
-    c->sched_zc = zc;
-    c->sched_per_sm = per_sm;
+    int4*& d = energy ? c->d_esched : c->d_sched;
+    int*& d_off = energy ? c->d_esched_off : c->d_sched_off;
+    cudaFree(d);
+    cudaFree(d_off);
+    d = nullptr;
+    d_off = nullptr;
+    CU(cudaMalloc(&d, sizeof(int4) * std::max<size_t>(1, flat.size())));
+    CU(cudaMalloc(&d_off, sizeof(int) * off.size()));
+    CU(cudaMemcpy(d, flat.data(), sizeof(int4) * flat.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+    if (energy) {
+        c->esched_ctas = G;
+        c->esched_zc = zc;
+    } else {
+        c->sched_ctas = G;
+        c->sched_zc = zc;
+        c->sched_per_sm = per_sm;
+    }
     return TGV_OK;
 }
 
-template <int SLOTS, typename CT, bool PEER>
+template <int SLOTS, typename CT, bool PEER, bool DEEP = false>
 int launch_fused_tma_tp(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
-    const size_t smem = sizeof(TmaSmem<TMA_TY, HB>) + 128;
+    const size_t smem = sizeof(TmaSmem<TMA_TY, HB, DEEP>) + 128;
     // the attribute is per device: set it once for each device this process launches on
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = 1ull << (c->device & 63);
     if (!(attr_set.load() & bit)) {
-        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT, PEER>,
+        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT, PEER, DEEP>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set.fetch_or(bit);
     }
-    fused_tma_kernel<TMA_TY, SLOTS, CT, PEER><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
+    fused_tma_kernel<TMA_TY, SLOTS, CT, PEER, DEEP><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
         c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
     return TGV_OK;
 }
 template <int SLOTS, typename CT>
 int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
-    return c->peer_now ? launch_fused_tma_tp<SLOTS, CT, true>(c, A, grd) : launch_fused_tma_tp<SLOTS, CT, false>(c, A, grd);
+    if (c->peer_now) return launch_fused_tma_tp<SLOTS, CT, true>(c, A, grd);
+    if constexpr (SLOTS == 8 && sizeof(CT) == 1) {  // u8 counts, 8 bins: the deeper x ring fits
+        if (env_int("TGV_FUSED_DEEP", 0)) return launch_fused_tma_tp<SLOTS, CT, false, true>(c, A, grd);
+    }
+    return launch_fused_tma_tp<SLOTS, CT, false>(c, A, grd);
 }
 
 int launch_fused_tma(tgv_ctx* c)
@@ -871,12 +886,57 @@ EnergySched energy_sched(const Geo& g, int blocks)
     return es;
 }
 
-template <int SLOTS, typename CT>
-void launch_energy_t(tgv_ctx* c, const EnergyArgs& ea)
+// chunk of the energy sweep's lock-step schedule: the iteration sweep's rule (fused_zc)
+int energy_zc(const Geo& g)
 {
-    const EnergySched es = energy_sched(c->g, c->energy_blocks);
-    energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(
-        ea, c->g, energy_consts(c->centers, c->nbins, SLOTS), es, c->partials);
+    if (g.nzl <= 256) return g.nzl;
+    for (int d = 128; d >= 112; --d)
+        if (g.nzl % d == 0) return d;
+    return 128;
+}
+
+// (a4) energy partials; returns the number of partial blocks (energy_final_kernel's input).
+// Default: the TMA-staged sweep (tgv_energy_tma.cuh); TGV_ENERGY_IMPL=regs selects the
+// register-streaming energy_partial_kernel (the A/B baseline).
+template <int SLOTS, typename CT>
+int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblocks)
+{
+    const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
+    const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
+    if (impl && !strcmp(impl, "regs")) {
+        const EnergySched es = energy_sched(c->g, c->energy_blocks);
+        energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
+        *nblocks = c->energy_blocks;
+        return TGV_OK;
+    }
+    constexpr int HB = SLOTS * (int)sizeof(CT);
+    const int zc = energy_zc(c->g);
+    int rc;
+    if (c->esched_zc != zc && (rc = build_schedule(c, zc, 1, true))) return rc;
+    EnTmaArgs A{};
+    A.g = c->g;
+    A.s_u = slotU(b.cu);
+    A.s_v = slotV(b.cu, 0);
+    A.s_p = slotP(b.cp, 0);
+    A.s_q = slotQ(b.cp, 0);
+    A.sched = c->d_esched;
+    A.sched_off = c->d_esched_off;
+    A.alpha1 = (float)ea.alpha1;
+    A.alpha0 = (float)ea.alpha0;
+    A.lambda = (float)ea.lambda;
+    A.V = (float)ea.V;
+    const size_t smem = sizeof(EnSmem<TMA_TY, HB>) + 128;
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = 1ull << (c->device & 63);
+    if (!(attr_set.load() & bit)) {
+        CU(cudaFuncSetAttribute(energy_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+        attr_set.fetch_or(bit);
+    }
+    energy_tma_kernel<TMA_TY, SLOTS, CT><<<c->esched_ctas, dim3(32, TMA_TY), smem, c->stream>>>(
+        c->m_ld1, c->m_ld3, c->m_ld6, c->m_h, A, K, c->partials);
+    *nblocks = c->esched_ctas;
+    return TGV_OK;
 }
 
 int64_t env_int(const char* name, int64_t dflt)
@@ -1978,12 +2038,14 @@ static int energy_launch(tgv_ctx* c)
     ea.lambda = c->lambda;
     ea.V = c->model == TGV_MODEL_TVL1 ? 0.0 : 2.0;  // TV-L1 has no v to bound (R14, R21)
     ea.nbins = c->nbins;
-    if (c->slots == 8 && c->count_bytes == 1) launch_energy_t<8, uint8_t>(c, ea);
-    else if (c->slots == 8) launch_energy_t<8, uint16_t>(c, ea);
-    else if (c->count_bytes == 1) launch_energy_t<16, uint8_t>(c, ea);
-    else launch_energy_t<16, uint16_t>(c, ea);
+    int nb = 0;
+    if (c->slots == 8 && c->count_bytes == 1) rc = launch_energy_t<8, uint8_t>(c, ea, b, &nb);
+    else if (c->slots == 8) rc = launch_energy_t<8, uint16_t>(c, ea, b, &nb);
+    else if (c->count_bytes == 1) rc = launch_energy_t<16, uint8_t>(c, ea, b, &nb);
+    else rc = launch_energy_t<16, uint16_t>(c, ea, b, &nb);
+    if (rc) return rc;
     CU(cudaGetLastError());
-    energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, c->energy_blocks, c->d_out);
+    energy_final_kernel<<<1, 256, 0, c->stream>>>(c->partials, nb, c->d_out);
     CU(cudaGetLastError());
     return timer_end(c, sl);
 }
@@ -2357,6 +2419,8 @@ void tgv_destroy(tgv_ctx* c)
     if (c->s_out) cudaStreamDestroy(c->s_out);
     cudaFree(c->d_sched);
     cudaFree(c->d_sched_off);
+    cudaFree(c->d_esched);
+    cudaFree(c->d_esched_off);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -145,6 +145,31 @@ def test_energy_terms_from_random_state(shape, nb, scale, model):
     assert model == "tvl1" or abs(o.energy(V=0.0)["gap"] - eo["gap"]) > 100 * tol
 
 
+@pytest.mark.parametrize("shape,nb,scale", [((37, 23, 19), 8, 1), ((1, 1, 9), 8, 1), ((33, 1, 4), 8, 1),
+                                            ((29, 14, 12), 16, 1), ((40, 33, 17), 8, 100), ((70, 9, 21), 16, 100),
+                                            ((96, 45, 300), 8, 1)])
+def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
+    """(a4) the TMA-staged energy sweep (default) and the register-streaming one
+    (TGV_ENERGY_IMPL=regs) form the same fp32 per-voxel terms and differ only in the order
+    of the fp64 sums; max|v| is exact.  Ragged tiles, size-1 axes, u8 / u16 counts, 8 / 16
+    bins, and a 300-plane grid (lock-step chunks plus split remainder segments)."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nb * 7 + nx)
+    c = oracle.default_centers(nb)
+    h = (rng.integers(0, 6, size=(nz, ny, nx, nb)) * scale).astype(np.uint32)
+    s = solver_cls()(shape, [float(x) for x in c], **params()).load(h)
+    for k, a in random_state(shape, 90 + nx, "tgv").items():
+        s.set(k, a)
+    et = s.energy()
+    monkeypatch.setenv("TGV_ENERGY_IMPL", "regs")
+    er = s.energy()
+    monkeypatch.delenv("TGV_ENERGY_IMPL")
+    assert s.energy() == et  # deterministic
+    for k in ("E", "alpha1", "alpha0", "data", "gap"):
+        assert abs(et[k] - er[k]) <= 1e-12 * max(1.0, abs(er["E"]), abs(er["dual"])), (k, et[k], er[k])
+    assert et["vmax"] == er["vmax"]
+
+
 @pytest.mark.parametrize("schedule", SCHEDULES)
 def test_c1_full_count(schedule):
     wl = synth.workload("C1")
@@ -205,6 +230,26 @@ def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
     for key, o in outs.items():
         for f in ("u", "v", "p", "q"):
             assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
+
+
+@pytest.mark.parametrize("shape,zc", [((67, 41, 23), 0), ((45, 31, 26), 3), ((33, 15, 300), 0), ((96, 30, 9), 1)])
+def test_fused_deep_ring_equals_default_bitwise(monkeypatch, shape, zc):
+    """TGV_FUSED_DEEP (u8 counts, 8 bins: a fourth x-ring slot, outputs staged in the slot of
+    the plane being computed, one suv buffer) only moves data: the iterates equal the default
+    sweep's bit for bit, over ragged tiles, short chunks and split remainder segments."""
+    h = synth.random_histograms(shape, 14)
+    c = list(oracle.default_centers(8))
+    if zc:
+        monkeypatch.setenv("TGV_FUSED_ZC", str(zc))
+    outs = []
+    for deep in ("0", "1"):
+        monkeypatch.setenv("TGV_FUSED_DEEP", deep)
+        s = solver_cls()(shape, c).load(h).iterate(21)
+        assert s.info()["count_bytes"] == 1 and s.info()["fused_tma"]
+        outs.append({f: s.get(f) for f in ("u", "v", "p", "q")})
+        s.close()
+    for f in ("u", "v", "p", "q"):
+        assert np.array_equal(outs[0][f], outs[1][f]), f
 
 
 @pytest.mark.parametrize("impl", ["tma", "regs"])
