@@ -338,8 +338,9 @@ int tgv_read_field(tgv_ctx* ctx, int field, float* out, int64_t n_voxels);
 int tgv_write_field(tgv_ctx* ctx, int field, const float* in, int64_t n_voxels);
 
 /* COLLECTIVE.  Energy and restricted primal-dual gap of the current state
- * (R14), per-voxel terms in fp64 from the fp32
- * state, deterministic fixed-order reduction, fp64 NCCL all-reduce:
+ * (R14): per-voxel terms formed in fp32 from the
+ * fp32 state (one TMA-staged sweep over the grid), summed in fp64 in a fixed
+ * order (deterministic), fp64 NCCL all-reduce across ranks:
  *   out[0] E = alpha1-term + alpha0-term + data-term
  *   out[1] sum alpha1 |grad u - v|_2          out[2] sum alpha0 |E(v)|_F
  *   out[3] sum lambda sum_b h_b |u - c_b|

