@@ -287,7 +287,9 @@ void launch_brick_fused_t(tgv_bricks* c, const BrickFusedArgs& A)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrickFusedSmem));
         configured_dev = c->device;
     }
-    kern<<<2 * c->n_alist, dim3(32, BF_WARPS), sizeof(BrickFusedSmem), c->stream>>>(A);
+    // two CTAs per swept brick: A.n_alist rows of A.nb27 (all solved bricks, or the mixed
+    // set's fused subset -- never c->n_alist there)
+    if (A.n_alist) kern<<<2 * A.n_alist, dim3(32, BF_WARPS), sizeof(BrickFusedSmem), c->stream>>>(A);
 }
 
 // FUSED schedule: the frozen-face duals, then one single sweep over the solved bricks

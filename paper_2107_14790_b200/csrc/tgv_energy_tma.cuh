@@ -20,15 +20,11 @@
 
 namespace tgvk {
 
-// ring depth: planes s and s+1 are read at step s, the rest are in flight
-template <int HB>
-struct EnRing {
-    static constexpr int NS = HB <= 16 ? 5 : 4;
-};
-
-template <int TY, int HB>
+// NS: ring depth (planes s and s+1 are read at step s, the rest are in flight); NS = 3 runs
+// two CTAs per SM (u8 counts, 8 bins), deeper rings one
+template <int TY, int HB, int NS_>
 struct alignas(128) EnSmem {
-    static constexpr int R = TY + 2, NS = EnRing<HB>::NS;
+    static constexpr int R = TY + 2, NS = NS_;
     float f[NS][13][R][TMA_BW];   // u, v(3), p(3), q(6) of one plane (state slot order)
     uint8_t h[NS][TY][32 * HB];  // counts of the owned rows
     uint64_t bar[NS];
@@ -41,18 +37,20 @@ struct EnTmaArgs {
     const int4* sched;       // persistent (tile, z_begin, z_end) segments, as the fused sweep's
     const int* sched_off;
     float alpha1, alpha0, lambda, V;
+    unsigned long long* round_ctr;  // lock-step rounds (as fused_tma_kernel), or null
+    int rounds;
 };
 
-template <int TY, int SLOTS, typename CT>
-__global__ void __launch_bounds__(32 * TY, 1)
+template <int TY, int SLOTS, typename CT, int NS>
+__global__ void __launch_bounds__(32 * TY, NS <= 3 ? 2 : 1)
     energy_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
                       const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_h,
                       const EnTmaArgs A, const EnergyConsts K, double* __restrict__ partials)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
-    constexpr int R = TY + 2, NS = EnRing<HB>::NS;
+    constexpr int R = TY + 2;
     constexpr int F = R * TMA_BW;  // field stride in a ring slot
-    using Smem = EnSmem<TY, HB>;
+    using Smem = EnSmem<TY, HB, NS>;
     using Hist = HistRaw<SLOTS, CT>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -113,18 +111,26 @@ __global__ void __launch_bounds__(32 * TY, 1)
         // prologue: planes zs-1 .. zs+NS-2 fill the ring; after step s's barrier the slots of
         // planes <= s are free and the ring runs up to plane s+NS
         int nxt = zs - 1;
-        if (tid0)
+        const int jr = sgi - A.sched_off[blockIdx.x];  // this CTA's segment index (= round while < rounds)
+        if (tid0) {
             for (; nxt <= ze && nxt < zs - 1 + NS; ++nxt) issue(nxt);
+            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // (the other threads wait at the first barrier)
+                const unsigned long long want = (unsigned long long)jr * gridDim.x;
+                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
+            }
+        }
 
-        // carry-in: v and p_z of plane zs-1
+        // carry-in: v and p_z of plane zs-1 (its slot is refilled after step zs's barrier)
         mbar_wait(&S.bar[cw.st], cw.ph);
-        int sc = cw.st;
-        adv(cw);
         float vz0, vz1, vz2, pzm;
         {
-            const float* a = &S.f[sc][0][r][bc];
+            const float* a = &S.f[cw.st][0][r][bc];
             vz0 = a[F], vz1 = a[2 * F], vz2 = a[3 * F], pzm = a[6 * F];
         }
+        adv(cw);
+        mbar_wait(&S.bar[cw.st], cw.ph);  // plane zs
+        int sc = cw.st;
+        adv(cw);
         for (int s = zs; s < ze; ++s) {
             mbar_wait(&S.bar[cw.st], cw.ph);  // plane s+1 (plane s arrived a step earlier)
             const int sn = cw.st;
@@ -179,6 +185,9 @@ __global__ void __launch_bounds__(32 * TY, 1)
             adv(cw);
         }
         __syncthreads();  // the next segment's prologue refills every slot
+        if (A.round_ctr && tid0 && jr < A.rounds &&
+            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)
+            atomicExch(A.round_ctr, 0ull);
     }
 
     double vmd = (double)vm;

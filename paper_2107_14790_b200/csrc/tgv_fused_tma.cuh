@@ -135,29 +135,24 @@ constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
 // Ring depths: u is read at planes s and s+1, v / p / q / histogram at plane s only;
 // each ring prefetches two planes beyond what step s reads.
 // v, p, q and the histogram of a plane travel together on one ring ("x").
-// DEEP (u8 counts, 8 bins): a fourth x slot -- three planes in flight -- paid for by staging
-// the outputs in the x slot of the plane being computed (its inputs are in registers after
-// phase B; its refill waits for the bulk stores' reads) and by one suv buffer (written in
-// phase B, read in phase E: S2 orders a step's reads before the next step's writes).
-template <int HB, bool DEEP = false>
+template <int HB>
 struct TmaRings {
-    static constexpr int NU = 4, NX = DEEP ? 4 : (HB <= 16 ? 3 : 2);
+    static constexpr int NU = 4, NX = HB <= 16 ? 3 : 2;
 };
 
-template <int TY, int HB, bool DEEP = false>
+template <int TY, int HB>
 struct alignas(128) TmaSmem {
     static constexpr int R = TY + 2;
-    using Rg = TmaRings<HB, DEEP>;
+    using Rg = TmaRings<HB>;
     float u[Rg::NU][2][R][TMA_BW];   // ring: u_k, u_{k-1}
     float v[Rg::NX][6][R][TMA_BW];   // ring: v_k(3), v_{k-1}(3)
     float pq[Rg::NX][9][R][TMA_BW];  // ring: p_k(3), q_k(6)
-    float out[DEEP ? 1 : 13][TY][32];  // staged outputs: u, v(3), p(3), q(6) of iteration k+1 (DEEP: in the x slot)
+    float out[13][TY][32];            // staged outputs: u, v(3), p(3), q(6) of iteration k+1
     uint8_t h[Rg::NX][TY][32 * HB];  // ring: histograms of the owned rows
-    float suv[DEEP ? 1 : 2][4][R][TMA_CW];  // ubar, vbar(3) of plane s (parity; DEEP: one buffer)
+    float suv[2][4][R][TMA_CW];       // ubar, vbar(3) of plane s (parity)
     float sr[2][7][R][TMA_CW];        // p_x, p_y, q_xx, q_xy, q_xz, q_yy, q_yz of D(s) (parity)
     uint64_t bar_u[Rg::NU], bar_x[Rg::NX];
 };
-static_assert(sizeof(TmaSmem<14, 8, true>) + 128 <= 227 * 1024, "DEEP ring exceeds the 227 KB opt-in shared memory");
 
 struct TmaArgs {
     Geo g;
@@ -170,6 +165,12 @@ struct TmaArgs {
     int s_un, s_vn, s_pn, s_qn;              // output slots
     int keep_halo_dual;  // NEXT-3 leaves: also store p at plane -1 and q at plane nzl (no exchange refreshes them)
     int hints;           // L2 policy: bit 0 the output stores evict first, bit 1 the count loads evict first
+    // Lock-step rounds (optional): the first `rounds` segments of every CTA are whole
+    // (tile, chunk) items dealt round-robin; before its round j a CTA waits (bounded: never
+    // a correctness dependency) until all G CTAs finished round j-1, so that persistent CTAs
+    // cannot drift rounds apart and neighbouring tiles keep sharing their halos in L2.
+    unsigned long long* round_ctr;  // null: off; else + 1 per CTA per round, reset by the last increment
+    int rounds;
     // Peer halo mode: the kernel itself writes the next iterate of its
     // boundary planes into the neighbours' halo planes (NVLink / same-device stores,
     // tile by tile as they are computed) -- down: u, v, q of plane 0 into the lower
@@ -190,7 +191,7 @@ struct TmaArgs {
 };
 
 // PEER: the peer halo mode instantiation (the single-GPU kernel carries none of its code)
-template <int TY, int SLOTS, typename CT, bool PEER = false, bool DEEP = false>
+template <int TY, int SLOTS, typename CT, bool PEER = false>
 __global__ void __launch_bounds__(32 * (TY + 3), 1)
     fused_tma_kernel(const __grid_constant__ CUtensorMap m_ld1, const __grid_constant__ CUtensorMap m_ld3,
                      const __grid_constant__ CUtensorMap m_ld6, const __grid_constant__ CUtensorMap m_st1,
@@ -199,9 +200,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
     constexpr int R = TY + 2;
-    using Smem = TmaSmem<TY, HB, DEEP>;
+    using Smem = TmaSmem<TY, HB>;
     using Hist = HistRaw<SLOTS, CT>;
-    using Rg = TmaRings<HB, DEEP>;
+    using Rg = TmaRings<HB>;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);  // dynamic smem starts 128-B aligned (checked below)
     const Geo& g = A.g;
@@ -303,9 +304,14 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
         };
 
+        const int jr = sgi - A.sched_off[blockIdx.x];  // this CTA's segment index (= round while < rounds)
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
             for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
             for (int tz = zs - 1; tz < zs - 1 + Rg::NX - 1; ++tz) issue_x(tz);
+            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // (the other threads wait at S1)
+                const unsigned long long want = (unsigned long long)jr * gridDim.x;
+                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
+            }
         }
         mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
         int su = cu.st;
@@ -331,12 +337,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             // ---- phase B: this cell's inputs of plane s (and u at s+1) into registers
             const float* U0 = &S.u[su][0][r][bc];
             const float* U1 = &S.u[cu.st][0][r][bc];
-            const int xs = cx.st;  // x slot of plane s (DEEP: the output staging after S1)
-            float* const Ouvp = DEEP ? &S.v[xs][0][0][0] : &S.out[0][0][0];  // u, v(3), p(3): [7][TY][32]
-            float* const Oq = DEEP ? &S.pq[xs][0][0][0] : Ouvp + 7 * TY * 32;          // q(6): [6][TY][32]
-            auto OUT = [&](int f, int row) -> float* {
-                return f < 7 ? Ouvp + (f * TY + row) * 32 : Oq + ((f - 7) * TY + row) * 32;
-            };
+            auto OUT = [&](int f, int row) -> float* { return &S.out[f][row][0]; };
             const float* V0 = &S.v[cx.st][0][r][bc];
             const float* PQ = &S.pq[cx.st][0][r][bc];
             constexpr int F = R * TMA_BW;  // field stride in a ring slot
@@ -372,10 +373,10 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     }
                 }
             }
-            S.suv[DEEP ? 0 : par][0][r][cc] = ub;
-            S.suv[DEEP ? 0 : par][1][r][cc] = vb[0];
-            S.suv[DEEP ? 0 : par][2][r][cc] = vb[1];
-            S.suv[DEEP ? 0 : par][3][r][cc] = vb[2];
+            S.suv[par][0][r][cc] = ub;
+            S.suv[par][1][r][cc] = vb[0];
+            S.suv[par][2][r][cc] = vb[1];
+            S.suv[par][3][r][cc] = vb[2];
             if (tid0) tma_wait_read0();  // the previous step's output staging has been read
             __syncthreads();             // S1
             if (tid0) {  // the ring slots of plane s-1 are free: prefetch what later steps consume
@@ -398,8 +399,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                 const bool needQ = ROLE == 0 || ROLE == 2 || (ROLE == 3 && lane >= 16 && r >= 1 && r <= TY);
                 const bool xl_ = INT || xl, yl_ = INT || yl, xf_ = INT || xf, yf_ = INT || yf;
                 if (needP) {
-                    const float ux = S.suv[DEEP ? 0 : par][0][r][cc + 1];
-                    const float uy = S.suv[DEEP ? 0 : par][0][r + 1][cc];
+                    const float ux = S.suv[par][0][r][cc + 1];
+                    const float uy = S.suv[par][0][r + 1][cc];
                     const float g0 = xl_ ? ux - ub : 0.f, g1 = yl_ ? uy - ub : 0.f, g2 = zl ? ub1 - ub : 0.f;
                     pn[0] = fmaf(sp.sigma, g0 - vb[0], pk[0]);
                     pn[1] = fmaf(sp.sigma, g1 - vb[1], pk[1]);
@@ -415,8 +416,8 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
                     float dx[3], dy[3], dz[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        const float vx = S.suv[DEEP ? 0 : par][1 + k][r][cc - 1];
-                        const float vy = S.suv[DEEP ? 0 : par][1 + k][r - 1][cc];
+                        const float vx = S.suv[par][1 + k][r][cc - 1];
+                        const float vy = S.suv[par][1 + k][r - 1][cc];
                         dx[k] = fmaf(INT ? 1.f : mxl, vb[k], -vx);  // (x < nx-1 ? vb : 0) - vb(x-1)
                         dy[k] = fmaf(INT ? 1.f : myl, vb[k], -vy);
                         dz[k] = fmaf(zl ? 1.f : 0.f, vb[k], -in.vb[k]);
@@ -569,6 +570,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             if (s + 1 > ze) break;
             step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
         }
+        if (A.round_ctr && tid0 && jr < A.rounds &&  // round jr done (after S2 of its last step); the launch's
+            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)  // last increment: no
+            atomicExch(A.round_ctr, 0ull);  // CTA waits any more, the next launch (stream-ordered) starts from 0
     }
     if (PEER && A.done) {  // peer mode: publish once every CTA's halo stores are visible system-wide
         __threadfence_system();

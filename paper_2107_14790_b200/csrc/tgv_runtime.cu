@@ -88,9 +88,11 @@ struct tgv_ctx {
     int4* d_sched = nullptr;  // persistent-kernel schedule (fused TMA kernel)
     int* d_sched_off = nullptr;
     int sched_ctas = 0, sched_zc = -1, sched_per_sm = 1;
+    int sched_rounds = 0;                 // whole lock-step rounds of the schedule (items / G)
+    cudaGraphExec_t gexec = nullptr;      // GRAPH_K iterations, re-captured and updated per tgv_iterate call
     int4* d_esched = nullptr;  // the energy sweep's own copy (its chunk and CTA count never change)
     int* d_esched_off = nullptr;
-    int esched_ctas = 0, esched_zc = -1;
+    int esched_ctas = 0, esched_zc = -1, esched_rounds = 0, esched_per_sm = 0;
     bool fused_tma = true;  // TMA-staged fused kernel (TGV_FUSED_IMPL=regs selects the register one)
     CUtensorMap m_ld1{}, m_ld3{}, m_ld6{}, m_st1{}, m_st3{}, m_st6{}, m_h{};
 
@@ -320,6 +322,7 @@ void launch_tvl1_fused_t(tgv_ctx* c, const FusedArgs& A, dim3 grd)
 }
 
 int build_schedule(tgv_ctx* c, int zc, int per_sm = 1, bool energy = false);
+int64_t env_int(const char* name, int64_t dflt);
 int fused_zc(const tgv_ctx* c);
 
 template <int SLOTS, typename CT>
@@ -370,6 +373,10 @@ int launch_tvl1_fused(tgv_ctx* c)
         if ((c->sched_zc != A.zc || c->sched_per_sm != 2) && (rc = build_schedule(c, A.zc, 2))) return rc;
         A.sched = c->d_sched;
         A.sched_off = c->d_sched_off;
+        if (env_int("TGV_ROUND_SYNC", 1) && c->sched_rounds > 1 && !c->group) {  // as launch_fused_tma
+            A.round_ctr = c->flags + 4;
+            A.rounds = c->sched_rounds;
+        }
         dim3 grd(c->sched_ctas, 1, 1);
         if (c->slots == 8 && c->count_bytes == 1) rc = launch_tvl1_tma_t<8, uint8_t>(c, A, grd);
         else if (c->slots == 8) rc = launch_tvl1_tma_t<8, uint16_t>(c, A, grd);
@@ -507,6 +514,9 @@ int build_schedule(tgv_ctx* c, int zc, int per_sm, bool energy)
                                             env_int("TGV_PERSIST_CTAS", (int64_t)c->num_sms * per_sm));  // dev knob
     const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, (planes + 7) / 8));
     std::vector<std::vector<int4>> per(G);
+    // items in chunk-major order: every tile of chunk 0, then chunk 1, ...  (A band-major
+    // order -- G tiles climbing all the chunks before the next band -- measured no different
+    // on C4 with the round sync, profiles/r2m_bands_probe.txt.)
     const int64_t whole = items / G * G;
     auto item = [&](int64_t i, int* t, int* z0, int* z1) {
         const int ch = (int)(i / tiles);
@@ -565,39 +575,38 @@ int build_schedule(tgv_ctx* c, int zc, int per_sm, bool energy)
     if (energy) {
         c->esched_ctas = G;
         c->esched_zc = zc;
+        c->esched_rounds = (int)(whole / G);
+        c->esched_per_sm = per_sm;
     } else {
         c->sched_ctas = G;
         c->sched_zc = zc;
         c->sched_per_sm = per_sm;
+        c->sched_rounds = (int)(whole / G);
     }
     return TGV_OK;
 }
 
-template <int SLOTS, typename CT, bool PEER, bool DEEP = false>
+template <int SLOTS, typename CT, bool PEER>
 int launch_fused_tma_tp(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
-    const size_t smem = sizeof(TmaSmem<TMA_TY, HB, DEEP>) + 128;
+    const size_t smem = sizeof(TmaSmem<TMA_TY, HB>) + 128;
     // the attribute is per device: set it once for each device this process launches on
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = 1ull << (c->device & 63);
     if (!(attr_set.load() & bit)) {
-        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT, PEER, DEEP>,
+        CU(cudaFuncSetAttribute(fused_tma_kernel<TMA_TY, SLOTS, CT, PEER>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set.fetch_or(bit);
     }
-    fused_tma_kernel<TMA_TY, SLOTS, CT, PEER, DEEP><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
+    fused_tma_kernel<TMA_TY, SLOTS, CT, PEER><<<grd, dim3(32, TMA_TY + 3), smem, c->stream>>>(
         c->m_ld1, c->m_ld3, c->m_ld6, c->m_st1, c->m_st3, c->m_st6, c->m_h, A);
     return TGV_OK;
 }
 template <int SLOTS, typename CT>
 int launch_fused_tma_t(tgv_ctx* c, const TmaArgs& A, dim3 grd)
 {
-    if (c->peer_now) return launch_fused_tma_tp<SLOTS, CT, true>(c, A, grd);
-    if constexpr (SLOTS == 8 && sizeof(CT) == 1) {  // u8 counts, 8 bins: the deeper x ring fits
-        if (env_int("TGV_FUSED_DEEP", 0)) return launch_fused_tma_tp<SLOTS, CT, false, true>(c, A, grd);
-    }
-    return launch_fused_tma_tp<SLOTS, CT, false>(c, A, grd);
+    return c->peer_now ? launch_fused_tma_tp<SLOTS, CT, true>(c, A, grd) : launch_fused_tma_tp<SLOTS, CT, false>(c, A, grd);
 }
 
 int launch_fused_tma(tgv_ctx* c)
@@ -641,6 +650,14 @@ int launch_fused_tma(tgv_ctx* c)
     if ((c->sched_zc != A.zc || c->sched_per_sm != 1) && (rc = build_schedule(c, A.zc, 1))) return rc;
     A.sched = c->d_sched;
     A.sched_off = c->d_sched_off;
+    // lock-step rounds (flags[4] counts finished rounds): C4 24.2 vs 26.0-26.2 ms per launch
+    // without (profiles/r2l_*); TGV_ROUND_SYNC=0 turns it off.  Only for a kernel that has the
+    // GPU to itself: the members of an in-process group (and peer-mode ranks, which may share
+    // a device) run concurrently, and a round wait needs every CTA of its grid resident.
+    if (env_int("TGV_ROUND_SYNC", 1) && c->sched_rounds > 1 && !c->group && !c->peer_now) {
+        A.round_ctr = c->flags + 4;
+        A.rounds = c->sched_rounds;
+    }
     dim3 grd(c->sched_ctas, 1, 1);
     if (c->slots == 8 && c->count_bytes == 1) rc = launch_fused_tma_t<8, uint8_t>(c, A, grd);
     else if (c->slots == 8) rc = launch_fused_tma_t<8, uint16_t>(c, A, grd);
@@ -896,23 +913,17 @@ int energy_zc(const Geo& g)
 }
 
 // (a4) energy partials; returns the number of partial blocks (energy_final_kernel's input).
-// Default: the TMA-staged sweep (tgv_energy_tma.cuh); TGV_ENERGY_IMPL=regs selects the
-// register-streaming energy_partial_kernel (the A/B baseline).
-template <int SLOTS, typename CT>
-int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblocks)
+// Default: the register-streaming energy_partial_kernel.  TGV_ENERGY_IMPL=tma: the
+// TMA-staged sweep (tgv_energy_tma.cuh), one CTA per SM with a 5-plane ring (4 with 16-B
+// counts); =tma2 (u8 counts, 8 bins): two CTAs per SM with 3-plane rings.  Measured:
+// profiles/r2m_*, r2n_*.
+template <int SLOTS, typename CT, int NS>
+int launch_energy_tma(tgv_ctx* c, const EnergyArgs& ea, const EnergyConsts& K, const Bufs& b, int per_sm, int* nblocks)
 {
-    const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
-    const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
-    if (impl && !strcmp(impl, "regs")) {
-        const EnergySched es = energy_sched(c->g, c->energy_blocks);
-        energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
-        *nblocks = c->energy_blocks;
-        return TGV_OK;
-    }
     constexpr int HB = SLOTS * (int)sizeof(CT);
     const int zc = energy_zc(c->g);
     int rc;
-    if (c->esched_zc != zc && (rc = build_schedule(c, zc, 1, true))) return rc;
+    if ((c->esched_zc != zc || c->esched_per_sm != per_sm) && (rc = build_schedule(c, zc, per_sm, true))) return rc;
     EnTmaArgs A{};
     A.g = c->g;
     A.s_u = slotU(b.cu);
@@ -925,17 +936,39 @@ int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblock
     A.alpha0 = (float)ea.alpha0;
     A.lambda = (float)ea.lambda;
     A.V = (float)ea.V;
-    const size_t smem = sizeof(EnSmem<TMA_TY, HB>) + 128;
+    if (env_int("TGV_ROUND_SYNC", 1) && c->esched_rounds > 1 && !c->group) {  // as launch_fused_tma
+        A.round_ctr = c->flags + 5;
+        A.rounds = c->esched_rounds;
+    }
+    const size_t smem = sizeof(EnSmem<TMA_TY, HB, NS>) + 128;
     static std::atomic<uint64_t> attr_set{0};
     const uint64_t bit = 1ull << (c->device & 63);
     if (!(attr_set.load() & bit)) {
-        CU(cudaFuncSetAttribute(energy_tma_kernel<TMA_TY, SLOTS, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CU(cudaFuncSetAttribute(energy_tma_kernel<TMA_TY, SLOTS, CT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
         attr_set.fetch_or(bit);
     }
-    energy_tma_kernel<TMA_TY, SLOTS, CT><<<c->esched_ctas, dim3(32, TMA_TY), smem, c->stream>>>(
+    energy_tma_kernel<TMA_TY, SLOTS, CT, NS><<<c->esched_ctas, dim3(32, TMA_TY), smem, c->stream>>>(
         c->m_ld1, c->m_ld3, c->m_ld6, c->m_h, A, K, c->partials);
     *nblocks = c->esched_ctas;
+    return TGV_OK;
+}
+
+template <int SLOTS, typename CT>
+int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblocks)
+{
+    constexpr int HB = SLOTS * (int)sizeof(CT);
+    const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
+    const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
+    if (impl && !strcmp(impl, "tma2") && HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
+    if (impl && !strncmp(impl, "tma", 3)) return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
+    EnergySched es = energy_sched(c->g, c->energy_blocks);
+    if (env_int("TGV_ROUND_SYNC", 1) && es.items / c->energy_blocks > 1 && !c->group) {  // as launch_fused_tma
+        es.round_ctr = c->flags + 6;
+        es.rounds = es.items / c->energy_blocks;
+    }
+    energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
+    *nblocks = c->energy_blocks;
     return TGV_OK;
 }
 
@@ -1788,6 +1821,95 @@ int tgv_sync(tgv_ctx* c)
     return sync_stream(c);
 }
 
+// One iteration's launches (and, with several ranks, its halo exchanges) on c->stream.
+static int iterate_one(tgv_ctx* c)
+{
+    int rc;
+    if (c->model == TGV_MODEL_TVL1 && c->schedule == TGV_SCHEDULE_FUSED) {
+        if ((rc = halo_exchange(c, plan_tvl1_fused(c->k)))) return rc;
+        if ((rc = launch_tvl1_fused(c))) return rc;
+    } else if (c->model == TGV_MODEL_TVL1) {
+        if ((rc = halo_exchange(c, plan_tvl1_a(c->k)))) return rc;
+        if ((rc = launch_tvl1(c, 0))) return rc;
+        if ((rc = halo_exchange(c, plan_tvl1_b(c->k)))) return rc;
+        if ((rc = launch_tvl1(c, 1))) return rc;
+    } else if (c->schedule == TGV_SCHEDULE_SPLIT) {
+        if ((rc = halo_exchange(c, plan_split_a(c->k)))) return rc;
+        if ((rc = launch_split(c, 0))) return rc;
+        if ((rc = halo_exchange(c, plan_split_b(c->k)))) return rc;
+        if ((rc = launch_split(c, 1))) return rc;
+    } else if (peer_ready(c)) {  // peer halo mode: the previous launch already wrote our halos
+        if (c->halo_fresh) {
+            c->peer_wait = c->seq;
+        } else {
+            if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
+            c->peer_wait = 0;
+        }
+        c->peer_now = true;
+        rc = launch_fused(c);
+        c->peer_now = false;
+        if (rc) return rc;
+        c->halo_fresh = true;
+    } else {
+        if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
+        if ((rc = launch_fused(c))) return rc;
+    }
+    if (!peer_ready(c)) c->halo_fresh = false;
+    c->k += 1;
+    return TGV_OK;
+}
+
+// CUDA graph of the iteration loop (one GPU, no exchanges, no per-launch timing): the state
+// buffers rotate with period GRAPH_K (u / v over 3 slots, p / q over 2), so GRAPH_K
+// iterations captured from k = 0 mod GRAPH_K replay for every later block.  Each
+// tgv_iterate call re-captures them (whatever changed since -- schedule, model, counts,
+// knobs -- is captured as it is now) and updates the executable graph in place; the first
+// iterations of the call run directly, so every lazily built resource (persistent
+// schedule, kernel attributes) exists before the capture.  TGV_GRAPH=0 turns it off.
+constexpr int GRAPH_K = 6;
+
+static bool graph_ok(tgv_ctx* c, int32_t n)
+{
+    return n >= 3 * GRAPH_K && c->nranks == 1 && !c->timing && !peer_ready(c) && env_int("TGV_GRAPH", 1);
+}
+
+// capture GRAPH_K iterations into c->gexec; false (nothing enqueued, k unchanged) on failure
+static bool graph_capture(tgv_ctx* c)
+{
+    const int64_t k0 = c->k;
+    const bool poisoned0 = c->poisoned;  // a call the capture rejects is not a device fault
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    int rc = TGV_OK;
+    for (int i = 0; i < GRAPH_K && rc == TGV_OK; ++i) rc = iterate_one(c);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->k = k0;
+    c->halo_fresh = false;
+    bool ok = rc == TGV_OK && e == cudaSuccess && g;
+    if (ok && c->gexec) {
+        cudaGraphExecUpdateResultInfo info{};
+        if (cudaGraphExecUpdate(c->gexec, g, &info) != cudaSuccess) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+    }
+    if (ok && !c->gexec && cudaGraphInstantiate(&c->gexec, g, 0) != cudaSuccess) {
+        c->gexec = nullptr;
+        ok = false;
+    }
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {  // the direct path runs instead (and meets any real fault itself)
+        cudaGetLastError();
+        c->poisoned = poisoned0;
+        c->err[0] = 0;
+    }
+    return ok;
+}
+
 static int iterate_enqueue(tgv_ctx* c, int32_t n)
 {
     int rc = check_ready(c);
@@ -1795,39 +1917,22 @@ static int iterate_enqueue(tgv_ctx* c, int32_t n)
     if (n < 0) return fail(c, TGV_EINVAL, "n < 0");
     if (!c->loaded) return fail(c, TGV_ESTATE, "iterate before load");
     if (c->group) return fail(c, TGV_ESTATE, "grouped context: use tgv_group_iterate");
-    for (int32_t it = 0; it < n; ++it) {
-        if (c->model == TGV_MODEL_TVL1 && c->schedule == TGV_SCHEDULE_FUSED) {
-            if ((rc = halo_exchange(c, plan_tvl1_fused(c->k)))) return rc;
-            if ((rc = launch_tvl1_fused(c))) return rc;
-        } else if (c->model == TGV_MODEL_TVL1) {
-            if ((rc = halo_exchange(c, plan_tvl1_a(c->k)))) return rc;
-            if ((rc = launch_tvl1(c, 0))) return rc;
-            if ((rc = halo_exchange(c, plan_tvl1_b(c->k)))) return rc;
-            if ((rc = launch_tvl1(c, 1))) return rc;
-        } else if (c->schedule == TGV_SCHEDULE_SPLIT) {
-            if ((rc = halo_exchange(c, plan_split_a(c->k)))) return rc;
-            if ((rc = launch_split(c, 0))) return rc;
-            if ((rc = halo_exchange(c, plan_split_b(c->k)))) return rc;
-            if ((rc = launch_split(c, 1))) return rc;
-        } else if (peer_ready(c)) {  // peer halo mode: the previous launch already wrote our halos
-            if (c->halo_fresh) {
-                c->peer_wait = c->seq;
-            } else {
-                if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
-                c->peer_wait = 0;
+    int32_t it = 0;
+    if (graph_ok(c, n)) {
+        // direct until k = 0 mod GRAPH_K, at least one iteration
+        do {
+            if ((rc = iterate_one(c))) return rc;
+            ++it;
+        } while (c->k % GRAPH_K);
+        if (graph_capture(c)) {
+            for (; n - it >= GRAPH_K; it += GRAPH_K) {
+                CU(cudaGraphLaunch(c->gexec, c->stream));
+                c->k += GRAPH_K;
             }
-            c->peer_now = true;
-            rc = launch_fused(c);
-            c->peer_now = false;
-            if (rc) return rc;
-            c->halo_fresh = true;
-        } else {
-            if ((rc = halo_exchange(c, plan_fused(c->k)))) return rc;
-            if ((rc = launch_fused(c))) return rc;
         }
-        if (!peer_ready(c)) c->halo_fresh = false;
-        c->k += 1;
     }
+    for (; it < n; ++it)
+        if ((rc = iterate_one(c))) return rc;
     return TGV_OK;
 }
 
@@ -2421,6 +2526,7 @@ void tgv_destroy(tgv_ctx* c)
     cudaFree(c->d_sched_off);
     cudaFree(c->d_esched);
     cudaFree(c->d_esched_off);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

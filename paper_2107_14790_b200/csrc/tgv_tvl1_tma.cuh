@@ -120,9 +120,14 @@ __global__ void __launch_bounds__(32 * (TY + 3), 2)
             tma_load3(&S.h[st][0][0], &m_h, &S.bar_x[st], 8 * x0, y0, min(max(s, 0), g.nzl - 1));
         };
 
+        const int jr = sgi - A.sched_off[blockIdx.x];  // this CTA's segment index (= round while < rounds)
         if (tid0) {
             for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
             for (int tz = zs - 1; tz < zs - 1 + Rg::NX - 1; ++tz) issue_x(tz);
+            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // lock-step rounds, as fused_tma_kernel
+                const unsigned long long want = (unsigned long long)jr * gridDim.x;
+                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
+            }
         }
         mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
         int su = cu.st;
@@ -232,6 +237,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 2)
         }
         __syncthreads();  // the last step's outputs are complete (its parity counts from step zs-1)
         if (tid0) store((ze - (zs - 1)) & 1, ze);
+        if (A.round_ctr && tid0 && jr < A.rounds &&
+            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)
+            atomicExch(A.round_ctr, 0ull);
     }
     if (tid0) tma_wait0();
 }

@@ -1,4 +1,4 @@
-"""A/B the two dense energy sweeps (TMA-staged default vs TGV_ENERGY_IMPL=regs) on C4 and
+"""A/B the dense energy sweeps (register-streaming default, TGV_ENERGY_IMPL=tma / tma2) on C4 and
 C2 after a few iterations, timing each with the library's per-launch CUDA events (dev tool).
 Prints ms per energy launch, the implied algorithmic GB/s (60 B/voxel with u8 counts) and
 the relative difference of E and the gap between the two."""
@@ -22,11 +22,8 @@ for name in ("C4", "C2"):
     nvox = wl.shape[0] * wl.shape[1] * wl.shape[2]
     for rep in range(3):
         res = {}
-        for impl in ("tma", "regs"):
-            if impl == "regs":
-                os.environ["TGV_ENERGY_IMPL"] = "regs"
-            else:
-                os.environ.pop("TGV_ENERGY_IMPL", None)
+        for impl in ("regs", "tma", "tma2"):
+            os.environ["TGV_ENERGY_IMPL"] = impl
             s.energy()
             s.set_timing(True)
             for _ in range(5):
@@ -37,8 +34,10 @@ for name in ("C4", "C2"):
             res[impl] = (ms, e)
             print(f"{name} rep{rep} {impl}: {ms:.3f} ms per energy launch, {60 * nvox / ms / 1e6:.0f} GB/s algorithmic, "
                   f"E {e['E']:.12g} gap {e['gap']:.12g} vmax {e['vmax']:.9g}", flush=True)
-        (a, ea), (b, eb) = res["tma"], res["regs"]
-        print(f"{name} rep{rep} rel dE {abs(ea['E'] - eb['E']) / abs(eb['E']):.2e} "
-              f"d gap {abs(ea['gap'] - eb['gap']) / abs(eb['E']):.2e} speedup {b / a:.3f}", flush=True)
+        b, eb = res["regs"]
+        for impl in ("tma", "tma2"):
+            a, ea = res[impl]
+            print(f"{name} rep{rep} {impl} vs regs: rel dE {abs(ea['E'] - eb['E']) / abs(eb['E']):.2e} "
+                  f"d gap {abs(ea['gap'] - eb['gap']) / abs(eb['E']):.2e} speedup {b / a:.3f}", flush=True)
     os.environ.pop("TGV_ENERGY_IMPL", None)
     s.close()

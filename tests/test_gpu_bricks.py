@@ -239,3 +239,4 @@ def test_fused_schedule_edge_sets():
         assert np.array_equal(out["fused"][0], out["split"][0])
         assert np.array_equal(out["fused"][1], out["split"][1])
         assert np.array_equal(out["fused"][0][frozen], u0[frozen].astype(np.float32))
+

@@ -149,10 +149,11 @@ def test_energy_terms_from_random_state(shape, nb, scale, model):
                                             ((29, 14, 12), 16, 1), ((40, 33, 17), 8, 100), ((70, 9, 21), 16, 100),
                                             ((96, 45, 300), 8, 1)])
 def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
-    """(a4) the TMA-staged energy sweep (default) and the register-streaming one
-    (TGV_ENERGY_IMPL=regs) form the same fp32 per-voxel terms and differ only in the order
-    of the fp64 sums; max|v| is exact.  Ragged tiles, size-1 axes, u8 / u16 counts, 8 / 16
-    bins, and a 300-plane grid (lock-step chunks plus split remainder segments)."""
+    """(a4) the three energy sweeps -- register-streaming (default), TMA-staged with one CTA per
+    SM (TGV_ENERGY_IMPL=tma) and with two (=tma2, u8 counts and 8 bins) -- form the same fp32
+    per-voxel terms and differ only in the order of the fp64 sums; max|v| is exact; each is
+    deterministic.  Ragged tiles, size-1 axes, u8 / u16 counts, 8 / 16 bins, and a 300-plane
+    grid (lock-step chunks, round sync, split remainder segments)."""
     nx, ny, nz = shape
     rng = np.random.default_rng(nb * 7 + nx)
     c = oracle.default_centers(nb)
@@ -160,14 +161,18 @@ def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
     s = solver_cls()(shape, [float(x) for x in c], **params()).load(h)
     for k, a in random_state(shape, 90 + nx, "tgv").items():
         s.set(k, a)
-    et = s.energy()
-    monkeypatch.setenv("TGV_ENERGY_IMPL", "regs")
     er = s.energy()
+    monkeypatch.setenv("TGV_ROUND_SYNC", "0")  # the round sync only orders the items
+    assert s.energy() == er
+    monkeypatch.delenv("TGV_ROUND_SYNC")
+    for impl in ("tma", "tma2"):
+        monkeypatch.setenv("TGV_ENERGY_IMPL", impl)
+        et = s.energy()
+        assert s.energy() == et  # deterministic
+        for k in ("E", "alpha1", "alpha0", "data", "gap"):
+            assert abs(et[k] - er[k]) <= 1e-12 * max(1.0, abs(er["E"]), abs(er["gap"])), (impl, k, et[k], er[k])
+        assert et["vmax"] == er["vmax"], impl
     monkeypatch.delenv("TGV_ENERGY_IMPL")
-    assert s.energy() == et  # deterministic
-    for k in ("E", "alpha1", "alpha0", "data", "gap"):
-        assert abs(et[k] - er[k]) <= 1e-12 * max(1.0, abs(er["E"]), abs(er["dual"])), (k, et[k], er[k])
-    assert et["vmax"] == er["vmax"]
 
 
 @pytest.mark.parametrize("schedule", SCHEDULES)
@@ -232,23 +237,41 @@ def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
             assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
 
 
-@pytest.mark.parametrize("shape,zc", [((67, 41, 23), 0), ((45, 31, 26), 3), ((33, 15, 300), 0), ((96, 30, 9), 1)])
-def test_fused_deep_ring_equals_default_bitwise(monkeypatch, shape, zc):
-    """TGV_FUSED_DEEP (u8 counts, 8 bins: a fourth x-ring slot, outputs staged in the slot of
-    the plane being computed, one suv buffer) only moves data: the iterates equal the default
-    sweep's bit for bit, over ragged tiles, short chunks and split remainder segments."""
-    h = synth.random_histograms(shape, 14)
+@pytest.mark.parametrize("knobs", [{"TGV_ROUND_SYNC": "1"}])
+@pytest.mark.parametrize("shape", [(256, 140, 43), (512, 150, 12)])
+def test_fused_schedule_knobs_equal_default_bitwise(monkeypatch, knobs, shape):
+    """The lock-step round sync (TGV_ROUND_SYNC, default: CTAs wait for each round before the
+    next) only orders the work: many rounds of (tile, short chunk) items plus remainder
+    segments, bitwise the unsynchronised sweep, over launches in a row (the round counter
+    resets at the end of each launch)."""
+    monkeypatch.setenv("TGV_FUSED_ZC", "4" if shape[2] > 20 else "3")
+    h = synth.random_histograms(shape, 15)
     c = list(oracle.default_centers(8))
-    if zc:
-        monkeypatch.setenv("TGV_FUSED_ZC", str(zc))
     outs = []
-    for deep in ("0", "1"):
-        monkeypatch.setenv("TGV_FUSED_DEEP", deep)
-        s = solver_cls()(shape, c).load(h).iterate(21)
-        assert s.info()["count_bytes"] == 1 and s.info()["fused_tma"]
+    for on in (False, True):
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v if on else "0")
+        s = solver_cls()(shape, c).load(h).iterate(7)
         outs.append({f: s.get(f) for f in ("u", "v", "p", "q")})
         s.close()
     for f in ("u", "v", "p", "q"):
+        assert np.array_equal(outs[0][f], outs[1][f]), f
+
+
+def test_tvl1_round_sync_equals_unsynchronised_bitwise(monkeypatch):
+    """TV-L1's TMA sweep (two CTAs per SM) under the lock-step round sync: bitwise the
+    unsynchronised sweep over many rounds of short chunks."""
+    shape = (256, 140, 43)
+    monkeypatch.setenv("TGV_FUSED_ZC", "2")
+    h = synth.random_histograms(shape, 17)
+    c = list(oracle.default_centers(8))
+    outs = []
+    for on in ("0", "1"):
+        monkeypatch.setenv("TGV_ROUND_SYNC", on)
+        s = solver_cls()(shape, c).set_model("tvl1").load(h).iterate(9)
+        outs.append({f: s.get(f) for f in ("u", "p")})
+        s.close()
+    for f in ("u", "p"):
         assert np.array_equal(outs[0][f], outs[1][f]), f
 
 
@@ -442,3 +465,25 @@ def test_staged_load_and_async_read_equal_the_synchronous_path(dtype):
         tgv.tgv_load_staged(s.ctx)  # nothing staged any more
     assert ei.value.status == tgv.TGV_ESTATE
     s.close()
+
+
+@pytest.mark.parametrize("model,schedule", [("tgv", "fused"), ("tgv", "split"), ("tvl1", "fused"), ("tvl1", "split")])
+def test_graph_replay_equals_direct_launches_bitwise(monkeypatch, model, schedule):
+    """tgv_iterate replays a captured CUDA graph of 6 iterations (the buffer-rotation period)
+    for long runs; the iterates equal plain launches bit for bit, from an unaligned k, across
+    a schedule / model change between calls (re-capture, in-place graph update) and a reload."""
+    shape = (45, 31, 26)
+    h = synth.random_histograms(shape, 16)
+    c = list(oracle.default_centers(8))
+    outs = []
+    for graph in ("0", "1"):
+        monkeypatch.setenv("TGV_GRAPH", graph)
+        s = solver_cls()(shape, c).set_model(model).set_schedule(schedule).load(h)
+        s.iterate(5).iterate(40)
+        s.set_schedule("split" if schedule == "fused" else "fused").iterate(23)
+        s.set_schedule(schedule).load(h).iterate(31)
+        outs.append({f: s.get(f) for f in ("u", "p")})
+        outs[-1]["E"] = s.energy()["E"]
+        s.close()
+    for f in ("u", "p", "E"):
+        assert np.array_equal(outs[0][f], outs[1][f]), f
