@@ -229,7 +229,8 @@ int tgv_leaf_rebind(tgv_ctx* ctx, int64_t z_begin, int64_t z_end);
  * side 0 if the record's owner is its lower neighbour (slab just below) or 1 if its
  * upper.  From then on the fused TGV kernel of the importer writes its boundary
  * planes into that neighbour's halo planes and both hand over through the flags;
- * both neighbours must map each other, and destroy is then collective.
+ * both neighbours must map each other, and the ranks must then be synchronised
+ * before tgv_destroy (which itself makes no collective call, see tgv_create).
  * Errors: TGV_EINVAL, TGV_ESTATE, TGV_ECUDA. */
 int tgv_peer_export(tgv_ctx* ctx, uint8_t rec[192]);
 int tgv_peer_import(tgv_ctx* ctx, int side, const uint8_t rec[192]);
@@ -281,8 +282,10 @@ int tgv_prolong_from(tgv_ctx* fine, const tgv_ctx* coarse);
  * term.  Multi-GPU: FUSED exchanges the one-plane halos of its
  * plan once per iteration by NCCL send/recv, SPLIT before each half-step; in
  * peer halo mode the fused kernel itself stores its boundary planes into the
- * neighbours' halo planes (no exchange between iterations).  Blocks until the
- * device work is done.
+ * neighbours' halo planes (no exchange between iterations).  On one GPU
+ * without per-kernel timing, long runs replay a captured CUDA graph of six
+ * iterations (the buffer-rotation period; TGV_GRAPH=0 disables it; the results
+ * are bitwise those of plain launches).  Blocks until the device work is done.
  * Errors: TGV_EINVAL (n < 0), TGV_ESTATE (before load / poisoned), TGV_ECUDA, TGV_ENCCL. */
 int tgv_iterate(tgv_ctx* ctx, int32_t n);
 

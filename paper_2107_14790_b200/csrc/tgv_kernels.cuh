@@ -981,8 +981,6 @@ __device__ __forceinline__ void energy_voxel_terms(const EnVoxel& e, const HistR
 // rows of one x tile, item = (x tile, 8-row group, z chunk); each warp marches its chunk in z.
 struct EnergySched {
     int ntx, nyg, zc, items;
-    unsigned long long* round_ctr;  // lock-step rounds of the grid-stride loop (as fused_tma_kernel), or null
-    int rounds;                     // full rounds: items / gridDim.x
 };
 
 // (a4) dense energy / restricted gap (R14).  HBM-bound: each of the
@@ -1006,15 +1004,7 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int sy = g.px, sz = g.plane;
     const float al1 = (float)ea.alpha1, al0 = (float)ea.alpha0, lam = (float)ea.lambda, VV = (float)ea.V;
-    for (int it = blockIdx.x, kr = 0; it < es.items; it += gridDim.x, ++kr) {
-        if (es.round_ctr && kr >= 1 && kr < es.rounds) {  // wait (bounded) until every block finished round kr-1
-            if (threadIdx.x == 0) {
-                const unsigned long long want = (unsigned long long)kr * gridDim.x;
-                for (uint32_t n = 0; *(volatile unsigned long long*)es.round_ctr < want && n < (1u << 22); ++n)
-                    __nanosleep(64);
-            }
-            __syncthreads();
-        }
+    for (int it = blockIdx.x; it < es.items; it += gridDim.x) {
         const int xt = it % es.ntx, r = it / es.ntx;
         // cells past the grid's x / y ends (ragged last tile / row group) march along on a
         // clamped in-grid cell without accumulating: every thread reaches the per-plane barrier
@@ -1065,11 +1055,6 @@ __global__ void __launch_bounds__(256, SLOTS == 8 ? 3 : 2)
             // ---- carry
             vm0 = v0, vm1 = v1, vm2 = v2, pzm = p2;
             uc = un, qzz = qzzn, qxz = qxzn, qyz = qyzn;
-        }
-        if (es.round_ctr && kr < es.rounds) {
-            __syncthreads();
-            if (threadIdx.x == 0 && atomicAdd(es.round_ctr, 1ull) == (unsigned long long)es.rounds * gridDim.x - 1)
-                atomicExch(es.round_ctr, 0ull);  // the launch's last increment
         }
     }
     __shared__ double red[EN_TERMS][8];

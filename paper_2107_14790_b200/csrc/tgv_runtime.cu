@@ -449,6 +449,17 @@ EncodeTiledFn encode_fn()
     return fn;
 }
 
+// L2 sector promotion of the TMA loads (TGV_TMA_PROMO: 0 none, 1 64 B, 2 128 B, 3 256 B = default)
+CUtensorMapL2promotion tma_promo()
+{
+    switch (env_int("TGV_TMA_PROMO", 3)) {
+        case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
+}
+
 // state as a 4-D tensor {x: nx, y: ny, plane: nzl+2 (halo'd), slot: NSLOT}; boxes of nf slots
 int make_state_map(tgv_ctx* c, CUtensorMap* m, int bw, int bh, int nf)
 {
@@ -460,7 +471,7 @@ int make_state_map(tgv_ctx* c, CUtensorMap* m, int bw, int bh, int nf)
     cuuint32_t box[4] = {(cuuint32_t)bw, (cuuint32_t)bh, 1, (cuuint32_t)nf};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c->state, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tma_promo(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled(state, box %dx%dx%d) = %d", bw, bh, nf, (int)r);
     return TGV_OK;
@@ -480,7 +491,7 @@ int make_hist_map(tgv_ctx* c)
     cuuint32_t box[3] = {256, (cuuint32_t)TMA_TY, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&c->m_h, dt, 3, const_cast<void*>(hist_ptr(c)), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tma_promo(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(c, TGV_ECUDA, "cuTensorMapEncodeTiled(hist) = %d", (int)r);
     return TGV_OK;
@@ -913,10 +924,12 @@ int energy_zc(const Geo& g)
 }
 
 // (a4) energy partials; returns the number of partial blocks (energy_final_kernel's input).
-// Default: the register-streaming energy_partial_kernel.  TGV_ENERGY_IMPL=tma: the
-// TMA-staged sweep (tgv_energy_tma.cuh), one CTA per SM with a 5-plane ring (4 with 16-B
-// counts); =tma2 (u8 counts, 8 bins): two CTAs per SM with 3-plane rings.  Measured:
-// profiles/r2m_*, r2n_*.
+// Default: the TMA-staged sweep (tgv_energy_tma.cuh) on the lock-step round schedule -- two
+// CTAs per SM with 3-plane rings when the grid fills whole rounds of 2 x 148 tiles (u8
+// counts, 8 bins): C4 13.7 ms = 0.72 of the measured copy; else one CTA per SM with a 5-plane
+// ring (4 with 16-B counts): C2 0.31 ms.  TGV_ENERGY_IMPL=regs | tma | tma2 forces one; the
+// register-streaming energy_partial_kernel measured 17.2-19.3 ms on C4, 0.29-0.34 ms on C2
+// (profiles/r2n_energy_zc_tvl1_probes.txt).
 template <int SLOTS, typename CT, int NS>
 int launch_energy_tma(tgv_ctx* c, const EnergyArgs& ea, const EnergyConsts& K, const Bufs& b, int per_sm, int* nblocks)
 {
@@ -960,13 +973,13 @@ int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblock
     constexpr int HB = SLOTS * (int)sizeof(CT);
     const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
     const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
-    if (impl && !strcmp(impl, "tma2") && HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
-    if (impl && !strncmp(impl, "tma", 3)) return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
-    EnergySched es = energy_sched(c->g, c->energy_blocks);
-    if (env_int("TGV_ROUND_SYNC", 1) && es.items / c->energy_blocks > 1 && !c->group) {  // as launch_fused_tma
-        es.round_ctr = c->flags + 6;
-        es.rounds = es.items / c->energy_blocks;
+    const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
+    const bool two = impl ? !strcmp(impl, "tma2") : tiles >= 2 * c->num_sms;
+    if (!impl || strcmp(impl, "regs")) {
+        if (two && HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
+        return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
     }
+    const EnergySched es = energy_sched(c->g, c->energy_blocks);
     energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
     *nblocks = c->energy_blocks;
     return TGV_OK;

@@ -22,8 +22,11 @@ for name in ("C4", "C2"):
     nvox = wl.shape[0] * wl.shape[1] * wl.shape[2]
     for rep in range(3):
         res = {}
-        for impl in ("regs", "tma", "tma2"):
-            os.environ["TGV_ENERGY_IMPL"] = impl
+        for impl in ("regs", "tma", "tma2", "default"):
+            if impl == "default":
+                os.environ.pop("TGV_ENERGY_IMPL", None)
+            else:
+                os.environ["TGV_ENERGY_IMPL"] = impl
             s.energy()
             s.set_timing(True)
             for _ in range(5):
@@ -35,7 +38,7 @@ for name in ("C4", "C2"):
             print(f"{name} rep{rep} {impl}: {ms:.3f} ms per energy launch, {60 * nvox / ms / 1e6:.0f} GB/s algorithmic, "
                   f"E {e['E']:.12g} gap {e['gap']:.12g} vmax {e['vmax']:.9g}", flush=True)
         b, eb = res["regs"]
-        for impl in ("tma", "tma2"):
+        for impl in ("tma", "tma2", "default"):
             a, ea = res[impl]
             print(f"{name} rep{rep} {impl} vs regs: rel dE {abs(ea['E'] - eb['E']) / abs(eb['E']):.2e} "
                   f"d gap {abs(ea['gap'] - eb['gap']) / abs(eb['E']):.2e} speedup {b / a:.3f}", flush=True)

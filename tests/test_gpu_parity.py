@@ -147,10 +147,11 @@ def test_energy_terms_from_random_state(shape, nb, scale, model):
 
 @pytest.mark.parametrize("shape,nb,scale", [((37, 23, 19), 8, 1), ((1, 1, 9), 8, 1), ((33, 1, 4), 8, 1),
                                             ((29, 14, 12), 16, 1), ((40, 33, 17), 8, 100), ((70, 9, 21), 16, 100),
-                                            ((96, 45, 300), 8, 1)])
+                                            ((96, 45, 300), 8, 1), ((300, 450, 3), 8, 1)])
 def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
-    """(a4) the three energy sweeps -- register-streaming (default), TMA-staged with one CTA per
-    SM (TGV_ENERGY_IMPL=tma) and with two (=tma2, u8 counts and 8 bins) -- form the same fp32
+    """(a4) the three energy sweeps -- TMA-staged with one CTA per SM (TGV_ENERGY_IMPL=tma) or
+    two (=tma2, u8 counts and 8 bins; the default picks by grid size) and register-streaming
+    (=regs) -- form the same fp32
     per-voxel terms and differ only in the order of the fp64 sums; max|v| is exact; each is
     deterministic.  Ragged tiles, size-1 axes, u8 / u16 counts, 8 / 16 bins, and a 300-plane
     grid (lock-step chunks, round sync, split remainder segments)."""
@@ -161,18 +162,23 @@ def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
     s = solver_cls()(shape, [float(x) for x in c], **params()).load(h)
     for k, a in random_state(shape, 90 + nx, "tgv").items():
         s.set(k, a)
-    er = s.energy()
+    ed = s.energy()  # default: the TMA sweep
     monkeypatch.setenv("TGV_ROUND_SYNC", "0")  # the round sync only orders the items
-    assert s.energy() == er
+    assert s.energy() == ed
     monkeypatch.delenv("TGV_ROUND_SYNC")
-    for impl in ("tma", "tma2"):
-        monkeypatch.setenv("TGV_ENERGY_IMPL", impl)
+    monkeypatch.setenv("TGV_ENERGY_IMPL", "regs")
+    er = s.energy()
+    for impl in ("tma", "tma2", None):
+        if impl:
+            monkeypatch.setenv("TGV_ENERGY_IMPL", impl)
+        else:
+            monkeypatch.delenv("TGV_ENERGY_IMPL")
         et = s.energy()
         assert s.energy() == et  # deterministic
         for k in ("E", "alpha1", "alpha0", "data", "gap"):
             assert abs(et[k] - er[k]) <= 1e-12 * max(1.0, abs(er["E"]), abs(er["gap"])), (impl, k, et[k], er[k])
         assert et["vmax"] == er["vmax"], impl
-    monkeypatch.delenv("TGV_ENERGY_IMPL")
+    assert et == ed
 
 
 @pytest.mark.parametrize("schedule", SCHEDULES)
