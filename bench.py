@@ -123,6 +123,17 @@ def render_shared(wl, rank, world):
     return [allmaps[i] for i in range(len(wl.cams))]
 
 
+def energy_roofline(tm, info, nvox, peak):
+    """Algorithmic GB/s of the energy sweep (13 fp32 state fields + the stored counts per
+    voxel, read once) from its per-launch CUDA-event time in the timed region."""
+    if not tm.get("energy_launches"):
+        return None
+    ms = tm["energy_ms"] / tm["energy_launches"]
+    bpv = 13 * 4 + info["count_slots"] * info["count_bytes"]
+    gbs = bpv * nvox / (ms * 1e-3) / 1e9
+    return {"kernel_ms": ms, "bytes_per_voxel": bpv, "achieved": gbs, "frac": gbs / peak}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -623,7 +634,9 @@ def run_ours(a):
                          "schedule": a.schedule, "bytes_per_voxel_iteration": bytes_per_it,
                          "count_bytes": info["count_bytes"],
                          "schedule_gbs": bytes_per_it * vox_its / (ms_max * 1e-3) / 1e9 / world,
-                         "kernel_share_of_step": step_kernel_ms / a.steps / ms},
+                         "kernel_share_of_step": step_kernel_ms / a.steps / ms,
+                         # (a4) the energy / gap sweep once per step: 13 fp32 fields + the counts per voxel
+                         "energy": energy_roofline(tm, info, nvox_local, peak)},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": int(round(launches_per_step * a.steps)),
             **({"slab_bitwise": check["slab_bitwise"], "halo_mode": check["halo_mode"],
                 "comm_ranks": check["comm_ranks"], "multi_gpu_check": check} if check else {}),

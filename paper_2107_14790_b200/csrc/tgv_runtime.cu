@@ -924,12 +924,12 @@ int energy_zc(const Geo& g)
 }
 
 // (a4) energy partials; returns the number of partial blocks (energy_final_kernel's input).
-// Default: the TMA-staged sweep (tgv_energy_tma.cuh) on the lock-step round schedule -- two
-// CTAs per SM with 3-plane rings when the grid fills whole rounds of 2 x 148 tiles (u8
-// counts, 8 bins): C4 13.7 ms = 0.72 of the measured copy; else one CTA per SM with a 5-plane
-// ring (4 with 16-B counts): C2 0.31 ms.  TGV_ENERGY_IMPL=regs | tma | tma2 forces one; the
-// register-streaming energy_partial_kernel measured 17.2-19.3 ms on C4, 0.29-0.34 ms on C2
-// (profiles/r2n_energy_zc_tvl1_probes.txt).
+// Default: on grids that fill whole rounds of 2 x 148 tiles (u8 counts, 8 bins) the
+// TMA-staged sweep (tgv_energy_tma.cuh) with two CTAs per SM and 3-plane rings on the
+// lock-step round schedule: C4 13.7 ms = 0.72 of the measured copy (register sweep 17.3 ms);
+// elsewhere the register-streaming energy_partial_kernel (C2 0.29 ms; the TMA sweep with one
+// CTA per SM 0.31 ms, two 0.46 ms).  TGV_ENERGY_IMPL=regs | tma | tma2 forces one
+// (profiles/r2n_energy_zc_tvl1_probes.txt, r2o_probes.txt).
 template <int SLOTS, typename CT, int NS>
 int launch_energy_tma(tgv_ctx* c, const EnergyArgs& ea, const EnergyConsts& K, const Bufs& b, int per_sm, int* nblocks)
 {
@@ -974,11 +974,10 @@ int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblock
     const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
     const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
     const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
-    const bool two = impl ? !strcmp(impl, "tma2") : tiles >= 2 * c->num_sms;
-    if (!impl || strcmp(impl, "regs")) {
-        if (two && HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
-        return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
+    if (impl ? !strcmp(impl, "tma2") : (tiles >= 2 * c->num_sms && HB == 8)) {
+        if (HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
     }
+    if (impl && !strncmp(impl, "tma", 3)) return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
     const EnergySched es = energy_sched(c->g, c->energy_blocks);
     energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
     *nblocks = c->energy_blocks;
