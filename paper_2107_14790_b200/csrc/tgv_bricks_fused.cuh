@@ -37,14 +37,6 @@ struct BrickFusedSmem {
     int nb[27];
 };
 
-// RING: the row warps' inputs (all fields but the counts) staged by cp.async two planes
-// ahead of use (u three) in per-thread ring slots after BrickFusedSmem, instead of one plane
-// ahead in registers: more bytes in flight per SM at the same register count.
-struct BrickRowRing {
-    float x[3][15][BF_R][32];  // v_k(3), v_{k-1}(3), p(3), q(6) of plane t (slot t mod 3), lane fastest
-    float u[4][2][BF_R][32];   // u_k, u_{k-1} of plane t (slot t mod 4)
-};
-
 // 4-byte asynchronous global -> shared copy (no register staging; visible to the
 // issuing thread after cp.async.wait_all)
 __device__ __forceinline__ void bf_cp_async4(void* dst, const float* src)
@@ -66,7 +58,7 @@ struct BrickFusedArgs {
     int fold_x;             // 1: this kernel stores the frozen x-faces' duals (else the face launch does)
 };
 
-template <int LE, int SLOTS, typename CT, bool RING = false>
+template <int LE, int SLOTS, typename CT>
 __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const BrickFusedArgs A)
 {
     constexpr int E = 1 << LE;
@@ -174,43 +166,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         return h;
     };
 
-    // RING: x fields of plane t and u of plane t+1 into this row thread's ring slots
-    [[maybe_unused]] BrickRowRing* RR = reinterpret_cast<BrickRowRing*>(bf_smem + sizeof(BrickFusedSmem));
-    constexpr int FS = BF_R * 32;  // field stride in a ring slot
-    auto rissue = [&](int t) {
-        if constexpr (RING) {
-            float* d = &RR->x[(t + 3) % 3][0][r][lane];
-            const int i = (t <= E) ? at(t) : -1;
-            if (i < 0) {
-#pragma unroll
-                for (int f = 0; f < 15; ++f) d[f * FS] = 0.f;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    bf_cp_async4(d + k * FS, a.vk[k] + i);
-                    bf_cp_async4(d + (3 + k) * FS, a.vm[k] + i);
-                }
-                if (needP) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) bf_cp_async4(d + (6 + k) * FS, a.pk[k] + i);
-                }
-                if (needQ) {
-#pragma unroll
-                    for (int m = 0; m < 6; ++m) bf_cp_async4(d + (9 + m) * FS, a.qk[m] + i);
-                }
-            }
-            float* du = &RR->u[(t + 5) & 3][0][r][lane];
-            const int iu = at(t + 1);
-            if (iu < 0) {
-                du[0] = 0.f;
-                du[FS] = 0.f;
-            } else {
-                bf_cp_async4(du, a.uk + iu);
-                bf_cp_async4(du + FS, a.um + iu);
-            }
-        }
-    };
-
     auto xissue = [&](int t) {  // x-face cells: plane t's second column into smem
         float* d = S.xb[(t + 3) % 3][role - 3][r];
         const int i = at(t);
@@ -259,7 +214,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
     };
     // commit groups of the x-halo columns: G(s) = {h(s+3), x(s+2)}, issued at step s; at
     // step s all but the newest group have landed: h(s), h(s+1), x(s)
-    // (RING row warps: G(s) = {x(s+2), u(s+3)}, the same two-groups-ahead discipline)
     if (role >= 3) {
         hissue(-1);
         hissue(0);
@@ -267,22 +221,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         asm volatile("cp.async.commit_group;" ::: "memory");
         hissue(1);
         if (xface) xissue(0);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    } else if constexpr (RING) {
-        {  // u(-1)
-            float* du = &RR->u[3][0][r][lane];
-            const int iu = at(-1);
-            if (iu < 0) {
-                du[0] = 0.f;
-                du[FS] = 0.f;
-            } else {
-                bf_cp_async4(du, a.uk + iu);
-                bf_cp_async4(du + FS, a.um + iu);
-            }
-        }
-        rissue(-1);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        rissue(0);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
 
@@ -294,15 +232,15 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         float qn[6];      // q_{k+1}(s-1)
     };
     Carry ca{};
-    U2 u0 = RING ? U2{0.f, 0.f} : load_u(-1), u1 = RING ? U2{0.f, 0.f} : load_u(0);
-    X x0 = RING ? X{} : load_x(-1);
+    U2 u0 = load_u(-1), u1 = load_u(0);
+    X x0 = load_x(-1);
     HistRaw<SLOTS, CT> h0{};
 
     for (int s = -1; s <= E; ++s) {
         const int par = s & 1, pr = par ^ 1;
         // prefetch: u at s+2, the other fields and the counts at s+1
-        const U2 u2 = RING ? U2{0.f, 0.f} : load_u(s + 2);
-        const X x1 = RING ? X{} : load_x(s + 1);
+        const U2 u2 = load_u(s + 2);
+        const X x1 = load_x(s + 1);
         const HistRaw<SLOTS, CT> h1 = load_h(s + 1);
 
         const bool xl = bit(xl_m, s), yl = bit(yl_m, s), zl = bit(own_ex, s + 1);
@@ -319,25 +257,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
             }
 #pragma unroll
             for (int m = 0; m < 6; ++m) x0.q[m] = d0[11 + m];
-        } else if constexpr (RING) {  // this row cell's planes from its ring slots (G(s-2), G(s-3) landed)
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-            const float* du0 = &RR->u[(s + 4) & 3][0][r][lane];
-            const float* du1 = &RR->u[(s + 5) & 3][0][r][lane];
-            u0.uk = du0[0], u0.um = du0[FS], u1.uk = du1[0], u1.um = du1[FS];
-            const float* dx = &RR->x[(s + 3) % 3][0][r][lane];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                x0.vk[k] = dx[k * FS];
-                x0.vm[k] = dx[(3 + k) * FS];
-            }
-            if (needP) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) x0.p[k] = dx[(6 + k) * FS];
-            }
-            if (needQ) {
-#pragma unroll
-                for (int m = 0; m < 6; ++m) x0.q[m] = dx[(9 + m) * FS];
-            }
         }
         // x-face cells: the second column into the frozen brick (same 32-B sectors),
         // copied one plane ahead with cp.async
@@ -354,9 +273,6 @@ __global__ void __launch_bounds__(32 * BF_WARPS, 1) brick_fused_kernel(const Bri
         if (role >= 3) {  // G(s)
             hissue(s + 3);
             if (xface && s + 2 <= E) xissue(s + 2);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        } else if constexpr (RING) {
-            rissue(s + 2);
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
         // (a3) over-relaxed iterate at planes s and s+1

@@ -278,27 +278,18 @@ void launch_brick_dual_le(tgv_bricks* c, const IterPtrs& a, const StepParams& sp
     if (n1) brick_dual_kernel<LE, 1><<<(n1 + 255) / 256, 256, 0, c->stream>>>(a, bgeo(c), sp, c->d_faces, n1);
 }
 
-template <int SLOTS, typename CT, bool RING>
-void launch_brick_fused_r(tgv_bricks* c, const BrickFusedArgs& A)
+template <int SLOTS, typename CT>
+void launch_brick_fused_t(tgv_bricks* c, const BrickFusedArgs& A)
 {
-    auto kern = brick_fused_kernel<5, SLOTS, CT, RING>;
-    const int smem = (int)(sizeof(BrickFusedSmem) + (RING ? sizeof(BrickRowRing) : 0));
+    auto kern = brick_fused_kernel<5, SLOTS, CT>;
     static thread_local int configured_dev = -1;  // the attribute is per device
     if (configured_dev != c->device) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BrickFusedSmem));
         configured_dev = c->device;
     }
     // two CTAs per swept brick: A.n_alist rows of A.nb27 (all solved bricks, or the mixed
     // set's fused subset -- never c->n_alist there)
-    if (A.n_alist) kern<<<2 * A.n_alist, dim3(32, BF_WARPS), smem, c->stream>>>(A);
-}
-
-// TGV_BRICK_RING (dev knob until measured): the row warps' inputs by cp.async two planes ahead
-template <int SLOTS, typename CT>
-void launch_brick_fused_t(tgv_bricks* c, const BrickFusedArgs& A)
-{
-    if (env_int("TGV_BRICK_RING", 0)) launch_brick_fused_r<SLOTS, CT, true>(c, A);
-    else launch_brick_fused_r<SLOTS, CT, false>(c, A);
+    if (A.n_alist) kern<<<2 * A.n_alist, dim3(32, BF_WARPS), sizeof(BrickFusedSmem), c->stream>>>(A);
 }
 
 // FUSED schedule: the frozen-face duals, then one single sweep over the solved bricks

@@ -241,32 +241,3 @@ def test_fused_schedule_edge_sets():
         assert np.array_equal(out["fused"][0][frozen], u0[frozen].astype(np.float32))
 
 
-
-@pytest.mark.parametrize("seed,nbins,big", [(0, 8, False), (1, 8, True), (3, 16, False)])
-def test_fused_row_ring_equals_split_bitwise(seed, nbins, big, monkeypatch):
-    """TGV_BRICK_RING: the fused brick sweep's row warps take their inputs from per-thread
-    cp.async rings two planes ahead instead of registers one plane ahead -- a change of
-    staging only: bitwise the SPLIT schedule on random sparse sets with frozen bricks,
-    u8 / u16 counts and 16 bins, plus a single brick and a line with frozen ends."""
-    from paper_2107_14790_b200.bricks import BrickSolver
-    monkeypatch.setenv("TGV_BRICK_RING", "1")
-    rng = np.random.default_rng(seed + 50)
-    cases = [(_rand_set(rng, 16, 3), None), (np.array([(3, 2, 1)]), np.array([False])),
-             (np.array([(x, 0, 0) for x in range(5)]), np.array([True, False, False, False, True]))]
-    centers = {8: None, 16: list(np.linspace(-0.95, 0.95, 16))}[nbins]
-    for coords, frozen in cases:
-        if frozen is None:
-            frozen = rng.random(len(coords)) < 0.3
-            frozen[0] = False
-        h = _counts(len(coords), 32, 80 + seed, nbins=nbins, max_count=300 if big else 12)
-        u0, v0 = _frozen_state(rng, len(coords), 32)
-        runs = {}
-        for sched in ("fused", "split"):
-            s = BrickSolver(32, coords, frozen, centers=centers, **KW).set_schedule(sched).load(h)
-            s.set_primal(np.where(frozen[:, None, None, None], u0, s.read_u()).astype(np.float32),
-                         (v0 * frozen[:, None, None, None, None]).astype(np.float32))
-            s.iterate(7)
-            runs[sched] = {n: s.get(n) for n in ("u", "v", "p", "q")}
-            s.close()
-        for n in ("u", "v", "p", "q"):
-            assert np.array_equal(runs["fused"][n], runs["split"][n]), n
