@@ -6,6 +6,7 @@ export PYTHONPATH=$PWD
 mkdir -p gpurun_out
 TGV_BUILD_INCREMENTAL=1 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_bricks.py tests/test_gpu_mixed.py -q -m gpu -x > gpurun_out/${T}_pytest_bricks.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "energy" > gpurun_out/${T}_pytest_energy.log 2>&1
 for rg in 0 1 0 1; do
   TGV_BRICK_RING=$rg timeout 900 python bench.py --workload C5 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/${T}_c5_ring${rg}_$(date +%s).json 2>> gpurun_out/${T}_c5.err
 done
