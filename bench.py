@@ -53,7 +53,7 @@ def parse():
                          "(host-resident counts and levels; a step = the whole solve, --levels levels)")
     ap.add_argument("--mixed", action="store_true",
                     help="C5: solve the finest brick level as a 2:1 mixed-level set (R27: frozen border of level-0 "
-                         "bricks or level-1 parent cubes), SPLIT mixed kernels")
+                         "bricks or level-1 parent cubes); its own default schedule (SPLIT) unless --schedule is given")
     ap.add_argument("--parts", type=int, default=0,
                     help="C5: solve the finest brick level in this many Morton parts with frozen shells (R26); "
                          "streamed through one GPU, or shared round-robin by the ranks of a torchrun job")
@@ -760,8 +760,11 @@ def run_bricks(a):
         if s_ is not None:
             s_.set_schedule(a.schedule)  # FUSED by default (32^3 bricks), SPLIT on request
     sols = bl.solvers
-    if a.mixed:  # R27: the finest level as a 2:1 mixed-level set (SPLIT mixed kernels)
-        sols = [bl.build_mixed()] + bl.solvers[1:]
+    if a.mixed:  # R27: the finest level as a 2:1 mixed-level set (SPLIT by default; an explicit --schedule applies)
+        m = bl.build_mixed()
+        if any(x == "--schedule" or x.startswith("--schedule=") for x in sys.argv):
+            m.set_schedule(a.schedule)
+        sols = [m] + bl.solvers[1:]
     vox = [int(s_.info()["nbricks"]) * 32 ** 3 for s_ in sols]
     infos = [s.info() for s in sols]
     solved = [i["solved_voxels"] for i in infos]

@@ -241,6 +241,7 @@ class PartSolver:
         cams, depths, origin, h, r = levels.vote_args
         self.kw = levels.kw
         self.sets = {}
+        self.ubufs = {}
         for p in self.mine:
             Ap = self.parts[p]
             Bp = shell(Ap, self.grid)
@@ -252,16 +253,20 @@ class PartSolver:
             if cnt.max() <= 255:
                 cnt = cnt.astype(np.uint8)
             ps.close()
-            if pinned:
+            ubuf = None
+            if pinned:  # pinned counts (H2D) and a pinned u buffer per part (D2H at full link speed)
                 import torch
                 cnt = torch.from_numpy(cnt).pin_memory().numpy()
+                ubuf = torch.empty(len(c) * self.E ** 3, dtype=torch.float32).pin_memory().numpy()
             self.sets[p] = (c, fr, cnt)
+            self.ubufs[p] = ubuf
 
     def solve(self, iters, pool=None):
         """Coarse levels (resident), then every owned part: H2D of its counts,
         prolongation from the next coarser level, iterations, D2H of its solved bricks'
         u.  pool (dict): keep each part's context between solves (allocation outside
-        the solve).  Returns {part: (coords of its solved bricks, u [n, E, E, E])}."""
+        the solve).  Returns {part: (coords of its solved bricks, u [n, E, E, E])}; with
+        pinned=True each u is a view of the part's pinned buffer, rewritten by the next solve."""
         bl = self.bl
         top = bl.levels - 1
         s = bl.solvers[top].reset().iterate(iters)
@@ -281,7 +286,7 @@ class PartSolver:
                     pool[p] = ps
             ps.load(cnt).prolong_from(s).iterate(iters)
             nA = int((~fr).sum())
-            out[p] = (c[:nA], ps.read_u()[:nA])
+            out[p] = (c[:nA], ps.read_u(self.ubufs[p])[:nA])
             if pool is None:
                 ps.close()
         return out

@@ -151,8 +151,14 @@ class BrickSolver:
         _bcheck(lib.tgv_bricks_iterate(self.ctx, int(n)), self.ctx)
         return self
 
-    def read(self, field):
-        out = np.empty(self.nvox, dtype=np.float32)
+    def read(self, field, out=None):
+        """One field of every brick as [nbricks, E, E, E] float32.  out: a C-contiguous float32
+        host buffer of nvox elements to fill instead of a new array (pinned: a fast D2H)."""
+        if out is None:
+            out = np.empty(self.nvox, dtype=np.float32)
+        elif not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous
+                  and out.size == self.nvox):
+            raise ValueError("out must be a C-contiguous float32 array of nvox elements")
         _bcheck(lib.tgv_bricks_read(self.ctx, int(field), out.ctypes.data, out.size), self.ctx)
         return out.reshape((self.nbricks,) + (self.E,) * 3)
 
@@ -162,8 +168,8 @@ class BrickSolver:
             return self.read(ids[0])
         return np.stack([self.read(f) for f in ids], axis=1)
 
-    def read_u(self):
-        return self.read(tgv.FIELD_U)
+    def read_u(self, out=None):
+        return self.read(tgv.FIELD_U, out)
 
     def energy(self):
         out = np.zeros(6, dtype=np.float64)

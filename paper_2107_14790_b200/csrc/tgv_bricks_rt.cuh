@@ -418,6 +418,37 @@ void launch_brick_pack(tgv_bricks* c, const void* src, int64_t nv, uint16_t* dst
 
 int bricks_init_state(tgv_bricks* c);
 
+// Stream-ordered allocations of the big per-context buffers (the state, the counts and the
+// load staging) from the device's default memory pool, whose release threshold is set to
+// "keep everything": a context destroyed and the next one created -- the parts of a brick
+// level streamed through one GPU -- reuse the same reserved device memory instead of
+// unmapping and re-mapping 10+ GB (cudaFree of a part's state took 6 ms to 2 s, and its
+// implicit device synchronisation stalls every stream; profiles/r2s_parts_probe.txt).
+void* pool_alloc(tgv_bricks* c, size_t bytes)
+{
+    static std::atomic<uint64_t> thr_set{0};
+    const uint64_t bit = 1ull << (c->device & 63);
+    if (!(thr_set.load() & bit)) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        thr_set.fetch_or(bit);
+    }
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void pool_free(tgv_bricks* c, void* p)
+{
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
 // shared tail of tgv_bricks_load / tgv_bricks_vote_depth_maps: range check of the
 // u16 counts in h16 (max in c->d_maxc), u8 narrowing, state initialisation (R9)
 int bricks_finish_counts(tgv_bricks* c, const uint16_t* h16)
@@ -429,15 +460,12 @@ int bricks_finish_counts(tgv_bricks* c, const uint16_t* h16)
     if (maxc > 65535u) return bfail(c, TGV_ERANGE, "histogram count %u exceeds 65535", maxc);
     const int cb = maxc <= 255u && env_int("TGV_FORCE_U16", 0) == 0 ? 1 : 2;
     if (c->hist && cb != c->count_bytes) {
-        cudaFree(c->hist);
+        pool_free(c, c->hist);
         c->device_bytes -= (int64_t)n16 * c->count_bytes;
         c->hist = nullptr;
     }
     if (!c->hist) {
-        if (cudaMalloc(&c->hist, n16 * cb) != cudaSuccess) {
-            cudaGetLastError();
-            return bfail(c, TGV_ENOMEM, "count store allocation failed");
-        }
+        if (!(c->hist = pool_alloc(c, n16 * cb))) return bfail(c, TGV_ENOMEM, "count store allocation failed");
         c->device_bytes += (int64_t)n16 * cb;
     }
     c->count_bytes = cb;
@@ -560,7 +588,7 @@ int bricks_create_impl(const tgv_brickset* S, const tgv_params* P, int dev, tgv_
     }
     c->energy_blocks = 148 * 4;
     const size_t state_bytes = sizeof(float) * (size_t)NSLOT * (size_t)nvox;
-    if (cudaMalloc(&c->state, state_bytes) != cudaSuccess || cudaMalloc(&c->nbr, sizeof(int) * 6 * (size_t)nb) != cudaSuccess ||
+    if (!(c->state = (float*)pool_alloc(c, state_bytes)) || cudaMalloc(&c->nbr, sizeof(int) * 6 * (size_t)nb) != cudaSuccess ||
         cudaMalloc(&c->frozen, (size_t)nb) != cudaSuccess || cudaMalloc(&c->aface, (size_t)nb) != cudaSuccess ||
         cudaMalloc(&c->partials, sizeof(double) * EN_TERMS * c->energy_blocks) != cudaSuccess ||
         cudaMalloc(&c->d_out, sizeof(double) * EN_TERMS) != cudaSuccess ||
@@ -569,6 +597,7 @@ int bricks_create_impl(const tgv_brickset* S, const tgv_params* P, int dev, tgv_
         bfail(c, TGV_ENOMEM, "device allocation failed (%zu B of state)", state_bytes);
         return bail(TGV_ENOMEM);
     }
+    cudaStreamSynchronize(c->stream);  // the pool allocation is usable from any stream from here on
     c->device_bytes = (int64_t)state_bytes + 7 * nb + (int64_t)sizeof(double) * EN_TERMS * (c->energy_blocks + 1);
     std::vector<uint8_t> fr((size_t)nb, 0), af((size_t)nb, 0);
     if (S->frozen)
@@ -860,7 +889,9 @@ int build_mixed_tables(tgv_bricks* c, const tgv_brickset* S, const uint8_t* leve
         return bfail(c, TGV_ENOMEM, "mixed-level brick lists allocation failed");
     }
     c->mixed = true;
-    c->schedule = E == 32 ? TGV_SCHEDULE_FUSED : TGV_SCHEDULE_SPLIT;
+    // SPLIT by default: on C5's mixed finest level it measured 19.6 G solved vox-it/s against
+    // FUSED's 19.0 G on the same box (profiles/r2t_*); tgv_bricks_set_schedule(FUSED) for E = 32
+    c->schedule = TGV_SCHEDULE_SPLIT;
     c->levels_h.assign(levels, levels + nb);
     if (cudaMalloc(&c->d_level, (size_t)nb) != cudaSuccess || cudaMalloc(&c->d_kind, (size_t)nb * 6) != cudaSuccess ||
         cudaMalloc(&c->d_nbr4, sizeof(int) * (size_t)nb * 24) != cudaSuccess ||
@@ -910,22 +941,18 @@ int tgv_bricks_load(tgv_bricks* c, const void* counts, int count_bytes, int64_t 
         return bfail(c, TGV_EINVAL, "n_counts %lld != %lld", (long long)n_counts, (long long)(c->nvox * c->nbins));
     c->loaded = false;
     // u16 store of every count, filled chunk by chunk from a device staging buffer
-    uint16_t* h16 = nullptr;
     const size_t n16 = (size_t)c->nvox * c->slots;
-    if (cudaMalloc(&h16, sizeof(uint16_t) * n16) != cudaSuccess) {
-        cudaGetLastError();
-        return bfail(c, TGV_ENOMEM, "u16 count staging allocation failed");
-    }
+    uint16_t* h16 = (uint16_t*)pool_alloc(c, sizeof(uint16_t) * n16);
+    if (!h16) return bfail(c, TGV_ENOMEM, "u16 count staging allocation failed");
     const int64_t chunk = std::max<int64_t>(1, (64ll << 20) / (c->nbins * count_bytes));  // voxels per chunk
-    void* stg = nullptr;
-    if (cudaMalloc(&stg, (size_t)std::min(chunk, c->nvox) * c->nbins * count_bytes) != cudaSuccess) {
-        cudaGetLastError();
-        cudaFree(h16);
+    void* stg = pool_alloc(c, (size_t)std::min(chunk, c->nvox) * c->nbins * count_bytes);
+    if (!stg) {
+        pool_free(c, h16);
         return bfail(c, TGV_ENOMEM, "count staging allocation failed");
     }
-    auto done = [&](int code) {
-        cudaFree(stg);
-        cudaFree(h16);
+    auto done = [&](int code) {  // stream-ordered: after the pack kernels that read them
+        pool_free(c, stg);
+        pool_free(c, h16);
         return code;
     };
     if (cudaMemsetAsync(c->d_maxc, 0, sizeof(unsigned int), c->stream) != cudaSuccess) return done(bfail(c, TGV_ECUDA, "memset"));
@@ -1104,7 +1131,7 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
-    cudaFree(c->state);
+    pool_free(c, c->state);
     cudaFree(c->nbr);
     cudaFree(c->frozen);
     cudaFree(c->aface);
@@ -1123,7 +1150,7 @@ void tgv_bricks_destroy(tgv_bricks* c)
     cudaFree(c->d_alist_gen);
     cudaFree(c->d_fnb27);
     cudaFree(c->d_alist_fgen);
-    cudaFree(c->hist);
+    pool_free(c, c->hist);
     cudaFree(c->partials);
     cudaFree(c->d_out);
     cudaFree(c->d_maxc);
