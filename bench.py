@@ -842,15 +842,19 @@ def run_bricks(a):
     e2e = None
     if not a.no_e2e:
         hu = None
+        # the step's host data in pinned memory (the contract's "from pinned host memory"):
+        # the depth maps in, the finest level's u out
+        pdepths = [torch.from_numpy(np.ascontiguousarray(d)).pin_memory().numpy() for d in depths]
+        hbuf = torch.empty(int(sols[0].nvox), dtype=torch.float32).pin_memory().numpy()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(a.steps):
             for lev, s in enumerate(sols):
                 # a mixed set votes each brick at its own level (level 0 here)
-                s.vote(cams, depths, voxel_size=float(1 << lev), voxel_radius=wl.voxel_radius * (1 << lev))
+                s.vote(cams, pdepths, voxel_size=float(1 << lev), voxel_radius=wl.voxel_radius * (1 << lev))
             f = solve(iters)
             f.energy()
-            hu = f.read_u()
+            hu = f.read_u(hbuf)
         el = (time.perf_counter() - t0) / a.steps
         h2d = levels * sum(int(d.nbytes) for d in depths)
         e2e = {"value": vox_its / el, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(hu.nbytes) + 48,
