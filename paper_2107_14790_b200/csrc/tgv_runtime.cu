@@ -72,6 +72,7 @@ struct tgv_ctx {
     bool leaf = false;  // NEXT-3: frozen-border leaf (tgv_create_leaf)
     // peer halo mode: the fused TMA kernel writes the neighbours' halo planes
     bool peer = false;          // neighbours' state and flags are mapped
+    bool peer_same_dev = false; // a mapped neighbour runs on this context's GPU
     bool halo_fresh = false;    // our halos hold the current iterate (the neighbours' last launch wrote them)
     float* pdn = nullptr;       // lower / upper neighbour's state (same-process pointer or CUDA IPC mapping)
     float* pup = nullptr;
@@ -663,9 +664,9 @@ int launch_fused_tma(tgv_ctx* c)
     A.sched_off = c->d_sched_off;
     // lock-step rounds (flags[4] counts finished rounds): C4 24.2 vs 26.0-26.2 ms per launch
     // without (profiles/r2l_*); TGV_ROUND_SYNC=0 turns it off.  Only for a kernel that has the
-    // GPU to itself: the members of an in-process group (and peer-mode ranks, which may share
-    // a device) run concurrently, and a round wait needs every CTA of its grid resident.
-    if (env_int("TGV_ROUND_SYNC", 1) && c->sched_rounds > 1 && !c->group && !c->peer_now) {
+    // GPU to itself: the members of an in-process group (and peer-mode ranks whose neighbour
+    // shares the GPU) run concurrently, and a round wait needs every CTA of its grid resident.
+    if (env_int("TGV_ROUND_SYNC", 1) && c->sched_rounds > 1 && !c->group && !(c->peer_now && c->peer_same_dev)) {
         A.round_ctr = c->flags + 4;
         A.rounds = c->sched_rounds;
     }
@@ -1045,6 +1046,7 @@ int tgv_get_unique_id(uint8_t uid[128])
 struct IpcRecord {
     cudaIpcMemHandle_t state, flags;
     int64_t fs, nzl;
+    unsigned char uuid[16];  // the exporter's GPU (neighbours sharing a GPU: no lock-step round sync)
 };
 static_assert(sizeof(IpcRecord) <= 192, "tgv_peer_export record size");
 
@@ -1057,6 +1059,9 @@ static int peer_export(tgv_ctx* c, IpcRecord* rec)
     }
     rec->fs = c->g.fs;
     rec->nzl = c->g.nzl;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess) memcpy(rec->uuid, prop.uuid.bytes, 16);
+    cudaGetLastError();
     return TGV_OK;
 }
 
@@ -1086,6 +1091,10 @@ static int peer_import(tgv_ctx* c, int side, const IpcRecord& n)
     }
     c->peer = true;
     c->halo_fresh = false;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess || !memcmp(prop.uuid.bytes, n.uuid, 16))
+        c->peer_same_dev = true;  // (or unknown: assume shared)
+    cudaGetLastError();
     return TGV_OK;
 }
 
