@@ -925,17 +925,19 @@ int energy_zc(const Geo& g)
 }
 
 // (a4) energy partials; returns the number of partial blocks (energy_final_kernel's input).
-// Default: on grids that fill whole rounds of 2 x 148 tiles (u8 counts, 8 bins) the
-// TMA-staged sweep (tgv_energy_tma.cuh) with two CTAs per SM and 3-plane rings on the
-// lock-step round schedule: C4 13.7 ms = 0.72 of the measured copy (register sweep 17.3 ms);
-// elsewhere the register-streaming energy_partial_kernel (C2 0.29 ms; the TMA sweep with one
-// CTA per SM 0.31 ms, two 0.46 ms).  TGV_ENERGY_IMPL=regs | tma | tma2 forces one
-// (profiles/r2n_energy_zc_tvl1_probes.txt, r2o_probes.txt).
+// Default (u8 counts, 8 bins): the TMA-staged sweep (tgv_energy_tma.cuh) with two CTAs per SM
+// and 3-plane rings on the lock-step round schedule wherever the grid makes a whole round of
+// 2 x 148 (tile, chunk) items with chunks of >= 32 planes: C4 13.7 ms = 0.72 of the measured
+// copy (register sweep 17.3 ms), C2 with 128-plane chunks 0.248 ms (register sweep 0.287,
+// one round-less 256-plane chunk 0.45); elsewhere the register-streaming
+// energy_partial_kernel.  TGV_ENERGY_IMPL=regs | tma | tma2 forces one
+// (profiles/r2n_energy_zc_tvl1_probes.txt, r2o_probes.txt, r2x_energy_zc_probe.txt).
 template <int SLOTS, typename CT, int NS>
-int launch_energy_tma(tgv_ctx* c, const EnergyArgs& ea, const EnergyConsts& K, const Bufs& b, int per_sm, int* nblocks)
+int launch_energy_tma(tgv_ctx* c, const EnergyArgs& ea, const EnergyConsts& K, const Bufs& b, int per_sm, int zc,
+                      int* nblocks)
 {
     constexpr int HB = SLOTS * (int)sizeof(CT);
-    const int zc = energy_zc(c->g);
+    zc = (int)std::max<int64_t>(1, env_int("TGV_ENERGY_ZC", zc));  // dev knob
     int rc;
     if ((c->esched_zc != zc || c->esched_per_sm != per_sm) && (rc = build_schedule(c, zc, per_sm, true))) return rc;
     EnTmaArgs A{};
@@ -974,11 +976,18 @@ int launch_energy_t(tgv_ctx* c, const EnergyArgs& ea, const Bufs& b, int* nblock
     constexpr int HB = SLOTS * (int)sizeof(CT);
     const EnergyConsts K = energy_consts(c->centers, c->nbins, SLOTS);
     const char* impl = getenv("TGV_ENERGY_IMPL");  // dev knob (A/B)
+    // two CTAs per SM need at least one whole round of 2 x 148 (tile, chunk) items: deep grids
+    // take the iteration sweep's chunks, shallower ones chunks cut to make the round (>= 32 planes)
     const int tiles = ((c->g.nx + 31) / 32) * ((c->g.ny + TMA_TY - 1) / TMA_TY);
-    if (impl ? !strcmp(impl, "tma2") : (tiles >= 2 * c->num_sms && HB == 8)) {
-        if (HB == 8) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, nblocks);
+    int zc2 = energy_zc(c->g);
+    if ((int64_t)tiles * ((c->g.nzl + zc2 - 1) / zc2) < 2 * c->num_sms) {
+        const int nch = (2 * c->num_sms + tiles - 1) / tiles;
+        zc2 = (c->g.nzl + nch - 1) / nch;
     }
-    if (impl && !strncmp(impl, "tma", 3)) return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, nblocks);
+    const bool two = HB == 8 && (impl ? !strcmp(impl, "tma2") : zc2 >= 32);
+    if (two) return launch_energy_tma<SLOTS, CT, 3>(c, ea, K, b, 2, zc2, nblocks);
+    if (impl && !strncmp(impl, "tma", 3))
+        return launch_energy_tma<SLOTS, CT, HB <= 16 ? 5 : 4>(c, ea, K, b, 1, energy_zc(c->g), nblocks);
     const EnergySched es = energy_sched(c->g, c->energy_blocks);
     energy_partial_kernel<SLOTS, CT><<<c->energy_blocks, 256, 0, c->stream>>>(ea, c->g, K, es, c->partials);
     *nblocks = c->energy_blocks;

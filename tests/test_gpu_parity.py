@@ -147,7 +147,7 @@ def test_energy_terms_from_random_state(shape, nb, scale, model):
 
 @pytest.mark.parametrize("shape,nb,scale", [((37, 23, 19), 8, 1), ((1, 1, 9), 8, 1), ((33, 1, 4), 8, 1),
                                             ((29, 14, 12), 16, 1), ((40, 33, 17), 8, 100), ((70, 9, 21), 16, 100),
-                                            ((96, 45, 300), 8, 1), ((300, 450, 3), 8, 1)])
+                                            ((96, 45, 300), 8, 1), ((300, 450, 3), 8, 1), ((320, 140, 96), 8, 1)])
 def test_energy_sweeps_agree(shape, nb, scale, monkeypatch):
     """(a4) the three energy sweeps -- TMA-staged with one CTA per SM (TGV_ENERGY_IMPL=tma) or
     two (=tma2, u8 counts and 8 bins; the default picks by grid size) and register-streaming
