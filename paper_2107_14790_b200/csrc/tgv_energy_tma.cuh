@@ -114,10 +114,7 @@ __global__ void __launch_bounds__(32 * TY, NS <= 3 ? 2 : 1)
         const int jr = sgi - A.sched_off[blockIdx.x];  // this CTA's segment index (= round while < rounds)
         if (tid0) {
             for (; nxt <= ze && nxt < zs - 1 + NS; ++nxt) issue(nxt);
-            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // (the other threads wait at the first barrier)
-                const unsigned long long want = (unsigned long long)jr * gridDim.x;
-                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
-            }
+            round_wait(A.round_ctr, jr, A.rounds);  // lock-step rounds, as fused_tma_kernel
         }
 
         // carry-in: v and p_z of plane zs-1 (its slot is refilled after step zs's barrier)
@@ -185,9 +182,7 @@ __global__ void __launch_bounds__(32 * TY, NS <= 3 ? 2 : 1)
             adv(cw);
         }
         __syncthreads();  // the next segment's prologue refills every slot
-        if (A.round_ctr && tid0 && jr < A.rounds &&
-            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)
-            atomicExch(A.round_ctr, 0ull);
+        if (tid0) round_done(A.round_ctr, jr, A.rounds);
     }
 
     double vmd = (double)vm;

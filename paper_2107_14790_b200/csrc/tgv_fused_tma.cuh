@@ -128,6 +128,32 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 }
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
+// Lock-step round sync of the persistent sweeps: before its round jr the
+// issuing thread of a CTA waits until all gridDim.x CTAs finished round jr-1 (ctr counts the
+// finished rounds, the launch's last increment resets it).  The wait is bounded and never a
+// correctness dependency: one that runs out (the grid's CTAs not all resident, e.g. another
+// kernel holding SMs) sets the launch's give-up word ctr[4], and no CTA waits again until the
+// launch ends.
+__device__ __forceinline__ void round_wait(unsigned long long* ctr, int jr, int rounds)
+{
+    if (!ctr || jr < 1 || jr >= rounds || *(volatile unsigned long long*)(ctr + 4)) return;
+    const unsigned long long want = (unsigned long long)jr * gridDim.x;
+    for (uint32_t n = 0; ld_acquire_sys(ctr) < want; ++n) {
+        if (n > (1u << 18)) {  // ~20-40 ms: far beyond any honest skew between CTAs of one round
+            atomicExch(ctr + 4, 1ull);
+            return;
+        }
+        __nanosleep(64);
+    }
+}
+__device__ __forceinline__ void round_done(unsigned long long* ctr, int jr, int rounds)
+{
+    if (ctr && jr < rounds && atomicAdd(ctr, 1ull) == (unsigned long long)rounds * gridDim.x - 1) {
+        atomicExch(ctr, 0ull);  // the launch's last increment: no CTA waits any more, the next
+        atomicExch(ctr + 4, 0ull);  // launch (stream-ordered) starts from zero
+    }
+}
+
 // ---- shared memory ---------------------------------------------------------------
 constexpr int TMA_BW = 40;  // input box width: x0-4 .. x0+35 (the inner start must be 16-B aligned)
 constexpr int TMA_CW = 34;  // exchange plane width: x0-1 .. x0+32
@@ -308,10 +334,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
         if (tid0) {  // prologue: all but one slot of every ring (planes zs-1, zs, ...)
             for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
             for (int tz = zs - 1; tz < zs - 1 + Rg::NX - 1; ++tz) issue_x(tz);
-            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // (the other threads wait at S1)
-                const unsigned long long want = (unsigned long long)jr * gridDim.x;
-                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
-            }
+            round_wait(A.round_ctr, jr, A.rounds);  // (the other threads wait at S1)
         }
         mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
         int su = cu.st;
@@ -570,9 +593,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1)
             if (s + 1 > ze) break;
             step(std::integral_constant<int, 1>{}, s + 1, cb, ca);
         }
-        if (A.round_ctr && tid0 && jr < A.rounds &&  // round jr done (after S2 of its last step); the launch's
-            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)  // last increment: no
-            atomicExch(A.round_ctr, 0ull);  // CTA waits any more, the next launch (stream-ordered) starts from 0
+        if (tid0) round_done(A.round_ctr, jr, A.rounds);  // round jr done (after S2 of its last step)
     }
     if (PEER && A.done) {  // peer mode: publish once every CTA's halo stores are visible system-wide
         __threadfence_system();

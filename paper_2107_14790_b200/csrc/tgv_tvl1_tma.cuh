@@ -124,10 +124,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 2)
         if (tid0) {
             for (int tz = zs - 1; tz < zs - 1 + Rg::NU - 1; ++tz) issue_u(tz);
             for (int tz = zs - 1; tz < zs - 1 + Rg::NX - 1; ++tz) issue_x(tz);
-            if (A.round_ctr && jr >= 1 && jr < A.rounds) {  // lock-step rounds, as fused_tma_kernel
-                const unsigned long long want = (unsigned long long)jr * gridDim.x;
-                for (uint32_t n = 0; ld_acquire_sys(A.round_ctr) < want && n < (1u << 22); ++n) __nanosleep(64);
-            }
+            round_wait(A.round_ctr, jr, A.rounds);  // lock-step rounds, as fused_tma_kernel
         }
         mbar_wait(&S.bar_u[cu.st], cu.ph);  // u at plane zs-1
         int su = cu.st;
@@ -237,9 +234,7 @@ __global__ void __launch_bounds__(32 * (TY + 3), 2)
         }
         __syncthreads();  // the last step's outputs are complete (its parity counts from step zs-1)
         if (tid0) store((ze - (zs - 1)) & 1, ze);
-        if (A.round_ctr && tid0 && jr < A.rounds &&
-            atomicAdd(A.round_ctr, 1ull) == (unsigned long long)A.rounds * gridDim.x - 1)
-            atomicExch(A.round_ctr, 0ull);
+        if (tid0) round_done(A.round_ctr, jr, A.rounds);
     }
     if (tid0) tma_wait0();
 }
