@@ -522,8 +522,11 @@ int build_schedule(tgv_ctx* c, int zc, int per_sm, bool energy)
     const int nch = (nzl + zc - 1) / zc;
     const int64_t items = (int64_t)tiles * nch;
     const int64_t planes = (int64_t)tiles * nzl;
-    const int ctas = (int)std::min<int64_t>((int64_t)c->num_sms * per_sm,
-                                            env_int("TGV_PERSIST_CTAS", (int64_t)c->num_sms * per_sm));  // dev knob
+    // TGV_PERSIST_CTAS (dev knob) caps the persistent grid; TGV_PERSIST_OVERSUB (test hook)
+    // multiplies it beyond what can be resident, which only the round sync's give-up path survives
+    const int ctas = (int)(std::min<int64_t>((int64_t)c->num_sms * per_sm,
+                                             env_int("TGV_PERSIST_CTAS", (int64_t)c->num_sms * per_sm)) *
+                           (energy ? 1 : std::max<int64_t>(1, env_int("TGV_PERSIST_OVERSUB", 1))));
     const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, (planes + 7) / 8));
     std::vector<std::vector<int4>> per(G);
     // items in chunk-major order: every tile of chunk 0, then chunk 1, ...  (A band-major
@@ -633,6 +636,7 @@ int launch_fused_tma(tgv_ctx* c)
     A.keep_halo_dual = c->leaf ? 1 : 0;
     A.zc = fused_zc(c);
     A.hints = (int)env_int("TGV_L2_HINTS", 0);  // dev knob until measured
+    A.s2mb = (int)env_int("TGV_S2_MBAR", 0);    // dev knob until measured
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
     A.s_vk = slotV(b.cu, 0);

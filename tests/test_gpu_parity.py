@@ -243,13 +243,13 @@ def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
             assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
 
 
-@pytest.mark.parametrize("knobs", [{"TGV_ROUND_SYNC": "1"}])
-@pytest.mark.parametrize("shape", [(256, 140, 43), (512, 150, 12)])
+@pytest.mark.parametrize("knobs", [{"TGV_ROUND_SYNC": "1"}, {"TGV_S2_MBAR": "1"}])
+@pytest.mark.parametrize("shape", [(256, 140, 43), (512, 150, 12), (45, 31, 26)])
 def test_fused_schedule_knobs_equal_default_bitwise(monkeypatch, knobs, shape):
-    """The lock-step round sync (TGV_ROUND_SYNC, default: CTAs wait for each round before the
-    next) only orders the work: many rounds of (tile, short chunk) items plus remainder
-    segments, bitwise the unsynchronised sweep, over launches in a row (the round counter
-    resets at the end of each launch)."""
+    """Knobs that only order the work: the lock-step round sync (TGV_ROUND_SYNC, default: CTAs
+    wait for each round before the next) over many rounds of (tile, short chunk) items plus
+    remainder segments, and the step's second barrier as an mbarrier only the storing thread
+    waits on (TGV_S2_MBAR) -- bitwise the plain sweep, over launches in a row."""
     monkeypatch.setenv("TGV_FUSED_ZC", "4" if shape[2] > 20 else "3")
     h = synth.random_histograms(shape, 15)
     c = list(oracle.default_centers(8))
@@ -493,3 +493,27 @@ def test_graph_replay_equals_direct_launches_bitwise(monkeypatch, model, schedul
         s.close()
     for f in ("u", "p", "E"):
         assert np.array_equal(outs[0][f], outs[1][f]), f
+
+
+@pytest.mark.parametrize("model", ["tgv", "tvl1"])
+def test_round_sync_gives_up_when_the_grid_is_not_resident(monkeypatch, model):
+    """TGV_PERSIST_OVERSUB=2 launches twice the persistent CTAs that can be resident, so the
+    first wave's round waits can never be met: the bounded wait must give up (once per launch)
+    and the sweep finish with the unsynchronised result bit for bit, in bounded time."""
+    import time
+    shape = (256, 140, 43)
+    monkeypatch.setenv("TGV_FUSED_ZC", "4" if model == "tgv" else "2")
+    h = synth.random_histograms(shape, 18)
+    c = list(oracle.default_centers(8))
+    outs, secs = [], []
+    for sync, over in (("0", "1"), ("1", "2")):
+        monkeypatch.setenv("TGV_ROUND_SYNC", sync)
+        monkeypatch.setenv("TGV_PERSIST_OVERSUB", over)
+        s = solver_cls()(shape, c).set_model(model).load(h)
+        t0 = time.perf_counter()
+        s.iterate(5)
+        secs.append(time.perf_counter() - t0)
+        outs.append(s.get("u"))
+        s.close()
+    assert np.array_equal(outs[0], outs[1])
+    assert secs[1] < 5.0, secs  # one give-up per launch (~tens of ms), not one per round
