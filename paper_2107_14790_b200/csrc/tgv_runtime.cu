@@ -636,7 +636,6 @@ int launch_fused_tma(tgv_ctx* c)
     A.keep_halo_dual = c->leaf ? 1 : 0;
     A.zc = fused_zc(c);
     A.hints = (int)env_int("TGV_L2_HINTS", 0);  // dev knob until measured
-    A.s2mb = (int)env_int("TGV_S2_MBAR", 0);    // dev knob until measured
     A.s_uk = slotU(b.cu);
     A.s_um = slotU(b.pu);
     A.s_vk = slotV(b.cu, 0);

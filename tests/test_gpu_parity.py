@@ -243,13 +243,13 @@ def test_schedules_and_count_widths_agree_bitwise(monkeypatch):
             assert np.array_equal(o[f], ref[f]), (key, f, np.max(np.abs(o[f] - ref[f])))
 
 
-@pytest.mark.parametrize("knobs", [{"TGV_ROUND_SYNC": "1"}, {"TGV_S2_MBAR": "1"}])
+@pytest.mark.parametrize("knobs", [{"TGV_ROUND_SYNC": "1"}])
 @pytest.mark.parametrize("shape", [(256, 140, 43), (512, 150, 12), (45, 31, 26)])
 def test_fused_schedule_knobs_equal_default_bitwise(monkeypatch, knobs, shape):
-    """Knobs that only order the work: the lock-step round sync (TGV_ROUND_SYNC, default: CTAs
-    wait for each round before the next) over many rounds of (tile, short chunk) items plus
-    remainder segments, and the step's second barrier as an mbarrier only the storing thread
-    waits on (TGV_S2_MBAR) -- bitwise the plain sweep, over launches in a row."""
+    """The lock-step round sync (TGV_ROUND_SYNC, default: CTAs wait for each round before the
+    next) only orders the work: many rounds of (tile, short chunk) items plus remainder
+    segments, bitwise the unsynchronised sweep, over launches in a row (the round counter
+    resets at the end of each launch)."""
     monkeypatch.setenv("TGV_FUSED_ZC", "4" if shape[2] > 20 else "3")
     h = synth.random_histograms(shape, 15)
     c = list(oracle.default_centers(8))
